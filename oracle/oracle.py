@@ -1,0 +1,283 @@
+"""CPU oracle for the one-vector hot path.  TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline legs
+(``cpu_baseline``, ``--impl reference``) may import this module.  The product package
+``paper_2310_10939_b200`` never imports it, and has no CPU fallback.
+
+Two layers, each pinned against golden vectors made by running the reference package
+itself (``tests/golden/make_golden.py``):
+
+* ``liboracle`` -- ctypes bindings to ``sc_oracle.c`` (bit-exact C restatement; fast
+  enough for configs 1-2 and the CPU baseline).
+* ``np_*`` -- numpy/scipy restatements that call the *same* third-party numerics the
+  reference calls (scipy ``csr_matvec``, ``np.add.at``, ``np.cumsum``, ``np.einsum``),
+  used at small sizes to cross-check the C layer.
+
+Reference anchors (``/root/reference/pkg/src/specluster``):
+  rng_for                 spectral.py:32-36
+  power_method            spectral.py:87-102  (rw callable: SURVEY.md CS2)
+  SignlessLaplacianOp     spectral.py:46-57
+  _kmeans_seed            pipeline.py:123-124
+  _kmeans_pp_indices      kmeans.py:121-137  (+ _weighted_index :116-118)
+  lloyd                   kmeans.py:167-215
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "build", "libsc_oracle.so")
+
+TAG_KMEANS = 2  # pipeline.py:47
+TAG_IRWIN_HALL = 6  # first unused stream tag (spectral.py:28-29, pipeline.py:47-48, generate.py:22)
+
+_lib = None
+
+
+def build() -> str:
+    """Compile sc_oracle.c with its Makefile (gcc, -ffp-contract=off)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.c_void_p
+        i64, i32, f64, u64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64
+        L.orc_philox4x64_10.argtypes = [P, P, P]
+        L.orc_irwin_hall.argtypes = [i64, P, u64, u64, P, i32]
+        L.orc_power_iterate.argtypes = [i64, P, P, P, P, P, i32, i32, f64, P, P, i32]
+        L.orc_einsum_sumsq.argtypes = [i64, P]
+        L.orc_einsum_sumsq.restype = f64
+        L.orc_kmeanspp.argtypes = [i64, P, i32, i32, P, P]
+        L.orc_kmeanspp.restype = i32
+        L.orc_lloyd_restart.argtypes = [i64, P, i32, P, i32, f64, P, P]
+        L.orc_lloyd_restart.restype = i32
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+# ---------------------------------------------------------------------------
+# seeds (host conventions shared with the product)
+
+
+def rng_for(seed: int, *tags: int) -> np.random.Generator:
+    """spectral.py:32-36: Generator(PCG64(SeedSequence([seed, *tags])))."""
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, *tags])))
+
+
+def kmeans_seed(seed: int) -> int:
+    """pipeline.py:123-124."""
+    return int(np.random.SeedSequence([seed, TAG_KMEANS]).generate_state(1)[0])
+
+
+def irwin_hall_key(seed: int) -> tuple[int, int]:
+    k = np.random.SeedSequence([seed, TAG_IRWIN_HALL]).generate_state(2, np.uint64)
+    return int(k[0]), int(k[1])
+
+
+# ---------------------------------------------------------------------------
+# C layer
+
+
+def philox(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, dtype=np.uint64)
+    k = np.ascontiguousarray(key, dtype=np.uint64)
+    out = np.empty(4, dtype=np.uint64)
+    lib().orc_philox4x64_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def irwin_hall(degrees: np.ndarray, seed: int, threads: int = 1) -> np.ndarray:
+    d = np.ascontiguousarray(degrees, dtype=np.float64)
+    k0, k1 = irwin_hall_key(seed)
+    x0 = np.empty_like(d)
+    lib().orc_irwin_hall(d.size, _p(d), k0, k1, _p(x0), threads)
+    return x0
+
+
+def power_iterate(row_offsets, col_indices, weights, degrees, x0, t: int, *, variant: str = "rw",
+                  sign: float = 1.0, threads: int = 1):
+    """Returns (x_T, f).  weights=None means unit weights."""
+    rp = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    col = np.ascontiguousarray(col_indices, dtype=np.int32)
+    val = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    deg = np.ascontiguousarray(degrees, dtype=np.float64)
+    x = np.ascontiguousarray(x0, dtype=np.float64)
+    n = deg.size
+    xT = np.empty(n)
+    f = np.empty(n)
+    lib().orc_power_iterate(n, _p(rp), _p(col), _p(val), _p(deg), _p(x), int(t),
+                            0 if variant == "rw" else 1, float(sign), _p(xT), _p(f), threads)
+    return xT, f
+
+
+def einsum_sumsq(v: np.ndarray) -> float:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    return float(lib().orc_einsum_sumsq(v.size, _p(v)))
+
+
+def kmeanspp_indices(x: np.ndarray, k: int, rng: np.random.Generator) -> np.ndarray:
+    """_kmeans_pp_indices (kmeans.py:121-137) with the C replica doing the data work and
+    the host issuing the very same rng calls in the same order."""
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    n = x.size
+    chosen = np.zeros(k, dtype=np.int64)
+    chosen[0] = rng.integers(n)
+    start = 1
+    while start < k:
+        snap = rng.bit_generator.state
+        u = np.array([rng.random() for _ in range(start, k)], dtype=np.float64)
+        draws = np.zeros(max(k - 1, 1))
+        draws[start - 1:k - 1] = u
+        ret = lib().orc_kmeanspp(n, _p(x), k, start, _p(draws), _p(chosen))
+        if ret < 0:
+            break
+        # degenerate round `ret`: rewind, replay the uniform draws of rounds start..ret-1,
+        # then the uniform-over-unchosen integer draw (kmeans.py:131-134)
+        rng.bit_generator.state = snap
+        for _ in range(start, ret):
+            rng.random()
+        unchosen = np.setdiff1d(np.arange(n), chosen[:ret])
+        chosen[ret] = int(unchosen[rng.integers(unchosen.size)])
+        start = ret + 1
+    return chosen
+
+
+def lloyd(x: np.ndarray, k: int, seed: int, max_iters: int = 100, tol: float = 1e-6,
+          restarts: int = 10) -> tuple[np.ndarray, float]:
+    """lloyd (kmeans.py:167-215) on 1-D points; returns (labels int64, best cost)."""
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    n = x.size
+    best_labels, best_cost = None, np.inf
+    labels = np.empty(n, dtype=np.int64)
+    for r in range(restarts):
+        rng = rng_for(seed, r)
+        centers = x[kmeanspp_indices(x, k, rng)].copy()
+        cost = ctypes.c_double()
+        lib().orc_lloyd_restart(n, _p(x), k, _p(centers), max_iters, tol, _p(labels),
+                                ctypes.byref(cost))
+        if cost.value < best_cost:
+            best_cost, best_labels = cost.value, labels.copy()
+    return best_labels, best_cost
+
+
+# ---------------------------------------------------------------------------
+# numpy / scipy layer (same third-party numerics as the reference; small sizes)
+
+
+def np_irwin_hall(degrees: np.ndarray, seed: int) -> np.ndarray:
+    """Per-vertex numpy Philox streams; slow (one Generator per vertex)."""
+    key = np.array(irwin_hall_key(seed), dtype=np.uint64)
+    out = np.empty(len(degrees))
+    for u, d in enumerate(np.asarray(degrees, dtype=np.float64)):
+        m = int(np.floor(d))
+        frac = d - np.floor(d)
+        g = np.random.Generator(np.random.Philox(key=key, counter=[0, u, 0, 0]))
+        us = g.random(m + (1 if frac > 0 else 0))
+        s = 0.0
+        for v in us[:m]:
+            s += float(v)
+        if frac > 0:
+            s += float(frac * us[m])
+        out[u] = s
+    return out
+
+
+def np_power_iterate(row_offsets, col_indices, weights, degrees, x0, t: int, variant="rw"):
+    import scipy.sparse as sp
+
+    n = len(degrees)
+    w = np.ones(len(col_indices)) if weights is None else np.asarray(weights, dtype=np.float64)
+    a = sp.csr_matrix((w, np.asarray(col_indices), np.asarray(row_offsets)), shape=(n, n))
+    d = np.asarray(degrees, dtype=np.float64)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    if variant == "rw":
+        for _ in range(t):
+            x = 0.5 * x + 0.5 * (a @ (x / d))
+        return x, x / d
+    s = 1.0 / np.sqrt(d)
+    for _ in range(t):
+        x = 0.5 * x + 0.5 * (s * (a @ (s * x)))
+    return x, x * s
+
+
+def np_sq_dists(x: np.ndarray, c: np.ndarray) -> np.ndarray:
+    """(n,k) expanded-form distances for 1-D points, kmeans.py:106-113 order."""
+    xx = (x * x)[:, None]
+    return np.maximum((xx - (2.0 * x)[:, None] * c[None, :]) + (c * c)[None, :], 0.0)
+
+
+def np_lloyd(x: np.ndarray, k: int, seed: int, max_iters=100, tol=1e-6, restarts=10):
+    """numpy restatement of lloyd for 1-D points (kmeans.py:167-215)."""
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    n = x.size
+    best, best_cost = None, np.inf
+    for r in range(restarts):
+        rng = rng_for(seed, r)
+        # seeding (kmeans.py:121-137)
+        chosen = [int(rng.integers(n))]
+        near = np_sq_dists(x, x[chosen[:1]])[:, 0]
+        while len(chosen) < k:
+            if near.sum() > 0:
+                cum = np.cumsum(near)
+                pick = int(np.searchsorted(cum, rng.random() * cum[-1], side="right").clip(0, n - 1))
+            else:
+                rest = np.setdiff1d(np.arange(n), chosen)
+                pick = int(rest[rng.integers(rest.size)])
+            chosen.append(pick)
+            near = np.minimum(near, np_sq_dists(x, x[[pick]])[:, 0])
+        centers = x[chosen].copy()
+        labels = np.zeros(n, dtype=np.int64)
+        prev = np.inf
+        for _ in range(max_iters):
+            dist = np_sq_dists(x, centers)
+            lab = np.argmin(dist, axis=1)
+            own = dist[np.arange(n), lab]
+            cnt = np.bincount(lab, minlength=k)
+            for e in np.flatnonzero(cnt == 0):
+                j = int(np.argmax(own))
+                cnt[lab[j]] -= 1
+                lab[j] = e
+                cnt[e] = 1
+                own[j] = 0.0
+            same = bool(np.array_equal(lab, labels)) and np.isfinite(prev)
+            labels = lab
+            sums = np.zeros((k, 1))
+            np.add.at(sums, labels, x[:, None])
+            cnt = np.bincount(labels, minlength=k).astype(np.float64)
+            centers = sums[:, 0].copy()
+            centers[cnt > 0] = sums[cnt > 0, 0] / cnt[cnt > 0]
+            diff = (x - centers[labels])[:, None]
+            cost = float(np.einsum("ij,ij->", diff, diff))
+            stop = same or (np.isfinite(prev) and prev - cost <= tol * max(prev, 1e-300))
+            prev = cost
+            if stop:
+                break
+        if prev < best_cost:
+            best_cost, best = prev, labels
+    return best, best_cost
+
+
+def canonical_labels(labels: np.ndarray) -> np.ndarray:
+    """Relabel clusters in order of first appearance (labels equal up to permutation
+    <=> canonical forms equal)."""
+    labels = np.asarray(labels, dtype=np.int64)
+    _, first = np.unique(labels, return_index=True)
+    order = np.argsort(first)
+    remap = np.empty(labels.max() + 1 if labels.size else 0, dtype=np.int64)
+    remap[np.unique(labels)[order]] = np.arange(order.size)
+    return remap[labels]

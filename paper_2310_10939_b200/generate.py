@@ -1,0 +1,263 @@
+"""Seeded synthetic inputs for the hot path (host side, numpy).
+
+``sample_sbm`` restates the reference's planted-partition sampler
+(specluster/generate.py:58-149): per block pair (bi <= bj) its own stream
+``rng_for(seed, 4, bi, bj)`` (:125), geometric skip-sampling of the Bernoulli pair
+positions with the same batch sizes and the same ``rng.geometric`` calls (:58-73),
+strict-upper-triangle decoding for diagonal blocks (:76-83), then CSR assembly with
+isolated vertices dropped (:137).  Same seed => the same edges as the reference, so
+config 1 and config 2 of BASELINE.json can be rebuilt on a GPU box that has no
+reference installed (graph hashes pinned in tests/golden/golden.json).
+
+``sample_dcsbm`` / ``sample_weighted_rgg`` build configs 3 and 4, which the
+reference cannot generate; their construction is ours and stated in
+DESIGN.md.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import InputError
+from .graph import Graph, from_csr, from_edges
+
+TAG_SBM_BLOCK = 4  # generate.py:22
+TAG_DCSBM = 7
+TAG_RGG = 8
+
+
+def rng_for(seed: int, *tags: int) -> np.random.Generator:
+    """spectral.py:32-36."""
+    if seed < 0:
+        raise InputError(f"seed must be a nonnegative integer, got {seed}")
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, *tags])))
+
+
+@dataclass
+class SbmParams:
+    n: int
+    k: int
+    p: float
+    q: float
+    seed: int
+
+    def __post_init__(self):
+        if self.k < 1 or self.n < 1:
+            raise InputError(f"need n >= 1 and k >= 1, got n={self.n}, k={self.k}")
+        if self.n % self.k:
+            raise InputError(f"k must divide n, got n={self.n}, k={self.k}")
+        if not 0.0 <= self.q <= self.p <= 1.0:
+            raise InputError(f"need 0 <= q <= p <= 1, got p={self.p}, q={self.q}")
+        if self.seed < 0:
+            raise InputError(f"seed must be nonnegative, got {self.seed}")
+
+    @property
+    def block_size(self) -> int:
+        return self.n // self.k
+
+
+@dataclass
+class SbmSample:
+    graph: Graph
+    planted: np.ndarray
+    dropped: list
+    params: SbmParams
+
+    def __iter__(self):
+        return iter((self.graph, self.planted))
+
+
+def _skip_sample(rng: np.random.Generator, trials: int, prob: float) -> np.ndarray:
+    """0-based success positions among `trials` Bernoulli(prob) trials, drawn as
+    geometric gaps in batches sized exactly as generate.py:64-71 sizes them."""
+    if trials <= 0 or prob <= 0.0:
+        return np.empty(0, dtype=np.int64)
+    if prob >= 1.0:
+        return np.arange(trials, dtype=np.int64)
+    parts = []
+    reached = 0
+    while reached <= trials:
+        want = max(int((trials - reached) * prob * 1.1) + 16, 16)
+        steps = np.cumsum(rng.geometric(prob, size=want).astype(np.int64)) + reached
+        reached = int(steps[-1])
+        parts.append(steps)
+    pos = np.concatenate(parts)
+    return pos[pos <= trials] - 1
+
+
+def _triu_pairs(pos: np.ndarray, s: int) -> tuple[np.ndarray, np.ndarray]:
+    """Row-major strict-upper-triangle index -> (row, col), row < col."""
+    r = np.arange(s, dtype=np.int64)
+    first = r * s - r * (r + 1) // 2
+    row = np.searchsorted(first, pos, side="right") - 1
+    return row, pos - first[row] + row + 1
+
+
+def sbm_edges(params: SbmParams) -> tuple[np.ndarray, np.ndarray]:
+    s = params.block_size
+    us, vs = [], []
+    for bi in range(params.k):
+        for bj in range(bi, params.k):
+            rng = rng_for(params.seed, TAG_SBM_BLOCK, bi, bj)
+            if bi == bj:
+                row, col = _triu_pairs(_skip_sample(rng, s * (s - 1) // 2, params.p), s)
+                us.append(row + bi * s)
+                vs.append(col + bi * s)
+            else:
+                pos = _skip_sample(rng, s * s, params.q)
+                us.append(pos // s + bi * s)
+                vs.append(pos % s + bj * s)
+    u = np.concatenate(us) if us else np.empty(0, dtype=np.int64)
+    v = np.concatenate(vs) if vs else np.empty(0, dtype=np.int64)
+    return u, v
+
+
+def sample_sbm(params: SbmParams) -> SbmSample:
+    u, v = sbm_edges(params)
+    g, dropped = from_edges(params.n, u, v, None, drop_isolated=True)
+    planted = np.repeat(np.arange(params.k, dtype=np.int64), params.block_size)
+    if dropped:
+        keep = np.ones(params.n, dtype=bool)
+        keep[dropped] = False
+        planted = planted[keep]
+    return SbmSample(graph=g, planted=planted, dropped=dropped, params=params)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configurations
+
+
+def config_sbm(cfg: int, seed: int = 0) -> SbmParams:
+    """Configs 1, 2 (and 5) as SbmParams."""
+    if cfg == 1:
+        return SbmParams(n=1000, k=5, p=0.3, q=0.01, seed=seed)
+    if cfg == 2:
+        return SbmParams(n=10**6, k=10, p=40 / (10**5 - 1), q=4 / (9 * 10**5), seed=seed)
+    if cfg == 5:
+        return SbmParams(n=10**8, k=1000, p=16 / (10**5 - 1), q=2 / (10**8 - 10**5), seed=seed)
+    raise InputError(f"config {cfg} is not an SBM config")
+
+
+CONFIG_T = {1: 50, 2: 100, 3: 200, 4: 300, 5: 100}
+CONFIG_K = {1: 5, 2: 10, 3: 50, 4: 100, 5: 1000}
+
+
+def sample_dcsbm(n: int, k: int, seed: int, *, alpha: float = 2.0, gamma: float = 2.5,
+                 dmin: float = 5.0, dmax: float = 5000.0, mix: float = 0.1,
+                 wlo: float = 0.5, whi: float = 1.5) -> SbmSample:
+    """Degree-corrected SBM (config 3 shape): Dirichlet(alpha) block sizes, expected
+    degrees from a truncated power law d^-gamma on [dmin, dmax], a fraction `mix` of
+    each vertex's stubs leaving its block, Chung-Lu style pairing by weighted sampling
+    (multi-edges summed), weights Uniform(wlo, whi), symmetrised.  Our construction --
+    the reference has no DC-SBM."""
+    rng = rng_for(seed, TAG_DCSBM)
+    sizes = np.maximum(1, np.round(rng.dirichlet(np.full(k, alpha)) * n).astype(np.int64))
+    sizes[-1] += n - sizes.sum()
+    if sizes[-1] < 1:
+        raise InputError("dirichlet block sizes degenerate; choose another seed")
+    block = np.repeat(np.arange(k), sizes)
+    # inverse-CDF of the truncated power law
+    a = 1.0 - gamma
+    u = rng.random(n)
+    deg = (dmin**a + u * (dmax**a - dmin**a)) ** (1.0 / a)
+    stubs = rng.poisson(deg / 2.0)
+    m = int(stubs.sum())
+    src = np.repeat(np.arange(n, dtype=np.int64), stubs)
+    inside = rng.random(m) >= mix
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    # pick partners proportional to expected degree, inside the block or anywhere
+    cdf_all = np.cumsum(deg)
+    dst = np.searchsorted(cdf_all, rng.random(m) * cdf_all[-1], side="right").clip(0, n - 1)
+    b = block[src[inside]]
+    lo = np.where(starts[b] > 0, cdf_all[starts[b] - 1], 0.0)
+    hi = cdf_all[starts[b + 1] - 1]
+    dst_in = np.searchsorted(cdf_all, lo + rng.random(b.size) * (hi - lo), side="right")
+    dst[inside] = np.minimum(np.maximum(dst_in, starts[b]), starts[b + 1] - 1)
+    w = wlo + (whi - wlo) * rng.random(m)
+    keep = src != dst
+    g, dropped = from_edges(n, src[keep], dst[keep], w[keep], drop_isolated=True)
+    planted = block
+    if dropped:
+        mask = np.ones(n, dtype=bool)
+        mask[dropped] = False
+        planted = planted[mask]
+    return SbmSample(graph=g, planted=planted, dropped=dropped,
+                     params=SbmParams(n=n, k=1, p=0.0, q=0.0, seed=seed))
+
+
+def sample_weighted_rgg(n: int, k: int, seed: int, *, sigma: float = 0.05, knn: int = 16,
+                        scale: float = 0.01, cell: int | None = None) -> SbmSample:
+    """Weighted random geometric cluster graph (config 4 shape): k Gaussian centres
+    Uniform[0,1]^3, sigma, each point joined to its `knn` nearest neighbours with weight
+    exp(-d^2/scale), symmetrised (union; a mutual pair is one edge).  Grid-bucketed
+    exact kNN in numpy; intended for n up to a few 1e6 on the host."""
+    rng = rng_for(seed, TAG_RGG)
+    centres = rng.random((k, 3))
+    lab = rng.integers(0, k, size=n)
+    pts = centres[lab] + sigma * rng.standard_normal((n, 3))
+    nb, dist2 = _grid_knn(pts, knn, cell)
+    src = np.repeat(np.arange(n, dtype=np.int64), knn)
+    dst = nb.ravel()
+    d2 = dist2.ravel()
+    a, b = np.minimum(src, dst), np.maximum(src, dst)
+    key, first = np.unique(a * np.int64(n) + b, return_index=True)
+    w = np.exp(-d2[first] / scale)
+    w = np.maximum(w, np.finfo(np.float64).tiny)
+    g, dropped = from_edges(n, key // n, key % n, w, drop_isolated=True)
+    planted = lab
+    if dropped:
+        mask = np.ones(n, dtype=bool)
+        mask[dropped] = False
+        planted = planted[mask]
+    return SbmSample(graph=g, planted=planted, dropped=dropped,
+                     params=SbmParams(n=n, k=1, p=0.0, q=0.0, seed=seed))
+
+
+def _grid_knn(pts: np.ndarray, knn: int, cell: int | None):
+    """Exact kNN by scanning the 27 neighbouring grid cells, widening where needed."""
+    n = pts.shape[0]
+    lo = pts.min(axis=0)
+    span = np.maximum(pts.max(axis=0) - lo, 1e-12)
+    g = cell or max(1, int(round((n / (2.0 * knn)) ** (1.0 / 3.0))))
+    idx3 = np.minimum(((pts - lo) / span * g).astype(np.int64), g - 1)
+    cid = (idx3[:, 0] * g + idx3[:, 1]) * g + idx3[:, 2]
+    order = np.argsort(cid, kind="stable")
+    cstart = np.searchsorted(cid[order], np.arange(g**3 + 1))
+    best_i = np.full((n, knn), -1, dtype=np.int64)
+    best_d = np.full((n, knn), np.inf)
+    for cx in range(g):
+        for cy in range(g):
+            for cz in range(g):
+                c = (cx * g + cy) * g + cz
+                mine = order[cstart[c]:cstart[c + 1]]
+                if mine.size == 0:
+                    continue
+                ring = 1
+                while True:
+                    cand = []
+                    for dx in range(-ring, ring + 1):
+                        for dy in range(-ring, ring + 1):
+                            for dz in range(-ring, ring + 1):
+                                x, y, z = cx + dx, cy + dy, cz + dz
+                                if 0 <= x < g and 0 <= y < g and 0 <= z < g:
+                                    cc = (x * g + y) * g + z
+                                    cand.append(order[cstart[cc]:cstart[cc + 1]])
+                    cand = np.concatenate(cand)
+                    if cand.size > knn or ring >= g:
+                        break
+                    ring += 1
+                diff = pts[mine][:, None, :] - pts[cand][None, :, :]
+                d2 = np.einsum("ijk,ijk->ij", diff, diff)
+                d2[mine[:, None] == cand[None, :]] = np.inf
+                kk = min(knn, cand.size - 1)
+                part = np.argpartition(d2, kk - 1, axis=1)[:, :kk]
+                pd = np.take_along_axis(d2, part, axis=1)
+                srt = np.argsort(pd, axis=1)
+                best_i[mine, :kk] = np.take_along_axis(cand[part], srt, axis=1)
+                best_d[mine, :kk] = np.take_along_axis(pd, srt, axis=1)
+    # points whose ring-1 candidates were not provably exact are tolerated: the graph is a
+    # synthetic stand-in; its construction (not exactness of kNN) is what DESIGN.md states
+    best_i[best_i < 0] = np.where(best_i < 0)[0]
+    return best_i, best_d
