@@ -1,0 +1,269 @@
+"""Benchmark: power-iteration GNNZ/s (nnz x iters / s) of the one-vector hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 2]
+
+One step = one full pass of the hot path's dominant stage over the workload: T lazy-
+random-walk iterations (T=100 at config 2) of the fused sm_100a SpMV, from a resident
+Irwin-Hall x0, ending in f = D^-1 x_T.  `value` is device-timed with
+CUDA events on the library's stream, inputs resident in HBM; `e2e` is the same metric
+through the public API fast_spectral_cluster() from pinned host buffers (graph upload,
+x0, T iterations, D^-1, 1-D k-means, labels + embedding read back), and `cluster_ms` is
+that end-to-end cluster time.  The CSR streamed per iteration (>= 0.2 GB) is larger than
+L2, so no flush is needed between timed iterations.
+
+For N > 1 (torchrun, one rank per GPU) the CSR is row-block sharded by nnz and z is
+all-gathered over NCCL every iteration (paper_2310_10939_b200/distributed.py); per-GPU
+work is fixed (weak scaling: each rank holds one config-2 sized block).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "power-iter GNNZ/s (nnz*iters/s)"
+UNIT = "GNNZ/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--weighted", action="store_true",
+                    help="force the weighted kernel (reads val even for unit weights)")
+    return ap.parse_args()
+
+
+def build_config(cfg: int):
+    from paper_2310_10939_b200.generate import CONFIG_K, CONFIG_T, config_sbm, sample_dcsbm, sample_sbm
+
+    if cfg in (1, 2, 5):
+        g = sample_sbm(config_sbm(cfg)).graph
+    elif cfg == 3:
+        g = sample_dcsbm(4_000_000, 50, seed=0).graph
+    else:
+        raise SystemExit(f"config {cfg} not wired into bench.py yet")
+    return g, CONFIG_T[cfg], CONFIG_K[cfg]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def traffic_from_profiles(cfg: int, unit: bool):
+    """dram bytes per launch of the SpMV kernel from the committed ncu summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get(f"c{cfg}_{'unit' if unit else 'weighted'}")
+
+
+def cpu_baseline(g, T, threads):
+    """Oracle port (sc_oracle.c, bit-exact restatement of the reference rw power_method)
+    on the host cores: one full T-iteration pass over the same graph."""
+    from oracle import oracle as O
+
+    x0 = O.irwin_hall(g.degrees, 0, threads=threads)
+    t = time.perf_counter()
+    O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, T, threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": g.nnz * T / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"config workload, {T} rw iterations, n={g.n}, nnz={g.nnz}, "
+                      f"oracle/sc_oracle.c row-parallel on {threads} threads ({dt:.2f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    g, T, k = build_config(args.config)
+    threads = os.cpu_count() or 1
+    from oracle import oracle as O
+
+    x0 = O.irwin_hall(g.degrees, 0, threads=threads)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, T, threads=threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t)
+    tot = sum(times)
+    val = g.nnz * T * len(times) / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"config{args.config}", "n": g.n,
+                                        "nnz": g.nnz, "T": T, "k": k},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{T} rw iterations of config{args.config} per step, "
+                                   f"oracle/sc_oracle.c on {threads} threads"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    import torch
+
+    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    out = t.numpy().view(a.dtype)[: a.size].reshape(a.shape)
+    out[...] = a
+    out._keep = t  # noqa: SLF001  (keep the pinned allocation alive)
+    return out
+
+
+def run_b200(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2310_10939_b200 import distributed
+
+        return distributed.bench_main(args, METRIC, UNIT)
+    from paper_2310_10939_b200 import DeviceGraph, SpectralParams, fast_spectral_cluster
+    from paper_2310_10939_b200.graph import Graph
+
+    g, T, k = build_config(args.config)
+    unit = g.unit_weights() and not args.weighted
+    dev = DeviceGraph(g)
+    info = dev.info()
+    dev.sample_irwin_hall(0)
+    for _ in range(max(args.warmup, 3)):
+        dev.power_iterate(T, want_x=False, want_f=False, force_weighted=args.weighted)
+    times = []
+    with ClockSampler() as clk:
+        for _ in range(args.steps):
+            dev.power_iterate(T, want_x=False, want_f=False, force_weighted=args.weighted)
+            times.append(dev.last_timing["power_ms"])
+    clocks = clk.summary()
+    tot_ms = sum(times)
+    value = g.nnz * T * args.steps / (tot_ms / 1e3) / 1e9
+    kernel_ms = tot_ms / (args.steps * T)
+    n = g.n
+    idx_val = 4 + (0 if unit else 8)
+    alg_bytes = g.nnz * idx_val + 16 * n
+    compulsory = g.nnz * idx_val + n * ((8 if info["rp64"] else 4) + 8 + 8 + 8 + 8)
+    peak, peak_kind = peak_hbm()
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = traffic_from_profiles(args.config, unit)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "alg_bytes_per_launch": alg_bytes,
+                "alg_bytes_formula": f"nnz*{idx_val} + 16n" + ("" if unit else " (idx+val)"),
+                "compulsory_bytes_per_launch": compulsory,
+                "compulsory_frac": compulsory / (kernel_ms / 1e3) / 1e9 / peak,
+                "kernel_ms": kernel_ms}
+    # ---- end to end through the public API, pinned host buffers
+    gp = Graph(n=g.n, row_offsets=pinned_copy(g.row_offsets), col_indices=pinned_copy(g.col_indices),
+               weights=None if g.weights is None else pinned_copy(g.weights),
+               degrees=pinned_copy(g.degrees))
+    params = SpectralParams(k=k, t=T, mode="one_vector", seed=0)
+    e2e_t, res = [], None
+    fast_spectral_cluster(gp, params)  # warm (module load, context)
+    for _ in range(args.e2e_steps):
+        t = time.perf_counter()
+        res = fast_spectral_cluster(gp, params)
+        e2e_t.append(time.perf_counter() - t)
+    e2e_s = statistics.median(e2e_t)
+    h2d = g.row_offsets.nbytes + g.nnz * 4 + g.degrees.nbytes + (0 if g.weights is None or g.unit_weights() else g.nnz * 8)
+    d2h = n * 8 + n * 8  # labels (int64) + embedding f
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}", "graph": "SBM (reference sample_sbm semantics)",
+                   "n": n, "nnz": g.nnz, "T": T, "k": k, "unit_weight_kernel": unit,
+                   "l2": "inputs larger than L2 (CSR streamed per iteration >= 0.2 GB)",
+                   "parallelism": "single GPU"},
+        "roofline": roofline,
+        "e2e": {"value": g.nnz * T / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "cluster_ms": e2e_s * 1e3,
+                "stages_ms": {k_: round(v, 3) for k_, v in res.timings.items()},
+                "upload_ms": res.device_timings.get("upload_ms")},
+        "gpu_launches": args.steps * (T + 1),
+        "clocks": clocks,
+        "graph_info": {k_: info[k_] for k_ in ("ntiles", "long_rows", "rp64", "device_bytes")},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(g, T, os.cpu_count() or 1)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

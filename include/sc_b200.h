@@ -1,0 +1,150 @@
+/*
+ * sc_b200.h -- C-ABI of the B200-native one-vector clustering path.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types), callable from ctypes, cgo, JNI
+ * or C++.  Every entry point returns an int status: 0 = ok, -1..-99 = input error
+ * (maps to specluster.errors.InputError, CLI exit 2), <= -100 = CUDA / internal error
+ * (maps to SpeclusterError, CLI exit 1); see specluster/errors.py:8-29 and
+ * specluster/cli.py:411-427.  The message of the last failure on the calling thread
+ * is returned by sc_last_error().
+ *
+ * Which reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/specluster):
+ *
+ *   sc_graph_create        Graph CSR arrays (graph.py:28-45) + SignlessLaplacianOp
+ *                          .__init__ (spectral.py:46-50: caches the adjacency and
+ *                          deg^{-1/2}); uploads once, builds the nnz-balanced tiling.
+ *   sc_sample_irwin_hall   the start vector x0(u) ~ IW(deg u) of the one-vector method
+ *                          (PAPER.md:20); stands where sample_gaussian_vectors
+ *                          (spectral.py:183-195) stands for Algorithm 2.
+ *   sc_set_x0              an x0 supplied by the caller (the reference's own vector).
+ *   sc_power_iterate       power_method(op, x0, t) (spectral.py:87-102) with op the lazy
+ *                          random walk x -> 0.5 x +/- 0.5 A D^-1 x (or, with
+ *                          SC_SYM_VARIANT, SignlessLaplacianOp.matvec spectral.py:52-57),
+ *                          followed by the degree normalisation (pipeline.py:157 analogue:
+ *                          f = D^-1 x_T for rw, f = D^-1/2 x_T for sym).
+ *   sc_kmeans_*            lloyd (kmeans.py:167-215) on the 1-D embedding, bit-exact
+ *                          replica of its k-means++ seeding (kmeans.py:116-137) and Lloyd
+ *                          iterations; the host replays the PCG64 draws
+ *                          (rng_for(seed, r), spectral.py:32-36).
+ *   sc_shard_*             row-block shard of the CSR for 1/2/4/8-GPU runs (no reference
+ *                          counterpart).
+ */
+#ifndef SC_B200_H
+#define SC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SC_OK 0
+#define SC_E_INVALID (-1)      /* bad argument (null pointer, size, dtype contract) */
+#define SC_E_RANGE (-2)        /* index out of range / inconsistent CSR */
+#define SC_E_STATE (-3)        /* call order violated (e.g. power_iterate before x0) */
+#define SC_E_CUDA (-100)       /* CUDA runtime error */
+#define SC_E_OOM (-101)        /* device allocation failed */
+#define SC_E_INTERNAL (-102)
+
+/* sc_power_iterate flags */
+#define SC_SYM_VARIANT 0x1u    /* signless symmetric operator (reference Algorithm-2 op) */
+#define SC_NO_CUDA_GRAPH 0x2u  /* launch T kernels instead of replaying a captured graph */
+#define SC_L2_PERSIST 0x4u     /* pin the gathered z vector in L2 (access-policy window) */
+#define SC_FORCE_WEIGHTED 0x8u /* use the weighted kernel even if all weights are 1.0 */
+
+typedef struct sc_graph sc_graph;
+typedef struct sc_kmeans sc_kmeans;
+
+typedef struct sc_graph_info {
+    int64_t n;            /* local rows */
+    int64_t nnz;          /* local stored entries */
+    int64_t ncols;        /* length of the gathered z space */
+    int64_t col_offset;   /* where local row i's z lives in z space */
+    int64_t ntiles;       /* nnz-balanced row tiles */
+    int64_t long_rows;    /* rows handled by single-row tiles */
+    int32_t unit_weights; /* 1 if the val array was elided */
+    int32_t rp64;         /* 1 if row offsets are kept as int64 on device */
+    int64_t device_bytes; /* device memory owned by the handle */
+    int32_t device;
+    int32_t sm_count;
+} sc_graph_info;
+
+typedef struct sc_timing {
+    double sample_ms;     /* Irwin-Hall / x0 upload + z0 */
+    double power_ms;      /* T iterations, CUDA events on the handle's stream */
+    double kernel_ms;     /* power_ms / T */
+    double d2h_ms;
+} sc_timing;
+
+int32_t sc_version(void);
+const char *sc_last_error(void);
+int32_t sc_device_count(void);
+
+/* ---- graph handle ------------------------------------------------------- */
+/* row_ptr int64[n+1] (host), col int32[nnz] (host), val double[nnz] or NULL (unit),
+ * deg double[n] (host, copied verbatim -- never recomputed).  The handle owns the
+ * device copies and one CUDA stream on `device`. */
+int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double *val,
+                        const double *deg, int64_t n, int64_t nnz, int32_t device,
+                        sc_graph **out);
+/* Row-block shard: rows are the local block, columns index a z space of length ncols in
+ * which this shard's own rows live at [col_offset, col_offset + n). */
+int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double *val,
+                        const double *deg, int64_t n, int64_t nnz, int64_t ncols,
+                        int64_t col_offset, int64_t global_row0, int32_t device,
+                        sc_graph **out);
+void sc_graph_destroy(sc_graph *g);
+int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *out);
+
+/* ---- start vector ------------------------------------------------------- */
+/* x0(u) = sum of floor(deg u) uniforms (+ frac(deg u) * one more), uniform j of global
+ * vertex u = word j%4 of Philox4x64-10(key, counter (j/4+1, u, 0, 0)) as
+ * (raw >> 11) * 2^-53.  x0_out (host, nullable) receives the local x0. */
+int32_t sc_sample_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x0_out);
+int32_t sc_set_x0(sc_graph *g, const double *x0_host);
+
+/* ---- power iteration ---------------------------------------------------- */
+/* T steps of x <- 0.5 x + sign*0.5 A D^-1 x (sign = +1 or -1) from the current x0;
+ * xT_out / f_out are host buffers (nullable).  After the call f stays resident on the
+ * device for sc_kmeans_create_from_graph. */
+int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, double *xT_out,
+                         double *f_out, sc_timing *t_out);
+
+/* ---- device-pointer shard step (multi-GPU composition) ------------------ */
+/* One iteration on a shard using caller-owned device buffers on caller stream:
+ * reads z_in[ncols] (gathered), x_in[n]; writes x_out[n], z_out[col_offset + i]. */
+int32_t sc_shard_step(sc_graph *g, const double *z_in, const double *x_in, double *x_out,
+                      double *z_out, double sign, uint32_t flags, void *stream);
+/* z_out[col_offset + i] = x[i] / deg[i] (or * deg^-1/2 with SC_SYM_VARIANT) */
+int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t flags,
+                       void *stream);
+/* x0 for the shard rows (global ids global_row0..), device output */
+int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x_out,
+                            void *stream);
+
+/* ---- 1-D k-means replica ------------------------------------------------ */
+/* points: host f (n doubles) or, with _from_graph, the f left on the device by the last
+ * sc_power_iterate.  restarts batches independent restarts on the device. */
+int32_t sc_kmeans_create(const double *points_host, int64_t n, int32_t device,
+                         sc_kmeans **out);
+int32_t sc_kmeans_create_from_graph(sc_graph *g, sc_kmeans **out);
+void sc_kmeans_destroy(sc_kmeans *km);
+/* k-means++ seeding for `restarts` restarts at once.  chosen[r*k + i] (in/out);
+ * rounds start_round[r]..k-1 are run with uniforms[r*(k-1) + i-1] as round i's
+ * rng.random() draw.  degenerate_out[r] = -1 if complete, else the first round at which
+ * every D^2 weight was 0 (the caller replays rng.integers on the host and resumes). */
+int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t restarts, const int32_t *start_round,
+                     const double *uniforms, int64_t *chosen, int32_t *degenerate_out);
+/* Lloyd from the points at chosen[r*k..], max_iters / tol as lloyd(); writes the final
+ * cost and iteration count of every restart and the labels of the winning restart (first
+ * restart with the strictly smallest cost). */
+int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t restarts, const int64_t *chosen,
+                        int32_t max_iters, double tol, int64_t *labels_out, double *costs_out,
+                        int32_t *iters_out, int32_t *best_restart_out, double *ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SC_B200_H */

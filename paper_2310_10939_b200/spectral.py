@@ -1,0 +1,222 @@
+"""Device-resident operators, the Irwin-Hall start vector and the power method.
+
+Mirrors the operator half of specluster/spectral.py:
+  * ``rng_for``            spectral.py:32-36 (SeedSequence([seed, *tags]) -> PCG64)
+  * ``SignlessLaplacianOp`` spectral.py:39-64 -- same ``.n`` / ``.matvec`` protocol,
+    executed by the sm_100a kernel with the symmetric variant flag
+  * ``RandomWalkOp``        the one-vector operator M x = 0.5 x +/- 0.5 A D^-1 x
+    (PAPER.md:19 with the '+' sign of PAPER.md:109,134,162)
+  * ``power_method``       spectral.py:87-102 -- T fused steps on the GPU
+  * ``EmbeddingMatrix``    spectral.py:109-135
+  * ``sample_irwin_hall``  x0(u) ~ IW(deg u); counter-based Philox4x64-10,
+    stream tag 6 (tags 1-5 are taken: spectral.py:28-29, pipeline.py:47-48, generate.py:22)
+
+Everything numeric runs in libsc_b200.so; this module only moves arrays and keys.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import InputError
+from .graph import Graph, as_graph
+
+TAG_IRWIN_HALL = 6
+GENERATOR_NAME = "philox4x64-10-irwin-hall"
+
+
+def rng_for(seed: int, *tags: int) -> np.random.Generator:
+    if seed < 0:
+        raise InputError(f"seed must be a nonnegative integer, got {seed}")
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, *tags])))
+
+
+def irwin_hall_key(seed: int) -> tuple[int, int]:
+    """Philox key of the Irwin-Hall stream: SeedSequence([seed, 6]) -> two u64 words."""
+    if seed < 0:
+        raise InputError(f"seed must be a nonnegative integer, got {seed}")
+    k = np.random.SeedSequence([seed, TAG_IRWIN_HALL]).generate_state(2, np.uint64)
+    return int(k[0]), int(k[1])
+
+
+@dataclass
+class EmbeddingMatrix:
+    """n x l block, one vertex per row (spectral.py:109-135)."""
+
+    data: np.ndarray
+    scaled: bool
+    seed: int = 0
+
+    def __post_init__(self):
+        self.data = np.ascontiguousarray(self.data, dtype=np.float64)
+        if self.data.ndim != 2 or self.data.shape[1] < 1:
+            raise InputError("embedding must be a 2-D array with at least one column")
+        if not np.all(np.isfinite(self.data)):
+            raise InputError("embedding contains NaN or Inf")
+
+    @property
+    def n(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def l(self) -> int:
+        return self.data.shape[1]
+
+
+class DeviceGraph:
+    """Owns an ``sc_graph`` handle: the CSR uploaded once to one GPU (graph.py:28-45
+    layout; degrees copied verbatim, never recomputed)."""
+
+    def __init__(self, graph, device: int = 0):
+        g = as_graph(graph)
+        g.validate()
+        L = _lib.require_device()
+        self.graph = g
+        self.n = g.n
+        self.nnz = g.nnz
+        self._rp = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
+        self._col = np.ascontiguousarray(g.col_indices, dtype=np.int32)
+        self._deg = np.ascontiguousarray(g.degrees, dtype=np.float64)
+        w = None if (g.weights is None or g.unit_weights()) else np.ascontiguousarray(
+            g.weights, dtype=np.float64)
+        h = ctypes.c_void_p()
+        _lib.check(L.sc_graph_create(_lib.ptr(self._rp), _lib.ptr(self._col), _lib.ptr(w),
+                                     _lib.ptr(self._deg), g.n, g.nnz, device, ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        self.last_timing = None
+
+    # -- lifecycle
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.load().sc_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise InputError("device graph is closed")
+        return self._h
+
+    def info(self) -> dict:
+        gi = _lib.GraphInfo()
+        _lib.check(_lib.load().sc_graph_info_get(self.handle, ctypes.byref(gi)))
+        return {f: getattr(gi, f) for f, _ in gi._fields_}
+
+    # -- start vector
+    def sample_irwin_hall(self, seed: int, return_host: bool = False):
+        k0, k1 = irwin_hall_key(seed)
+        out = np.empty(self.n) if return_host else None
+        _lib.check(_lib.load().sc_sample_irwin_hall(self.handle, k0, k1, _lib.ptr(out)))
+        return out
+
+    def set_x0(self, x0) -> None:
+        x = np.ascontiguousarray(x0, dtype=np.float64)
+        if x.shape != (self.n,):
+            raise InputError(f"x0 has shape {x.shape}, expected ({self.n},)")
+        if not np.all(np.isfinite(x)):
+            raise InputError("x0 contains NaN or Inf")
+        _lib.check(_lib.load().sc_set_x0(self.handle, _lib.ptr(x)))
+
+    # -- power iteration
+    def power_iterate(self, t: int, *, sign: float = 1.0, sym: bool = False,
+                      want_x: bool = True, want_f: bool = True, cuda_graph: bool = True,
+                      l2_persist: bool = False, force_weighted: bool = False):
+        if t < 0:
+            raise InputError(f"power method step count must be >= 0, got {t}")
+        flags = ((_lib.SC_SYM_VARIANT if sym else 0) | (0 if cuda_graph else _lib.SC_NO_CUDA_GRAPH)
+                 | (_lib.SC_L2_PERSIST if l2_persist else 0)
+                 | (_lib.SC_FORCE_WEIGHTED if force_weighted else 0))
+        xT = np.empty(self.n) if want_x else None
+        f = np.empty(self.n) if want_f else None
+        tm = _lib.Timing()
+        _lib.check(_lib.load().sc_power_iterate(self.handle, int(t), float(sign), flags,
+                                                 _lib.ptr(xT), _lib.ptr(f), ctypes.byref(tm)))
+        self.last_timing = {"power_ms": tm.power_ms, "kernel_ms": tm.kernel_ms,
+                            "d2h_ms": tm.d2h_ms}
+        return xT, f
+
+
+class _DeviceOp:
+    """Operator protocol of spectral.py:52-59/71-79 (``.n``, ``.matvec``) backed by a
+    DeviceGraph; ``power(x0, t)`` runs t fused steps without host round trips."""
+
+    _sym = False
+
+    def __init__(self, graph, device: int = 0, sign: float = 1.0):
+        self.dev = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
+        self.graph = self.dev.graph
+        self.n = self.dev.n
+        self.sign = sign
+
+    def power(self, x0: np.ndarray, t: int) -> np.ndarray:
+        x0 = np.asarray(x0, dtype=np.float64)
+        if x0.shape[0] != self.n:
+            raise InputError(f"operand has {x0.shape[0]} rows, operator expects {self.n}")
+        if x0.ndim == 1:
+            self.dev.set_x0(x0)
+            xT, _ = self.dev.power_iterate(t, sign=self.sign, sym=self._sym, want_f=False)
+            return xT
+        cols = [self.power(x0[:, i], t) for i in range(x0.shape[1])]
+        return np.stack(cols, axis=1)
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        return self.power(x, 1)
+
+    __call__ = matvec
+
+
+class RandomWalkOp(_DeviceOp):
+    """M x = 0.5 x + sign * 0.5 * A (x / d): the one-vector lazy random walk."""
+
+
+class SignlessLaplacianOp(_DeviceOp):
+    """M x = 0.5 x + 0.5 s (A (s x)), s = deg^-1/2 (spectral.py:39-57), on the GPU."""
+
+    _sym = True
+
+    @property
+    def inv_sqrt_degrees(self) -> np.ndarray:
+        return 1.0 / np.sqrt(self.graph.degrees)
+
+
+def power_method(op, x0: np.ndarray, t: int) -> np.ndarray:
+    """M^t x0, no normalisation (spectral.py:87-102).  Device operators run t fused
+    steps on the GPU; a plain callable is the caller's own operator and is applied t
+    times as given (nothing here computes on the CPU on its behalf)."""
+    if t < 0:
+        raise InputError(f"power method step count must be >= 0, got {t}")
+    if isinstance(op, _DeviceOp):
+        return op.power(x0, int(t))
+    if isinstance(op, (Graph,)):
+        return RandomWalkOp(op).power(x0, int(t))
+    if callable(op) and not isinstance(op, np.ndarray):
+        x = np.array(x0, dtype=np.float64, copy=True)
+        for _ in range(int(t)):
+            x = op(x)
+        return x
+    raise InputError(f"cannot interpret {type(op).__name__} as a device operator; wrap the "
+                     "graph in RandomWalkOp or SignlessLaplacianOp")
+
+
+def sample_irwin_hall(graph, seed: int, device: int = 0) -> EmbeddingMatrix:
+    """x0(u) ~ IW(deg u) drawn on the GPU, returned as an n x 1 EmbeddingMatrix."""
+    dev = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
+    x0 = dev.sample_irwin_hall(seed, return_host=True)
+    return EmbeddingMatrix(data=x0[:, None], scaled=False, seed=seed)
