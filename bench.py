@@ -172,13 +172,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+_PINNED = []  # keeps the pinned host allocations alive
+
+
 def pinned_copy(a: np.ndarray) -> np.ndarray:
     import torch
 
-    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    _PINNED.append(t)
     out = t.numpy().view(a.dtype)[: a.size].reshape(a.shape)
     out[...] = a
-    out._keep = t  # noqa: SLF001  (keep the pinned allocation alive)
     return out
 
 

@@ -144,6 +144,13 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t restarts, const int64_
                         int32_t max_iters, double tol, int64_t *labels_out, double *costs_out,
                         int32_t *iters_out, int32_t *best_restart_out, double *ms_out);
 
+/* ---- exact sequential sums (the k-means replica's engine, exposed for testing) ---- */
+/* totals[s] = ((vals[lo] + vals[lo+1]) + ...) left to right in double, lo..hi = segment s;
+ * bit-identical to a scalar loop / np.cumsum(...)[-1].  chunk_starts (nullable) receives
+ * the running value at every 256-element chunk start. */
+int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *seg_off, int32_t device,
+                  double *totals, double *chunk_starts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,7 +43,7 @@ EXPORTS = (
     "sc_graph_destroy", "sc_graph_info_get", "sc_sample_irwin_hall", "sc_set_x0",
     "sc_power_iterate", "sc_shard_step", "sc_shard_scale", "sc_shard_irwin_hall",
     "sc_kmeans_create", "sc_kmeans_create_from_graph", "sc_kmeans_destroy", "sc_kmeans_pp",
-    "sc_kmeans_lloyd",
+    "sc_kmeans_lloyd", "sc_seqsum",
 )
 
 _lib = None
@@ -81,6 +81,7 @@ def load() -> ctypes.CDLL:
         "sc_kmeans_destroy": ([P], None),
         "sc_kmeans_pp": ([P, i32, i32, P, P, P, P], i32),
         "sc_kmeans_lloyd": ([P, i32, i32, P, i32, f64, P, P, P, P, P], i32),
+        "sc_seqsum": ([P, i32, P, i32, P, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

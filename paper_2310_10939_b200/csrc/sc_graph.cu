@@ -49,91 +49,158 @@ int32_t fail(int32_t code, const char *fmt, ...) {
     return code;
 }
 
-constexpr int kTPB = 256;         // threads per tile CTA
-constexpr int kChunk = 2048;      // stored entries per shared-memory chunk
-constexpr int kRowsMax = 1024;    // rows per tile
+constexpr int kTPB = 256;         // threads per tile CTA (8 warps)
+constexpr int kChunk = 2048;      // stored entries per multi-row tile / per long-row chunk
+constexpr int kRowsMax = 128;     // rows per multi-row tile (upper bound; see rows_cap)
+constexpr int kPerThread = kChunk / kTPB;            // 8 entries per thread in phase A
+constexpr int kPadded = kChunk + 16 * kRowsMax + 16; // padded product slots (32.1 KB)
 
 struct StepArgs {
     const void *rp;        // int32 or int64 row offsets (local, rebased to 0)
-    const int32_t *col;    // padded to a multiple of 4 (+4)
+    const uint32_t *col;   // packed: (tile-local row << col_bits) | column; padded (+8)
     const double *val;     // padded, or null for unit weights
     const double *scale;   // deg (rw) or deg^-1/2 (sym)
     const double *x_in;
-    const double *z_in;    // gathered vector, indexed by col
+    const double *z_in;    // gathered vector, indexed by column
     double *x_out;
     double *z_out;         // written at col_offset + row
-    const int32_t *tiles;  // ntiles + 1 row boundaries
+    const int64_t *tile_b; // ntiles + 1 first stored entry of each tile
+    const int32_t *tile_r; // ntiles + 1 first row of each tile
     int64_t col_offset;
     double hs;             // +0.5 or -0.5
+    uint32_t col_mask;
+    int col_bits;
 };
 
-template <typename RP, bool UNIT>
-__device__ __forceinline__ void gather_products(const StepArgs &a, RP cb, RP ce, double *prod) {
-    const RP a0 = cb & ~RP(3);
-    for (RP j4 = a0 + RP(4) * threadIdx.x; j4 < ce; j4 += RP(4) * kTPB) {
-        const int4 c = ld_stream_int4(reinterpret_cast<const int4 *>(a.col + j4));
-        double v0 = 1.0, v1 = 1.0, v2 = 1.0, v3 = 1.0;
-        if (!UNIT) {
-            const double2 w01 = ld_stream_d2(reinterpret_cast<const double2 *>(a.val + j4));
-            const double2 w23 = ld_stream_d2(reinterpret_cast<const double2 *>(a.val + j4 + 2));
-            v0 = w01.x; v1 = w01.y; v2 = w23.x; v3 = w23.y;
-        }
-        const int cc[4] = {c.x, c.y, c.z, c.w};
-        const double vv[4] = {v0, v1, v2, v3};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const RP j = j4 + q;
-            if (j >= cb && j < ce) {
-                const double zv = __ldg(a.z_in + cc[q]);
-                prod[j - cb] = UNIT ? zv : __dmul_rn(vv[q], zv);
-            }
-        }
+// Shared-memory slot of row i's first product (pre = unpadded tile offset of the row).
+// start == i (mod 16): the 16 lanes of a half-warp that read the t-th product of 16
+// consecutive rows hit 16 distinct 8-byte bank pairs, so the sequential row sums of
+// phase B are bank-conflict free; consecutive segments never overlap.
+__device__ __forceinline__ int padded_start(int i, int pre) {
+    return pre + 16 * i + ((i - pre) & 15);
+}
+
+// Long-row path: products of [cb, ce) into prod[0..), lane-linear coalesced loads.
+template <bool UNIT>
+__device__ __forceinline__ void gather_linear(const StepArgs &a, int64_t cb, int64_t ce,
+                                              double *prod) {
+    for (int64_t j = cb + threadIdx.x; j < ce; j += kTPB) {
+        const uint32_t c = __ldcs(a.col + j) & a.col_mask;
+        const double zv = __ldg(a.z_in + c);
+        prod[j - cb] = UNIT ? zv : __dmul_rn(__ldcs(a.val + j), zv);
     }
 }
 
 template <bool SYM>
-__device__ __forceinline__ void row_epilogue(const StepArgs &a, int64_t r, double s) {
-    const double sc = __ldcs(a.scale + r);
+__device__ __forceinline__ void row_epilogue(const StepArgs &a, int64_t r, double s, double xr,
+                                             double sc) {
     if (SYM) s = __dmul_rn(sc, s);
-    const double y = __dadd_rn(__dmul_rn(0.5, __ldcs(a.x_in + r)), __dmul_rn(a.hs, s));
+    const double y = __dadd_rn(__dmul_rn(0.5, xr), __dmul_rn(a.hs, s));
     __stcs(a.x_out + r, y);
     a.z_out[a.col_offset + r] = SYM ? __dmul_rn(sc, y) : __ddiv_rn(y, sc);
 }
 
 template <typename RP, bool UNIT, bool SYM>
 __global__ void __launch_bounds__(kTPB) k_rw_step(StepArgs a) {
-    __shared__ double prod[kChunk];
-    __shared__ RP srp[kRowsMax + 1];
-    const int r0 = a.tiles[blockIdx.x];
-    const int r1 = a.tiles[blockIdx.x + 1];
-    const int nrows = r1 - r0;
-    const RP *rp = static_cast<const RP *>(a.rp);
-    for (int i = threadIdx.x; i <= nrows; i += kTPB) srp[i] = rp[r0 + i];
-    __syncthreads();
-    const RP b = srp[0], e = srp[nrows];
-    if (e - b <= kChunk) {
-        gather_products<RP, UNIT>(a, b, e, prod);
-        __syncthreads();
-        for (int i = threadIdx.x; i < nrows; i += kTPB) {
-            const int lo = int(srp[i] - b), hi = int(srp[i + 1] - b);
-            double s = 0.0;
-            for (int j = lo; j < hi; ++j) s = __dadd_rn(s, prod[j]);
-            row_epilogue<SYM>(a, r0 + i, s);
-        }
-    } else {
+    __shared__ double prod[kPadded];
+    __shared__ int pbase[kRowsMax + 1];  // padded_start(i, pre_i) - pre_i, then pre_i
+    __shared__ int srp[kRowsMax + 1];    // tile-local row offsets
+    const int tid = threadIdx.x;
+    const int64_t b = a.tile_b[blockIdx.x], e = a.tile_b[blockIdx.x + 1];
+    const int r0 = a.tile_r[blockIdx.x];
+    const int nrows = a.tile_r[blockIdx.x + 1] - r0;
+    if (e - b > kChunk) {
         // single long row: products chunk by chunk, one thread keeps the running sum
+        double xr = 0.0, sc = 1.0;
+        if (tid == 0) {
+            xr = __ldcs(a.x_in + r0);
+            sc = __ldcs(a.scale + r0);
+        }
         double s = 0.0;
-        for (RP cb = b; cb < e; cb += kChunk) {
-            const RP ce = (e - cb > kChunk) ? cb + kChunk : e;
-            gather_products<RP, UNIT>(a, cb, ce, prod);
+        for (int64_t cb = b; cb < e; cb += kChunk) {
+            const int64_t ce = (e - cb > kChunk) ? cb + kChunk : e;
+            gather_linear<UNIT>(a, cb, ce, prod);
             __syncthreads();
-            if (threadIdx.x == 0) {
+            if (tid == 0) {
                 const int m = int(ce - cb);
                 for (int j = 0; j < m; ++j) s = __dadd_rn(s, prod[j]);
             }
             __syncthreads();
         }
-        if (threadIdx.x == 0) row_epilogue<SYM>(a, r0, s);
+        if (tid == 0) row_epilogue<SYM>(a, r0, s, xr, sc);
+        return;
+    }
+    const int nz = int(e - b);
+    // phase A: warp w owns tile entries [256w, 256w + 256) as 8 lane-linear windows;
+    // all col (+val) loads in flight first, then all gathers.  The tile-local row of each
+    // entry travels in the high bits of the packed column word (no search).
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wbase = warp * (32 * kPerThread);
+    uint32_t cw[kPerThread];
+    double v[kPerThread];
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k) {
+        const int jl = wbase + 32 * k + lane;
+        cw[k] = jl < nz ? __ldcs(a.col + b + jl) : 0u;
+        v[k] = (!UNIT && jl < nz) ? __ldcs(a.val + b + jl) : 1.0;
+    }
+    // epilogue operands of this thread's row and the tile's row offsets (independent loads)
+    double xr = 0.0, sc = 1.0;
+    const RP *rp = static_cast<const RP *>(a.rp);
+    if (tid < nrows) {
+        xr = __ldcs(a.x_in + r0 + tid);
+        sc = __ldcs(a.scale + r0 + tid);
+    }
+    if (tid <= nrows) {
+        const int pre = int(rp[r0 + tid] - b);
+        srp[tid] = pre;
+        pbase[tid] = padded_start(tid, pre) - pre;
+    }
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k) {
+        const int jl = wbase + 32 * k + lane;
+        if (jl < nz) {
+            const double zv = __ldg(a.z_in + (cw[k] & a.col_mask));
+            v[k] = UNIT ? zv : __dmul_rn(v[k], zv);
+        }
+    }
+    __syncthreads();  // pbase ready
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k) {
+        const int jl = wbase + 32 * k + lane;
+        if (jl < nz) prod[pbase[cw[k] >> a.col_bits] + jl] = v[k];
+    }
+    __syncthreads();
+    // phase B: one thread per row adds its products left to right (scipy csr_matvec order)
+    if (tid < nrows) {
+        const int pre = srp[tid], len = srp[tid + 1] - pre;
+        const double *p = prod + pbase[tid] + pre;
+        double s = 0.0;
+        int t = 0;
+        for (; t + 4 <= len; t += 4) {
+            const double p0 = p[t], p1 = p[t + 1], p2 = p[t + 2], p3 = p[t + 3];
+            s = __dadd_rn(s, p0);
+            s = __dadd_rn(s, p1);
+            s = __dadd_rn(s, p2);
+            s = __dadd_rn(s, p3);
+        }
+        for (; t < len; ++t) s = __dadd_rn(s, p[t]);
+        row_epilogue<SYM>(a, r0 + tid, s, xr, sc);
+    }
+}
+
+// Stamp each stored entry of a multi-row tile with its tile-local row (high bits).
+template <typename RP>
+__global__ void k_pack_rows(const RP *__restrict__ rp, const int64_t *__restrict__ tile_b,
+                            const int32_t *__restrict__ tile_r, uint32_t *__restrict__ col,
+                            int col_bits) {
+    const int64_t b = tile_b[blockIdx.x], e = tile_b[blockIdx.x + 1];
+    if (e - b > kChunk) return;  // long-row tile: local row 0
+    const int r0 = tile_r[blockIdx.x], nrows = tile_r[blockIdx.x + 1] - r0;
+    for (int i = threadIdx.x >> 5; i < nrows; i += blockDim.x >> 5) {
+        const int64_t lo = rp[r0 + i], hi = rp[r0 + i + 1];
+        for (int64_t j = lo + (threadIdx.x & 31); j < hi; j += 32)
+            col[j] |= (uint32_t)i << col_bits;
     }
 }
 
@@ -190,15 +257,17 @@ struct sc_graph {
     int64_t n = 0, nnz = 0, ncols = 0, col_offset = 0, global_row0 = 0;
     bool unit = false, rp64 = false;
     void *d_rp = nullptr;
-    int32_t *d_col = nullptr;
+    uint32_t *d_col = nullptr;  // packed (local row << col_bits) | column
     double *d_val = nullptr;
     double *d_deg = nullptr;
     double *d_isd = nullptr;
     double *d_x0 = nullptr;
     double *d_x[2] = {nullptr, nullptr};
     double *d_z[2] = {nullptr, nullptr};
-    int32_t *d_tiles = nullptr;
+    int64_t *d_tile_b = nullptr;
+    int32_t *d_tile_r = nullptr;
     int64_t ntiles = 0, long_rows = 0;
+    int col_bits = 1, rows_cap = 1;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool have_x0 = false;
@@ -222,35 +291,42 @@ static int32_t dmalloc(sc_graph *g, void **p, size_t bytes) {
     return SC_OK;
 }
 
-// Host tiling: greedy row packing, <= kChunk entries and <= kRowsMax rows per tile;
+// Host tiling: greedy row packing, <= kChunk entries and <= rows_cap rows per tile;
 // a row with more than kChunk entries is a tile of its own.
-static void build_tiles(const int64_t *rp, int64_t n, std::vector<int32_t> &tiles,
-                        int64_t &long_rows) {
-    tiles.clear();
-    tiles.reserve((size_t)(rp[n] / kChunk + n / kRowsMax + 16));
-    tiles.push_back(0);
+static void build_tiles(const int64_t *rp, int64_t n, int rows_cap, std::vector<int32_t> &tr,
+                        std::vector<int64_t> &tb, int64_t &long_rows) {
+    tr.clear();
+    tb.clear();
+    const size_t guess = (size_t)(rp[n] / kChunk + n / rows_cap + 16);
+    tr.reserve(guess);
+    tb.reserve(guess);
+    auto cut = [&](int64_t r) {
+        tr.push_back((int32_t)r);
+        tb.push_back(rp[r]);
+    };
+    cut(0);
     int64_t cur_nnz = 0;
     int cur_rows = 0;
     long_rows = 0;
     for (int64_t r = 0; r < n; ++r) {
         const int64_t len = rp[r + 1] - rp[r];
         if (len > kChunk) {
-            if (cur_rows) tiles.push_back((int32_t)r);
-            tiles.push_back((int32_t)(r + 1));
+            if (cur_rows) cut(r);
+            cut(r + 1);
             ++long_rows;
             cur_nnz = 0;
             cur_rows = 0;
             continue;
         }
-        if (cur_rows && (cur_nnz + len > kChunk || cur_rows == kRowsMax)) {
-            tiles.push_back((int32_t)r);
+        if (cur_rows && (cur_nnz + len > kChunk || cur_rows == rows_cap)) {
+            cut(r);
             cur_nnz = 0;
             cur_rows = 0;
         }
         cur_nnz += len;
         ++cur_rows;
     }
-    if (cur_rows) tiles.push_back((int32_t)n);
+    if (cur_rows) cut(n);
 }
 
 static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const double *val,
@@ -298,9 +374,13 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->unit = unit;
     g->rp64 = nnz >= (int64_t(1) << 31) - kChunk;
 
-    std::vector<int32_t> tiles;
-    build_tiles(row_ptr, n, tiles, g->long_rows);
-    g->ntiles = (int64_t)tiles.size() - 1;
+    g->col_bits = 1;
+    while (g->col_bits < 31 && (int64_t(1) << g->col_bits) < ncols) ++g->col_bits;
+    g->rows_cap = (int)std::min<int64_t>(kRowsMax, int64_t(1) << (32 - g->col_bits));
+    std::vector<int32_t> tile_r;
+    std::vector<int64_t> tile_b;
+    build_tiles(row_ptr, n, g->rows_cap, tile_r, tile_b, g->long_rows);
+    g->ntiles = (int64_t)tile_r.size() - 1;
 
     int32_t st;
     auto cleanup = [&](int32_t code) {
@@ -322,7 +402,8 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if ((st = dmalloc(g, (void **)&zz, (size_t)ncols * 16))) return cleanup(st);
     g->d_z[0] = zz;
     g->d_z[1] = zz + ncols;
-    if ((st = dmalloc(g, (void **)&g->d_tiles, tiles.size() * 4))) return cleanup(st);
+    if ((st = dmalloc(g, (void **)&g->d_tile_r, tile_r.size() * 4))) return cleanup(st);
+    if ((st = dmalloc(g, (void **)&g->d_tile_b, tile_b.size() * 8))) return cleanup(st);
 
     cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&g->ev0);
@@ -347,8 +428,20 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(g->d_deg, deg, (size_t)n * 8, cudaMemcpyHostToDevice, g->stream);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(g->d_tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice,
+        e = cudaMemcpyAsync(g->d_tile_r, tile_r.data(), tile_r.size() * 4, cudaMemcpyHostToDevice,
                             g->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(g->d_tile_b, tile_b.data(), tile_b.size() * 8, cudaMemcpyHostToDevice,
+                            g->stream);
+    if (e == cudaSuccess && g->ntiles) {
+        if (g->rp64)
+            k_pack_rows<int64_t><<<(unsigned)g->ntiles, 256, 0, g->stream>>>(
+                (const int64_t *)g->d_rp, g->d_tile_b, g->d_tile_r, g->d_col, g->col_bits);
+        else
+            k_pack_rows<int32_t><<<(unsigned)g->ntiles, 256, 0, g->stream>>>(
+                (const int32_t *)g->d_rp, g->d_tile_b, g->d_tile_r, g->d_col, g->col_bits);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
     if (e != cudaSuccess) {
@@ -389,8 +482,11 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.z_in = z_in;
     a.x_out = x_out;
     a.z_out = z_out;
-    a.tiles = g->d_tiles;
+    a.tile_b = g->d_tile_b;
+    a.tile_r = g->d_tile_r;
     a.col_offset = g->col_offset;
+    a.col_bits = g->col_bits;
+    a.col_mask = g->col_bits >= 32 ? 0xffffffffu : ((1u << g->col_bits) - 1u);
     a.hs = sign < 0 ? -0.5 : 0.5;
     const dim3 grid((unsigned)g->ntiles);
 #define SC_LAUNCH(RP, U, S) k_rw_step<RP, U, S><<<grid, kTPB, 0, s>>>(a)
@@ -492,7 +588,8 @@ void sc_graph_destroy(sc_graph *g) {
     cudaFree(g->d_x[0]);
     cudaFree(g->d_x[1]);
     cudaFree(g->d_z[0]);
-    cudaFree(g->d_tiles);
+    cudaFree(g->d_tile_b);
+    cudaFree(g->d_tile_r);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
     if (g->stream) cudaStreamDestroy(g->stream);

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "sc_common.cuh"
+#include "sc_seqsum.cuh"
 
 namespace sc {
 const double *graph_f_device(const sc_graph *g);
@@ -45,7 +46,6 @@ struct sc_kmeans {
     int32_t *d_keys_alt = nullptr;
     double *d_vals = nullptr;      // [R*n] sorted points
     double *d_vals_alt = nullptr;
-    double *d_own = nullptr;       // [n] repair scratch
     void *d_cub = nullptr;
     size_t cub_bytes = 0;
     int64_t *d_chosen = nullptr;   // [R][k]
@@ -60,6 +60,12 @@ struct sc_kmeans {
     int32_t *d_changed = nullptr;  // [R]
     int32_t *d_active = nullptr;   // [R]
     int32_t *d_empty = nullptr;    // [R]
+    // exact sequential-sum workspaces (sc_seqsum.cuh)
+    int64_t cap_chunks = 0;
+    double *d_A = nullptr, *d_vmax = nullptr, *d_cstart = nullptr, *d_total = nullptr;
+    int32_t *d_kpred = nullptr, *d_neg = nullptr, *d_round_on = nullptr, *d_on = nullptr;
+    int64_t *d_q0 = nullptr, *d_q1 = nullptr, *d_cofs = nullptr, *d_nchunks = nullptr;
+    int64_t *d_segkpp = nullptr;   // [R+1] restart segments over d_best
 };
 
 namespace sc {
@@ -67,13 +73,226 @@ namespace sc {
 constexpr int kEinsumBuf = 8192;  // numpy nditer buffer size (elements)
 
 // ---------------------------------------------------------------------------
+// Segmented exact sequential sums (sc_seqsum.cuh) over a batch of segments.
+//
+// Segment s covers elements [seg_off[s], seg_off[s+1]) of vals and chunks
+// [cofs[s], cofs[s+1]) (kSeqChunk elements per chunk).  Segments whose `on` flag is 0 are
+// skipped (finished restarts).
+
+struct SegView {
+    const double *vals;
+    const int64_t *seg_off;  // S + 1
+    const int64_t *cofs;     // S + 1
+    int S;
+    const int32_t *on;       // per group of `on_div` segments (nullable = all on)
+    int on_div;
+};
+
+struct SeqWork {
+    double *A;        // approximate chunk sums
+    double *vmax;     // chunk max element
+    int32_t *kpred;   // predicted grid exponent per chunk (kNoGrid = step it)
+    int64_t *q0, *q1; // chunk parity map
+    double *cstart;   // exact running sum at each chunk start
+    int32_t *neg;     // per segment: any negative / non-finite element
+    double *total;    // per segment exact total
+};
+
+__device__ __forceinline__ int seg_of_chunk(const SegView &v, int64_t c) {
+    int lo = 0, hi = v.S;  // cofs[lo] <= c < cofs[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (v.cofs[mid] <= c) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ bool seg_on(const SegView &v, int s) {
+    return v.on == nullptr || v.on[s / v.on_div] != 0;
+}
+
+// load the chunk's elements 8 per lane, lane-contiguous; returns the element count
+__device__ __forceinline__ int load_chunk(const SegView &v, int s, int64_t c,
+                                          double (&a)[kSeqPerLane], int64_t &first) {
+    const int lane = threadIdx.x & 31;
+    const int64_t lo = v.seg_off[s] + (c - v.cofs[s]) * kSeqChunk;
+    const int64_t hi = min(lo + kSeqChunk, v.seg_off[s + 1]);
+    first = lo;
+#pragma unroll
+    for (int t = 0; t < kSeqPerLane; ++t) {
+        const int64_t j = lo + lane * kSeqPerLane + t;
+        a[t] = j < hi ? v.vals[j] : 0.0;
+    }
+    return int(hi - lo);
+}
+
+__global__ void k_seq_summarize(SegView v, SeqWork w, const int64_t *__restrict__ pn) {
+    const int64_t nchunks = *pn;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = wid; c < nchunks; c += nw) {
+        const int s = seg_of_chunk(v, c);
+        if (!seg_on(v, s)) continue;
+        double a[kSeqPerLane];
+        int64_t first;
+        const int m = load_chunk(v, s, c, a, first);
+        double sum = 0.0, mx = 0.0;
+        int bad = 0;
+#pragma unroll
+        for (int t = 0; t < kSeqPerLane; ++t) {
+            if (lane * kSeqPerLane + t < m) {
+                sum += a[t];
+                mx = fmax(mx, a[t]);
+                bad |= !(a[t] >= 0.0) || !isfinite(a[t]);
+            }
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+        }
+        if (lane == 0) {
+            w.A[c] = sum;
+            w.vmax[c] = mx;
+            if (bad) w.neg[s] = 1;
+        }
+    }
+}
+
+// one warp per segment: approximate chunk starts -> predicted grid per chunk
+__global__ void k_seq_predict(SegView v, SeqWork w) {
+    const int lane = threadIdx.x & 31;
+    const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (s >= v.S || !seg_on(v, s)) return;
+    const int64_t c0 = v.cofs[s], c1 = v.cofs[s + 1];
+    double carry = 0.0;
+    const double lo_f = 1.0 - 1.0 / 1048576.0, hi_f = 1.0 + 1.0 / 1048576.0;
+    for (int64_t g = c0; g < c1; g += 32) {
+        const int64_t c = g + lane;
+        const double A = c < c1 ? w.A[c] : 0.0;
+        double incl = A;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const double P = carry + (incl - A);
+        if (c < c1) {
+            int kp = kNoGrid;
+            const double plo = P * lo_f, phi = (P + A + w.vmax[c]) * hi_f;
+            if (plo >= 2.2250738585072014e-308) {
+                const Grid a = grid_of(plo), b = grid_of(phi);
+                if (a.k == b.k) kp = a.k;
+            }
+            w.kpred[c] = kp;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+// one warp per chunk: parity map of the chunk on its predicted grid
+__global__ void k_seq_chunkmap(SegView v, SeqWork w, const int64_t *__restrict__ pn) {
+    const int64_t nchunks = *pn;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = wid; c < nchunks; c += nw) {
+        const int kp = w.kpred[c];
+        if (kp == kNoGrid) continue;
+        const int s = seg_of_chunk(v, c);
+        if (!seg_on(v, s)) continue;
+        double a[kSeqPerLane];
+        int64_t first;
+        const int m = load_chunk(v, s, c, a, first);
+        PMap lm = pmap_id();
+#pragma unroll
+        for (int t = 0; t < kSeqPerLane; ++t)
+            if (lane * kSeqPerLane + t < m) lm = pmap_then(lm, pmap_elem(to_units(a[t], kp)));
+        const PMap tot = warp_scan_pmap(lm);
+        if (lane == 31) {
+            w.q0[c] = tot.i0;
+            w.q1[c] = tot.i1;
+        }
+    }
+}
+
+// one warp per segment: exact composition of the chunk maps (see sc_seqsum.cuh)
+__global__ void k_seq_compose(SegView v, SeqWork w) {
+    const int lane = threadIdx.x & 31;
+    const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (s >= v.S || !seg_on(v, s)) return;
+    const int64_t c0 = v.cofs[s], c1 = v.cofs[s + 1];
+    double run = 0.0;
+    if (w.neg[s]) {
+        // a segment with negative (or non-finite) elements: plain sequential sum
+        for (int64_t c = c0; c < c1; ++c) {
+            double a[kSeqPerLane];
+            int64_t first;
+            const int m = load_chunk(v, s, c, a, first);
+            if (lane == 0) w.cstart[c] = run;
+            for (int j = 0; j < m; ++j) {
+                const double x = __shfl_sync(0xffffffffu, a[j % kSeqPerLane], j / kSeqPerLane);
+                run = __dadd_rn(run, x);
+            }
+        }
+        if (lane == 0) w.total[s] = run;
+        return;
+    }
+    int64_t c = c0;
+    while (c < c1) {
+        const Grid g = grid_of(run);
+        const int64_t S0 = (int64_t)to_units(run, g.k);
+        const int64_t cl = c + lane;
+        bool ok = false;
+        PMap m = pmap_id();
+        double vmu = 0.0;
+        if (cl < c1 && g.top == (int64_t(1) << 53) && w.kpred[cl] == g.k) {
+            m = PMap{w.q0[cl], w.q1[cl]};
+            vmu = to_units(w.vmax[cl], g.k);
+            ok = true;
+        }
+        const PMap excl = warp_exclusive(warp_scan_pmap(m));
+        const int64_t Sl = pmap_apply(excl, S0);
+        if (ok) {
+            const int64_t qmax = max(m.i0, m.i1);
+            ok = (double)(g.top - Sl - qmax) >= vmu && Sl + qmax <= g.top;
+        }
+        const unsigned okm = __ballot_sync(0xffffffffu, ok || cl >= c1);
+        const int L = okm == 0xffffffffu ? 32 : __ffs(~okm) - 1;  // first lane to step
+        if (lane < L && cl < c1) w.cstart[cl] = from_units(Sl, g.k);
+        const int nadv = min(L, (int)(c1 - c));
+        if (nadv > 0) {
+            // running value at the start of chunk c + nadv
+            const int src = nadv - 1;
+            const int64_t Send = __shfl_sync(0xffffffffu, pmap_apply(m, Sl), src);
+            run = from_units(Send, g.k);
+            c += nadv;
+        }
+        if (L < 32 && c < c1) {
+            // step chunk c element by element
+            if (lane == 0) w.cstart[c] = run;
+            double a[kSeqPerLane];
+            int64_t first;
+            const int mcount = load_chunk(v, s, c, a, first);
+            warp_step_elements(a, mcount, run, -1.0, false);
+            ++c;
+        }
+    }
+    if (lane == 0) w.total[s] = run;
+}
+
+// ---------------------------------------------------------------------------
 // k-means++
 
 // best[r][j] = min over chosen[r][0..start_r-1] of d2(x_j, x[chosen])
 __global__ void k_kpp_init(const double *__restrict__ x, int64_t n, int k,
                            const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
-                           double *__restrict__ best) {
+                           const int32_t *__restrict__ on, double *__restrict__ best) {
     const int r = blockIdx.y;
+    if (!on[r]) return;
     const int s = start[r];
     double *b = best + (int64_t)r * n;
     const int64_t *ch = chosen + (int64_t)r * k;
@@ -86,13 +305,13 @@ __global__ void k_kpp_init(const double *__restrict__ x, int64_t n, int k,
     }
 }
 
-// best = min(best, d2(x, x[chosen[r][i]])) for restarts whose round i just picked
+// best = min(best, d2(x, x[chosen[r][i-1]])) when round i-1 was picked in this call
 __global__ void k_kpp_update(const double *__restrict__ x, int64_t n, int k, int i,
                              const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
-                             const int32_t *__restrict__ degen, double *__restrict__ best) {
+                             const int32_t *__restrict__ on, double *__restrict__ best) {
     const int r = blockIdx.y;
-    if (i < start[r] || degen[r] >= 0) return;
-    const double c = x[chosen[(int64_t)r * k + i]];
+    if (!on[r] || i - 1 < start[r]) return;
+    const double c = x[chosen[(int64_t)r * k + i - 1]];
     double *b = best + (int64_t)r * n;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x) {
@@ -101,70 +320,53 @@ __global__ void k_kpp_update(const double *__restrict__ x, int64_t n, int k, int
     }
 }
 
-// One CTA per restart: round i of _kmeans_pp_indices.  v0: the sequential cumsum is one
-// thread walking the weights with 8-deep prefetch (np.cumsum order); "any weight > 0" is a
-// block reduction (== best_d2.sum() > 0 for nonnegative weights).
-__global__ void __launch_bounds__(256) k_kpp_pick(int64_t n, int k, int i,
-                                                  const double *__restrict__ best,
-                                                  const double *__restrict__ u,
-                                                  int64_t *__restrict__ chosen,
-                                                  const int32_t *__restrict__ start,
-                                                  int32_t *__restrict__ degen) {
-    const int r = blockIdx.x;
-    if (i < start[r] || degen[r] >= 0) return;
-    const double *b = best + (int64_t)r * n;
-    __shared__ int any;
-    if (threadIdx.x == 0) any = 0;
-    __syncthreads();
-    int mine = 0;
-    for (int64_t j = threadIdx.x; j < n && !mine; j += blockDim.x) mine = b[j] > 0.0;
-    if (mine) any = 1;
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    if (!any) {
-        degen[r] = i;
+// per-round segment flags: restart still seeding and round i belongs to this call
+__global__ void k_kpp_round_on(int R, int i, const int32_t *__restrict__ start,
+                               const int32_t *__restrict__ on, int32_t *__restrict__ round_on,
+                               int32_t *__restrict__ neg) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    round_on[r] = on[r] && i >= start[r];
+    neg[r] = 0;
+}
+
+// Round i pick, one warp per restart: target = u * cumsum[-1] (exact), then
+// searchsorted(cumsum, target, 'right') clipped to n-1 (kmeans.py:116-118).  A zero total
+// (every weight 0) is the degenerate branch (kmeans.py:128-134): reported to the host.
+__global__ void k_kpp_search(SegView v, SeqWork w, int64_t n, int k, int i,
+                             const double *__restrict__ u, int64_t *__restrict__ chosen,
+                             int32_t *__restrict__ on, int32_t *__restrict__ degen) {
+    const int lane = threadIdx.x & 31;
+    const int r = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (r >= v.S || !seg_on(v, r)) return;
+    const double tot = w.total[r];
+    if (!(tot > 0.0)) {
+        if (lane == 0) {
+            degen[r] = i;
+            on[r] = 0;
+        }
         return;
     }
-    double tot = 0.0;
-    int64_t j = 0;
-    for (; j + 8 <= n; j += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = b[j + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) tot = __dadd_rn(tot, v[q]);
-    }
-    for (; j < n; ++j) tot = __dadd_rn(tot, b[j]);
     const double target = __dmul_rn(u[(int64_t)r * (k - 1) + (i - 1)], tot);
-    double cum = 0.0;
+    const int64_t c0 = v.cofs[r], c1 = v.cofs[r + 1];
+    // first chunk whose end exceeds target: last chunk with cstart <= target ... then check
+    int64_t lo = c0, hi = c1;  // find first chunk c with end(c) > target; end(c) = cstart[c+1]
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const double end = mid + 1 < c1 ? w.cstart[mid + 1] : tot;
+        if (end > target) hi = mid;
+        else lo = mid + 1;
+    }
     int64_t idx = n - 1;
-    for (j = 0; j + 8 <= n; j += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = b[j + q];
-        bool hit = false;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (!hit) {
-                cum = __dadd_rn(cum, v[q]);
-                if (cum > target) {
-                    hit = true;
-                    idx = j + q;
-                }
-            }
-        }
-        if (hit) break;
+    if (lo < c1) {
+        double run = w.cstart[lo];
+        double a[kSeqPerLane];
+        int64_t first;
+        const int m = load_chunk(v, r, lo, a, first);
+        const int hit = warp_step_elements(a, m, run, target, true);
+        if (hit >= 0) idx = first - v.seg_off[r] + hit;
     }
-    if (j + 8 > n) {
-        for (; j < n; ++j) {
-            cum = __dadd_rn(cum, b[j]);
-            if (cum > target) {
-                idx = j;
-                break;
-            }
-        }
-    }
-    chosen[(int64_t)r * k + i] = idx;
+    if (lane == 0) chosen[(int64_t)r * k + i] = idx;
 }
 
 // ---------------------------------------------------------------------------
@@ -319,62 +521,82 @@ __global__ void k_seg_offsets(int rk, int64_t total, const int32_t *__restrict__
     seg[t] = lo;
 }
 
-// ordered per-cluster sums (np.add.at order) and means; v0: one thread per segment
-__global__ void k_seg_means(int rk, int k, const int64_t *__restrict__ seg,
-                            const double *__restrict__ vals, const int32_t *__restrict__ active,
-                            double *__restrict__ cen) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= rk) return;
-    if (!active[t / k]) return;
-    const int64_t lo = seg[t], hi = seg[t + 1];
-    double s = 0.0;
-    int64_t j = lo;
-    for (; j + 8 <= hi; j += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = vals[j + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, v[q]);
+// chunk offsets of the (restart, cluster) segments: cofs[s] = sum ceil(len/kSeqChunk)
+__global__ void k_chunk_offsets(int S, const int64_t *__restrict__ seg, int64_t *__restrict__ cofs,
+                                int64_t *__restrict__ total) {
+    __shared__ int64_t part[1024];
+    int64_t carry = 0;
+    for (int base = 0; base < S; base += 1024) {
+        const int i = base + threadIdx.x;
+        const int64_t len = i < S ? seg[i + 1] - seg[i] : 0;
+        part[threadIdx.x] = (len + kSeqChunk - 1) / kSeqChunk;
+        __syncthreads();
+        for (int d = 1; d < 1024; d <<= 1) {
+            const int64_t o = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+            __syncthreads();
+            part[threadIdx.x] += o;
+            __syncthreads();
+        }
+        const int64_t incl = part[threadIdx.x];
+        const int64_t mine = (len + kSeqChunk - 1) / kSeqChunk;
+        if (i < S) cofs[i] = carry + incl - mine;
+        carry += part[1023];
+        __syncthreads();
     }
-    for (; j < hi; ++j) s = __dadd_rn(s, vals[j]);
-    const int64_t c = hi - lo;
-    cen[t] = c > 0 ? __ddiv_rn(s, (double)c) : s;
+    if (threadIdx.x == 0) {
+        cofs[S] = carry;
+        *total = carry;
+    }
 }
 
-// einsum lane partials: thread (r, buffer, lane) sums its lane of one 8192-element buffer
+// means = ordered sum / count (cluster_means, kmeans.py:86-93); empty clusters keep 0
+__global__ void k_seg_means(int rk, int k, const int64_t *__restrict__ seg,
+                            const double *__restrict__ total, const int32_t *__restrict__ active,
+                            double *__restrict__ cen) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rk || !active[t / k]) return;
+    const int64_t c = seg[t + 1] - seg[t];
+    cen[t] = c > 0 ? __ddiv_rn(total[t], (double)c) : 0.0;
+}
+
+// kmeans_cost in numpy einsum order (sc_oracle.c orc_einsum_sumsq): one thread per
+// 8192-element buffer carries both SSE lanes
 __global__ void k_cost_lanes(const double *__restrict__ x, int64_t n, int k,
                              const int32_t *__restrict__ lab, const double *__restrict__ cen,
                              const int32_t *__restrict__ active, int64_t nbuf,
                              double *__restrict__ part) {
     const int r = blockIdx.y;
     if (!active[r]) return;
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= nbuf * 2) return;
-    const int64_t bufi = t >> 1;
-    const int lane = (int)(t & 1);
+    const int64_t bufi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (bufi >= nbuf) return;
     const int32_t *lb = lab + (int64_t)r * n;
     const double *c = cen + (int64_t)r * k;
     const int64_t base = bufi * kEinsumBuf;
-    const int64_t m = std::min<int64_t>(kEinsumBuf, n - base);
-    double acc = 0.0;
+    const int64_t m = min((int64_t)kEinsumBuf, n - base);
+    double a0 = 0.0, a1 = 0.0;
     int64_t i = 0;
     for (; m - i >= 8; i += 8) {
+        double d[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t j = base + i + q;
+            d[q] = __dsub_rn(x[j], c[lb[j]]);
+        }
 #pragma unroll
         for (int blk = 3; blk >= 0; --blk) {
-            const int64_t j = base + i + 2 * blk + lane;
-            const double d = __dsub_rn(x[j], c[lb[j]]);
-            acc = __dadd_rn(__dmul_rn(d, d), acc);
+            a0 = __dadd_rn(__dmul_rn(d[2 * blk], d[2 * blk]), a0);
+            a1 = __dadd_rn(__dmul_rn(d[2 * blk + 1], d[2 * blk + 1]), a1);
         }
     }
     for (; i < m; i += 2) {
-        double d = 0.0;
-        if (i + lane < m) {
-            const int64_t j = base + i + lane;
-            d = __dsub_rn(x[j], c[lb[j]]);
-        }
-        acc = __dadd_rn(__dmul_rn(d, d), acc);
+        const double d0 = __dsub_rn(x[base + i], c[lb[base + i]]);
+        a0 = __dadd_rn(__dmul_rn(d0, d0), a0);
+        double d1 = 0.0;
+        if (i + 1 < m) d1 = __dsub_rn(x[base + i + 1], c[lb[base + i + 1]]);
+        a1 = __dadd_rn(__dmul_rn(d1, d1), a1);
     }
-    part[((int64_t)r * nbuf + bufi) * 2 + lane] = acc;
+    part[((int64_t)r * nbuf + bufi) * 2 + 0] = a0;
+    part[((int64_t)r * nbuf + bufi) * 2 + 1] = a1;
 }
 
 // buffer totals (l0 + l1) added into the running output in buffer order
@@ -411,6 +633,9 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     k = std::max(k, km->cap_k);
     const int64_t n = km->n;
     const int64_t nbuf = (n + kEinsumBuf - 1) / kEinsumBuf;
+    // chunks: kpp uses R * ceil(n/C); Lloyd's R*k segments need at most R*n/C + R*k
+    const int64_t nch = (int64_t)R * ((n + kSeqChunk - 1) / kSeqChunk) + (int64_t)R * k + 1;
+    const int64_t S = (int64_t)R * k + 1;
     int32_t st;
     if ((st = grow(&km->d_best, (size_t)R * n))) return st;
     if ((st = grow(&km->d_lab[0], (size_t)R * n))) return st;
@@ -419,19 +644,31 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_keys_alt, (size_t)R * n))) return st;
     if ((st = grow(&km->d_vals, (size_t)R * n))) return st;
     if ((st = grow(&km->d_vals_alt, (size_t)R * n))) return st;
-    if ((st = grow(&km->d_own, (size_t)n))) return st;
     if ((st = grow(&km->d_chosen, (size_t)R * k))) return st;
     if ((st = grow(&km->d_u, (size_t)R * k))) return st;
     if ((st = grow(&km->d_start, (size_t)R))) return st;
     if ((st = grow(&km->d_degen, (size_t)R))) return st;
     if ((st = grow(&km->d_cen, (size_t)R * k))) return st;
     if ((st = grow(&km->d_cnt, (size_t)R * k))) return st;
-    if ((st = grow(&km->d_seg, (size_t)R * k + 1))) return st;
+    if ((st = grow(&km->d_seg, (size_t)S))) return st;
     if ((st = grow(&km->d_part, (size_t)R * nbuf * 2))) return st;
     if ((st = grow(&km->d_cost, (size_t)R))) return st;
     if ((st = grow(&km->d_changed, (size_t)R))) return st;
     if ((st = grow(&km->d_active, (size_t)R))) return st;
     if ((st = grow(&km->d_empty, (size_t)R))) return st;
+    if ((st = grow(&km->d_A, (size_t)nch))) return st;
+    if ((st = grow(&km->d_vmax, (size_t)nch))) return st;
+    if ((st = grow(&km->d_cstart, (size_t)nch))) return st;
+    if ((st = grow(&km->d_kpred, (size_t)nch))) return st;
+    if ((st = grow(&km->d_q0, (size_t)nch))) return st;
+    if ((st = grow(&km->d_q1, (size_t)nch))) return st;
+    if ((st = grow(&km->d_total, (size_t)S))) return st;
+    if ((st = grow(&km->d_neg, (size_t)S))) return st;
+    if ((st = grow(&km->d_cofs, (size_t)S + 1))) return st;
+    if ((st = grow(&km->d_nchunks, 1))) return st;
+    if ((st = grow(&km->d_round_on, (size_t)R))) return st;
+    if ((st = grow(&km->d_on, (size_t)R))) return st;
+    if ((st = grow(&km->d_segkpp, (size_t)R + 1))) return st;
     size_t need = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, need, km->d_keys, km->d_keys_alt, km->d_vals,
                                     km->d_vals_alt, (int64_t)R * n, 0, 31, km->stream);
@@ -439,7 +676,21 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     km->cub_bytes = need;
     km->cap_r = R;
     km->cap_k = k;
+    km->cap_chunks = nch;
     return SC_OK;
+}
+
+static SeqWork seq_work(sc_kmeans *km) {
+    SeqWork w;
+    w.A = km->d_A;
+    w.vmax = km->d_vmax;
+    w.kpred = km->d_kpred;
+    w.q0 = km->d_q0;
+    w.q1 = km->d_q1;
+    w.cstart = km->d_cstart;
+    w.neg = km->d_neg;
+    w.total = km->d_total;
+    return w;
 }
 
 static int grid_1d(const sc_kmeans *km, int64_t work, int tpb) {
@@ -497,9 +748,12 @@ void sc_kmeans_destroy(sc_kmeans *km) {
     cudaSetDevice(km->device);
     if (km->stream) cudaStreamSynchronize(km->stream);
     void *ptrs[] = {km->d_x, km->d_best, km->d_lab[0], km->d_lab[1], km->d_keys, km->d_keys_alt,
-                    km->d_vals, km->d_vals_alt, km->d_own, km->d_cub, km->d_chosen, km->d_u,
+                    km->d_vals, km->d_vals_alt, km->d_cub, km->d_chosen, km->d_u,
                     km->d_start, km->d_degen, km->d_cen, km->d_cnt, km->d_seg, km->d_part,
-                    km->d_cost, km->d_changed, km->d_active, km->d_empty};
+                    km->d_cost, km->d_changed, km->d_active, km->d_empty, km->d_A,
+                    km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
+                    km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
+                    km->d_segkpp};
     for (void *p : ptrs) cudaFree(p);
     if (km->stream) cudaStreamDestroy(km->stream);
     delete km;
@@ -531,15 +785,47 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     SC_CUDA(cudaMemcpyAsync(km->d_start, start_round, (size_t)R * 4, cudaMemcpyHostToDevice, s));
     SC_CUDA(cudaMemsetAsync(km->d_degen, 0xff, (size_t)R * 4, s));
     int smin = k;
-    for (int r = 0; r < R; ++r) smin = std::min(smin, start_round[r]);
+    std::vector<int32_t> on(R);
+    for (int r = 0; r < R; ++r) {
+        smin = std::min(smin, start_round[r]);
+        on[r] = start_round[r] < k;
+    }
+    SC_CUDA(cudaMemcpyAsync(km->d_on, on.data(), (size_t)R * 4, cudaMemcpyHostToDevice, s));
+    // segments r over the D^2 weights best[r][0..n)
+    const int64_t cps = (n + kSeqChunk - 1) / kSeqChunk;
+    std::vector<int64_t> segoff(R + 1), cofs(R + 1);
+    for (int r = 0; r <= R; ++r) {
+        segoff[r] = (int64_t)r * n;
+        cofs[r] = (int64_t)r * cps;
+    }
+    const int64_t nch = (int64_t)R * cps;
+    SC_CUDA(cudaMemcpyAsync(km->d_segkpp, segoff.data(), (size_t)(R + 1) * 8, cudaMemcpyHostToDevice, s));
+    SC_CUDA(cudaMemcpyAsync(km->d_cofs, cofs.data(), (size_t)(R + 1) * 8, cudaMemcpyHostToDevice, s));
+    SC_CUDA(cudaMemcpyAsync(km->d_nchunks, &nch, 8, cudaMemcpyHostToDevice, s));
+    SegView v;
+    v.vals = km->d_best;
+    v.seg_off = km->d_segkpp;
+    v.cofs = km->d_cofs;
+    v.S = R;
+    v.on = km->d_round_on;
+    v.on_div = 1;
+    const SeqWork w = seq_work(km);
     const dim3 g2(grid_1d(km, n, 256) / std::max(1, std::min(R, 8)) + 1, R);
-    k_kpp_init<<<g2, 256, 0, s>>>(km->d_x, n, k, km->d_chosen, km->d_start, km->d_best);
+    const int gw = grid_1d(km, nch * 32, 256);
+    const int gs = (R * 32 + 255) / 256;
+    k_kpp_init<<<g2, 256, 0, s>>>(km->d_x, n, k, km->d_chosen, km->d_start, km->d_on, km->d_best);
     SC_CUDA(cudaGetLastError());
     for (int i = smin; i < k; ++i) {
-        k_kpp_pick<<<R, 256, 0, s>>>(n, k, i, km->d_best, km->d_u, km->d_chosen, km->d_start,
-                                      km->d_degen);
-        k_kpp_update<<<g2, 256, 0, s>>>(km->d_x, n, k, i, km->d_chosen, km->d_start,
-                                         km->d_degen, km->d_best);
+        k_kpp_update<<<g2, 256, 0, s>>>(km->d_x, n, k, i, km->d_chosen, km->d_start, km->d_on,
+                                         km->d_best);
+        k_kpp_round_on<<<(R + 127) / 128, 128, 0, s>>>(R, i, km->d_start, km->d_on,
+                                                       km->d_round_on, km->d_neg);
+        k_seq_summarize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
+        k_seq_predict<<<gs, 256, 0, s>>>(v, w);
+        k_seq_chunkmap<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
+        k_seq_compose<<<gs, 256, 0, s>>>(v, w);
+        k_kpp_search<<<gs, 256, 0, s>>>(v, w, n, k, i, km->d_u, km->d_chosen, km->d_on,
+                                         km->d_degen);
     }
     SC_CUDA(cudaGetLastError());
     SC_CUDA(cudaMemcpyAsync(chosen, km->d_chosen, (size_t)R * k * 8, cudaMemcpyDeviceToHost, s));
@@ -583,7 +869,17 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     if (k > 48 * 1024)
         SC_CUDA(cudaFuncSetAttribute(k_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, k));
     const dim3 ga(grid_1d(km, n, 256) / std::max(1, std::min(R, 8)) + 1, R);
-    const dim3 gc((unsigned)((nbuf * 2 + 127) / 128), R);
+    const dim3 gc((unsigned)((nbuf + 127) / 128), R);
+    SegView vm;
+    vm.vals = km->d_vals_alt;
+    vm.seg_off = km->d_seg;
+    vm.cofs = km->d_cofs;
+    vm.S = rk;
+    vm.on = km->d_active;
+    vm.on_div = k;
+    const SeqWork wm = seq_work(km);
+    const int gwm = grid_1d(km, ((int64_t)R * n / kSeqChunk + rk) * 32, 256);
+    const int gsm = (rk * 32 + 255) / 256;
     for (int it = 0; it < max_iters; ++it) {
         int nact = 0;
         for (int r = 0; r < R; ++r) nact += active[r];
@@ -614,8 +910,14 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                                 end_bit, s));
         k_seg_offsets<<<(rk + 1 + 255) / 256, 256, 0, s>>>(rk, (int64_t)R * n, km->d_keys_alt,
                                                            km->d_seg);
-        k_seg_means<<<(rk + 127) / 128, 128, 0, s>>>(rk, k, km->d_seg, km->d_vals_alt,
-                                                     km->d_active, km->d_cen);
+        k_chunk_offsets<<<1, 1024, 0, s>>>(rk, km->d_seg, km->d_cofs, km->d_nchunks);
+        SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)rk * 4, s));
+        k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
+        k_seq_predict<<<gsm, 256, 0, s>>>(vm, wm);
+        k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
+        k_seq_compose<<<gsm, 256, 0, s>>>(vm, wm);
+        k_seg_means<<<(rk + 127) / 128, 128, 0, s>>>(rk, k, km->d_seg, km->d_total, km->d_active,
+                                                     km->d_cen);
         k_cost_lanes<<<gc, 128, 0, s>>>(km->d_x, n, k, km->d_lab[nxt], km->d_cen, km->d_active,
                                         nbuf, km->d_part);
         k_cost_combine<<<R, 32, 0, s>>>(nbuf, km->d_part, km->d_active, km->d_cost);
@@ -662,3 +964,54 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
 }
 
 }  // extern "C"
+
+extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *seg_off,
+                             int32_t device, double *totals, double *chunk_starts) {
+    SC_REQUIRE(vals && seg_off && totals && nseg >= 1, SC_E_INVALID, "null argument");
+    for (int s = 0; s < nseg; ++s)
+        SC_REQUIRE(seg_off[s + 1] >= seg_off[s], SC_E_RANGE, "segment offsets decrease");
+    SC_CUDA(cudaSetDevice(device));
+    const int64_t n = seg_off[nseg];
+    std::vector<int64_t> cofs(nseg + 1, 0);
+    for (int s = 0; s < nseg; ++s)
+        cofs[s + 1] = cofs[s] + (seg_off[s + 1] - seg_off[s] + kSeqChunk - 1) / kSeqChunk;
+    const int64_t nch = cofs[nseg];
+    double *d_vals = nullptr, *d_A = nullptr, *d_vmax = nullptr, *d_cs = nullptr, *d_tot = nullptr;
+    int64_t *d_seg = nullptr, *d_cofs = nullptr, *d_q0 = nullptr, *d_q1 = nullptr, *d_nch = nullptr;
+    int32_t *d_kp = nullptr, *d_neg = nullptr;
+    auto al = [](void **p, size_t b) { return cudaMalloc(p, b ? b : 16); };
+    cudaError_t e = al((void **)&d_vals, n * 8);
+    if (!e) e = al((void **)&d_A, nch * 8);
+    if (!e) e = al((void **)&d_vmax, nch * 8);
+    if (!e) e = al((void **)&d_cs, nch * 8);
+    if (!e) e = al((void **)&d_tot, nseg * 8);
+    if (!e) e = al((void **)&d_seg, (nseg + 1) * 8);
+    if (!e) e = al((void **)&d_cofs, (nseg + 1) * 8);
+    if (!e) e = al((void **)&d_q0, nch * 8);
+    if (!e) e = al((void **)&d_q1, nch * 8);
+    if (!e) e = al((void **)&d_nch, 8);
+    if (!e) e = al((void **)&d_kp, nch * 4);
+    if (!e) e = al((void **)&d_neg, nseg * 4);
+    if (!e) e = cudaMemcpy(d_vals, vals, n * 8, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(d_seg, seg_off, (nseg + 1) * 8, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(d_cofs, cofs.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(d_nch, &nch, 8, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemset(d_neg, 0, nseg * 4);
+    if (!e) {
+        SegView v{d_vals, d_seg, d_cofs, nseg, nullptr, 1};
+        SeqWork w{d_A, d_vmax, d_kp, d_q0, d_q1, d_cs, d_neg, d_tot};
+        const int gw = (int)std::min<int64_t>((nch * 32 + 255) / 256 + 1, 148 * 8);
+        const int gs = (nseg * 32 + 255) / 256;
+        k_seq_summarize<<<gw, 256>>>(v, w, d_nch);
+        k_seq_predict<<<gs, 256>>>(v, w);
+        k_seq_chunkmap<<<gw, 256>>>(v, w, d_nch);
+        k_seq_compose<<<gs, 256>>>(v, w);
+        e = cudaDeviceSynchronize();
+    }
+    if (!e) e = cudaMemcpy(totals, d_tot, nseg * 8, cudaMemcpyDeviceToHost);
+    if (!e && chunk_starts) e = cudaMemcpy(chunk_starts, d_cs, nch * 8, cudaMemcpyDeviceToHost);
+    void *ps[] = {d_vals, d_A, d_vmax, d_cs, d_tot, d_seg, d_cofs, d_q0, d_q1, d_nch, d_kp, d_neg};
+    for (void *p : ps) cudaFree(p);
+    SC_CUDA(e);
+    return SC_OK;
+}

@@ -187,6 +187,8 @@ def _nth_unchosen(taken_sorted: np.ndarray, m: int) -> int:
 
 
 def _as_1d(points) -> np.ndarray:
+    if isinstance(points, np.ndarray) and points.ndim == 1:
+        points = points[:, None]
     c = points.coords if isinstance(points, PointSet) else PointSet(np.asarray(points)).coords
     if c.shape[1] != 1:
         raise InputError(f"the B200 k-means path clusters 1-D embeddings; got d={c.shape[1]}")

@@ -202,3 +202,23 @@ def test_c2_properties(c2_graph):
     assert np.all(xT >= 0)
     assert abs(xT.sum() - x0.sum()) <= 1e-9 * x0.sum()
     assert np.array_equal(f, xT / c2_graph.degrees)
+
+
+@pytest.mark.parametrize("case", ["dyadic", "integers", "wide_range", "tiny_subnormal", "big_n"])
+def test_lloyd_exact_sums_stress(case):
+    """Inputs that stress the exact sequential-sum machinery (ties to even, many binade
+    crossings, subnormals, long segments) against the C oracle replica."""
+    rng = np.random.default_rng(5)
+    if case == "dyadic":
+        x, k = rng.integers(0, 4096, 30000) * 0.125, 7
+    elif case == "integers":
+        x, k = rng.integers(0, 50, 20000).astype(np.float64), 5
+    elif case == "wide_range":
+        x, k = np.exp(rng.normal(0, 12, 20000)), 9
+    elif case == "tiny_subnormal":
+        x, k = rng.random(5000) * 1e-300, 4
+    else:
+        x, k = rng.random(300000) * 1e-3 + 0.5, 20
+    lab_o, cost_o = O.lloyd(x, k, 77)
+    part = lloyd(x[:, None], k, seed=77)
+    assert np.array_equal(part.labels, lab_o), case
