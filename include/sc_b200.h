@@ -62,13 +62,14 @@ typedef struct sc_graph_info {
     int64_t nnz;          /* local stored entries */
     int64_t ncols;        /* length of the gathered z space */
     int64_t col_offset;   /* where local row i's z lives in z space */
-    int64_t ntiles;       /* nnz-balanced row tiles */
-    int64_t long_rows;    /* rows handled by single-row tiles */
+    int64_t ntiles;       /* SELL-32 slices (32 renumbered rows each) */
+    int64_t long_rows;    /* wide rows (> 256 entries), one warp each */
     int32_t unit_weights; /* 1 if the val array was elided */
     int32_t rp64;         /* 1 if row offsets are kept as int64 on device */
     int64_t device_bytes; /* device memory owned by the handle */
     int32_t device;
     int32_t sm_count;
+    int64_t stored_entries; /* SELL-32 entries incl. padding (+ wide-row entries excluded) */
 } sc_graph_info;
 
 typedef struct sc_timing {
@@ -90,13 +91,21 @@ int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double
                         const double *deg, int64_t n, int64_t nnz, int32_t device,
                         sc_graph **out);
 /* Row-block shard: rows are the local block, columns index a z space of length ncols in
- * which this shard's own rows live at [col_offset, col_offset + n). */
+ * which this shard's own rows live at [col_offset, col_offset + n).  Columns must already
+ * be renamed into the renumbered z space (every shard's sc_sell_order permutation). */
 int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double *val,
                         const double *deg, int64_t n, int64_t nnz, int64_t ncols,
                         int64_t col_offset, int64_t global_row0, int32_t device,
                         sc_graph **out);
 void sc_graph_destroy(sc_graph *g);
 int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *out);
+/* The device layout renumbers rows (SELL-32-sigma: length-sorted inside 4096-row windows,
+ * rows longer than 256 last).  sc_sell_order returns that permutation for a row_ptr
+ * (perm[p] = original row of renumbered row p) so a multi-GPU driver can rename columns
+ * across shards; sc_graph_order returns a handle's permutation.  Host-facing vectors
+ * (x0, x_T, f) are always in ORIGINAL order; shard device buffers are renumbered. */
+int32_t sc_sell_order(const int64_t *row_ptr, int64_t n, int32_t *perm_out);
+int32_t sc_graph_order(const sc_graph *g, int32_t *perm_out);
 
 /* ---- start vector ------------------------------------------------------- */
 /* x0(u) = sum of floor(deg u) uniforms (+ frac(deg u) * one more), uniform j of global

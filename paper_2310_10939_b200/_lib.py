@@ -30,6 +30,7 @@ class GraphInfo(ctypes.Structure):
         ("col_offset", ctypes.c_int64), ("ntiles", ctypes.c_int64), ("long_rows", ctypes.c_int64),
         ("unit_weights", ctypes.c_int32), ("rp64", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
         ("device", ctypes.c_int32), ("sm_count", ctypes.c_int32),
+        ("stored_entries", ctypes.c_int64),
     ]
 
 
@@ -43,7 +44,7 @@ EXPORTS = (
     "sc_graph_destroy", "sc_graph_info_get", "sc_sample_irwin_hall", "sc_set_x0",
     "sc_power_iterate", "sc_shard_step", "sc_shard_scale", "sc_shard_irwin_hall",
     "sc_kmeans_create", "sc_kmeans_create_from_graph", "sc_kmeans_destroy", "sc_kmeans_pp",
-    "sc_kmeans_lloyd", "sc_seqsum",
+    "sc_kmeans_lloyd", "sc_seqsum", "sc_sell_order", "sc_graph_order",
 )
 
 _lib = None
@@ -82,6 +83,8 @@ def load() -> ctypes.CDLL:
         "sc_kmeans_pp": ([P, i32, i32, P, P, P, P], i32),
         "sc_kmeans_lloyd": ([P, i32, i32, P, i32, f64, P, P, P, P, P], i32),
         "sc_seqsum": ([P, i32, P, i32, P, P], i32),
+        "sc_sell_order": ([P, i64, P], i32),
+        "sc_graph_order": ([P, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

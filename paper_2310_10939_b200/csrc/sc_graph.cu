@@ -1,5 +1,5 @@
 // sc_graph.cu -- graph handle, Irwin-Hall start vector (K1) and the fused lazy-random-walk
-// CSR SpMV (K2 + K3) for sm_100a.
+// SpMV (K2 + K3) for sm_100a.
 //
 // Reference semantics (paths under /root/reference/pkg/src/specluster):
 //   power_method           spectral.py:87-102   x <- M x, t times, no normalisation
@@ -8,20 +8,30 @@
 //   scipy csr_matvec       (sparsetools)        per row: sum = 0; sum += A_ij * v_j in
 //                                               stored column order, no FMA
 //
-// Kernel design: the CSR is cut on the host into row tiles holding at most
-// kChunk stored entries (rows longer than kChunk get a tile of their own).  One CTA per
-// tile streams the tile's col/val with 128-bit evict-first loads, gathers z = D^-1 x
-// through L1/L2, forms the products into shared memory, and then one thread per row adds
-// its products left to right -- the scipy order, so the result is bit-identical to the
-// reference.  The epilogue fuses the lazy blend 0.5 x + sign 0.5 s and the degree scaling
-// of the next iterate: it writes x_{t+1} and z_{t+1} = x_{t+1} / d (the gathered vector
-// of the next step, and after the last step the embedding f = D^-1 x_T itself).
+// Layout: the CSR is re-laid out once, on the device, as SELL-32-sigma.
+//   * rows are renumbered: inside every window of kSigma consecutive rows, rows are
+//     stably sorted by decreasing length; rows longer than kSellMax ("wide" rows) go to
+//     the end.  Column indices are renamed with the same permutation.  Renaming changes
+//     WHERE z values live, never the ORDER of the products inside a row, so every row sum
+//     stays bit-identical to scipy's.
+//   * 32 consecutive renumbered rows form a slice stored column-major (entry t of the
+//     slice's row `lane` at slice_base + 32 t + lane), padded to the slice's longest row.
+//     One warp owns a slice, one lane owns a row: entry loads are perfectly coalesced
+//     128-byte lines, each lane adds its own products strictly left to right, and there
+//     is no shared memory and no barrier on the hot path -- the kernel runs at the
+//     random-gather limit of the L1/L2 request path.
+//   * wide rows: one warp per row; 32 entries per step are gathered in parallel and the
+//     warp folds them in order with shuffles (every lane holds the same running sum).
+// The epilogue fuses the lazy blend 0.5 x + sign*0.5 s and the degree scaling of the next
+// iterate: it writes x_{t+1} and z_{t+1} = x_{t+1} / d, the vector the next step gathers,
+// and after the last step the embedding f = D^-1 x_T itself.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
-#include <mutex>
+#include <cub/device/device_scan.cuh>
 #include <vector>
 
 #include "sc_common.cuh"
@@ -49,47 +59,30 @@ int32_t fail(int32_t code, const char *fmt, ...) {
     return code;
 }
 
-constexpr int kTPB = 256;         // threads per tile CTA (8 warps)
-constexpr int kChunk = 2048;      // stored entries per multi-row tile / per long-row chunk
-constexpr int kRowsMax = 128;     // rows per multi-row tile (upper bound; see rows_cap)
-constexpr int kPerThread = kChunk / kTPB;            // 8 entries per thread in phase A
-constexpr int kPadded = kChunk + 16 * kRowsMax + 16; // padded product slots (32.1 KB)
+constexpr int kSlice = 32;         // rows per slice (one per lane)
+constexpr int kSigma = 4096;       // sorting window (rows)
+constexpr int kSellMax = 256;      // longer rows are "wide" rows
+constexpr uint32_t kPad = 0xffffffffu;  // padding entry of a slice
+constexpr int kStepTPB = 256;      // 8 warps per CTA
+constexpr int kUnroll = 8;         // slice steps in flight per lane
 
 struct StepArgs {
-    const void *rp;        // int32 or int64 row offsets (local, rebased to 0)
-    const uint32_t *col;   // packed: (tile-local row << col_bits) | column; padded (+8)
-    const double *val;     // padded, or null for unit weights
-    const double *scale;   // deg (rw) or deg^-1/2 (sym)
+    const int64_t *slice_ptr;  // nslices + 1 (entries, multiples of 32)
+    const uint32_t *col;       // SELL column-major entries (renamed columns / kPad)
+    const double *val;         // SELL weights or null (unit)
+    const int64_t *wide_ptr;   // nwide + 1 into wcol / wval
+    const uint32_t *wcol;
+    const double *wval;
+    const double *scale;       // deg (rw) or deg^-1/2 (sym), renumbered order
     const double *x_in;
-    const double *z_in;    // gathered vector, indexed by column
+    const double *z_in;        // gathered vector, indexed by renamed column
     double *x_out;
-    double *z_out;         // written at col_offset + row
-    const int64_t *tile_b; // ntiles + 1 first stored entry of each tile
-    const int32_t *tile_r; // ntiles + 1 first row of each tile
+    double *z_out;             // written at col_offset + row
+    int64_t n_sell, n_wide, nslices;
     int64_t col_offset;
-    double hs;             // +0.5 or -0.5
-    uint32_t col_mask;
-    int col_bits;
+    int wide_blocks;           // leading CTAs that process wide rows
+    double hs;                 // +0.5 or -0.5
 };
-
-// Shared-memory slot of row i's first product (pre = unpadded tile offset of the row).
-// start == i (mod 16): the 16 lanes of a half-warp that read the t-th product of 16
-// consecutive rows hit 16 distinct 8-byte bank pairs, so the sequential row sums of
-// phase B are bank-conflict free; consecutive segments never overlap.
-__device__ __forceinline__ int padded_start(int i, int pre) {
-    return pre + 16 * i + ((i - pre) & 15);
-}
-
-// Long-row path: products of [cb, ce) into prod[0..), lane-linear coalesced loads.
-template <bool UNIT>
-__device__ __forceinline__ void gather_linear(const StepArgs &a, int64_t cb, int64_t ce,
-                                              double *prod) {
-    for (int64_t j = cb + threadIdx.x; j < ce; j += kTPB) {
-        const uint32_t c = __ldcs(a.col + j) & a.col_mask;
-        const double zv = __ldg(a.z_in + c);
-        prod[j - cb] = UNIT ? zv : __dmul_rn(__ldcs(a.val + j), zv);
-    }
-}
 
 template <bool SYM>
 __device__ __forceinline__ void row_epilogue(const StepArgs &a, int64_t r, double s, double xr,
@@ -100,108 +93,82 @@ __device__ __forceinline__ void row_epilogue(const StepArgs &a, int64_t r, doubl
     a.z_out[a.col_offset + r] = SYM ? __dmul_rn(sc, y) : __ddiv_rn(y, sc);
 }
 
-template <typename RP, bool UNIT, bool SYM>
-__global__ void __launch_bounds__(kTPB) k_rw_step(StepArgs a) {
-    __shared__ double prod[kPadded];
-    __shared__ int pbase[kRowsMax + 1];  // padded_start(i, pre_i) - pre_i, then pre_i
-    __shared__ int srp[kRowsMax + 1];    // tile-local row offsets
-    const int tid = threadIdx.x;
-    const int64_t b = a.tile_b[blockIdx.x], e = a.tile_b[blockIdx.x + 1];
-    const int r0 = a.tile_r[blockIdx.x];
-    const int nrows = a.tile_r[blockIdx.x + 1] - r0;
-    if (e - b > kChunk) {
-        // single long row: products chunk by chunk, one thread keeps the running sum
-        double xr = 0.0, sc = 1.0;
-        if (tid == 0) {
-            xr = __ldcs(a.x_in + r0);
-            sc = __ldcs(a.scale + r0);
-        }
+template <bool UNIT, bool SYM>
+__global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    if ((int)blockIdx.x < a.wide_blocks) {
+        // ---- wide rows: one warp per row, in-order fold through shuffles
+        const int64_t w = (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
+        if (w >= a.n_wide) return;
+        const int64_t r = a.n_sell + w;
+        const double xr = __ldcs(a.x_in + r), sc = __ldcs(a.scale + r);
+        const int64_t lo = a.wide_ptr[w], hi = a.wide_ptr[w + 1];
         double s = 0.0;
-        for (int64_t cb = b; cb < e; cb += kChunk) {
-            const int64_t ce = (e - cb > kChunk) ? cb + kChunk : e;
-            gather_linear<UNIT>(a, cb, ce, prod);
-            __syncthreads();
-            if (tid == 0) {
-                const int m = int(ce - cb);
-                for (int j = 0; j < m; ++j) s = __dadd_rn(s, prod[j]);
+        for (int64_t base = lo; base < hi; base += 32 * 4) {
+            double p[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t j = base + 32 * q + lane;
+                p[q] = 0.0;
+                if (j < hi) {
+                    const double zv = __ldg(a.z_in + __ldcs(a.wcol + j));
+                    p[q] = UNIT ? zv : __dmul_rn(__ldcs(a.wval + j), zv);
+                }
             }
-            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t jb = base + 32 * q;
+                const int m = (int)(hi - jb < 32 ? hi - jb : 32);
+                for (int t = 0; t < m; ++t) s = __dadd_rn(s, __shfl_sync(0xffffffffu, p[q], t));
+            }
         }
-        if (tid == 0) row_epilogue<SYM>(a, r0, s, xr, sc);
+        if (lane == 0) row_epilogue<SYM>(a, r, s, xr, sc);
         return;
     }
-    const int nz = int(e - b);
-    // phase A: warp w owns tile entries [256w, 256w + 256) as 8 lane-linear windows;
-    // all col (+val) loads in flight first, then all gathers.  The tile-local row of each
-    // entry travels in the high bits of the packed column word (no search).
-    const int warp = tid >> 5, lane = tid & 31;
-    const int wbase = warp * (32 * kPerThread);
-    uint32_t cw[kPerThread];
-    double v[kPerThread];
-#pragma unroll
-    for (int k = 0; k < kPerThread; ++k) {
-        const int jl = wbase + 32 * k + lane;
-        cw[k] = jl < nz ? __ldcs(a.col + b + jl) : 0u;
-        v[k] = (!UNIT && jl < nz) ? __ldcs(a.val + b + jl) : 1.0;
-    }
-    // epilogue operands of this thread's row and the tile's row offsets (independent loads)
+    // ---- SELL slices: one warp per slice, one lane per row
+    const int64_t sl = (int64_t)(blockIdx.x - a.wide_blocks) * (kStepTPB / 32) + warp;
+    if (sl >= a.nslices) return;
+    const int64_t r = sl * kSlice + lane;
+    const bool live = r < a.n_sell;
     double xr = 0.0, sc = 1.0;
-    const RP *rp = static_cast<const RP *>(a.rp);
-    if (tid < nrows) {
-        xr = __ldcs(a.x_in + r0 + tid);
-        sc = __ldcs(a.scale + r0 + tid);
+    if (live) {
+        xr = __ldcs(a.x_in + r);
+        sc = __ldcs(a.scale + r);
     }
-    if (tid <= nrows) {
-        const int pre = int(rp[r0 + tid] - b);
-        srp[tid] = pre;
-        pbase[tid] = padded_start(tid, pre) - pre;
-    }
+    const int64_t base = a.slice_ptr[sl];
+    const int width = (int)((a.slice_ptr[sl + 1] - base) >> 5);
+    const uint32_t *cp = a.col + base + lane;
+    const double *vp = UNIT ? nullptr : a.val + base + lane;
+    double s = 0.0;
+    int t = 0;
+    for (; t + kUnroll <= width; t += kUnroll) {
+        uint32_t c[kUnroll];
+        double v[kUnroll];
 #pragma unroll
-    for (int k = 0; k < kPerThread; ++k) {
-        const int jl = wbase + 32 * k + lane;
-        if (jl < nz) {
-            const double zv = __ldg(a.z_in + (cw[k] & a.col_mask));
-            v[k] = UNIT ? zv : __dmul_rn(v[k], zv);
+        for (int q = 0; q < kUnroll; ++q) {
+            c[q] = __ldcs(cp + (int64_t)(t + q) * kSlice);
+            if (!UNIT) v[q] = __ldcs(vp + (int64_t)(t + q) * kSlice);
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+            if (c[q] != kPad) {
+                const double zv = __ldg(a.z_in + c[q]);
+                v[q] = UNIT ? zv : __dmul_rn(v[q], zv);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q)
+            if (c[q] != kPad) s = __dadd_rn(s, v[q]);
+    }
+    for (; t < width; ++t) {
+        const uint32_t c = __ldcs(cp + (int64_t)t * kSlice);
+        if (c != kPad) {
+            const double zv = __ldg(a.z_in + c);
+            s = __dadd_rn(s, UNIT ? zv : __dmul_rn(__ldcs(vp + (int64_t)t * kSlice), zv));
         }
     }
-    __syncthreads();  // pbase ready
-#pragma unroll
-    for (int k = 0; k < kPerThread; ++k) {
-        const int jl = wbase + 32 * k + lane;
-        if (jl < nz) prod[pbase[cw[k] >> a.col_bits] + jl] = v[k];
-    }
-    __syncthreads();
-    // phase B: one thread per row adds its products left to right (scipy csr_matvec order)
-    if (tid < nrows) {
-        const int pre = srp[tid], len = srp[tid + 1] - pre;
-        const double *p = prod + pbase[tid] + pre;
-        double s = 0.0;
-        int t = 0;
-        for (; t + 4 <= len; t += 4) {
-            const double p0 = p[t], p1 = p[t + 1], p2 = p[t + 2], p3 = p[t + 3];
-            s = __dadd_rn(s, p0);
-            s = __dadd_rn(s, p1);
-            s = __dadd_rn(s, p2);
-            s = __dadd_rn(s, p3);
-        }
-        for (; t < len; ++t) s = __dadd_rn(s, p[t]);
-        row_epilogue<SYM>(a, r0 + tid, s, xr, sc);
-    }
-}
-
-// Stamp each stored entry of a multi-row tile with its tile-local row (high bits).
-template <typename RP>
-__global__ void k_pack_rows(const RP *__restrict__ rp, const int64_t *__restrict__ tile_b,
-                            const int32_t *__restrict__ tile_r, uint32_t *__restrict__ col,
-                            int col_bits) {
-    const int64_t b = tile_b[blockIdx.x], e = tile_b[blockIdx.x + 1];
-    if (e - b > kChunk) return;  // long-row tile: local row 0
-    const int r0 = tile_r[blockIdx.x], nrows = tile_r[blockIdx.x + 1] - r0;
-    for (int i = threadIdx.x >> 5; i < nrows; i += blockDim.x >> 5) {
-        const int64_t lo = rp[r0 + i], hi = rp[r0 + i + 1];
-        for (int64_t j = lo + (threadIdx.x & 31); j < hi; j += 32)
-            col[j] |= (uint32_t)i << col_bits;
-    }
+    if (live) row_epilogue<SYM>(a, r, s, xr, sc);
 }
 
 // z[col_offset + i] = x[i] / d[i]   (rw)   or   x[i] * d[i]^-1/2   (sym)
@@ -219,11 +186,12 @@ __global__ void k_inv_sqrt(const double *__restrict__ d, double *__restrict__ s,
         s[i] = __ddiv_rn(1.0, __dsqrt_rn(d[i]));
 }
 
-// K1: Irwin-Hall start vector.  Uniform j of global vertex u is word j%4 of
-// Philox4x64-10(key, (j/4 + 1, u, 0, 0)); floor(deg) uniforms are summed left to right,
-// a fractional degree adds frac * one more uniform (mean deg/2 for every degree).
-__global__ void k_irwin_hall(const double *__restrict__ deg, double *__restrict__ x0, int64_t n,
-                             int64_t global_row0, uint64_t k0, uint64_t k1) {
+// K1: Irwin-Hall start vector, written in renumbered order.  Uniform j of global vertex u
+// is word j%4 of Philox4x64-10(key, (j/4 + 1, u, 0, 0)); floor(deg) uniforms are summed
+// left to right, a fractional degree adds frac * one more uniform (mean deg/2 always).
+__global__ void k_irwin_hall(const double *__restrict__ deg, const int32_t *__restrict__ perm,
+                             double *__restrict__ x0, int64_t n, int64_t global_row0, uint64_t k0,
+                             uint64_t k1) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double d = deg[i];
@@ -231,7 +199,7 @@ __global__ void k_irwin_hall(const double *__restrict__ deg, double *__restrict_
         const int64_t m = (int64_t)fl;
         const double frac = __dsub_rn(d, fl);
         const int64_t need = m + (frac > 0.0 ? 1 : 0);
-        const uint64_t u = (uint64_t)(global_row0 + i);
+        const uint64_t u = (uint64_t)(global_row0 + perm[i]);
         double s = 0.0;
         for (int64_t blk = 0; 4 * blk < need; ++blk) {
             const u64x4 r = philox4x64_10(u64x4{(uint64_t)blk + 1u, u, 0, 0}, k0, k1);
@@ -247,6 +215,85 @@ __global__ void k_irwin_hall(const double *__restrict__ deg, double *__restrict_
     }
 }
 
+// out[i] = in[idx[i]]: original -> renumbered order with idx = perm, back with idx = iperm
+__global__ void k_gather_perm(const double *__restrict__ in, const int32_t *__restrict__ idx,
+                              double *__restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[idx[i]];
+}
+
+// ---- construction kernels (once per graph) ----------------------------------------------
+
+__global__ void k_inverse_perm(const int32_t *__restrict__ perm, int32_t *__restrict__ iperm,
+                               int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        iperm[perm[i]] = (int32_t)i;
+}
+
+__global__ void k_slice_sizes(const int64_t *__restrict__ rp, const int32_t *__restrict__ perm,
+                              int64_t n_sell, int64_t nslices, int64_t *__restrict__ sizes) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        int64_t w = 0;
+        for (int l = 0; l < kSlice; ++l) {
+            const int64_t p = s * kSlice + l;
+            if (p < n_sell) {
+                const int32_t r = perm[p];
+                w = max(w, rp[r + 1] - rp[r]);
+            }
+        }
+        sizes[s] = w * kSlice;
+    }
+}
+
+// one thread per renumbered SELL row: copy its entries column-major into its slice
+__global__ void k_fill_sell(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                            const double *__restrict__ val, const int32_t *__restrict__ perm,
+                            const int32_t *__restrict__ iperm, const int64_t *__restrict__ slice_ptr,
+                            int64_t n_sell, int64_t col_offset, int64_t n, int rename,
+                            uint32_t *__restrict__ scol, double *__restrict__ sval) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_sell;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = perm[p];
+        const int64_t s = p / kSlice, lane = p % kSlice;
+        const int64_t base = slice_ptr[s];
+        const int64_t width = (slice_ptr[s + 1] - base) / kSlice;
+        const int64_t lo = rp[r], len = rp[r + 1] - lo;
+        for (int64_t t = 0; t < width; ++t) {
+            const int64_t dst = base + t * kSlice + lane;
+            if (t < len) {
+                int64_t c = col[lo + t];
+                if (rename && c >= col_offset && c < col_offset + n)
+                    c = col_offset + iperm[c - col_offset];
+                scol[dst] = (uint32_t)c;
+                if (sval) sval[dst] = val[lo + t];
+            } else {
+                scol[dst] = kPad;
+                if (sval) sval[dst] = 0.0;
+            }
+        }
+    }
+}
+
+__global__ void k_fill_wide(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                            const double *__restrict__ val, const int32_t *__restrict__ perm,
+                            const int32_t *__restrict__ iperm, const int64_t *__restrict__ wide_ptr,
+                            int64_t n_sell, int64_t n_wide, int64_t col_offset, int64_t n,
+                            int rename, uint32_t *__restrict__ wcol, double *__restrict__ wval) {
+    const int64_t w = blockIdx.x;
+    if (w >= n_wide) return;
+    const int32_t r = perm[n_sell + w];
+    const int64_t lo = rp[r], len = rp[r + 1] - lo, dst = wide_ptr[w];
+    for (int64_t t = threadIdx.x; t < len; t += blockDim.x) {
+        int64_t c = col[lo + t];
+        if (rename && c >= col_offset && c < col_offset + n) c = col_offset + iperm[c - col_offset];
+        wcol[dst + t] = (uint32_t)c;
+        if (wval) wval[dst + t] = val[lo + t];
+    }
+}
+
 }  // namespace sc
 
 using namespace sc;
@@ -255,29 +302,33 @@ struct sc_graph {
     int device = 0;
     int sm_count = 0;
     int64_t n = 0, nnz = 0, ncols = 0, col_offset = 0, global_row0 = 0;
-    bool unit = false, rp64 = false;
-    void *d_rp = nullptr;
-    uint32_t *d_col = nullptr;  // packed (local row << col_bits) | column
+    int64_t n_sell = 0, n_wide = 0, nslices = 0, sell_entries = 0;
+    bool unit = false;
+    int32_t *d_perm = nullptr;    // renumbered row -> original local row
+    int32_t *d_iperm = nullptr;   // original local row -> renumbered row
+    int64_t *d_slice_ptr = nullptr;
+    uint32_t *d_col = nullptr;    // SELL entries
     double *d_val = nullptr;
-    double *d_deg = nullptr;
+    int64_t *d_wide_ptr = nullptr;
+    uint32_t *d_wcol = nullptr;
+    double *d_wval = nullptr;
+    double *d_deg = nullptr;      // renumbered
     double *d_isd = nullptr;
     double *d_x0 = nullptr;
     double *d_x[2] = {nullptr, nullptr};
     double *d_z[2] = {nullptr, nullptr};
-    int64_t *d_tile_b = nullptr;
-    int32_t *d_tile_r = nullptr;
-    int64_t ntiles = 0, long_rows = 0;
-    int col_bits = 1, rows_cap = 1;
+    double *d_tmp = nullptr;      // n doubles: host <-> device reorder staging
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool have_x0 = false;
-    int result = -1;  // buffer index holding x_T / f after the last power_iterate (2 = x0)
+    int result = -1;  // buffer index holding z_T (= f) after the last power_iterate
     cudaGraphExec_t gexec = nullptr;
     int32_t g_T = -1;
     uint32_t g_flags = 0;
     double g_sign = 0.0;
     int64_t bytes = 0;
     bool l2_window = false;
+    double *d_f_orig = nullptr;   // f in original vertex order (for the k-means context)
 };
 
 namespace sc {
@@ -291,47 +342,46 @@ static int32_t dmalloc(sc_graph *g, void **p, size_t bytes) {
     return SC_OK;
 }
 
-// Host tiling: greedy row packing, <= kChunk entries and <= rows_cap rows per tile;
-// a row with more than kChunk entries is a tile of its own.
-static void build_tiles(const int64_t *rp, int64_t n, int rows_cap, std::vector<int32_t> &tr,
-                        std::vector<int64_t> &tb, int64_t &long_rows) {
-    tr.clear();
-    tb.clear();
-    const size_t guess = (size_t)(rp[n] / kChunk + n / rows_cap + 16);
-    tr.reserve(guess);
-    tb.reserve(guess);
-    auto cut = [&](int64_t r) {
-        tr.push_back((int32_t)r);
-        tb.push_back(rp[r]);
-    };
-    cut(0);
-    int64_t cur_nnz = 0;
-    int cur_rows = 0;
-    long_rows = 0;
-    for (int64_t r = 0; r < n; ++r) {
-        const int64_t len = rp[r + 1] - rp[r];
-        if (len > kChunk) {
-            if (cur_rows) cut(r);
-            cut(r + 1);
-            ++long_rows;
-            cur_nnz = 0;
-            cur_rows = 0;
-            continue;
+// Renumbering (host, O(n)): inside each window of kSigma rows, rows of length <= kSellMax
+// in decreasing length (counting sort, stable), then all wide rows in original order.
+static int64_t sell_order(const int64_t *rp, int64_t n, std::vector<int32_t> &perm) {
+    perm.resize((size_t)n);
+    int64_t pos = 0;
+    std::vector<int32_t> cnt(kSellMax + 2);
+    for (int64_t w0 = 0; w0 < n; w0 += kSigma) {
+        const int64_t w1 = std::min(n, w0 + kSigma);
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int64_t r = w0; r < w1; ++r) {
+            const int64_t len = rp[r + 1] - rp[r];
+            if (len <= kSellMax) cnt[kSellMax - len]++;
         }
-        if (cur_rows && (cur_nnz + len > kChunk || cur_rows == rows_cap)) {
-            cut(r);
-            cur_nnz = 0;
-            cur_rows = 0;
+        int32_t acc = 0;
+        for (int b = 0; b <= kSellMax; ++b) {
+            const int32_t c = cnt[b];
+            cnt[b] = acc;
+            acc += c;
         }
-        cur_nnz += len;
-        ++cur_rows;
+        for (int64_t r = w0; r < w1; ++r) {
+            const int64_t len = rp[r + 1] - rp[r];
+            if (len <= kSellMax) perm[(size_t)(pos + cnt[kSellMax - len]++)] = (int32_t)r;
+        }
+        pos += acc;
     }
-    if (cur_rows) cut(n);
+    const int64_t n_sell = pos;
+    for (int64_t r = 0; r < n; ++r)
+        if (rp[r + 1] - rp[r] > kSellMax) perm[(size_t)pos++] = (int32_t)r;
+    return n_sell;
+}
+
+static int grid_for(const sc_graph *g, int64_t n, int tpb) {
+    int64_t want = (n + tpb - 1) / tpb;
+    int64_t cap = (int64_t)std::max(g->sm_count, 1) * 8;
+    return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
 static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const double *val,
                           const double *deg, int64_t n, int64_t nnz, int64_t ncols,
-                          int64_t col_offset, int64_t global_row0, int32_t device,
+                          int64_t col_offset, int64_t global_row0, int rename, int32_t device,
                           sc_graph **out) {
     SC_REQUIRE(out, SC_E_INVALID, "out is null");
     *out = nullptr;
@@ -340,8 +390,9 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
                (long long)n);
     SC_REQUIRE(nnz >= 0 && row_ptr[0] == 0 && row_ptr[n] == nnz, SC_E_RANGE,
                "row_ptr[0] must be 0 and row_ptr[n] must equal nnz=%lld", (long long)nnz);
-    SC_REQUIRE(ncols >= n && col_offset >= 0 && col_offset + n <= ncols, SC_E_RANGE,
-               "bad z-space geometry ncols=%lld col_offset=%lld", (long long)ncols,
+    SC_REQUIRE(ncols >= n && ncols < (int64_t(1) << 32) - 1 && col_offset >= 0 &&
+                   col_offset + n <= ncols,
+               SC_E_RANGE, "bad z-space geometry ncols=%lld col_offset=%lld", (long long)ncols,
                (long long)col_offset);
     for (int64_t i = 0; i < n; ++i)
         SC_REQUIRE(row_ptr[i + 1] >= row_ptr[i], SC_E_RANGE, "row_ptr decreases at %lld",
@@ -372,90 +423,132 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         for (int64_t j = 0; j < nnz && unit; ++j) unit = (val[j] == 1.0);
     }
     g->unit = unit;
-    g->rp64 = nnz >= (int64_t(1) << 31) - kChunk;
 
-    g->col_bits = 1;
-    while (g->col_bits < 31 && (int64_t(1) << g->col_bits) < ncols) ++g->col_bits;
-    g->rows_cap = (int)std::min<int64_t>(kRowsMax, int64_t(1) << (32 - g->col_bits));
-    std::vector<int32_t> tile_r;
-    std::vector<int64_t> tile_b;
-    build_tiles(row_ptr, n, g->rows_cap, tile_r, tile_b, g->long_rows);
-    g->ntiles = (int64_t)tile_r.size() - 1;
+    std::vector<int32_t> perm;
+    g->n_sell = sell_order(row_ptr, n, perm);
+    g->n_wide = n - g->n_sell;
+    g->nslices = (g->n_sell + kSlice - 1) / kSlice;
 
     int32_t st;
     auto cleanup = [&](int32_t code) {
         sc_graph_destroy(g);
         return code;
     };
-    const size_t rpb = (size_t)(n + 1) * (g->rp64 ? 8 : 4);
-    if ((st = dmalloc(g, &g->d_rp, rpb))) return cleanup(st);
-    if ((st = dmalloc(g, (void **)&g->d_col, (size_t)(nnz + 8) * 4))) return cleanup(st);
-    if (val && !unit)
-        if ((st = dmalloc(g, (void **)&g->d_val, (size_t)(nnz + 8) * 8))) return cleanup(st);
-    if ((st = dmalloc(g, (void **)&g->d_deg, (size_t)n * 8))) return cleanup(st);
-    if ((st = dmalloc(g, (void **)&g->d_x0, (size_t)n * 8))) return cleanup(st);
-    for (int b = 0; b < 2; ++b) {
-        if ((st = dmalloc(g, (void **)&g->d_x[b], (size_t)n * 8))) return cleanup(st);
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) {
+        fail(SC_E_CUDA, "stream/event creation failed");
+        return cleanup(SC_E_CUDA);
+    }
+    cudaStream_t s = g->stream;
+    // staging: the original CSR on the device, freed once the SELL layout is built
+    int64_t *t_rp = nullptr, *t_sizes = nullptr;
+    int32_t *t_col = nullptr;
+    double *t_val = nullptr, *t_deg = nullptr;
+    void *t_cub = nullptr;
+    auto free_tmp = [&]() {
+        cudaFree(t_rp);
+        cudaFree(t_col);
+        cudaFree(t_val);
+        cudaFree(t_deg);
+        cudaFree(t_sizes);
+        cudaFree(t_cub);
+    };
+    cudaError_t e = cudaMalloc(&t_rp, (size_t)(n + 1) * 8);
+    if (!e) e = cudaMalloc(&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4);
+    if (!e && !unit) e = cudaMalloc(&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8);
+    if (!e) e = cudaMalloc(&t_deg, (size_t)n * 8);
+    if (!e) e = cudaMalloc(&t_sizes, (size_t)(g->nslices + 1) * 8);
+    if (e) {
+        free_tmp();
+        fail(e == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA, "staging allocation: %s",
+             cudaGetErrorString(e));
+        return cleanup(SC_E_OOM);
+    }
+    if ((st = dmalloc(g, (void **)&g->d_perm, (size_t)n * 4)) ||
+        (st = dmalloc(g, (void **)&g->d_iperm, (size_t)n * 4)) ||
+        (st = dmalloc(g, (void **)&g->d_slice_ptr, (size_t)(g->nslices + 1) * 8)) ||
+        (st = dmalloc(g, (void **)&g->d_wide_ptr, (size_t)(g->n_wide + 1) * 8)) ||
+        (st = dmalloc(g, (void **)&g->d_deg, (size_t)n * 8)) ||
+        (st = dmalloc(g, (void **)&g->d_x0, (size_t)n * 8)) ||
+        (st = dmalloc(g, (void **)&g->d_x[0], (size_t)n * 8)) ||
+        (st = dmalloc(g, (void **)&g->d_x[1], (size_t)n * 8)) ||
+        (st = dmalloc(g, (void **)&g->d_tmp, (size_t)n * 8))) {
+        free_tmp();
+        return cleanup(st);
     }
     // both z buffers in one allocation so one L2 access-policy window covers them
     double *zz = nullptr;
-    if ((st = dmalloc(g, (void **)&zz, (size_t)ncols * 16))) return cleanup(st);
+    if ((st = dmalloc(g, (void **)&zz, (size_t)ncols * 16))) {
+        free_tmp();
+        return cleanup(st);
+    }
     g->d_z[0] = zz;
     g->d_z[1] = zz + ncols;
-    if ((st = dmalloc(g, (void **)&g->d_tile_r, tile_r.size() * 4))) return cleanup(st);
-    if ((st = dmalloc(g, (void **)&g->d_tile_b, tile_b.size() * 8))) return cleanup(st);
 
-    cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreate(&g->ev0);
-    if (e == cudaSuccess) e = cudaEventCreate(&g->ev1);
-    if (e == cudaSuccess) {
-        if (g->rp64) {
-            e = cudaMemcpyAsync(g->d_rp, row_ptr, rpb, cudaMemcpyHostToDevice, g->stream);
-        } else {
-            std::vector<int32_t> rp32((size_t)n + 1);
-            for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
-            e = cudaMemcpyAsync(g->d_rp, rp32.data(), rpb, cudaMemcpyHostToDevice, g->stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-        }
+    e = cudaMemcpyAsync(t_rp, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s);
+    if (!e && nnz) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s);
+    if (!e && t_val) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(t_deg, deg, (size_t)n * 8, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(g->d_perm, perm.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, s);
+    // wide-row offsets (host: few rows)
+    std::vector<int64_t> wptr((size_t)g->n_wide + 1, 0);
+    for (int64_t w = 0; w < g->n_wide; ++w) {
+        const int32_t r = perm[(size_t)(g->n_sell + w)];
+        wptr[(size_t)w + 1] = wptr[(size_t)w] + (row_ptr[r + 1] - row_ptr[r]);
     }
-    if (e == cudaSuccess && nnz)
-        e = cudaMemcpyAsync(g->d_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, g->stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(g->d_col + nnz, 0, 32, g->stream);
-    if (e == cudaSuccess && g->d_val) {
-        e = cudaMemcpyAsync(g->d_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, g->stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(g->d_val + nnz, 0, 64, g->stream);
-    }
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(g->d_deg, deg, (size_t)n * 8, cudaMemcpyHostToDevice, g->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(g->d_tile_r, tile_r.data(), tile_r.size() * 4, cudaMemcpyHostToDevice,
-                            g->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(g->d_tile_b, tile_b.data(), tile_b.size() * 8, cudaMemcpyHostToDevice,
-                            g->stream);
-    if (e == cudaSuccess && g->ntiles) {
-        if (g->rp64)
-            k_pack_rows<int64_t><<<(unsigned)g->ntiles, 256, 0, g->stream>>>(
-                (const int64_t *)g->d_rp, g->d_tile_b, g->d_tile_r, g->d_col, g->col_bits);
-        else
-            k_pack_rows<int32_t><<<(unsigned)g->ntiles, 256, 0, g->stream>>>(
-                (const int32_t *)g->d_rp, g->d_tile_b, g->d_tile_r, g->d_col, g->col_bits);
+    if (!e)
+        e = cudaMemcpyAsync(g->d_wide_ptr, wptr.data(), wptr.size() * 8, cudaMemcpyHostToDevice, s);
+    if (!e) {
+        k_inverse_perm<<<grid_for(g, n, 256), 256, 0, s>>>(g->d_perm, g->d_iperm, n);
+        k_gather_perm<<<grid_for(g, n, 256), 256, 0, s>>>(t_deg, g->d_perm, g->d_deg, n);
+        if (g->nslices)
+            k_slice_sizes<<<grid_for(g, g->nslices, 256), 256, 0, s>>>(t_rp, g->d_perm, g->n_sell,
+                                                                       g->nslices, t_sizes);
         e = cudaGetLastError();
     }
-    if (e == cudaSuccess) e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, g->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-    if (e != cudaSuccess) {
-        fail(SC_E_CUDA, "graph upload failed: %s", cudaGetErrorString(e));
+    if (!e) e = cudaMemsetAsync(t_sizes + g->nslices, 0, 8, s);
+    size_t cub_bytes = 0;
+    if (!e)
+        e = cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, t_sizes, g->d_slice_ptr,
+                                          g->nslices + 1, s);
+    if (!e) e = cudaMalloc(&t_cub, std::max<size_t>(cub_bytes, 16));
+    if (!e)
+        e = cub::DeviceScan::ExclusiveSum(t_cub, cub_bytes, t_sizes, g->d_slice_ptr,
+                                          g->nslices + 1, s);
+    if (!e)
+        e = cudaMemcpyAsync(&g->sell_entries, g->d_slice_ptr + g->nslices, 8,
+                            cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) {
+        free_tmp();
+        fail(SC_E_CUDA, "graph layout: %s", cudaGetErrorString(e));
+        return cleanup(SC_E_CUDA);
+    }
+    if ((st = dmalloc(g, (void **)&g->d_col, (size_t)g->sell_entries * 4 + 16)) ||
+        (!unit && (st = dmalloc(g, (void **)&g->d_val, (size_t)g->sell_entries * 8 + 16))) ||
+        (st = dmalloc(g, (void **)&g->d_wcol, (size_t)wptr.back() * 4 + 16)) ||
+        (!unit && (st = dmalloc(g, (void **)&g->d_wval, (size_t)wptr.back() * 8 + 16)))) {
+        free_tmp();
+        return cleanup(st);
+    }
+    if (g->n_sell)
+        k_fill_sell<<<grid_for(g, g->n_sell, 256), 256, 0, s>>>(
+            t_rp, t_col, t_val, g->d_perm, g->d_iperm, g->d_slice_ptr, g->n_sell, col_offset, n,
+            rename, g->d_col, g->d_val);
+    if (g->n_wide)
+        k_fill_wide<<<(unsigned)g->n_wide, 256, 0, s>>>(t_rp, t_col, t_val, g->d_perm, g->d_iperm,
+                                                        g->d_wide_ptr, g->n_sell, g->n_wide,
+                                                        col_offset, n, rename, g->d_wcol, g->d_wval);
+    e = cudaGetLastError();
+    if (!e) e = cudaStreamSynchronize(s);
+    free_tmp();
+    if (e) {
+        fail(SC_E_CUDA, "graph layout: %s", cudaGetErrorString(e));
         return cleanup(SC_E_CUDA);
     }
     *out = g;
     return SC_OK;
-}
-
-static int grid_for(const sc_graph *g, int64_t n, int tpb) {
-    int64_t want = (n + tpb - 1) / tpb;
-    int64_t cap = (int64_t)std::max(g->sm_count, 1) * 8;
-    return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
 static int32_t ensure_isd(sc_graph *g, cudaStream_t s) {
@@ -470,34 +563,36 @@ static int32_t ensure_isd(sc_graph *g, cudaStream_t s) {
 static int32_t launch_step(const sc_graph *g, const double *z_in, const double *x_in,
                            double *x_out, double *z_out, double sign, uint32_t flags,
                            cudaStream_t s) {
-    if (g->ntiles == 0) return SC_OK;
     const bool sym = flags & SC_SYM_VARIANT;
-    const bool unit = g->unit && !(flags & SC_FORCE_WEIGHTED && g->d_val);
     StepArgs a;
-    a.rp = g->d_rp;
+    a.slice_ptr = g->d_slice_ptr;
     a.col = g->d_col;
     a.val = g->d_val;
+    a.wide_ptr = g->d_wide_ptr;
+    a.wcol = g->d_wcol;
+    a.wval = g->d_wval;
     a.scale = sym ? g->d_isd : g->d_deg;
     a.x_in = x_in;
     a.z_in = z_in;
     a.x_out = x_out;
     a.z_out = z_out;
-    a.tile_b = g->d_tile_b;
-    a.tile_r = g->d_tile_r;
+    a.n_sell = g->n_sell;
+    a.n_wide = g->n_wide;
+    a.nslices = g->nslices;
     a.col_offset = g->col_offset;
-    a.col_bits = g->col_bits;
-    a.col_mask = g->col_bits >= 32 ? 0xffffffffu : ((1u << g->col_bits) - 1u);
     a.hs = sign < 0 ? -0.5 : 0.5;
-    const dim3 grid((unsigned)g->ntiles);
-#define SC_LAUNCH(RP, U, S) k_rw_step<RP, U, S><<<grid, kTPB, 0, s>>>(a)
-    if (g->rp64) {
-        if (unit) { if (sym) SC_LAUNCH(int64_t, true, true); else SC_LAUNCH(int64_t, true, false); }
-        else { if (sym) SC_LAUNCH(int64_t, false, true); else SC_LAUNCH(int64_t, false, false); }
+    constexpr int wpb = kStepTPB / 32;
+    a.wide_blocks = (int)((g->n_wide + wpb - 1) / wpb);
+    const int64_t blocks = a.wide_blocks + (g->nslices + wpb - 1) / wpb;
+    if (blocks == 0) return SC_OK;
+    const dim3 grid((unsigned)blocks);
+    if (g->unit) {
+        if (sym) k_rw_step<true, true><<<grid, kStepTPB, 0, s>>>(a);
+        else k_rw_step<true, false><<<grid, kStepTPB, 0, s>>>(a);
     } else {
-        if (unit) { if (sym) SC_LAUNCH(int32_t, true, true); else SC_LAUNCH(int32_t, true, false); }
-        else { if (sym) SC_LAUNCH(int32_t, false, true); else SC_LAUNCH(int32_t, false, false); }
+        if (sym) k_rw_step<false, true><<<grid, kStepTPB, 0, s>>>(a);
+        else k_rw_step<false, false><<<grid, kStepTPB, 0, s>>>(a);
     }
-#undef SC_LAUNCH
     SC_CUDA(cudaGetLastError());
     return SC_OK;
 }
@@ -542,11 +637,20 @@ static void set_l2_window(sc_graph *g, bool on) {
     g->l2_window = on;
 }
 
+// device vector (renumbered order) -> host vector (original order)
+static int32_t to_host_original(sc_graph *g, const double *dev, double *host) {
+    k_gather_perm<<<grid_for(g, g->n, 256), 256, 0, g->stream>>>(dev, g->d_iperm, g->d_tmp, g->n);
+    SC_CUDA(cudaGetLastError());
+    SC_CUDA(cudaMemcpyAsync(host, g->d_tmp, (size_t)g->n * 8, cudaMemcpyDeviceToHost, g->stream));
+    SC_CUDA(cudaStreamSynchronize(g->stream));
+    return SC_OK;
+}
+
 }  // namespace sc
 
 extern "C" {
 
-int32_t sc_version(void) { return 1; }
+int32_t sc_version(void) { return 2; }
 
 const char *sc_last_error(void) { return sc::g_last_error.c_str(); }
 
@@ -563,15 +667,24 @@ int32_t sc_device_count(void) {
 int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double *val,
                         const double *deg, int64_t n, int64_t nnz, int32_t device,
                         sc_graph **out) {
-    return graph_init(row_ptr, col, val, deg, n, nnz, n, 0, 0, device, out);
+    return graph_init(row_ptr, col, val, deg, n, nnz, n, 0, 0, 1, device, out);
 }
 
 int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double *val,
                         const double *deg, int64_t n, int64_t nnz, int64_t ncols,
                         int64_t col_offset, int64_t global_row0, int32_t device,
                         sc_graph **out) {
-    return graph_init(row_ptr, col, val, deg, n, nnz, ncols, col_offset, global_row0, device,
+    // columns arrive already renamed into the global renumbered z space (sc_sell_order)
+    return graph_init(row_ptr, col, val, deg, n, nnz, ncols, col_offset, global_row0, 0, device,
                       out);
+}
+
+int32_t sc_sell_order(const int64_t *row_ptr, int64_t n, int32_t *perm_out) {
+    SC_REQUIRE(row_ptr && perm_out && n >= 1, SC_E_INVALID, "null argument");
+    std::vector<int32_t> perm;
+    sell_order(row_ptr, n, perm);
+    std::memcpy(perm_out, perm.data(), (size_t)n * 4);
+    return SC_OK;
 }
 
 void sc_graph_destroy(sc_graph *g) {
@@ -579,17 +692,10 @@ void sc_graph_destroy(sc_graph *g) {
     cudaSetDevice(g->device);
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->gexec) cudaGraphExecDestroy(g->gexec);
-    cudaFree(g->d_rp);
-    cudaFree(g->d_col);
-    cudaFree(g->d_val);
-    cudaFree(g->d_deg);
-    cudaFree(g->d_isd);
-    cudaFree(g->d_x0);
-    cudaFree(g->d_x[0]);
-    cudaFree(g->d_x[1]);
-    cudaFree(g->d_z[0]);
-    cudaFree(g->d_tile_b);
-    cudaFree(g->d_tile_r);
+    void *ps[] = {g->d_perm, g->d_iperm, g->d_slice_ptr, g->d_col, g->d_val, g->d_wide_ptr,
+                  g->d_wcol, g->d_wval, g->d_deg, g->d_isd, g->d_x0, g->d_x[0], g->d_x[1],
+                  g->d_z[0], g->d_tmp, g->d_f_orig};
+    for (void *p : ps) cudaFree(p);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
     if (g->stream) cudaStreamDestroy(g->stream);
@@ -602,25 +708,34 @@ int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *o) {
     o->nnz = g->nnz;
     o->ncols = g->ncols;
     o->col_offset = g->col_offset;
-    o->ntiles = g->ntiles;
-    o->long_rows = g->long_rows;
+    o->ntiles = g->nslices;
+    o->long_rows = g->n_wide;
     o->unit_weights = g->unit;
-    o->rp64 = g->rp64;
+    o->rp64 = 0;
     o->device_bytes = g->bytes;
     o->device = g->device;
     o->sm_count = g->sm_count;
+    o->stored_entries = g->sell_entries;
+    return SC_OK;
+}
+
+int32_t sc_graph_order(const sc_graph *g, int32_t *perm_out) {
+    SC_REQUIRE(g && perm_out, SC_E_INVALID, "null argument");
+    SC_CUDA(cudaSetDevice(g->device));
+    SC_CUDA(cudaMemcpy(perm_out, g->d_perm, (size_t)g->n * 4, cudaMemcpyDeviceToHost));
     return SC_OK;
 }
 
 int32_t sc_sample_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x0_out) {
     SC_REQUIRE(g, SC_E_INVALID, "null graph");
     SC_CUDA(cudaSetDevice(g->device));
-    k_irwin_hall<<<grid_for(g, g->n, 128), 128, 0, g->stream>>>(g->d_deg, g->d_x0, g->n,
-                                                                g->global_row0, key0, key1);
+    k_irwin_hall<<<grid_for(g, g->n, 128), 128, 0, g->stream>>>(g->d_deg, g->d_perm, g->d_x0,
+                                                                g->n, g->global_row0, key0, key1);
     SC_CUDA(cudaGetLastError());
-    if (x0_out)
-        SC_CUDA(cudaMemcpyAsync(x0_out, g->d_x0, (size_t)g->n * 8, cudaMemcpyDeviceToHost,
-                                g->stream));
+    if (x0_out) {
+        int32_t st = to_host_original(g, g->d_x0, x0_out);
+        if (st) return st;
+    }
     SC_CUDA(cudaStreamSynchronize(g->stream));
     g->have_x0 = true;
     g->result = -1;
@@ -630,8 +745,11 @@ int32_t sc_sample_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *
 int32_t sc_set_x0(sc_graph *g, const double *x0_host) {
     SC_REQUIRE(g && x0_host, SC_E_INVALID, "null argument");
     SC_CUDA(cudaSetDevice(g->device));
-    SC_CUDA(cudaMemcpyAsync(g->d_x0, x0_host, (size_t)g->n * 8, cudaMemcpyHostToDevice,
+    SC_CUDA(cudaMemcpyAsync(g->d_tmp, x0_host, (size_t)g->n * 8, cudaMemcpyHostToDevice,
                             g->stream));
+    k_gather_perm<<<grid_for(g, g->n, 256), 256, 0, g->stream>>>(g->d_tmp, g->d_perm, g->d_x0,
+                                                                 g->n);
+    SC_CUDA(cudaGetLastError());
     SC_CUDA(cudaStreamSynchronize(g->stream));
     g->have_x0 = true;
     g->result = -1;
@@ -687,9 +805,8 @@ int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, do
     const double *xT = T == 0 ? g->d_x0 : g->d_x[g->result];
     const double *f = g->d_z[g->result];
     auto h0 = std::chrono::steady_clock::now();
-    if (xT_out)
-        SC_CUDA(cudaMemcpy(xT_out, xT, (size_t)g->n * 8, cudaMemcpyDeviceToHost));
-    if (f_out) SC_CUDA(cudaMemcpy(f_out, f, (size_t)g->n * 8, cudaMemcpyDeviceToHost));
+    if (xT_out && (st = to_host_original(g, xT, xT_out))) return st;
+    if (f_out && (st = to_host_original(g, f, f_out))) return st;
     auto h1 = std::chrono::steady_clock::now();
     if (t_out) {
         t_out->power_ms = ms;
@@ -730,8 +847,8 @@ int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x
     SC_REQUIRE(g && x_out, SC_E_INVALID, "null argument");
     SC_CUDA(cudaSetDevice(g->device));
     cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;
-    k_irwin_hall<<<grid_for(g, g->n, 128), 128, 0, s>>>(g->d_deg, x_out, g->n, g->global_row0,
-                                                        key0, key1);
+    k_irwin_hall<<<grid_for(g, g->n, 128), 128, 0, s>>>(g->d_deg, g->d_perm, x_out, g->n,
+                                                        g->global_row0, key0, key1);
     SC_CUDA(cudaGetLastError());
     return SC_OK;
 }
@@ -740,8 +857,14 @@ int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x
 
 // internal accessors for sc_kmeans.cu
 namespace sc {
-const double *graph_f_device(const sc_graph *g) {
-    return g->result < 0 ? nullptr : g->d_z[g->result];
+// f (= z_T) in ORIGINAL vertex order, materialised on the device on demand
+const double *graph_f_device(sc_graph *g) {
+    if (g->result < 0) return nullptr;
+    if (!g->d_f_orig && dmalloc(g, (void **)&g->d_f_orig, (size_t)g->n * 8)) return nullptr;
+    k_gather_perm<<<grid_for(g, g->n, 256), 256, 0, g->stream>>>(g->d_z[g->result], g->d_iperm,
+                                                                 g->d_f_orig, g->n);
+    if (cudaStreamSynchronize(g->stream) != cudaSuccess) return nullptr;
+    return g->d_f_orig;
 }
 int64_t graph_n(const sc_graph *g) { return g->n; }
 int graph_device(const sc_graph *g) { return g->device; }

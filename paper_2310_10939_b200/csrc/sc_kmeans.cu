@@ -27,7 +27,7 @@
 #include "sc_seqsum.cuh"
 
 namespace sc {
-const double *graph_f_device(const sc_graph *g);
+const double *graph_f_device(sc_graph *g);
 int64_t graph_n(const sc_graph *g);
 int graph_device(const sc_graph *g);
 }  // namespace sc

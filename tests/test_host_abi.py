@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
-    assert L.sc_version() == 1
+    assert L.sc_version() == 2
 
 
 def test_library_is_sm100a():
