@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--weighted", action="store_true",
                     help="force the weighted kernel (reads val even for unit weights)")
+    ap.add_argument("--no-weighted-probe", action="store_true")
     return ap.parse_args()
 
 
@@ -185,6 +186,60 @@ def pinned_copy(a: np.ndarray) -> np.ndarray:
     return out
 
 
+def time_power(dev, T, steps, warmup, clocks=False):
+    """Device time (CUDA events on the library's stream) of `steps` T-iteration passes."""
+    for _ in range(max(warmup, 3)):
+        dev.power_iterate(T, want_x=False, want_f=False)
+    times = []
+    clk = ClockSampler() if clocks else None
+    if clk:
+        clk.__enter__()
+    try:
+        for _ in range(steps):
+            dev.power_iterate(T, want_x=False, want_f=False)
+            times.append(dev.last_timing["power_ms"])
+    finally:
+        if clk:
+            clk.__exit__(None, None, None)
+    return times, (clk.summary() if clk else None)
+
+
+def roofline_for(g, info, kernel_ms, reads_val: bool):
+    """Algorithmic bytes per launch: nnz*(idx[+val]) + 8n gathered x +
+    8n written x; plus the compulsory bytes the kernel really streams (padded SELL
+    entries, row scale, x_in, x_out, z_out)."""
+    n, nnz = g.n, g.nnz
+    idx_val = 4 + (8 if reads_val else 0)
+    alg = nnz * idx_val + 16 * n
+    stored = int(info.get("stored_entries") or nnz)
+    compulsory = stored * idx_val + n * (8 + 8 + 8 + 8 + 8)
+    peak, peak_kind = peak_hbm()
+    achieved = alg / (kernel_ms / 1e3) / 1e9
+    r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+         "alg_bytes_per_launch": alg,
+         "alg_bytes_formula": f"nnz*{idx_val} + 16n" + (" (idx+val)" if reads_val else
+                                                      " (unit weights: val elided)"),
+         "compulsory_bytes_per_launch": compulsory,
+         "compulsory_frac": compulsory / (kernel_ms / 1e3) / 1e9 / peak,
+         "kernel_ms": kernel_ms}
+    gc = gather_ceiling()
+    if gc:
+        r["gather_ceiling"] = {"gathers_per_launch": nnz, "ceiling_ggather_s": gc["ggather_s"],
+                               "achieved_ggather_s": nnz / (kernel_ms / 1e3) / 1e9,
+                               "frac": nnz / (kernel_ms / 1e3) / 1e9 / gc["ggather_s"],
+                               "source": gc["source"]}
+    return r
+
+
+def gather_ceiling():
+    p = os.path.join(ROOT, "profiles", "gather_ceiling.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh)
+
+
 def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
@@ -196,34 +251,28 @@ def run_b200(args):
 
     g, T, k = build_config(args.config)
     unit = g.unit_weights() and not args.weighted
-    dev = DeviceGraph(g)
+    dev = DeviceGraph(g, keep_weights=args.weighted)
     info = dev.info()
     dev.sample_irwin_hall(0)
-    for _ in range(max(args.warmup, 3)):
-        dev.power_iterate(T, want_x=False, want_f=False, force_weighted=args.weighted)
-    times = []
-    with ClockSampler() as clk:
-        for _ in range(args.steps):
-            dev.power_iterate(T, want_x=False, want_f=False, force_weighted=args.weighted)
-            times.append(dev.last_timing["power_ms"])
-    clocks = clk.summary()
+    times, clocks = time_power(dev, T, args.steps, args.warmup, clocks=True)
     tot_ms = sum(times)
     value = g.nnz * T * args.steps / (tot_ms / 1e3) / 1e9
     kernel_ms = tot_ms / (args.steps * T)
-    n = g.n
-    idx_val = 4 + (0 if unit else 8)
-    alg_bytes = g.nnz * idx_val + 16 * n
-    compulsory = g.nnz * idx_val + n * ((8 if info["rp64"] else 4) + 8 + 8 + 8 + 8)
-    peak, peak_kind = peak_hbm()
-    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
-    traffic = traffic_from_profiles(args.config, unit)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                "alg_bytes_per_launch": alg_bytes,
-                "alg_bytes_formula": f"nnz*{idx_val} + 16n" + ("" if unit else " (idx+val)"),
-                "compulsory_bytes_per_launch": compulsory,
-                "compulsory_frac": compulsory / (kernel_ms / 1e3) / 1e9 / peak,
-                "kernel_ms": kernel_ms}
+    roofline = roofline_for(g, info, kernel_ms, reads_val=not unit)
+    roofline["traffic"] = traffic_from_profiles(args.config, unit)
+    dev.close()
+    # the same graph through the weighted kernel (weights streamed even though all 1.0):
+    # the north-star byte formula nnz*(idx+val) applies to this one
+    weighted = None
+    if unit and not args.no_weighted_probe:
+        with DeviceGraph(g, keep_weights=True) as dw:
+            iw = dw.info()
+            dw.sample_irwin_hall(0)
+            wt, _ = time_power(dw, T, max(3, args.steps // 2), 2)
+            wk = sum(wt) / (len(wt) * T)
+            weighted = {"value": g.nnz * T / (sum(wt) / len(wt) / 1e3) / 1e9, "unit": UNIT,
+                        "kernel_ms": wk, "roofline": roofline_for(g, iw, wk, reads_val=True)}
+            weighted["roofline"]["traffic"] = traffic_from_profiles(args.config, False)
     # ---- end to end through the public API, pinned host buffers
     gp = Graph(n=g.n, row_offsets=pinned_copy(g.row_offsets), col_indices=pinned_copy(g.col_indices),
                weights=None if g.weights is None else pinned_copy(g.weights),
@@ -236,13 +285,16 @@ def run_b200(args):
         res = fast_spectral_cluster(gp, params)
         e2e_t.append(time.perf_counter() - t)
     e2e_s = statistics.median(e2e_t)
-    h2d = g.row_offsets.nbytes + g.nnz * 4 + g.degrees.nbytes + (0 if g.weights is None or g.unit_weights() else g.nnz * 8)
+    n = g.n
+    h2d = g.row_offsets.nbytes + g.nnz * 4 + g.degrees.nbytes + (
+        0 if g.weights is None or g.unit_weights() else g.nnz * 8)
     d2h = n * 8 + n * 8  # labels (int64) + embedding f
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config{args.config}", "graph": "SBM (reference sample_sbm semantics)",
+        "config": {"workload": f"config{args.config}",
+                   "graph": "SBM, reference sample_sbm semantics (seed 0)",
                    "n": n, "nnz": g.nnz, "T": T, "k": k, "unit_weight_kernel": unit,
                    "l2": "inputs larger than L2 (CSR streamed per iteration >= 0.2 GB)",
                    "parallelism": "single GPU"},
@@ -250,11 +302,15 @@ def run_b200(args):
         "e2e": {"value": g.nnz * T / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "cluster_ms": e2e_s * 1e3,
                 "stages_ms": {k_: round(v, 3) for k_, v in res.timings.items()},
-                "upload_ms": res.device_timings.get("upload_ms")},
+                "upload_ms": res.device_timings.get("upload_ms"),
+                "path": "fast_spectral_cluster(graph in pinned host memory) -> labels + f on host"},
         "gpu_launches": args.steps * (T + 1),
         "clocks": clocks,
-        "graph_info": {k_: info[k_] for k_ in ("ntiles", "long_rows", "rp64", "device_bytes")},
+        "graph_info": {k_: info[k_] for k_ in ("ntiles", "long_rows", "stored_entries",
+                                               "device_bytes")},
     }
+    if weighted:
+        line["weighted_kernel"] = weighted
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(g, T, os.cpu_count() or 1)
     print(json.dumps(line), flush=True)

@@ -90,6 +90,12 @@ int32_t sc_device_count(void);
 int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double *val,
                         const double *deg, int64_t n, int64_t nnz, int32_t device,
                         sc_graph **out);
+/* As sc_graph_create; create_flags: SC_CREATE_KEEP_WEIGHTS keeps an all-ones weight array on
+ * the device (the weighted kernel then streams it) instead of eliding it. */
+#define SC_CREATE_KEEP_WEIGHTS 0x1u
+int32_t sc_graph_create_ex(const int64_t *row_ptr, const int32_t *col, const double *val,
+                           const double *deg, int64_t n, int64_t nnz, int32_t device,
+                           uint32_t create_flags, sc_graph **out);
 /* Row-block shard: rows are the local block, columns index a z space of length ncols in
  * which this shard's own rows live at [col_offset, col_offset + n).  Columns must already
  * be renamed into the renumbered z space (every shard's sc_sell_order permutation). */

@@ -22,6 +22,7 @@ SC_SYM_VARIANT = 0x1
 SC_NO_CUDA_GRAPH = 0x2
 SC_L2_PERSIST = 0x4
 SC_FORCE_WEIGHTED = 0x8
+SC_CREATE_KEEP_WEIGHTS = 0x1
 
 
 class GraphInfo(ctypes.Structure):
@@ -44,7 +45,7 @@ EXPORTS = (
     "sc_graph_destroy", "sc_graph_info_get", "sc_sample_irwin_hall", "sc_set_x0",
     "sc_power_iterate", "sc_shard_step", "sc_shard_scale", "sc_shard_irwin_hall",
     "sc_kmeans_create", "sc_kmeans_create_from_graph", "sc_kmeans_destroy", "sc_kmeans_pp",
-    "sc_kmeans_lloyd", "sc_seqsum", "sc_sell_order", "sc_graph_order",
+    "sc_kmeans_lloyd", "sc_seqsum", "sc_sell_order", "sc_graph_order", "sc_graph_create_ex",
 )
 
 _lib = None
@@ -84,6 +85,7 @@ def load() -> ctypes.CDLL:
         "sc_kmeans_lloyd": ([P, i32, i32, P, i32, f64, P, P, P, P, P], i32),
         "sc_seqsum": ([P, i32, P, i32, P, P], i32),
         "sc_sell_order": ([P, i64, P], i32),
+        "sc_graph_create_ex": ([P, P, P, P, i64, i64, i32, u32, PP], i32),
         "sc_graph_order": ([P, P], i32),
     }
     for name, (args, res) in sig.items():

@@ -381,10 +381,19 @@ static int grid_for(const sc_graph *g, int64_t n, int tpb) {
 
 static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const double *val,
                           const double *deg, int64_t n, int64_t nnz, int64_t ncols,
-                          int64_t col_offset, int64_t global_row0, int rename, int32_t device,
+                          int64_t col_offset, int64_t global_row0, int rename, uint32_t cflags, int32_t device,
                           sc_graph **out) {
     SC_REQUIRE(out, SC_E_INVALID, "out is null");
     *out = nullptr;
+    const bool prof = getenv("SC_GRAPH_PROFILE") != nullptr;
+    auto tp0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        if (!prof) return;
+        auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[sc_graph_create] %-22s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(t - tp0).count());
+        tp0 = t;
+    };
     SC_REQUIRE(row_ptr && deg && (col || nnz == 0), SC_E_INVALID, "null CSR array");
     SC_REQUIRE(n >= 1 && n < (int64_t(1) << 31) - 1, SC_E_INVALID, "n=%lld out of range",
                (long long)n);
@@ -394,15 +403,30 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
                    col_offset + n <= ncols,
                SC_E_RANGE, "bad z-space geometry ncols=%lld col_offset=%lld", (long long)ncols,
                (long long)col_offset);
-    for (int64_t i = 0; i < n; ++i)
-        SC_REQUIRE(row_ptr[i + 1] >= row_ptr[i], SC_E_RANGE, "row_ptr decreases at %lld",
-                   (long long)i);
-    for (int64_t i = 0; i < n; ++i)
-        SC_REQUIRE(deg[i] > 0.0 && deg[i] < 1e308, SC_E_RANGE,
-                   "degree of row %lld is not positive/finite", (long long)i);
-    for (int64_t j = 0; j < nnz; ++j)
-        SC_REQUIRE(col[j] >= 0 && col[j] < ncols, SC_E_RANGE, "col_indices[%lld]=%d out of range",
-                   (long long)j, col[j]);
+    {
+        // branch-free scans (vectorised by the compiler); locate the culprit only on failure
+        bool mono = true, dok = true;
+        for (int64_t i = 0; i < n; ++i) mono &= row_ptr[i + 1] >= row_ptr[i];
+        for (int64_t i = 0; i < n; ++i) dok &= (deg[i] > 0.0) & (deg[i] < 1e308);
+        int32_t cmin = 0, cmax = 0;
+        if (nnz) {
+            cmin = cmax = col[0];
+            for (int64_t j = 0; j < nnz; ++j) {
+                cmin = std::min(cmin, col[j]);
+                cmax = std::max(cmax, col[j]);
+            }
+        }
+        for (int64_t i = 0; !mono && i < n; ++i)
+            SC_REQUIRE(row_ptr[i + 1] >= row_ptr[i], SC_E_RANGE, "row_ptr decreases at %lld",
+                       (long long)i);
+        for (int64_t i = 0; !dok && i < n; ++i)
+            SC_REQUIRE(deg[i] > 0.0 && deg[i] < 1e308, SC_E_RANGE,
+                       "degree of row %lld is not positive/finite", (long long)i);
+        for (int64_t j = 0; (cmin < 0 || cmax >= ncols) && j < nnz; ++j)
+            SC_REQUIRE(col[j] >= 0 && col[j] < ncols, SC_E_RANGE,
+                       "col_indices[%lld]=%d out of range", (long long)j, col[j]);
+    }
+    lap("host validation");
     int ndev = 0;
     SC_CUDA(cudaGetDeviceCount(&ndev));
     SC_REQUIRE(device >= 0 && device < ndev, SC_E_INVALID, "device %d not present (%d GPUs)",
@@ -421,11 +445,14 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if (!unit) {
         unit = true;
         for (int64_t j = 0; j < nnz && unit; ++j) unit = (val[j] == 1.0);
+        if (cflags & SC_CREATE_KEEP_WEIGHTS) unit = false;
     }
     g->unit = unit;
 
+    lap("unit check");
     std::vector<int32_t> perm;
     g->n_sell = sell_order(row_ptr, n, perm);
+    lap("sell order");
     g->n_wide = n - g->n_sell;
     g->nslices = (g->n_sell + kSlice - 1) / kSlice;
 
@@ -520,6 +547,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         e = cudaMemcpyAsync(&g->sell_entries, g->d_slice_ptr + g->nslices, 8,
                             cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
+    lap("alloc + H2D + slices");
     if (e) {
         free_tmp();
         fail(SC_E_CUDA, "graph layout: %s", cudaGetErrorString(e));
@@ -543,6 +571,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     e = cudaGetLastError();
     if (!e) e = cudaStreamSynchronize(s);
     free_tmp();
+    lap("SELL fill + free");
     if (e) {
         fail(SC_E_CUDA, "graph layout: %s", cudaGetErrorString(e));
         return cleanup(SC_E_CUDA);
@@ -667,7 +696,15 @@ int32_t sc_device_count(void) {
 int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double *val,
                         const double *deg, int64_t n, int64_t nnz, int32_t device,
                         sc_graph **out) {
-    return graph_init(row_ptr, col, val, deg, n, nnz, n, 0, 0, 1, device, out);
+    return graph_init(row_ptr, col, val, deg, n, nnz, n, 0, 0, 1, 0u, device, out);
+}
+
+int32_t sc_graph_create_ex(const int64_t *row_ptr, const int32_t *col, const double *val,
+                           const double *deg, int64_t n, int64_t nnz, int32_t device,
+                           uint32_t create_flags, sc_graph **out) {
+    SC_REQUIRE(!(create_flags & SC_CREATE_KEEP_WEIGHTS) || val || nnz == 0, SC_E_INVALID,
+               "SC_CREATE_KEEP_WEIGHTS needs a weight array");
+    return graph_init(row_ptr, col, val, deg, n, nnz, n, 0, 0, 1, create_flags, device, out);
 }
 
 int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double *val,
@@ -675,7 +712,7 @@ int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double
                         int64_t col_offset, int64_t global_row0, int32_t device,
                         sc_graph **out) {
     // columns arrive already renamed into the global renumbered z space (sc_sell_order)
-    return graph_init(row_ptr, col, val, deg, n, nnz, ncols, col_offset, global_row0, 0, device,
+    return graph_init(row_ptr, col, val, deg, n, nnz, ncols, col_offset, global_row0, 0, 0u, device,
                       out);
 }
 

@@ -559,44 +559,43 @@ __global__ void k_seg_means(int rk, int k, const int64_t *__restrict__ seg,
     cen[t] = c > 0 ? __ddiv_rn(total[t], (double)c) : 0.0;
 }
 
-// kmeans_cost in numpy einsum order (sc_oracle.c orc_einsum_sumsq): one thread per
-// 8192-element buffer carries both SSE lanes
-__global__ void k_cost_lanes(const double *__restrict__ x, int64_t n, int k,
-                             const int32_t *__restrict__ lab, const double *__restrict__ cen,
-                             const int32_t *__restrict__ active, int64_t nbuf,
-                             double *__restrict__ part) {
+// kmeans_cost in numpy einsum("ij,ij->") order (sc_oracle.c orc_einsum_sumsq): one CTA
+// per (restart, 8192-element buffer) stages the buffer's squared deviations
+// fl(fl(x - c_label)^2) in shared memory with coalesced loads, then two threads run the two
+// SSE lane chains (8 elements per step in the order 6|7, 4|5, 2|3, 0|1, tail with zero fill)
+// out of shared memory at the FP64 add latency.
+__global__ void __launch_bounds__(256) k_cost_buf(const double *__restrict__ x, int64_t n, int k,
+                                                  const int32_t *__restrict__ lab,
+                                                  const double *__restrict__ cen,
+                                                  const int32_t *__restrict__ active, int64_t nbuf,
+                                                  double *__restrict__ part) {
+    extern __shared__ double sqb[];
     const int r = blockIdx.y;
     if (!active[r]) return;
-    const int64_t bufi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (bufi >= nbuf) return;
-    const int32_t *lb = lab + (int64_t)r * n;
-    const double *c = cen + (int64_t)r * k;
+    const int64_t bufi = blockIdx.x;
     const int64_t base = bufi * kEinsumBuf;
-    const int64_t m = min((int64_t)kEinsumBuf, n - base);
-    double a0 = 0.0, a1 = 0.0;
-    int64_t i = 0;
+    const int m = (int)min((int64_t)kEinsumBuf, n - base);
+    const int32_t *lb = lab + (int64_t)r * n + base;
+    const double *c = cen + (int64_t)r * k;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        const double d = __dsub_rn(x[base + j], c[lb[j]]);
+        sqb[j] = __dmul_rn(d, d);
+    }
+    __syncthreads();
+    if (threadIdx.x >= 2) return;
+    const int lane = threadIdx.x;
+    double acc = 0.0;
+    int i = 0;
     for (; m - i >= 8; i += 8) {
-        double d[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int64_t j = base + i + q;
-            d[q] = __dsub_rn(x[j], c[lb[j]]);
-        }
-#pragma unroll
-        for (int blk = 3; blk >= 0; --blk) {
-            a0 = __dadd_rn(__dmul_rn(d[2 * blk], d[2 * blk]), a0);
-            a1 = __dadd_rn(__dmul_rn(d[2 * blk + 1], d[2 * blk + 1]), a1);
-        }
+        const double p6 = sqb[i + 6 + lane], p4 = sqb[i + 4 + lane], p2 = sqb[i + 2 + lane],
+                     p0 = sqb[i + lane];
+        acc = __dadd_rn(p6, acc);
+        acc = __dadd_rn(p4, acc);
+        acc = __dadd_rn(p2, acc);
+        acc = __dadd_rn(p0, acc);
     }
-    for (; i < m; i += 2) {
-        const double d0 = __dsub_rn(x[base + i], c[lb[base + i]]);
-        a0 = __dadd_rn(__dmul_rn(d0, d0), a0);
-        double d1 = 0.0;
-        if (i + 1 < m) d1 = __dsub_rn(x[base + i + 1], c[lb[base + i + 1]]);
-        a1 = __dadd_rn(__dmul_rn(d1, d1), a1);
-    }
-    part[((int64_t)r * nbuf + bufi) * 2 + 0] = a0;
-    part[((int64_t)r * nbuf + bufi) * 2 + 1] = a1;
+    for (; i < m; i += 2) acc = __dadd_rn(i + lane < m ? sqb[i + lane] : 0.0, acc);
+    part[((int64_t)r * nbuf + bufi) * 2 + lane] = acc;
 }
 
 // buffer totals (l0 + l1) added into the running output in buffer order
@@ -869,7 +868,9 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     if (k > 48 * 1024)
         SC_CUDA(cudaFuncSetAttribute(k_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, k));
     const dim3 ga(grid_1d(km, n, 256) / std::max(1, std::min(R, 8)) + 1, R);
-    const dim3 gc((unsigned)((nbuf + 127) / 128), R);
+    const dim3 gc((unsigned)nbuf, R);
+    SC_CUDA(cudaFuncSetAttribute(k_cost_buf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kEinsumBuf * 8));
     SegView vm;
     vm.vals = km->d_vals_alt;
     vm.seg_off = km->d_seg;
@@ -880,6 +881,11 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     const SeqWork wm = seq_work(km);
     const int gwm = grid_1d(km, ((int64_t)R * n / kSeqChunk + rk) * 32, 256);
     const int gsm = (rk * 32 + 255) / 256;
+    const bool prof = getenv("SC_KMEANS_PROFILE") != nullptr;
+    cudaEvent_t pe[5];
+    double pacc[4] = {0, 0, 0, 0};
+    if (prof)
+        for (auto &ev : pe) cudaEventCreate(&ev);
     for (int it = 0; it < max_iters; ++it) {
         int nact = 0;
         for (int r = 0; r < R; ++r) nact += active[r];
@@ -888,6 +894,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         SC_CUDA(cudaMemcpyAsync(km->d_active, active.data(), (size_t)R * 4, cudaMemcpyHostToDevice, s));
         SC_CUDA(cudaMemsetAsync(km->d_cnt, 0, (size_t)rk * 4, s));
         SC_CUDA(cudaMemsetAsync(km->d_changed, 0, (size_t)R * 4, s));
+        if (prof) cudaEventRecord(pe[0], s);
         k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, k, km->d_cen, km->d_active,
                                                km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
                                                km->d_changed);
@@ -902,6 +909,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                         (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
         // np.add.at order: stable radix sort on (restart, label) keeps point-index order
         // inside every cluster; then ordered segment sums
+        if (prof) cudaEventRecord(pe[1], s);
         k_make_keys<<<grid_1d(km, (int64_t)R * n, 256), 256, 0, s>>>(
             n, k, km->d_lab[nxt], km->d_keys, km->d_vals, km->d_x, R);
         size_t tb = km->cub_bytes;
@@ -910,6 +918,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                                 end_bit, s));
         k_seg_offsets<<<(rk + 1 + 255) / 256, 256, 0, s>>>(rk, (int64_t)R * n, km->d_keys_alt,
                                                            km->d_seg);
+        if (prof) cudaEventRecord(pe[2], s);
         k_chunk_offsets<<<1, 1024, 0, s>>>(rk, km->d_seg, km->d_cofs, km->d_nchunks);
         SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)rk * 4, s));
         k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
@@ -918,13 +927,21 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         k_seq_compose<<<gsm, 256, 0, s>>>(vm, wm);
         k_seg_means<<<(rk + 127) / 128, 128, 0, s>>>(rk, k, km->d_seg, km->d_total, km->d_active,
                                                      km->d_cen);
-        k_cost_lanes<<<gc, 128, 0, s>>>(km->d_x, n, k, km->d_lab[nxt], km->d_cen, km->d_active,
-                                        nbuf, km->d_part);
+        if (prof) cudaEventRecord(pe[3], s);
+        k_cost_buf<<<gc, 256, kEinsumBuf * 8, s>>>(km->d_x, n, k, km->d_lab[nxt], km->d_cen,
+                                                   km->d_active, nbuf, km->d_part);
         k_cost_combine<<<R, 32, 0, s>>>(nbuf, km->d_part, km->d_active, km->d_cost);
         SC_CUDA(cudaGetLastError());
+        if (prof) cudaEventRecord(pe[4], s);
         SC_CUDA(cudaMemcpyAsync(cost.data(), km->d_cost, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
         SC_CUDA(cudaMemcpyAsync(changed.data(), km->d_changed, (size_t)R * 4, cudaMemcpyDeviceToHost, s));
         SC_CUDA(cudaStreamSynchronize(s));
+        if (prof)
+            for (int q = 0; q < 4; ++q) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, pe[q], pe[q + 1]);
+                pacc[q] += ms;
+            }
         for (int r = 0; r < R; ++r) {
             if (!active[r]) continue;
             // kmeans.py:202-210, in the same double arithmetic
@@ -938,6 +955,11 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             if (unchanged || small_gain) active[r] = 0;
         }
         cur = nxt;
+    }
+    if (prof) {
+        fprintf(stderr, "[sc_kmeans_lloyd] assign+repair %.3f ms, sort %.3f ms, ordered sums %.3f ms, cost %.3f ms\n",
+                pacc[0], pacc[1], pacc[2], pacc[3]);
+        for (auto &ev : pe) cudaEventDestroy(ev);
     }
     int best = -1;
     double best_cost = INFINITY;

@@ -67,13 +67,26 @@ class EmbeddingMatrix:
         return self.data.shape[1]
 
 
+def _check_shapes(g: Graph) -> None:
+    n = int(g.n)
+    if n < 1:
+        raise InputError(f"graph must have n >= 1 vertices, got {n}")
+    if np.shape(g.row_offsets) != (n + 1,) or np.shape(g.degrees) != (n,):
+        raise InputError("row_offsets must have length n+1 and degrees length n")
+    nnz = int(g.row_offsets[-1])
+    if np.shape(g.col_indices) != (nnz,):
+        raise InputError("col_indices length must equal row_offsets[-1]")
+    if g.weights is not None and np.shape(g.weights) != (nnz,):
+        raise InputError("weights length must equal row_offsets[-1]")
+
+
 class DeviceGraph:
     """Owns an ``sc_graph`` handle: the CSR uploaded once to one GPU (graph.py:28-45
     layout; degrees copied verbatim, never recomputed)."""
 
-    def __init__(self, graph, device: int = 0):
+    def __init__(self, graph, device: int = 0, keep_weights: bool = False):
         g = as_graph(graph)
-        g.validate()
+        _check_shapes(g)  # content (ranges, monotonicity, degrees) is validated by the C-ABI
         L = _lib.require_device()
         self.graph = g
         self.n = g.n
@@ -81,11 +94,18 @@ class DeviceGraph:
         self._rp = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
         self._col = np.ascontiguousarray(g.col_indices, dtype=np.int32)
         self._deg = np.ascontiguousarray(g.degrees, dtype=np.float64)
-        w = None if (g.weights is None or g.unit_weights()) else np.ascontiguousarray(
-            g.weights, dtype=np.float64)
+        if keep_weights:
+            # benchmark/diagnostic mode: stream the weight array even if it is all ones
+            w = (np.ones(g.nnz) if g.weights is None
+                 else np.ascontiguousarray(g.weights, dtype=np.float64))
+        else:
+            w = None if (g.weights is None or g.unit_weights()) else np.ascontiguousarray(
+                g.weights, dtype=np.float64)
         h = ctypes.c_void_p()
-        _lib.check(L.sc_graph_create(_lib.ptr(self._rp), _lib.ptr(self._col), _lib.ptr(w),
-                                     _lib.ptr(self._deg), g.n, g.nnz, device, ctypes.byref(h)))
+        _lib.check(L.sc_graph_create_ex(_lib.ptr(self._rp), _lib.ptr(self._col), _lib.ptr(w),
+                                        _lib.ptr(self._deg), g.n, g.nnz, device,
+                                        _lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0,
+                                        ctypes.byref(h)))
         self._h = h
         self.device = device
         self.last_timing = None
