@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--weighted", action="store_true",
                     help="force the weighted kernel (reads val even for unit weights)")
     ap.add_argument("--no-weighted-probe", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-block sharded (torch.distributed) path even at N=1")
     return ap.parse_args()
 
 
@@ -242,7 +244,7 @@ def gather_ceiling():
 
 def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.sharded:
         from paper_2310_10939_b200 import distributed
 
         return distributed.bench_main(args, METRIC, UNIT)

@@ -128,7 +128,8 @@ int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, do
                          double *f_out, sc_timing *t_out);
 
 /* ---- device-pointer shard step (multi-GPU composition) ------------------ */
-/* One iteration on a shard using caller-owned device buffers on caller stream:
+/* One iteration on a shard using caller-owned device buffers, launched on `stream` (a
+ * cudaStream_t; 0 = the legacy default stream), all buffers in renumbered order:
  * reads z_in[ncols] (gathered), x_in[n]; writes x_out[n], z_out[col_offset + i]. */
 int32_t sc_shard_step(sc_graph *g, const double *z_in, const double *x_in, double *x_out,
                       double *z_out, double sign, uint32_t flags, void *stream);

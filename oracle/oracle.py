@@ -54,7 +54,7 @@ def lib() -> ctypes.CDLL:
         P = ctypes.c_void_p
         i64, i32, f64, u64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64
         L.orc_philox4x64_10.argtypes = [P, P, P]
-        L.orc_irwin_hall.argtypes = [i64, P, u64, u64, P, i32]
+        L.orc_irwin_hall.argtypes = [i64, P, u64, u64, P, i32, i64]
         L.orc_power_iterate.argtypes = [i64, P, P, P, P, P, i32, i32, f64, P, P, i32]
         L.orc_einsum_sumsq.argtypes = [i64, P]
         L.orc_einsum_sumsq.restype = f64
@@ -62,6 +62,7 @@ def lib() -> ctypes.CDLL:
         L.orc_kmeanspp.restype = i32
         L.orc_lloyd_restart.argtypes = [i64, P, i32, P, i32, f64, P, P]
         L.orc_lloyd_restart.restype = i32
+        L.orc_rw_rows.argtypes = [i64, P, P, P, P, P, P, i32, f64, P, P]
         _lib = L
     return _lib
 
@@ -101,11 +102,12 @@ def philox(ctr, key) -> np.ndarray:
     return out
 
 
-def irwin_hall(degrees: np.ndarray, seed: int, threads: int = 1) -> np.ndarray:
+def irwin_hall(degrees: np.ndarray, seed: int, threads: int = 1, row0: int = 0) -> np.ndarray:
+    """x0 for vertices row0 .. row0+len(degrees)-1 (global ids)."""
     d = np.ascontiguousarray(degrees, dtype=np.float64)
     k0, k1 = irwin_hall_key(seed)
     x0 = np.empty_like(d)
-    lib().orc_irwin_hall(d.size, _p(d), k0, k1, _p(x0), threads)
+    lib().orc_irwin_hall(d.size, _p(d), k0, k1, _p(x0), threads, int(row0))
     return x0
 
 
@@ -123,6 +125,22 @@ def power_iterate(row_offsets, col_indices, weights, degrees, x0, t: int, *, var
     lib().orc_power_iterate(n, _p(rp), _p(col), _p(val), _p(deg), _p(x), int(t),
                             0 if variant == "rw" else 1, float(sign), _p(xT), _p(f), threads)
     return xT, f
+
+
+def rw_rows(row_offsets, col_indices, weights, degrees, x, z, *, variant="rw", sign=1.0):
+    """One step for a block of rows given the full gathered z; returns (y, z_out)."""
+    rp = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    col = np.ascontiguousarray(col_indices, dtype=np.int32)
+    val = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    deg = np.ascontiguousarray(degrees, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    n = deg.size
+    y = np.empty(n)
+    zo = np.empty(n)
+    lib().orc_rw_rows(n, _p(rp), _p(col), _p(val), _p(deg), _p(x), _p(z),
+                      0 if variant == "rw" else 1, float(sign), _p(y), _p(zo))
+    return y, zo
 
 
 def einsum_sumsq(v: np.ndarray) -> float:

@@ -86,7 +86,7 @@ static inline double u53(uint64_t r) { return (double)(r >> 11) * (1.0 / 9007199
 /* ------------------------------------------------------------------------- */
 /* Irwin-Hall start vector                                                     */
 
-typedef struct { const double *deg; uint64_t key[2]; double *x0; } ih_ctx;
+typedef struct { const double *deg; uint64_t key[2]; double *x0; int64_t row0; } ih_ctx;
 
 static void ih_range(void *p, int64_t lo, int64_t hi) {
     ih_ctx *c = (ih_ctx *)p;
@@ -100,7 +100,7 @@ static void ih_range(void *p, int64_t lo, int64_t hi) {
         uint64_t buf[4];
         for (int64_t j = 0; j < need; ++j) {
             if ((j & 3) == 0) {
-                uint64_t ctr[4] = {(uint64_t)(j >> 2) + 1u, (uint64_t)u, 0, 0};
+                uint64_t ctr[4] = {(uint64_t)(j >> 2) + 1u, (uint64_t)(c->row0 + u), 0, 0};
                 orc_philox4x64_10(ctr, c->key, buf);
             }
             double un = u53(buf[j & 3]);
@@ -112,8 +112,8 @@ static void ih_range(void *p, int64_t lo, int64_t hi) {
 }
 
 void orc_irwin_hall(int64_t n, const double *deg, uint64_t key0, uint64_t key1, double *x0,
-                    int32_t nthreads) {
-    ih_ctx c = {deg, {key0, key1}, x0};
+                    int32_t nthreads, int64_t row0) {
+    ih_ctx c = {deg, {key0, key1}, x0, row0};
     orc_parallel_for(n, nthreads, ih_range, &c);
 }
 
@@ -171,6 +171,23 @@ void orc_power_iterate(int64_t n, const int64_t *rp, const int32_t *col, const d
     memcpy(xT, x, sizeof(double) * (size_t)n);
     for (int64_t i = 0; i < n; ++i) f[i] = (variant == 1) ? x[i] * s[i] : x[i] / deg[i];
     free(x); free(y); free(z); free(s);
+}
+
+/* One rw/sym step for a block of rows given the full gathered vector z (multi-GPU shard
+ * oracle): y[i] = 0.5*x[i] + sgn*0.5*sum_j val_j*z[col_j] (sym: scaled by s[i]), then
+ * zout[i] = y[i]/deg[i] (sym: y[i]*s[i]).  Same per-row order as orc_power_iterate. */
+void orc_rw_rows(int64_t n, const int64_t *rp, const int32_t *col, const double *val,
+                 const double *deg, const double *x, const double *z, int32_t variant, double sgn,
+                 double *y, double *zout) {
+    const double hs = sgn < 0 ? -0.5 : 0.5;
+    for (int64_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int64_t j = rp[i]; j < rp[i + 1]; ++j) acc = acc + (val ? val[j] : 1.0) * z[col[j]];
+        double s = variant == 1 ? 1.0 / sqrt(deg[i]) : 0.0;
+        if (variant == 1) acc = s * acc;
+        y[i] = 0.5 * x[i] + hs * acc;
+        zout[i] = variant == 1 ? y[i] * s : y[i] / deg[i];
+    }
 }
 
 /* ------------------------------------------------------------------------- */

@@ -857,7 +857,7 @@ int32_t sc_shard_step(sc_graph *g, const double *z_in, const double *x_in, doubl
                       double *z_out, double sign, uint32_t flags, void *stream) {
     SC_REQUIRE(g && z_in && x_in && x_out && z_out, SC_E_INVALID, "null argument");
     SC_CUDA(cudaSetDevice(g->device));
-    cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;
+    cudaStream_t s = (cudaStream_t)stream;  // the caller's stream, 0 = legacy default stream
     int32_t st;
     if (flags & SC_SYM_VARIANT)
         if ((st = ensure_isd(g, s))) return st;
@@ -868,7 +868,7 @@ int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t fla
                        void *stream) {
     SC_REQUIRE(g && x && z_out, SC_E_INVALID, "null argument");
     SC_CUDA(cudaSetDevice(g->device));
-    cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;
+    cudaStream_t s = (cudaStream_t)stream;  // the caller's stream, 0 = legacy default stream
     const bool sym = flags & SC_SYM_VARIANT;
     int32_t st;
     if (sym)
@@ -883,7 +883,7 @@ int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x
                             void *stream) {
     SC_REQUIRE(g && x_out, SC_E_INVALID, "null argument");
     SC_CUDA(cudaSetDevice(g->device));
-    cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;
+    cudaStream_t s = (cudaStream_t)stream;  // the caller's stream, 0 = legacy default stream
     k_irwin_hall<<<grid_for(g, g->n, 128), 128, 0, s>>>(g->d_deg, g->d_perm, x_out, g->n,
                                                         g->global_row0, key0, key1);
     SC_CUDA(cudaGetLastError());

@@ -125,6 +125,41 @@ def sample_sbm(params: SbmParams) -> SbmSample:
     return SbmSample(graph=g, planted=planted, dropped=dropped, params=params)
 
 
+def sbm_rows(params: SbmParams, lo: int, hi: int):
+    """Rows [lo, hi) of the SBM of ``params`` (global column ids), generating only the block
+    pairs that touch those rows with the very streams ``sample_sbm`` uses -- so the shards of
+    all ranks concatenate to ``sample_sbm(params).graph`` whenever no vertex is isolated
+    (which sample_sbm would drop and compact).  Returns (row_ptr int64, col int32,
+    degrees float64, isolated count)."""
+    s = params.block_size
+    b_lo, b_hi = lo // s, (hi - 1) // s
+    rows, cols = [], []
+    for bi in range(params.k):
+        for bj in range(bi, params.k):
+            if not (b_lo <= bi <= b_hi or b_lo <= bj <= b_hi):
+                continue
+            rng = rng_for(params.seed, TAG_SBM_BLOCK, bi, bj)
+            if bi == bj:
+                r, c = _triu_pairs(_skip_sample(rng, s * (s - 1) // 2, params.p), s)
+                u, v = r + bi * s, c + bi * s
+            else:
+                pos = _skip_sample(rng, s * s, params.q)
+                u, v = pos // s + bi * s, pos % s + bj * s
+            for a, b in ((u, v), (v, u)):
+                m = (a >= lo) & (a < hi)
+                rows.append(a[m] - lo)
+                cols.append(b[m])
+    n = hi - lo
+    r = np.concatenate(rows) if rows else np.empty(0, dtype=np.int64)
+    c = np.concatenate(cols) if cols else np.empty(0, dtype=np.int64)
+    key = np.unique(r * np.int64(params.n) + c)
+    r, c = key // params.n, key % params.n
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=rp[1:])
+    deg = np.diff(rp).astype(np.float64)
+    return rp, c.astype(np.int32), deg, int(np.count_nonzero(deg == 0))
+
+
 # ---------------------------------------------------------------------------
 # BASELINE.json configurations
 
