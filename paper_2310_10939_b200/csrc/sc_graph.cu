@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cub/device/device_scan.cuh>
+#include <thread>
 #include <vector>
 
 #include "sc_common.cuh"
@@ -373,6 +374,31 @@ static int64_t sell_order(const int64_t *rp, int64_t n, std::vector<int32_t> &pe
     return n_sell;
 }
 
+// min / max of the column array; the scan is host-memory-bandwidth bound, so large arrays
+// are split over up to 8 threads
+static void col_minmax(const int32_t *col, int64_t nnz, int32_t &mn, int32_t &mx) {
+    mn = mx = 0;
+    if (nnz <= 0) return;
+    auto scan = [col](int64_t lo, int64_t hi, int32_t *omn, int32_t *omx) {
+        int32_t a = col[lo], b = col[lo];
+        for (int64_t j = lo; j < hi; ++j) {
+            a = std::min(a, col[j]);
+            b = std::max(b, col[j]);
+        }
+        *omn = a;
+        *omx = b;
+    };
+    const int nt = nnz > (int64_t(1) << 22) ? 8 : 1;
+    std::vector<int32_t> a(nt), b(nt);
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t)
+        th.emplace_back(scan, nnz * t / nt, nnz * (t + 1) / nt, &a[t], &b[t]);
+    scan(0, nnz / nt, &a[0], &b[0]);
+    for (auto &x : th) x.join();
+    mn = *std::min_element(a.begin(), a.end());
+    mx = *std::max_element(b.begin(), b.end());
+}
+
 static int grid_for(const sc_graph *g, int64_t n, int tpb) {
     int64_t want = (n + tpb - 1) / tpb;
     int64_t cap = (int64_t)std::max(g->sm_count, 1) * 8;
@@ -409,13 +435,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         for (int64_t i = 0; i < n; ++i) mono &= row_ptr[i + 1] >= row_ptr[i];
         for (int64_t i = 0; i < n; ++i) dok &= (deg[i] > 0.0) & (deg[i] < 1e308);
         int32_t cmin = 0, cmax = 0;
-        if (nnz) {
-            cmin = cmax = col[0];
-            for (int64_t j = 0; j < nnz; ++j) {
-                cmin = std::min(cmin, col[j]);
-                cmax = std::max(cmax, col[j]);
-            }
-        }
+        col_minmax(col, nnz, cmin, cmax);
         for (int64_t i = 0; !mono && i < n; ++i)
             SC_REQUIRE(row_ptr[i + 1] >= row_ptr[i], SC_E_RANGE, "row_ptr decreases at %lld",
                        (long long)i);
@@ -461,6 +481,13 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         sc_graph_destroy(g);
         return code;
     };
+    {
+        cudaMemPool_t pool;  // keep freed graph memory in the pool for the next graph
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) {
         fail(SC_E_CUDA, "stream/event creation failed");
@@ -473,18 +500,18 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     double *t_val = nullptr, *t_deg = nullptr;
     void *t_cub = nullptr;
     auto free_tmp = [&]() {
-        cudaFree(t_rp);
-        cudaFree(t_col);
-        cudaFree(t_val);
-        cudaFree(t_deg);
-        cudaFree(t_sizes);
-        cudaFree(t_cub);
+        if (t_rp) cudaFreeAsync(t_rp, s);
+        if (t_col) cudaFreeAsync(t_col, s);
+        if (t_val) cudaFreeAsync(t_val, s);
+        if (t_deg) cudaFreeAsync(t_deg, s);
+        if (t_sizes) cudaFreeAsync(t_sizes, s);
+        if (t_cub) cudaFreeAsync(t_cub, s);
     };
-    cudaError_t e = cudaMalloc(&t_rp, (size_t)(n + 1) * 8);
-    if (!e) e = cudaMalloc(&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4);
-    if (!e && !unit) e = cudaMalloc(&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8);
-    if (!e) e = cudaMalloc(&t_deg, (size_t)n * 8);
-    if (!e) e = cudaMalloc(&t_sizes, (size_t)(g->nslices + 1) * 8);
+    cudaError_t e = cudaMallocAsync((void **)&t_rp, (size_t)(n + 1) * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4, s);
+    if (!e && !unit) e = cudaMallocAsync((void **)&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&t_deg, (size_t)n * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&t_sizes, (size_t)(g->nslices + 1) * 8, s);
     if (e) {
         free_tmp();
         fail(e == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA, "staging allocation: %s",
@@ -499,7 +526,8 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         (st = dmalloc(g, (void **)&g->d_x0, (size_t)n * 8)) ||
         (st = dmalloc(g, (void **)&g->d_x[0], (size_t)n * 8)) ||
         (st = dmalloc(g, (void **)&g->d_x[1], (size_t)n * 8)) ||
-        (st = dmalloc(g, (void **)&g->d_tmp, (size_t)n * 8))) {
+        (st = dmalloc(g, (void **)&g->d_tmp, (size_t)n * 8)) ||
+        (st = dmalloc(g, (void **)&g->d_f_orig, (size_t)n * 8))) {
         free_tmp();
         return cleanup(st);
     }
@@ -539,7 +567,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if (!e)
         e = cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, t_sizes, g->d_slice_ptr,
                                           g->nslices + 1, s);
-    if (!e) e = cudaMalloc(&t_cub, std::max<size_t>(cub_bytes, 16));
+    if (!e) e = cudaMallocAsync(&t_cub, std::max<size_t>(cub_bytes, 16), s);
     if (!e)
         e = cub::DeviceScan::ExclusiveSum(t_cub, cub_bytes, t_sizes, g->d_slice_ptr,
                                           g->nslices + 1, s);
@@ -732,7 +760,9 @@ void sc_graph_destroy(sc_graph *g) {
     void *ps[] = {g->d_perm, g->d_iperm, g->d_slice_ptr, g->d_col, g->d_val, g->d_wide_ptr,
                   g->d_wcol, g->d_wval, g->d_deg, g->d_isd, g->d_x0, g->d_x[0], g->d_x[1],
                   g->d_z[0], g->d_tmp, g->d_f_orig};
-    for (void *p : ps) cudaFree(p);
+    for (void *p : ps)
+        cudaFree(p);
+    if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
     if (g->stream) cudaStreamDestroy(g->stream);

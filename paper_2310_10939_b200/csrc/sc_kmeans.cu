@@ -162,7 +162,9 @@ __global__ void k_seq_summarize(SegView v, SeqWork w, const int64_t *__restrict_
     }
 }
 
-// one warp per segment: approximate chunk starts -> predicted grid per chunk
+// one warp per segment: approximate chunk starts -> predicted grid per chunk.  Chunk data
+// are read 256 at a time (8 independent loads per lane) so the walk pays one memory latency
+// per 256 chunks.
 __global__ void k_seq_predict(SegView v, SeqWork w) {
     const int lane = threadIdx.x & 31;
     const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -170,26 +172,35 @@ __global__ void k_seq_predict(SegView v, SeqWork w) {
     const int64_t c0 = v.cofs[s], c1 = v.cofs[s + 1];
     double carry = 0.0;
     const double lo_f = 1.0 - 1.0 / 1048576.0, hi_f = 1.0 + 1.0 / 1048576.0;
-    for (int64_t g = c0; g < c1; g += 32) {
-        const int64_t c = g + lane;
-        const double A = c < c1 ? w.A[c] : 0.0;
-        double incl = A;
+    for (int64_t blk = c0; blk < c1; blk += 256) {
+        double A[8], V[8];
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += o;
+        for (int t = 0; t < 8; ++t) {
+            const int64_t c = blk + 32 * t + lane;
+            A[t] = c < c1 ? w.A[c] : 0.0;
+            V[t] = c < c1 ? w.vmax[c] : 0.0;
         }
-        const double P = carry + (incl - A);
-        if (c < c1) {
-            int kp = kNoGrid;
-            const double plo = P * lo_f, phi = (P + A + w.vmax[c]) * hi_f;
-            if (plo >= 2.2250738585072014e-308) {
-                const Grid a = grid_of(plo), b = grid_of(phi);
-                if (a.k == b.k) kp = a.k;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            double incl = A[t];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const double o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
             }
-            w.kpred[c] = kp;
+            const double P = carry + (incl - A[t]);
+            const int64_t c = blk + 32 * t + lane;
+            if (c < c1) {
+                int kp = kNoGrid;
+                const double plo = P * lo_f, phi = (P + A[t] + V[t]) * hi_f;
+                if (plo >= 2.2250738585072014e-308) {
+                    const Grid ga = grid_of(plo), gb = grid_of(phi);
+                    if (ga.k == gb.k) kp = ga.k;
+                }
+                w.kpred[c] = kp;
+            }
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
 }
 
@@ -219,11 +230,24 @@ __global__ void k_seq_chunkmap(SegView v, SeqWork w, const int64_t *__restrict__
     }
 }
 
-// one warp per segment: exact composition of the chunk maps (see sc_seqsum.cuh)
-__global__ void k_seq_compose(SegView v, SeqWork w) {
-    const int lane = threadIdx.x & 31;
-    const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+// one warp per segment: exact composition of the chunk maps (see sc_seqsum.cuh).  Each
+// warp stages 256 chunks' maps in its slice of shared memory (one memory latency per 256
+// chunks), then advances up to 32 chunks per step; a chunk whose exact start contradicts its
+// prediction is stepped element by element.
+constexpr int kMetaBlk = 256;
+constexpr int kComposeWarps = 4;
+constexpr size_t kComposeSmem = (size_t)kComposeWarps * kMetaBlk * (8 + 8 + 8 + 4);
+
+__global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, SeqWork w) {
+    extern __shared__ unsigned char cm_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int s = blockIdx.x * kComposeWarps + wib;
     if (s >= v.S || !seg_on(v, s)) return;
+    int64_t *sq0 = reinterpret_cast<int64_t *>(cm_raw) + wib * kMetaBlk;
+    int64_t *sq1 = reinterpret_cast<int64_t *>(cm_raw) + (kComposeWarps + wib) * kMetaBlk;
+    double *svm = reinterpret_cast<double *>(cm_raw) + (2 * kComposeWarps + wib) * kMetaBlk;
+    int32_t *skp = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(cm_raw) +
+                                               3 * kComposeWarps * kMetaBlk) + wib * kMetaBlk;
     const int64_t c0 = v.cofs[s], c1 = v.cofs[s + 1];
     double run = 0.0;
     if (w.neg[s]) {
@@ -241,17 +265,33 @@ __global__ void k_seq_compose(SegView v, SeqWork w) {
         if (lane == 0) w.total[s] = run;
         return;
     }
-    int64_t c = c0;
+    int64_t c = c0, blk = -1, blk_end = -1;
     while (c < c1) {
+        if (c >= blk_end) {
+            blk = c;
+            blk_end = min(c + kMetaBlk, c1);
+            __syncwarp();
+            for (int t = lane; t < kMetaBlk; t += 32) {
+                const int64_t cc = blk + t;
+                if (cc < blk_end) {
+                    sq0[t] = w.q0[cc];
+                    sq1[t] = w.q1[cc];
+                    svm[t] = w.vmax[cc];
+                    skp[t] = w.kpred[cc];
+                }
+            }
+            __syncwarp();
+        }
         const Grid g = grid_of(run);
         const int64_t S0 = (int64_t)to_units(run, g.k);
         const int64_t cl = c + lane;
+        const bool valid = cl < blk_end;
         bool ok = false;
         PMap m = pmap_id();
         double vmu = 0.0;
-        if (cl < c1 && g.top == (int64_t(1) << 53) && w.kpred[cl] == g.k) {
-            m = PMap{w.q0[cl], w.q1[cl]};
-            vmu = to_units(w.vmax[cl], g.k);
+        if (valid && g.top == (int64_t(1) << 53) && skp[cl - blk] == g.k) {
+            m = PMap{sq0[cl - blk], sq1[cl - blk]};
+            vmu = to_units(svm[cl - blk], g.k);
             ok = true;
         }
         const PMap excl = warp_exclusive(warp_scan_pmap(m));
@@ -260,18 +300,18 @@ __global__ void k_seq_compose(SegView v, SeqWork w) {
             const int64_t qmax = max(m.i0, m.i1);
             ok = (double)(g.top - Sl - qmax) >= vmu && Sl + qmax <= g.top;
         }
-        const unsigned okm = __ballot_sync(0xffffffffu, ok || cl >= c1);
-        const int L = okm == 0xffffffffu ? 32 : __ffs(~okm) - 1;  // first lane to step
-        if (lane < L && cl < c1) w.cstart[cl] = from_units(Sl, g.k);
-        const int nadv = min(L, (int)(c1 - c));
+        const unsigned badm = __ballot_sync(0xffffffffu, valid && !ok);
+        const unsigned valm = __ballot_sync(0xffffffffu, valid);
+        const int Lb = badm ? __ffs(badm) - 1 : 32;   // first chunk to step
+        const int Le = __popc(valm);                  // valid lanes form a prefix
+        const int nadv = min(Lb, Le);
+        if (lane < nadv) w.cstart[cl] = from_units(Sl, g.k);
         if (nadv > 0) {
-            // running value at the start of chunk c + nadv
-            const int src = nadv - 1;
-            const int64_t Send = __shfl_sync(0xffffffffu, pmap_apply(m, Sl), src);
+            const int64_t Send = __shfl_sync(0xffffffffu, pmap_apply(m, Sl), nadv - 1);
             run = from_units(Send, g.k);
             c += nadv;
         }
-        if (L < 32 && c < c1) {
+        if (Lb < Le) {
             // step chunk c element by element
             if (lane == 0) w.cstart[c] = run;
             double a[kSeqPerLane];
@@ -495,14 +535,17 @@ __global__ void __launch_bounds__(1024) k_repair(const double *__restrict__ x, i
     if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&changed[r], ch);
 }
 
+// sort keys for the still-active restarts only: slot s = s-th active restart (act[s]),
+// key = s*k + label, value = the point (a stable sort then keeps point-index order inside
+// every (restart, cluster) segment -- the np.add.at order)
 __global__ void k_make_keys(int64_t n, int k, const int32_t *__restrict__ lab,
-                            int32_t *__restrict__ keys, double *__restrict__ vals,
-                            const double *__restrict__ x, int R) {
-    const int64_t tot = (int64_t)R * n;
+                            const int32_t *__restrict__ act, int nact, int32_t *__restrict__ keys,
+                            double *__restrict__ vals, const double *__restrict__ x) {
+    const int64_t tot = (int64_t)nact * n;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = t / n, j = t - r * n;
-        keys[t] = (int32_t)(r * k + lab[t]);
+        const int64_t s = t / n, j = t - s * n;
+        keys[t] = (int32_t)(s * k + lab[(int64_t)act[s] * n + j]);
         vals[t] = x[j];
     }
 }
@@ -550,13 +593,13 @@ __global__ void k_chunk_offsets(int S, const int64_t *__restrict__ seg, int64_t 
 }
 
 // means = ordered sum / count (cluster_means, kmeans.py:86-93); empty clusters keep 0
-__global__ void k_seg_means(int rk, int k, const int64_t *__restrict__ seg,
-                            const double *__restrict__ total, const int32_t *__restrict__ active,
+__global__ void k_seg_means(int nseg, int k, const int64_t *__restrict__ seg,
+                            const double *__restrict__ total, const int32_t *__restrict__ act,
                             double *__restrict__ cen) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= rk || !active[t / k]) return;
+    if (t >= nseg) return;
     const int64_t c = seg[t + 1] - seg[t];
-    cen[t] = c > 0 ? __ddiv_rn(total[t], (double)c) : 0.0;
+    cen[(int64_t)act[t / k] * k + t % k] = c > 0 ? __ddiv_rn(total[t], (double)c) : 0.0;
 }
 
 // kmeans_cost in numpy einsum("ij,ij->") order (sc_oracle.c orc_einsum_sumsq): one CTA
@@ -616,10 +659,12 @@ __global__ void k_gather_centers(const double *__restrict__ x, const int64_t *__
 }
 
 template <typename T>
-static int32_t grow(T **p, size_t count) {
-    if (*p) cudaFree(*p);
+static int32_t grow(T **p, size_t count, cudaStream_t s) {
+    // stream-ordered allocations from the device's default pool (kept warm, see km_init):
+    // repeated clusterings reuse the pool instead of paying cudaMalloc/cudaFree each time
+    if (*p) cudaFreeAsync(*p, s);
     *p = nullptr;
-    cudaError_t e = cudaMalloc((void **)p, std::max<size_t>(count, 1) * sizeof(T));
+    cudaError_t e = cudaMallocAsync((void **)p, std::max<size_t>(count, 1) * sizeof(T), s);
     if (e != cudaSuccess)
         return fail(e == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA, "cudaMalloc: %s",
                     cudaGetErrorString(e));
@@ -636,42 +681,42 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     const int64_t nch = (int64_t)R * ((n + kSeqChunk - 1) / kSeqChunk) + (int64_t)R * k + 1;
     const int64_t S = (int64_t)R * k + 1;
     int32_t st;
-    if ((st = grow(&km->d_best, (size_t)R * n))) return st;
-    if ((st = grow(&km->d_lab[0], (size_t)R * n))) return st;
-    if ((st = grow(&km->d_lab[1], (size_t)R * n))) return st;
-    if ((st = grow(&km->d_keys, (size_t)R * n))) return st;
-    if ((st = grow(&km->d_keys_alt, (size_t)R * n))) return st;
-    if ((st = grow(&km->d_vals, (size_t)R * n))) return st;
-    if ((st = grow(&km->d_vals_alt, (size_t)R * n))) return st;
-    if ((st = grow(&km->d_chosen, (size_t)R * k))) return st;
-    if ((st = grow(&km->d_u, (size_t)R * k))) return st;
-    if ((st = grow(&km->d_start, (size_t)R))) return st;
-    if ((st = grow(&km->d_degen, (size_t)R))) return st;
-    if ((st = grow(&km->d_cen, (size_t)R * k))) return st;
-    if ((st = grow(&km->d_cnt, (size_t)R * k))) return st;
-    if ((st = grow(&km->d_seg, (size_t)S))) return st;
-    if ((st = grow(&km->d_part, (size_t)R * nbuf * 2))) return st;
-    if ((st = grow(&km->d_cost, (size_t)R))) return st;
-    if ((st = grow(&km->d_changed, (size_t)R))) return st;
-    if ((st = grow(&km->d_active, (size_t)R))) return st;
-    if ((st = grow(&km->d_empty, (size_t)R))) return st;
-    if ((st = grow(&km->d_A, (size_t)nch))) return st;
-    if ((st = grow(&km->d_vmax, (size_t)nch))) return st;
-    if ((st = grow(&km->d_cstart, (size_t)nch))) return st;
-    if ((st = grow(&km->d_kpred, (size_t)nch))) return st;
-    if ((st = grow(&km->d_q0, (size_t)nch))) return st;
-    if ((st = grow(&km->d_q1, (size_t)nch))) return st;
-    if ((st = grow(&km->d_total, (size_t)S))) return st;
-    if ((st = grow(&km->d_neg, (size_t)S))) return st;
-    if ((st = grow(&km->d_cofs, (size_t)S + 1))) return st;
-    if ((st = grow(&km->d_nchunks, 1))) return st;
-    if ((st = grow(&km->d_round_on, (size_t)R))) return st;
-    if ((st = grow(&km->d_on, (size_t)R))) return st;
-    if ((st = grow(&km->d_segkpp, (size_t)R + 1))) return st;
+    if ((st = grow(&km->d_best, (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_lab[0], (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_lab[1], (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_keys, (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_keys_alt, (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_vals, (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_vals_alt, (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_chosen, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_u, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_start, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_degen, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_cen, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_cnt, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_seg, (size_t)S, km->stream))) return st;
+    if ((st = grow(&km->d_part, (size_t)R * nbuf * 2, km->stream))) return st;
+    if ((st = grow(&km->d_cost, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_changed, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_active, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_empty, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_A, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_vmax, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_cstart, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_kpred, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_q0, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_q1, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_total, (size_t)S, km->stream))) return st;
+    if ((st = grow(&km->d_neg, (size_t)S, km->stream))) return st;
+    if ((st = grow(&km->d_cofs, (size_t)S + 1, km->stream))) return st;
+    if ((st = grow(&km->d_nchunks, 1, km->stream))) return st;
+    if ((st = grow(&km->d_round_on, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_on, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_segkpp, (size_t)R + 1, km->stream))) return st;
     size_t need = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, need, km->d_keys, km->d_keys_alt, km->d_vals,
                                     km->d_vals_alt, (int64_t)R * n, 0, 31, km->stream);
-    if ((st = grow((unsigned char **)&km->d_cub, need))) return st;
+    if ((st = grow((unsigned char **)&km->d_cub, need, km->stream))) return st;
     km->cub_bytes = need;
     km->cap_r = R;
     km->cap_k = k;
@@ -702,8 +747,15 @@ static int32_t km_init(int device, int64_t n, sc_kmeans **out) {
     km->device = device;
     km->n = n;
     cudaDeviceGetAttribute(&km->sm_count, cudaDevAttrMultiProcessorCount, device);
+    // keep freed workspace memory in the device pool across contexts (repeated clusterings)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     cudaError_t e = cudaStreamCreateWithFlags(&km->stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMalloc(&km->d_x, (size_t)n * 8);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&km->d_x, (size_t)n * 8, km->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(km->stream);
     if (e != cudaSuccess) {
         sc_kmeans_destroy(km);
         return fail(SC_E_CUDA, "k-means context: %s", cudaGetErrorString(e));
@@ -753,8 +805,12 @@ void sc_kmeans_destroy(sc_kmeans *km) {
                     km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
                     km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
                     km->d_segkpp};
-    for (void *p : ptrs) cudaFree(p);
-    if (km->stream) cudaStreamDestroy(km->stream);
+    for (void *p : ptrs)
+        if (p) cudaFreeAsync(p, km->stream);
+    if (km->stream) {
+        cudaStreamSynchronize(km->stream);
+        cudaStreamDestroy(km->stream);
+    }
     delete km;
 }
 
@@ -822,7 +878,7 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
         k_seq_summarize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
         k_seq_predict<<<gs, 256, 0, s>>>(v, w);
         k_seq_chunkmap<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
-        k_seq_compose<<<gs, 256, 0, s>>>(v, w);
+        k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(v, w);
         k_kpp_search<<<gs, 256, 0, s>>>(v, w, n, k, i, km->d_u, km->d_chosen, km->d_on,
                                          km->d_degen);
     }
@@ -876,11 +932,9 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     vm.seg_off = km->d_seg;
     vm.cofs = km->d_cofs;
     vm.S = rk;
-    vm.on = km->d_active;
-    vm.on_div = k;
+    vm.on = nullptr;  // segments are built for active restarts only
+    vm.on_div = 1;
     const SeqWork wm = seq_work(km);
-    const int gwm = grid_1d(km, ((int64_t)R * n / kSeqChunk + rk) * 32, 256);
-    const int gsm = (rk * 32 + 255) / 256;
     const bool prof = getenv("SC_KMEANS_PROFILE") != nullptr;
     cudaEvent_t pe[5];
     double pacc[4] = {0, 0, 0, 0};
@@ -891,7 +945,14 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         for (int r = 0; r < R; ++r) nact += active[r];
         if (!nact) break;
         const int nxt = cur ^ 1;
+        std::vector<int32_t> act;
+        for (int r = 0; r < R; ++r)
+            if (active[r]) act.push_back(r);
+        const int nseg = nact * k;
+        int end_bit = 1;
+        while ((1ll << end_bit) < (long long)nseg) ++end_bit;
         SC_CUDA(cudaMemcpyAsync(km->d_active, active.data(), (size_t)R * 4, cudaMemcpyHostToDevice, s));
+        SC_CUDA(cudaMemcpyAsync(km->d_empty, act.data(), (size_t)nact * 4, cudaMemcpyHostToDevice, s));
         SC_CUDA(cudaMemsetAsync(km->d_cnt, 0, (size_t)rk * 4, s));
         SC_CUDA(cudaMemsetAsync(km->d_changed, 0, (size_t)R * 4, s));
         if (prof) cudaEventRecord(pe[0], s);
@@ -901,32 +962,28 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, k, km->d_cen, km->d_active,
                                               km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
                                               km->d_changed, km->d_best);
-        // inactive restarts carry their final labels forward so every restart's labels
-        // live in d_lab[nxt] (the sort below covers all restarts)
-        for (int r = 0; r < R; ++r)
-            if (!active[r])
-                SC_CUDA(cudaMemcpyAsync(km->d_lab[nxt] + (size_t)r * n, km->d_lab[cur] + (size_t)r * n,
-                                        (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
-        // np.add.at order: stable radix sort on (restart, label) keeps point-index order
-        // inside every cluster; then ordered segment sums
+        // np.add.at order: stable radix sort of the active restarts' points on
+        // (slot, label) keeps point-index order inside every cluster; then exact ordered sums
         if (prof) cudaEventRecord(pe[1], s);
-        k_make_keys<<<grid_1d(km, (int64_t)R * n, 256), 256, 0, s>>>(
-            n, k, km->d_lab[nxt], km->d_keys, km->d_vals, km->d_x, R);
+        const int64_t m = (int64_t)nact * n;
+        k_make_keys<<<grid_1d(km, m, 256), 256, 0, s>>>(n, k, km->d_lab[nxt], km->d_empty, nact,
+                                                         km->d_keys, km->d_vals, km->d_x);
         size_t tb = km->cub_bytes;
         SC_CUDA(cub::DeviceRadixSort::SortPairs(km->d_cub, tb, km->d_keys, km->d_keys_alt,
-                                                km->d_vals, km->d_vals_alt, (int64_t)R * n, 0,
-                                                end_bit, s));
-        k_seg_offsets<<<(rk + 1 + 255) / 256, 256, 0, s>>>(rk, (int64_t)R * n, km->d_keys_alt,
-                                                           km->d_seg);
+                                                km->d_vals, km->d_vals_alt, m, 0, end_bit, s));
+        k_seg_offsets<<<(nseg + 1 + 255) / 256, 256, 0, s>>>(nseg, m, km->d_keys_alt, km->d_seg);
         if (prof) cudaEventRecord(pe[2], s);
-        k_chunk_offsets<<<1, 1024, 0, s>>>(rk, km->d_seg, km->d_cofs, km->d_nchunks);
-        SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)rk * 4, s));
+        k_chunk_offsets<<<1, 1024, 0, s>>>(nseg, km->d_seg, km->d_cofs, km->d_nchunks);
+        SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)nseg * 4, s));
+        vm.S = nseg;
+        const int gwm = grid_1d(km, (m / kSeqChunk + nseg) * 32, 256);
+        const int gsm = (nseg * 32 + 255) / 256;
         k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
         k_seq_predict<<<gsm, 256, 0, s>>>(vm, wm);
         k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
-        k_seq_compose<<<gsm, 256, 0, s>>>(vm, wm);
-        k_seg_means<<<(rk + 127) / 128, 128, 0, s>>>(rk, k, km->d_seg, km->d_total, km->d_active,
-                                                     km->d_cen);
+        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(vm, wm);
+        k_seg_means<<<(nseg + 127) / 128, 128, 0, s>>>(nseg, k, km->d_seg, km->d_total, km->d_empty,
+                                                       km->d_cen);
         if (prof) cudaEventRecord(pe[3], s);
         k_cost_buf<<<gc, 256, kEinsumBuf * 8, s>>>(km->d_x, n, k, km->d_lab[nxt], km->d_cen,
                                                    km->d_active, nbuf, km->d_part);
@@ -1027,7 +1084,7 @@ extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *se
         k_seq_summarize<<<gw, 256>>>(v, w, d_nch);
         k_seq_predict<<<gs, 256>>>(v, w);
         k_seq_chunkmap<<<gw, 256>>>(v, w, d_nch);
-        k_seq_compose<<<gs, 256>>>(v, w);
+        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem>>>(v, w);
         e = cudaDeviceSynchronize();
     }
     if (!e) e = cudaMemcpy(totals, d_tot, nseg * 8, cudaMemcpyDeviceToHost);

@@ -14,7 +14,7 @@ from paper_2310_10939_b200.pipeline import _kmeans_seed  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 g = sample_sbm(config_sbm(cfg)).graph
 T, k = (100, 10) if cfg == 2 else (50, 5)
-for rep in range(3):
+for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     t0 = time.perf_counter()
     dg = DeviceGraph(g)
     t1 = time.perf_counter()
