@@ -54,14 +54,17 @@ def parse():
 
 
 def build_config(cfg: int):
-    from paper_2310_10939_b200.generate import CONFIG_K, CONFIG_T, config_sbm, sample_dcsbm, sample_sbm
+    from paper_2310_10939_b200.generate import (CONFIG_K, CONFIG_T, config_sbm, sample_dcsbm,
+                                                sample_sbm, sample_weighted_rgg)
 
     if cfg in (1, 2, 5):
         g = sample_sbm(config_sbm(cfg)).graph
     elif cfg == 3:
         g = sample_dcsbm(4_000_000, 50, seed=0).graph
+    elif cfg == 4:
+        g = sample_weighted_rgg(10_000_000, 100, seed=0).graph
     else:
-        raise SystemExit(f"config {cfg} not wired into bench.py yet")
+        raise SystemExit(f"unknown config {cfg}")
     return g, CONFIG_T[cfg], CONFIG_K[cfg]
 
 

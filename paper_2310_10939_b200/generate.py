@@ -223,23 +223,27 @@ def sample_dcsbm(n: int, k: int, seed: int, *, alpha: float = 2.0, gamma: float 
 
 
 def sample_weighted_rgg(n: int, k: int, seed: int, *, sigma: float = 0.05, knn: int = 16,
-                        scale: float = 0.01, cell: int | None = None) -> SbmSample:
+                        scale: float = 0.01) -> SbmSample:
     """Weighted random geometric cluster graph (config 4 shape): k Gaussian centres
     Uniform[0,1]^3, sigma, each point joined to its `knn` nearest neighbours with weight
-    exp(-d^2/scale), symmetrised (union; a mutual pair is one edge).  Grid-bucketed
-    exact kNN in numpy; intended for n up to a few 1e6 on the host."""
+    exp(-d^2/scale), symmetrised as a union (a mutual pair is one edge).  Exact kNN with
+    scipy's cKDTree on all host cores.  Our construction (the reference's kNN builder is
+    brute force, unit weights and refuses n > 50,000: generate.py:178,199-200)."""
+    from scipy.spatial import cKDTree
+
     rng = rng_for(seed, TAG_RGG)
     centres = rng.random((k, 3))
     lab = rng.integers(0, k, size=n)
     pts = centres[lab] + sigma * rng.standard_normal((n, 3))
-    nb, dist2 = _grid_knn(pts, knn, cell)
+    dist, nb = cKDTree(pts).query(pts, k=knn + 1, workers=-1)
     src = np.repeat(np.arange(n, dtype=np.int64), knn)
-    dst = nb.ravel()
-    d2 = dist2.ravel()
+    dst = nb[:, 1:].ravel().astype(np.int64)
+    d2 = dist[:, 1:].ravel() ** 2
+    keep = src != dst  # duplicate points can displace self from column 0
+    src, dst, d2 = src[keep], dst[keep], d2[keep]
     a, b = np.minimum(src, dst), np.maximum(src, dst)
     key, first = np.unique(a * np.int64(n) + b, return_index=True)
-    w = np.exp(-d2[first] / scale)
-    w = np.maximum(w, np.finfo(np.float64).tiny)
+    w = np.maximum(np.exp(-d2[first] / scale), np.finfo(np.float64).tiny)
     g, dropped = from_edges(n, key // n, key % n, w, drop_isolated=True)
     planted = lab
     if dropped:
@@ -248,51 +252,3 @@ def sample_weighted_rgg(n: int, k: int, seed: int, *, sigma: float = 0.05, knn: 
         planted = planted[mask]
     return SbmSample(graph=g, planted=planted, dropped=dropped,
                      params=SbmParams(n=n, k=1, p=0.0, q=0.0, seed=seed))
-
-
-def _grid_knn(pts: np.ndarray, knn: int, cell: int | None):
-    """Exact kNN by scanning the 27 neighbouring grid cells, widening where needed."""
-    n = pts.shape[0]
-    lo = pts.min(axis=0)
-    span = np.maximum(pts.max(axis=0) - lo, 1e-12)
-    g = cell or max(1, int(round((n / (2.0 * knn)) ** (1.0 / 3.0))))
-    idx3 = np.minimum(((pts - lo) / span * g).astype(np.int64), g - 1)
-    cid = (idx3[:, 0] * g + idx3[:, 1]) * g + idx3[:, 2]
-    order = np.argsort(cid, kind="stable")
-    cstart = np.searchsorted(cid[order], np.arange(g**3 + 1))
-    best_i = np.full((n, knn), -1, dtype=np.int64)
-    best_d = np.full((n, knn), np.inf)
-    for cx in range(g):
-        for cy in range(g):
-            for cz in range(g):
-                c = (cx * g + cy) * g + cz
-                mine = order[cstart[c]:cstart[c + 1]]
-                if mine.size == 0:
-                    continue
-                ring = 1
-                while True:
-                    cand = []
-                    for dx in range(-ring, ring + 1):
-                        for dy in range(-ring, ring + 1):
-                            for dz in range(-ring, ring + 1):
-                                x, y, z = cx + dx, cy + dy, cz + dz
-                                if 0 <= x < g and 0 <= y < g and 0 <= z < g:
-                                    cc = (x * g + y) * g + z
-                                    cand.append(order[cstart[cc]:cstart[cc + 1]])
-                    cand = np.concatenate(cand)
-                    if cand.size > knn or ring >= g:
-                        break
-                    ring += 1
-                diff = pts[mine][:, None, :] - pts[cand][None, :, :]
-                d2 = np.einsum("ijk,ijk->ij", diff, diff)
-                d2[mine[:, None] == cand[None, :]] = np.inf
-                kk = min(knn, cand.size - 1)
-                part = np.argpartition(d2, kk - 1, axis=1)[:, :kk]
-                pd = np.take_along_axis(d2, part, axis=1)
-                srt = np.argsort(pd, axis=1)
-                best_i[mine, :kk] = np.take_along_axis(cand[part], srt, axis=1)
-                best_d[mine, :kk] = np.take_along_axis(pd, srt, axis=1)
-    # points whose ring-1 candidates were not provably exact are tolerated: the graph is a
-    # synthetic stand-in; its construction (not exactness of kNN) is what DESIGN.md states
-    best_i[best_i < 0] = np.where(best_i < 0)[0]
-    return best_i, best_d

@@ -16,7 +16,9 @@ cfg = 2
 if "--cfg" in sys.argv:
     cfg = int(sys.argv[sys.argv.index("--cfg") + 1])
 t = time.time()
-g = sample_sbm(config_sbm(cfg)).graph
+import bench  # noqa: E402
+
+g, _, _ = bench.build_config(cfg)
 print(f"graph n={g.n} nnz={g.nnz} in {time.time()-t:.1f}s", flush=True)
 dg = DeviceGraph(g)
 dg.sample_irwin_hall(0)
