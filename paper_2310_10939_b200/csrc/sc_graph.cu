@@ -62,7 +62,8 @@ int32_t fail(int32_t code, const char *fmt, ...) {
 
 constexpr int kSlice = 32;         // rows per slice (one per lane)
 constexpr int kSigma = 4096;       // sorting window (rows)
-constexpr int kSellMax = 256;      // longer rows are "wide" rows
+constexpr int kSellMax = 256;      // longer rows are laid out first, globally length-sorted
+constexpr int kExtreme = kSellMax;  // longer rows ("wide") get one warp each
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry of a slice
 constexpr int kStepTPB = 256;      // 8 warps per CTA
 constexpr int kUnroll = 8;         // slice steps in flight per lane
@@ -94,41 +95,64 @@ __device__ __forceinline__ void row_epilogue(const StepArgs &a, int64_t r, doubl
     a.z_out[a.col_offset + r] = SYM ? __dmul_rn(sc, y) : __ddiv_rn(y, sc);
 }
 
+// Wide rows (> kExtreme entries): one warp per row.  The warp gathers 128 products per
+// step into its double-buffered shared-memory slot and lane 0 adds them strictly in order
+// (the scipy order) while the next 128 gathers are already in flight.
+constexpr int kWideBatch = 128;
+
+template <bool UNIT, bool SYM>
+__global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
+    __shared__ double wbuf[kStepTPB / 32][2][kWideBatch];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t w = (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
+    if (w >= a.n_wide) return;
+    const int64_t r = a.n_sell + w;
+    const double xr = __ldcs(a.x_in + r), sc = __ldcs(a.scale + r);
+    const int64_t lo = a.wide_ptr[w], hi = a.wide_ptr[w + 1];
+    double *buf0 = wbuf[warp][0], *buf1 = wbuf[warp][1];
+    auto gather = [&](int64_t base, double (&p)[kWideBatch / 32]) {
+#pragma unroll
+        for (int q = 0; q < kWideBatch / 32; ++q) {
+            const int64_t j = base + 32 * q + lane;
+            p[q] = 0.0;
+            if (j < hi) {
+                const double zv = __ldg(a.z_in + __ldcs(a.wcol + j));
+                p[q] = UNIT ? zv : __dmul_rn(__ldcs(a.wval + j), zv);
+            }
+        }
+    };
+    double p[kWideBatch / 32];
+    gather(lo, p);
+#pragma unroll
+    for (int q = 0; q < kWideBatch / 32; ++q) buf0[32 * q + lane] = p[q];
+    double s = 0.0;
+    for (int64_t base = lo; base < hi; base += kWideBatch) {
+        __syncwarp();
+        const bool more = base + kWideBatch < hi;
+        if (more) gather(base + kWideBatch, p);  // in flight during the fold below
+        if (lane == 0) {
+            const int m = (int)(hi - base < kWideBatch ? hi - base : kWideBatch);
+            for (int t = 0; t < m; ++t) s = __dadd_rn(s, buf0[t]);
+        }
+        __syncwarp();
+        if (more) {
+#pragma unroll
+            for (int q = 0; q < kWideBatch / 32; ++q) buf1[32 * q + lane] = p[q];
+        }
+        double *tb = buf0;
+        buf0 = buf1;
+        buf1 = tb;
+    }
+    if (lane == 0) row_epilogue<SYM>(a, r, s, xr, sc);
+}
+
 template <bool UNIT, bool SYM>
 __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    if ((int)blockIdx.x < a.wide_blocks) {
-        // ---- wide rows: one warp per row, in-order fold through shuffles
-        const int64_t w = (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
-        if (w >= a.n_wide) return;
-        const int64_t r = a.n_sell + w;
-        const double xr = __ldcs(a.x_in + r), sc = __ldcs(a.scale + r);
-        const int64_t lo = a.wide_ptr[w], hi = a.wide_ptr[w + 1];
-        double s = 0.0;
-        for (int64_t base = lo; base < hi; base += 32 * 4) {
-            double p[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int64_t j = base + 32 * q + lane;
-                p[q] = 0.0;
-                if (j < hi) {
-                    const double zv = __ldg(a.z_in + __ldcs(a.wcol + j));
-                    p[q] = UNIT ? zv : __dmul_rn(__ldcs(a.wval + j), zv);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int64_t jb = base + 32 * q;
-                const int m = (int)(hi - jb < 32 ? hi - jb : 32);
-                for (int t = 0; t < m; ++t) s = __dadd_rn(s, __shfl_sync(0xffffffffu, p[q], t));
-            }
-        }
-        if (lane == 0) row_epilogue<SYM>(a, r, s, xr, sc);
-        return;
-    }
     // ---- SELL slices: one warp per slice, one lane per row
-    const int64_t sl = (int64_t)(blockIdx.x - a.wide_blocks) * (kStepTPB / 32) + warp;
+    const int64_t sl = (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
     if (sl >= a.nslices) return;
     const int64_t r = sl * kSlice + lane;
     const bool live = r < a.n_sell;
@@ -141,32 +165,38 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
     const int width = (int)((a.slice_ptr[sl + 1] - base) >> 5);
     const uint32_t *cp = a.col + base + lane;
     const double *vp = UNIT ? nullptr : a.val + base + lane;
-    double s = 0.0;
-    int t = 0;
-    for (; t + kUnroll <= width; t += kUnroll) {
-        uint32_t c[kUnroll];
-        double v[kUnroll];
+    // Software pipeline: batch i+1's column indices are loaded while batch i's z values
+    // (and weights, which do not depend on the indices) are fetched and added, so a slice
+    // pays about one memory latency per batch; the last batch is predicated, not peeled.
+    auto load_cols = [&](int t0, uint32_t (&cc)[kUnroll]) {
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
-            c[q] = __ldcs(cp + (int64_t)(t + q) * kSlice);
-            if (!UNIT) v[q] = __ldcs(vp + (int64_t)(t + q) * kSlice);
+            const int t = t0 + q;
+            cc[q] = t < width ? __ldcs(cp + (int64_t)t * kSlice) : kPad;
         }
+    };
+    uint32_t c[kUnroll];
+    load_cols(0, c);
+    double s = 0.0;
+    for (int t = 0; t < width; t += kUnroll) {
+        uint32_t cn[kUnroll];
+        const bool more = t + kUnroll < width;
+        if (more) load_cols(t + kUnroll, cn);
+        double p[kUnroll];
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
+            p[q] = 0.0;
             if (c[q] != kPad) {
                 const double zv = __ldg(a.z_in + c[q]);
-                v[q] = UNIT ? zv : __dmul_rn(v[q], zv);
+                p[q] = UNIT ? zv : __dmul_rn(__ldcs(vp + (int64_t)(t + q) * kSlice), zv);
             }
         }
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q)
-            if (c[q] != kPad) s = __dadd_rn(s, v[q]);
-    }
-    for (; t < width; ++t) {
-        const uint32_t c = __ldcs(cp + (int64_t)t * kSlice);
-        if (c != kPad) {
-            const double zv = __ldg(a.z_in + c);
-            s = __dadd_rn(s, UNIT ? zv : __dmul_rn(__ldcs(vp + (int64_t)t * kSlice), zv));
+            if (c[q] != kPad) s = __dadd_rn(s, p[q]);
+        if (more) {
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) c[q] = cn[q];
         }
     }
     if (live) row_epilogue<SYM>(a, r, s, xr, sc);
@@ -320,7 +350,8 @@ struct sc_graph {
     double *d_z[2] = {nullptr, nullptr};
     double *d_tmp = nullptr;      // n doubles: host <-> device reorder staging
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t side = nullptr;  // wide-row kernel, forked from / joined into the step stream
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_fork = nullptr, ev_join = nullptr;
     bool have_x0 = false;
     int result = -1;  // buffer index holding z_T (= f) after the last power_iterate
     cudaGraphExec_t gexec = nullptr;
@@ -343,14 +374,48 @@ static int32_t dmalloc(sc_graph *g, void **p, size_t bytes) {
     return SC_OK;
 }
 
-// Renumbering (host, O(n)): inside each window of kSigma rows, rows of length <= kSellMax
-// in decreasing length (counting sort, stable), then all wide rows in original order.
+// Renumbering (host, O(n log n) only over long rows):
+//   1. long rows (kSellMax < len <= kExtreme), globally stable-sorted by decreasing length --
+//      they come first so their (longer-running) slices are scheduled first, and global
+//      sorting packs rows of similar length into a slice (little padding);
+//   2. every window of kSigma rows: rows of length <= kSellMax in decreasing length
+//      (counting sort, stable) -- keeps the columns' locality;
+//   3. extreme rows (len > kExtreme) in original order: one warp per row.
+// Returns the number of rows laid out as SELL slices (groups 1 + 2).
 static int64_t sell_order(const int64_t *rp, int64_t n, std::vector<int32_t> &perm) {
     perm.resize((size_t)n);
     int64_t pos = 0;
+    {
+        std::vector<std::pair<int64_t, int32_t>> lng;
+        for (int64_t r = 0; r < n; ++r) {
+            const int64_t len = rp[r + 1] - rp[r];
+            if (len > kSellMax && len <= kExtreme) lng.emplace_back(-len, (int32_t)r);
+        }
+        std::stable_sort(lng.begin(), lng.end(),
+                         [](const std::pair<int64_t, int32_t> &a,
+                            const std::pair<int64_t, int32_t> &b) { return a.first < b.first; });
+        for (auto &pr : lng) perm[(size_t)pos++] = pr.second;
+    }
     std::vector<int32_t> cnt(kSellMax + 2);
-    for (int64_t w0 = 0; w0 < n; w0 += kSigma) {
-        const int64_t w1 = std::min(n, w0 + kSigma);
+    // Sorting window: kSigma rows keeps neighbouring rows (and their columns' locality)
+    // together; a heavy-tailed length distribution (max > 4x mean among SELL rows) is
+    // sorted globally instead, which packs equal lengths into slices and schedules the
+    // longest slices first.
+    int64_t sigma = kSigma;
+    {
+        int64_t cnt_rows = 0, sum = 0, mx = 0;
+        for (int64_t r = 0; r < n; ++r) {
+            const int64_t len = rp[r + 1] - rp[r];
+            if (len <= kSellMax) {
+                ++cnt_rows;
+                sum += len;
+                mx = std::max(mx, len);
+            }
+        }
+        if (cnt_rows && mx * cnt_rows > 4 * sum) sigma = n;
+    }
+    for (int64_t w0 = 0; w0 < n; w0 += sigma) {
+        const int64_t w1 = std::min(n, w0 + sigma);
         std::fill(cnt.begin(), cnt.end(), 0);
         for (int64_t r = w0; r < w1; ++r) {
             const int64_t len = rp[r + 1] - rp[r];
@@ -370,7 +435,7 @@ static int64_t sell_order(const int64_t *rp, int64_t n, std::vector<int32_t> &pe
     }
     const int64_t n_sell = pos;
     for (int64_t r = 0; r < n; ++r)
-        if (rp[r + 1] - rp[r] > kSellMax) perm[(size_t)pos++] = (int32_t)r;
+        if (rp[r + 1] - rp[r] > kExtreme) perm[(size_t)pos++] = (int32_t)r;
     return n_sell;
 }
 
@@ -489,7 +554,10 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         }
     }
     if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         fail(SC_E_CUDA, "stream/event creation failed");
         return cleanup(SC_E_CUDA);
     }
@@ -640,15 +708,34 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.hs = sign < 0 ? -0.5 : 0.5;
     constexpr int wpb = kStepTPB / 32;
     a.wide_blocks = (int)((g->n_wide + wpb - 1) / wpb);
-    const int64_t blocks = a.wide_blocks + (g->nslices + wpb - 1) / wpb;
-    if (blocks == 0) return SC_OK;
-    const dim3 grid((unsigned)blocks);
-    if (g->unit) {
-        if (sym) k_rw_step<true, true><<<grid, kStepTPB, 0, s>>>(a);
-        else k_rw_step<true, false><<<grid, kStepTPB, 0, s>>>(a);
-    } else {
-        if (sym) k_rw_step<false, true><<<grid, kStepTPB, 0, s>>>(a);
-        else k_rw_step<false, false><<<grid, kStepTPB, 0, s>>>(a);
+    const int64_t sblocks = (g->nslices + wpb - 1) / wpb;
+    // wide rows run concurrently on the side stream (fork / join through events, which a
+    // CUDA-graph capture records as parallel branches)
+    if (a.wide_blocks) {
+        SC_CUDA(cudaEventRecord(g->ev_fork, s));
+        SC_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
+        const dim3 wg((unsigned)a.wide_blocks);
+        if (g->unit) {
+            if (sym) k_rw_wide<true, true><<<wg, kStepTPB, 0, g->side>>>(a);
+            else k_rw_wide<true, false><<<wg, kStepTPB, 0, g->side>>>(a);
+        } else {
+            if (sym) k_rw_wide<false, true><<<wg, kStepTPB, 0, g->side>>>(a);
+            else k_rw_wide<false, false><<<wg, kStepTPB, 0, g->side>>>(a);
+        }
+    }
+    if (sblocks) {
+        const dim3 grid((unsigned)sblocks);
+        if (g->unit) {
+            if (sym) k_rw_step<true, true><<<grid, kStepTPB, 0, s>>>(a);
+            else k_rw_step<true, false><<<grid, kStepTPB, 0, s>>>(a);
+        } else {
+            if (sym) k_rw_step<false, true><<<grid, kStepTPB, 0, s>>>(a);
+            else k_rw_step<false, false><<<grid, kStepTPB, 0, s>>>(a);
+        }
+    }
+    if (a.wide_blocks) {
+        SC_CUDA(cudaEventRecord(g->ev_join, g->side));
+        SC_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
     }
     SC_CUDA(cudaGetLastError());
     return SC_OK;
@@ -765,6 +852,12 @@ void sc_graph_destroy(sc_graph *g) {
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+    if (g->ev_join) cudaEventDestroy(g->ev_join);
+    if (g->side) {
+        cudaStreamSynchronize(g->side);
+        cudaStreamDestroy(g->side);
+    }
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
 }
