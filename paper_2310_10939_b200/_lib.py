@@ -16,7 +16,7 @@ import numpy as np
 from .errors import DeviceError, InputError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsc_b200.so")
+LIB_PATH = os.environ.get("SC_LIB_PATH") or os.path.join(_HERE, "libsc_b200.so")
 
 SC_SYM_VARIANT = 0x1
 SC_NO_CUDA_GRAPH = 0x2

@@ -366,6 +366,8 @@ struct sc_graph {
 namespace sc {
 
 static int32_t dmalloc(sc_graph *g, void **p, size_t bytes) {
+    // plain cudaMalloc: persistent buffers live as long as the handle (the stream-ordered
+    // pool is used for the construction staging only)
     cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
     if (e != cudaSuccess)
         return fail(e == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA,
@@ -847,8 +849,7 @@ void sc_graph_destroy(sc_graph *g) {
     void *ps[] = {g->d_perm, g->d_iperm, g->d_slice_ptr, g->d_col, g->d_val, g->d_wide_ptr,
                   g->d_wcol, g->d_wval, g->d_deg, g->d_isd, g->d_x0, g->d_x[0], g->d_x[1],
                   g->d_z[0], g->d_tmp, g->d_f_orig};
-    for (void *p : ps)
-        cudaFree(p);
+    for (void *p : ps) cudaFree(p);
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
