@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--no-weighted-probe", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-block sharded (torch.distributed) path even at N=1")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="sharded path: issue every launch from the host (no CUDA graph)")
+    ap.add_argument("--pieces", type=int, default=0,
+                    help="sharded path: SpMV/all-gather pieces per step (0 = 4 if N > 1 else 1)")
     return ap.parse_args()
 
 

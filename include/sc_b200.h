@@ -133,7 +133,14 @@ int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, do
  * reads z_in[ncols] (gathered), x_in[n]; writes x_out[n], z_out[col_offset + i]. */
 int32_t sc_shard_step(sc_graph *g, const double *z_in, const double *x_in, double *x_out,
                       double *z_out, double sign, uint32_t flags, void *stream);
+/* Only renumbered rows [row_lo, row_hi) (slice aligned: multiples of 32 below the wide
+ * rows): the pieces of a pipelined multi-GPU step, each followed by its own all-gather. */
+int32_t sc_shard_step_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const double *z_in,
+                            const double *x_in, double *x_out, double *z_out, double sign,
+                            uint32_t flags, void *stream);
 /* z_out[col_offset + i] = x[i] / deg[i] (or * deg^-1/2 with SC_SYM_VARIANT) */
+int32_t sc_shard_scale_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const double *x,
+                             double *z_out, uint32_t flags, void *stream);
 int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t flags,
                        void *stream);
 /* x0 for the shard rows (global ids global_row0..), device output */

@@ -46,6 +46,7 @@ EXPORTS = (
     "sc_power_iterate", "sc_shard_step", "sc_shard_scale", "sc_shard_irwin_hall",
     "sc_kmeans_create", "sc_kmeans_create_from_graph", "sc_kmeans_destroy", "sc_kmeans_pp",
     "sc_kmeans_lloyd", "sc_seqsum", "sc_sell_order", "sc_graph_order", "sc_graph_create_ex",
+    "sc_shard_step_range", "sc_shard_scale_range",
 )
 
 _lib = None
@@ -86,6 +87,8 @@ def load() -> ctypes.CDLL:
         "sc_seqsum": ([P, i32, P, i32, P, P], i32),
         "sc_sell_order": ([P, i64, P], i32),
         "sc_graph_create_ex": ([P, P, P, P, i64, i64, i32, u32, PP], i32),
+        "sc_shard_step_range": ([P, i64, i64, P, P, P, P, f64, u32, P], i32),
+        "sc_shard_scale_range": ([P, i64, i64, P, P, u32, P], i32),
         "sc_graph_order": ([P, P], i32),
     }
     for name, (args, res) in sig.items():

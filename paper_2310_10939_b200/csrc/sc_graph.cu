@@ -81,8 +81,10 @@ struct StepArgs {
     double *x_out;
     double *z_out;             // written at col_offset + row
     int64_t n_sell, n_wide, nslices;
+    int64_t slice_lo, slice_hi; // slices of this launch (a row range of the shard)
+    int64_t wide_lo, wide_hi;   // wide rows of this launch
     int64_t col_offset;
-    int wide_blocks;           // leading CTAs that process wide rows
+    int wide_blocks;           // CTAs of the wide-row kernel
     double hs;                 // +0.5 or -0.5
 };
 
@@ -105,8 +107,8 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
     __shared__ double wbuf[kStepTPB / 32][2][kWideBatch];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int64_t w = (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
-    if (w >= a.n_wide) return;
+    const int64_t w = a.wide_lo + (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
+    if (w >= a.wide_hi) return;
     const int64_t r = a.n_sell + w;
     const double xr = __ldcs(a.x_in + r), sc = __ldcs(a.scale + r);
     const int64_t lo = a.wide_ptr[w], hi = a.wide_ptr[w + 1];
@@ -152,8 +154,8 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     // ---- SELL slices: one warp per slice, one lane per row
-    const int64_t sl = (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
-    if (sl >= a.nslices) return;
+    const int64_t sl = a.slice_lo + (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
+    if (sl >= a.slice_hi) return;
     const int64_t r = sl * kSlice + lane;
     const bool live = r < a.n_sell;
     double xr = 0.0, sc = 1.0;
@@ -687,11 +689,18 @@ static int32_t ensure_isd(sc_graph *g, cudaStream_t s) {
     return SC_OK;
 }
 
+// rows [row_lo, row_hi) of the renumbered shard; SELL boundaries must be slice-aligned
 static int32_t launch_step(const sc_graph *g, const double *z_in, const double *x_in,
                            double *x_out, double *z_out, double sign, uint32_t flags,
-                           cudaStream_t s) {
+                           cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = -1) {
     const bool sym = flags & SC_SYM_VARIANT;
+    if (row_hi < 0) row_hi = g->n;
     StepArgs a;
+    a.slice_lo = std::min(row_lo, g->n_sell) / kSlice;
+    a.slice_hi = (std::min(row_hi, g->n_sell) + kSlice - 1) / kSlice;
+    if (a.slice_hi < a.slice_lo) a.slice_hi = a.slice_lo;
+    a.wide_lo = std::max<int64_t>(row_lo - g->n_sell, 0);
+    a.wide_hi = std::max<int64_t>(row_hi - g->n_sell, 0);
     a.slice_ptr = g->d_slice_ptr;
     a.col = g->d_col;
     a.val = g->d_val;
@@ -709,8 +718,8 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.col_offset = g->col_offset;
     a.hs = sign < 0 ? -0.5 : 0.5;
     constexpr int wpb = kStepTPB / 32;
-    a.wide_blocks = (int)((g->n_wide + wpb - 1) / wpb);
-    const int64_t sblocks = (g->nslices + wpb - 1) / wpb;
+    a.wide_blocks = (int)((a.wide_hi - a.wide_lo + wpb - 1) / wpb);
+    const int64_t sblocks = (a.slice_hi - a.slice_lo + wpb - 1) / wpb;
     // wide rows run concurrently on the side stream (fork / join through events, which a
     // CUDA-graph capture records as parallel branches)
     if (a.wide_blocks) {
@@ -986,6 +995,43 @@ int32_t sc_shard_step(sc_graph *g, const double *z_in, const double *x_in, doubl
     if (flags & SC_SYM_VARIANT)
         if ((st = ensure_isd(g, s))) return st;
     return launch_step(g, z_in, x_in, x_out, z_out, sign, flags, s);
+}
+
+int32_t sc_shard_step_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const double *z_in,
+                            const double *x_in, double *x_out, double *z_out, double sign,
+                            uint32_t flags, void *stream) {
+    SC_REQUIRE(g && z_in && x_in && x_out && z_out, SC_E_INVALID, "null argument");
+    SC_REQUIRE(0 <= row_lo && row_lo <= row_hi && row_hi <= g->n, SC_E_RANGE,
+               "row range [%lld, %lld) outside [0, %lld)", (long long)row_lo, (long long)row_hi,
+               (long long)g->n);
+    SC_REQUIRE((row_lo >= g->n_sell || row_lo % kSlice == 0) &&
+                   (row_hi >= g->n_sell || row_hi % kSlice == 0),
+               SC_E_RANGE, "row range must be slice aligned (multiples of 32) below %lld",
+               (long long)g->n_sell);
+    SC_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    int32_t st;
+    if (flags & SC_SYM_VARIANT)
+        if ((st = ensure_isd(g, s))) return st;
+    return launch_step(g, z_in, x_in, x_out, z_out, sign, flags, s, row_lo, row_hi);
+}
+
+int32_t sc_shard_scale_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const double *x,
+                             double *z_out, uint32_t flags, void *stream) {
+    SC_REQUIRE(g && x && z_out, SC_E_INVALID, "null argument");
+    SC_REQUIRE(0 <= row_lo && row_lo <= row_hi && row_hi <= g->n, SC_E_RANGE, "bad row range");
+    SC_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool sym = flags & SC_SYM_VARIANT;
+    int32_t st;
+    if (sym)
+        if ((st = ensure_isd(g, s))) return st;
+    if (row_hi > row_lo)
+        k_scale<<<grid_for(g, row_hi - row_lo, 256), 256, 0, s>>>(
+            x + row_lo, (sym ? g->d_isd : g->d_deg) + row_lo, z_out, row_hi - row_lo,
+            g->col_offset + row_lo, sym);
+    SC_CUDA(cudaGetLastError());
+    return SC_OK;
 }
 
 int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t flags,

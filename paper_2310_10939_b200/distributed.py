@@ -1,20 +1,26 @@
 """Row-block sharding of the one-vector power iteration over 1/2/4/8 GPUs.
 
 One process per GPU (``torchrun``); ``torch.distributed`` is the plumbing.  Every rank owns a
-contiguous block of rows (balanced by stored entries) and its slot of the gathered vector
-z = D^-1 x; per step:
+contiguous block of rows (balanced by stored entries).  A step is pipelined over P pieces of
+each rank's rows:
 
-    local SpMV over the shard (sc_shard_step, writes the rank's own z slot)
-    all-gather of the z slots (NCCL over NVLink / NVSwitch)
+    for piece j:  local SpMV of piece j (sc_shard_step_range) -> writes piece j of z
+                  all-gather of piece j of z over NCCL, on a second stream, while the SpMV
+                  of piece j+1 runs
+    the next step waits for the last gather
+
+so only the last piece's gather is exposed.  The gathered vector is laid out piece-major --
+piece j of every rank sits in one contiguous block of W * pmax entries -- so every piece is a
+single in-place ``all_gather_into_tensor``.
 
 The device layout renumbers each shard's rows (SELL-32-sigma, ``sc_sell_order``); every rank
-learns all ranks' renumberings once and renames its columns into the global renumbered z
-space, whose slot r starts at r * n_max.  Rows are never split across ranks, so every row is
-still summed in scipy's order and the multi-GPU x_T / f are bit-identical to one GPU's.
+learns all ranks' renumberings once and renames its columns into the global z space.  Rows
+are never split across ranks, so every row is still summed in scipy's order and the
+multi-GPU x_T / f are bit-identical to one GPU's.
 
 The compute backend is pluggable: ``CudaShard`` (the product: libsc_b200.so on the rank's
 GPU) and, in the CPU tests only, an oracle backend -- the host protocol (partitioning,
-renumbering exchange, column renaming, slot layout, all-gather) is the same code.
+renumbering exchange, column renaming, piece layout, all-gathers) is the same code.
 """
 
 from __future__ import annotations
@@ -22,12 +28,14 @@ from __future__ import annotations
 import ctypes
 import json
 import os
-import time
 
 import numpy as np
 
 from . import _lib
 from .errors import InputError
+
+SELL_MAX = 256  # rows longer than this are "wide" rows (sc_graph.cu kSellMax / kExtreme)
+SLICE = 32
 
 
 # ---------------------------------------------------------------------------
@@ -57,27 +65,62 @@ def sell_order(row_ptr: np.ndarray) -> np.ndarray:
     return perm
 
 
-class ShardPlan:
-    """Row blocks, every rank's renumbering and the global renumbered z space."""
+def n_sell_rows(row_ptr: np.ndarray) -> int:
+    """Renumbered rows laid out as SELL slices (the rest are wide rows)."""
+    return int(np.count_nonzero(np.diff(np.asarray(row_ptr)) <= SELL_MAX))
 
-    def __init__(self, starts, perms):
+
+def piece_bounds(n: int, n_sell: int, pieces: int) -> np.ndarray:
+    """P contiguous pieces of a renumbered shard; boundaries inside the SELL rows are
+    slice aligned (the kernel processes whole 32-row slices)."""
+    b = np.array([j * n // pieces for j in range(pieces + 1)], dtype=np.int64)
+    inside = b < n_sell
+    b[inside] = (b[inside] // SLICE) * SLICE
+    b[0], b[-1] = 0, n
+    return np.maximum.accumulate(b)
+
+
+class ShardPlan:
+    """Row blocks, every rank's renumbering, the pieces and the global z space."""
+
+    def __init__(self, starts, perms, n_sells=None, pieces: int = 1):
         self.starts = np.asarray(starts, dtype=np.int64)
         self.world = self.starts.size - 1
         self.sizes = np.diff(self.starts)
         self.n_global = int(self.starts[-1])
-        self.n_max = int(self.sizes.max())
         self.perms = [np.asarray(p, dtype=np.int32) for p in perms]
+        self.pieces = int(pieces)
+        if n_sells is None:
+            n_sells = list(self.sizes)
+        self.n_sells = [int(v) for v in n_sells]
+        self.bounds = [piece_bounds(int(self.sizes[r]), self.n_sells[r], self.pieces)
+                       for r in range(self.world)]
+        self.pmax = max(1, int(max(np.diff(b).max() for b in self.bounds)))
+        self.n_max = int(self.sizes.max())
         # z slot of every global (original) vertex id
         slot = np.empty(self.n_global, dtype=np.int64)
         for r, p in enumerate(self.perms):
             inv = np.empty(p.size, dtype=np.int64)
-            inv[p] = np.arange(p.size, dtype=np.int64)
-            slot[self.starts[r]:self.starts[r + 1]] = r * self.n_max + inv
+            inv[p] = np.arange(p.size, dtype=np.int64)  # original local -> renumbered
+            b = self.bounds[r]
+            piece = np.searchsorted(b, inv, side="right") - 1
+            slot[self.starts[r]:self.starts[r + 1]] = (
+                piece * self.world * self.pmax + r * self.pmax + (inv - b[piece]))
         self.slot_of = slot
 
     @property
     def ncols(self) -> int:
-        return self.world * self.n_max
+        return self.pieces * self.world * self.pmax
+
+    def block(self, j: int) -> tuple[int, int]:
+        """z range of piece j (all ranks)."""
+        w = self.world * self.pmax
+        return j * w, (j + 1) * w
+
+    def own(self, j: int, rank: int) -> tuple[int, int]:
+        """z range owned by `rank` in piece j (length pmax)."""
+        lo = j * self.world * self.pmax + rank * self.pmax
+        return lo, lo + self.pmax
 
     def rename(self, col_global: np.ndarray) -> np.ndarray:
         return self.slot_of[np.asarray(col_global, dtype=np.int64)].astype(np.int32)
@@ -87,20 +130,22 @@ class ShardPlan:
 
 
 def exchange_plan(local_row_ptr: np.ndarray, starts: np.ndarray, rank: int, world: int,
-                  group=None) -> ShardPlan:
+                  group=None, pieces: int = 1) -> ShardPlan:
     """Every rank computes its renumbering and all-gathers it (padded to n_max)."""
     import torch
     import torch.distributed as dist
 
     perm = sell_order(local_row_ptr)
     n_max = int(np.diff(starts).max())
-    buf = torch.full((n_max,), -1, dtype=torch.int32)
+    buf = torch.full((n_max + 1,), -1, dtype=torch.int32)
     buf[: perm.size] = torch.from_numpy(perm)
+    buf[n_max] = n_sell_rows(local_row_ptr)
     dev = _group_device(group)
-    out = [torch.empty(n_max, dtype=torch.int32, device=dev) for _ in range(world)]
+    out = [torch.empty(n_max + 1, dtype=torch.int32, device=dev) for _ in range(world)]
     dist.all_gather(out, buf.to(dev), group=group)
     perms = [out[r][: int(starts[r + 1] - starts[r])].cpu().numpy() for r in range(world)]
-    return ShardPlan(starts, perms)
+    n_sells = [int(out[r][n_max].item()) for r in range(world)]
+    return ShardPlan(starts, perms, n_sells, pieces)
 
 
 def _group_device(group):
@@ -127,7 +172,6 @@ class CudaShard:
         L = _lib.require_device()
         self.rank, self.plan, self.device = rank, plan, device
         self.n = int(plan.sizes[rank])
-        self.off = rank * plan.n_max
         self._keep = (np.ascontiguousarray(rp, dtype=np.int64),
                       np.ascontiguousarray(col_renamed, dtype=np.int32),
                       None if val is None else np.ascontiguousarray(val, dtype=np.float64),
@@ -135,9 +179,13 @@ class CudaShard:
         rp_, col_, val_, deg_ = self._keep
         h = ctypes.c_void_p()
         _lib.check(L.sc_shard_create(_lib.ptr(rp_), _lib.ptr(col_), _lib.ptr(val_), _lib.ptr(deg_),
-                                     self.n, int(rp_[-1]), plan.ncols, self.off,
-                                     int(plan.starts[rank]), device, ctypes.byref(h)))
+                                     self.n, int(rp_[-1]), plan.ncols, 0, int(plan.starts[rank]),
+                                     device, ctypes.byref(h)))
         self.h = h
+        gi = _lib.GraphInfo()
+        _lib.check(L.sc_graph_info_get(h, ctypes.byref(gi)))
+        if self.n - gi.long_rows != plan.n_sells[rank]:
+            raise InputError("shard layout disagrees with the plan's SELL row count")
         self.torch = torch
         self.tdev = torch.device("cuda", device)
 
@@ -152,6 +200,12 @@ class CudaShard:
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.tdev).cuda_stream)
 
+    def _zout(self, z_full, j):
+        """pointer such that z_out[row] lands in this rank's slot of piece j"""
+        lo = int(self.plan.bounds[self.rank][j])
+        off = int(self.plan.own(j, self.rank)[0]) - lo
+        return ctypes.c_void_p(z_full.data_ptr() + 8 * off)
+
     def irwin_hall(self, seed, x_out):
         from .spectral import irwin_hall_key
 
@@ -159,58 +213,141 @@ class CudaShard:
         _lib.check(_lib.load().sc_shard_irwin_hall(self.h, k0, k1, ctypes.c_void_p(x_out.data_ptr()),
                                                    self._stream()))
 
-    def scale(self, x, z_full, sym=False):
-        _lib.check(_lib.load().sc_shard_scale(self.h, ctypes.c_void_p(x.data_ptr()),
-                                              ctypes.c_void_p(z_full.data_ptr()),
-                                              _lib.SC_SYM_VARIANT if sym else 0, self._stream()))
-
-    def step(self, z_in, x_in, x_out, z_out, sign=1.0, sym=False):
-        _lib.check(_lib.load().sc_shard_step(
-            self.h, ctypes.c_void_p(z_in.data_ptr()), ctypes.c_void_p(x_in.data_ptr()),
-            ctypes.c_void_p(x_out.data_ptr()), ctypes.c_void_p(z_out.data_ptr()), float(sign),
+    def scale_piece(self, j, x, z_full, sym=False):
+        b = self.plan.bounds[self.rank]
+        _lib.check(_lib.load().sc_shard_scale_range(
+            self.h, int(b[j]), int(b[j + 1]), ctypes.c_void_p(x.data_ptr()), self._zout(z_full, j),
             _lib.SC_SYM_VARIANT if sym else 0, self._stream()))
 
+    def step_piece(self, j, z_in, x_in, x_out, z_out, sign=1.0, sym=False):
+        b = self.plan.bounds[self.rank]
+        _lib.check(_lib.load().sc_shard_step_range(
+            self.h, int(b[j]), int(b[j + 1]), ctypes.c_void_p(z_in.data_ptr()),
+            ctypes.c_void_p(x_in.data_ptr()), ctypes.c_void_p(x_out.data_ptr()),
+            self._zout(z_out, j), float(sign), _lib.SC_SYM_VARIANT if sym else 0, self._stream()))
+
+    def local_z(self, z_full):
+        """this rank's z entries (renumbered local order) as a host array"""
+        b = self.plan.bounds[self.rank]
+        parts = []
+        for j in range(self.plan.pieces):
+            lo = self.plan.own(j, self.rank)[0]
+            parts.append(z_full[lo:lo + int(b[j + 1] - b[j])].cpu().numpy())
+        return np.concatenate(parts)
+
     def to_original(self, v_local):
-        """renumbered local vector -> numpy array in original local order"""
-        perm = self.plan.perms[self.rank]
+        """renumbered local vector (tensor or array) -> array in original local order"""
+        v = v_local.cpu().numpy() if hasattr(v_local, "cpu") else np.asarray(v_local)
         out = np.empty(self.n)
-        out[perm] = v_local[: self.n].cpu().numpy()
+        out[self.plan.perms[self.rank]] = v[: self.n]
         return out
 
 
-def allgather_slots(z_full, plan: ShardPlan, rank: int, group=None):
-    """In-place all-gather of the ranks' z slots (equal slot size n_max)."""
-    import torch.distributed as dist
+class PieceComm:
+    """All-gathers of z pieces.  NCCL: each piece's gather runs on a side stream after an
+    event recorded behind that piece's SpMV, overlapping the next piece's SpMV; gloo
+    (CPU tests): synchronous."""
 
-    own = z_full[rank * plan.n_max:(rank + 1) * plan.n_max]
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(z_full, own, group=group)
-    else:
-        parts = [z_full[r * plan.n_max:(r + 1) * plan.n_max] for r in range(plan.world)]
-        dist.all_gather(parts, own.clone(), group=group)
+    def __init__(self, plan: ShardPlan, rank: int, group=None):
+        import torch.distributed as dist
+
+        self.plan, self.rank, self.group = plan, rank, group
+        self.nccl = dist.get_backend(group) == "nccl"
+        if self.nccl:
+            import torch
+
+            self.torch = torch
+            self.side = torch.cuda.Stream()
+
+    def gather_piece(self, z_full, j):
+        import torch.distributed as dist
+
+        lo, hi = self.plan.block(j)
+        own_lo, own_hi = self.plan.own(j, self.rank)
+        if self.nccl:
+            torch = self.torch
+            main = torch.cuda.current_stream()
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                dist.all_gather_into_tensor(z_full[lo:hi], z_full[own_lo:own_hi], group=self.group)
+        else:
+            pm = self.plan.pmax
+            parts = [z_full[lo + r * pm:lo + (r + 1) * pm] for r in range(self.plan.world)]
+            dist.all_gather(parts, z_full[own_lo:own_hi].clone(), group=self.group)
+
+    def finish(self):
+        if self.nccl:
+            self.torch.cuda.current_stream().wait_stream(self.side)
+
+
+class ShardedPower:
+    """T pipelined steps over a shard with buffers allocated once.  With NCCL the whole
+    T-step sequence (per-piece SpMVs, side-stream all-gathers and their event fork/joins) can
+    be captured into one CUDA graph and replayed, so the pipeline is not bound by the host
+    issuing 2*P launches per step."""
+
+    def __init__(self, shard, plan: ShardPlan, rank: int, *, sign: float = 1.0,
+                 sym: bool = False, group=None):
+        self.shard, self.plan, self.rank = shard, plan, rank
+        self.sign, self.sym = sign, sym
+        n = int(plan.sizes[rank])
+        self.comm = PieceComm(plan, rank, group)
+        self.z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
+        self.x = [shard.zeros(n), shard.zeros(n)]
+        self.x0 = shard.zeros(n)
+        self.graph = None
+        self.graph_T = None
+
+    def _enqueue(self, T: int):
+        sh, plan, comm, z, x = self.shard, self.plan, self.comm, self.z, self.x
+        for j in range(plan.pieces):
+            sh.scale_piece(j, self.x0, z[0], self.sym)
+            comm.gather_piece(z[0], j)
+        comm.finish()
+        for t in range(T):
+            a, b = t & 1, (t & 1) ^ 1
+            xin = self.x0 if t == 0 else x[a]
+            for j in range(plan.pieces):
+                sh.step_piece(j, z[a], xin, x[b], z[b], self.sign, self.sym)
+                comm.gather_piece(z[b], j)
+            comm.finish()
+
+    def sample(self, seed: int):
+        self.shard.irwin_hall(seed, self.x0)
+
+    def capture(self, T: int):
+        """Record T steps (from the current x0 buffer) into a CUDA graph; NCCL only."""
+        import torch
+
+        if not self.comm.nccl:
+            raise InputError("CUDA-graph capture needs the NCCL backend")
+        self._enqueue(T)  # warm: communicator and side-stream setup outside the capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._enqueue(T)
+        torch.cuda.synchronize()
+        self.graph, self.graph_T = g, T
+
+    def run(self, T: int):
+        """T steps from x0; returns (x_T local renumbered, z space of step T)."""
+        if self.graph is not None and self.graph_T == T:
+            self.graph.replay()
+        else:
+            self._enqueue(T)
+        return (self.x0 if T == 0 else self.x[T & 1]), self.z[T & 1]
 
 
 def power_iterate_sharded(shard, plan: ShardPlan, rank: int, T: int, *, seed: int | None = 0,
                           x0_local_renumbered=None, sign: float = 1.0, sym: bool = False,
                           group=None):
-    """T steps over the shards; returns (x_T local renumbered, z_T = f local renumbered)."""
-    n = int(plan.sizes[rank])
-    z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
-    x = [shard.zeros(n), shard.zeros(n)]
-    x0 = shard.zeros(n)
+    """T steps over the shards; returns (x_T local renumbered, z space of step T)."""
+    p = ShardedPower(shard, plan, rank, sign=sign, sym=sym, group=group)
     if x0_local_renumbered is not None:
-        x0.copy_(x0_local_renumbered)
+        p.x0.copy_(x0_local_renumbered)
     else:
-        shard.irwin_hall(seed, x0)
-    off = rank * plan.n_max
-    shard.scale(x0, z[0], sym)
-    allgather_slots(z[0], plan, rank, group)
-    for t in range(T):
-        a, b = t & 1, (t & 1) ^ 1
-        shard.step(z[a], x0 if t == 0 else x[a], x[b], z[b], sign, sym)
-        allgather_slots(z[b], plan, rank, group)
-    xT = x0 if T == 0 else x[T & 1]
-    return xT, z[T & 1][off:off + n]
+        p.sample(seed)
+    return p.run(T)
 
 
 # ---------------------------------------------------------------------------
@@ -233,7 +370,7 @@ def _init_dist():
 def bench_main(args, metric: str, unit: str):
     """Weak scaling: rank r owns one config-2 sized row block (1e6 rows, 10 SBM blocks) of an
     SBM with n = N * 1e6, k = 10 N, expected in-block degree 40 and out-of-block degree 4;
-    T = 100 steps with an NCCL all-gather of z after each."""
+    T = 100 steps, each pipelined over P pieces with an NCCL all-gather per piece."""
     import torch
     import torch.distributed as dist
 
@@ -244,22 +381,29 @@ def bench_main(args, metric: str, unit: str):
     params = SbmParams(n=world * n_loc, k=10 * world, p=40 / (10**5 - 1),
                        q=4 / (world * n_loc - 10**5), seed=0)
     T = 100
+    pieces = int(getattr(args, "pieces", 0) or (4 if world > 1 else 1))
     starts = np.arange(world + 1, dtype=np.int64) * n_loc
     rp, col, deg, iso = sbm_rows(params, int(starts[rank]), int(starts[rank + 1]))
     iso_t = torch.tensor([iso], device="cuda")
     dist.all_reduce(iso_t)
     if int(iso_t.item()):
         raise InputError("isolated vertices in the scaling graph; choose another seed")
-    plan = exchange_plan(rp, starts, rank, world)
+    plan = exchange_plan(rp, starts, rank, world, pieces=pieces)
     shard = CudaShard(rp, plan.rename(col), None, deg, plan, rank, local)
     nnz_t = torch.tensor([int(rp[-1])], device="cuda", dtype=torch.int64)
     dist.all_reduce(nnz_t)
     nnz_total = int(nnz_t.item())
     stream = torch.cuda.current_stream()
+    runner = ShardedPower(shard, plan, rank)
+    use_graph = not getattr(args, "no_graph", False)
 
     def one_step():
-        return power_iterate_sharded(shard, plan, rank, T, seed=0)
+        runner.sample(0)
+        return runner.run(T)
 
+    runner.sample(0)
+    if use_graph:
+        runner.capture(T)
     for _ in range(max(args.warmup, 3)):
         one_step()
     torch.cuda.synchronize()
@@ -274,19 +418,22 @@ def bench_main(args, metric: str, unit: str):
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     tot_ms = float(ms.item())
-    # all-gather alone (NVLink): T gathers of the z space
+    # the all-gathers alone (NVLink): T steps x P pieces
     zbuf = shard.zeros(plan.ncols)
+    comm = PieceComm(plan, rank)
     torch.cuda.synchronize()
     dist.barrier()
     e0.record(stream)
     for _ in range(T):
-        allgather_slots(zbuf, plan, rank)
+        for j in range(plan.pieces):
+            comm.gather_piece(zbuf, j)
+        comm.finish()
     e1.record(stream)
     torch.cuda.synchronize()
     ag = torch.tensor([e0.elapsed_time(e1) / T], device="cuda", dtype=torch.float64)
     dist.all_reduce(ag, op=dist.ReduceOp.MAX)
     ag_ms = float(ag.item())
-    recv_bytes = (world - 1) * plan.n_max * 8
+    recv_bytes = (world - 1) * plan.pieces * plan.pmax * 8
     if rank == 0:
         value = nnz_total * T * args.steps / (tot_ms / 1e3) / 1e9
         line = {
@@ -294,11 +441,13 @@ def bench_main(args, metric: str, unit: str):
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config2 block per GPU (SBM n={params.n}, k={params.k})",
-                       "n_per_gpu": n_loc, "nnz_total": nnz_total, "T": T,
-                       "parallelism": f"row-block shards x{world}, NCCL all-gather of z per step"},
+                       "n_per_gpu": n_loc, "nnz_total": nnz_total, "T": T, "pieces": plan.pieces,
+                       "cuda_graph": use_graph,
+                       "parallelism": f"row-block shards x{world}, pipelined NCCL all-gather "
+                                      f"of z ({plan.pieces} pieces per step)"},
             "allgather": {"ms_per_step": ag_ms, "recv_bytes_per_gpu": recv_bytes,
-                          "gbs_per_gpu": recv_bytes / (ag_ms / 1e3) / 1e9},
-            "gpu_launches": args.steps * (T + 1),
+                          "gbs_per_gpu": recv_bytes / (ag_ms / 1e3) / 1e9 if world > 1 else 0.0},
+            "gpu_launches": args.steps * (1 + T * plan.pieces + plan.pieces),
         }
         print(json.dumps(line), flush=True)
     shard.close()
@@ -318,7 +467,3 @@ def gather_to_rank0(v_local_original: np.ndarray, plan: ShardPlan, rank: int, gr
     if rank != 0:
         return None
     return np.concatenate([out[r][: plan.sizes[r]].cpu().numpy() for r in range(plan.world)])
-
-
-def _now() -> float:
-    return time.perf_counter()

@@ -14,7 +14,8 @@ from paper_2310_10939_b200.generate import SbmParams, sample_sbm, sbm_rows
 
 
 class OracleShard:
-    """CPU stand-in for CudaShard (tests only): same renumbered layout, oracle arithmetic."""
+    """CPU stand-in for CudaShard (tests only): same renumbered layout and piece API, oracle
+    arithmetic."""
 
     def __init__(self, rp, col_global, val, deg, plan, rank, seed_row0):
         import torch
@@ -24,7 +25,6 @@ class OracleShard:
         perm = plan.perms[rank]
         self.perm = perm
         self.n = perm.size
-        self.off = rank * plan.n_max
         lens = np.diff(rp)[perm]
         self.rp = np.zeros(self.n + 1, dtype=np.int64)
         np.cumsum(lens, out=self.rp[1:])
@@ -42,18 +42,35 @@ class OracleShard:
         x = O.irwin_hall(self.deg_orig, seed, row0=self.row0)
         x_out.copy_(self.torch.from_numpy(x[self.perm]))
 
-    def scale(self, x, z_full, sym=False):
-        z_full[self.off:self.off + self.n] = self.torch.from_numpy(x.numpy() / self.deg)
+    def _slot(self, j):
+        lo, hi = (int(v) for v in self.plan.bounds[self.rank][j:j + 2])
+        return lo, hi, self.plan.own(j, self.rank)[0]
 
-    def step(self, z_in, x_in, x_out, z_out, sign=1.0, sym=False):
-        y, zo = O.rw_rows(self.rp, self.col, self.val, self.deg, x_in.numpy(), z_in.numpy(),
+    def scale_piece(self, j, x, z_full, sym=False):
+        lo, hi, o = self._slot(j)
+        z_full[o:o + hi - lo] = self.torch.from_numpy(x.numpy()[lo:hi] / self.deg[lo:hi])
+
+    def step_piece(self, j, z_in, x_in, x_out, z_out, sign=1.0, sym=False):
+        lo, hi, o = self._slot(j)
+        rp = self.rp[lo:hi + 1] - self.rp[lo]
+        col = self.col[self.rp[lo]:self.rp[hi]]
+        val = None if self.val is None else self.val[self.rp[lo]:self.rp[hi]]
+        y, zo = O.rw_rows(rp, col, val, self.deg[lo:hi], x_in.numpy()[lo:hi], z_in.numpy(),
                           sign=sign)
-        x_out.copy_(self.torch.from_numpy(y))
-        z_out[self.off:self.off + self.n] = self.torch.from_numpy(zo)
+        x_out[lo:hi] = self.torch.from_numpy(y)
+        z_out[o:o + hi - lo] = self.torch.from_numpy(zo)
+
+    def local_z(self, z_full):
+        parts = []
+        for j in range(self.plan.pieces):
+            lo, hi, o = self._slot(j)
+            parts.append(z_full[o:o + hi - lo].numpy())
+        return np.concatenate(parts)
 
     def to_original(self, v):
+        v = v.numpy() if hasattr(v, "numpy") else np.asarray(v)
         out = np.empty(self.n)
-        out[self.perm] = v[: self.n].numpy()
+        out[self.perm] = v[: self.n]
         return out
 
 
@@ -65,7 +82,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, graph, T, result_path):
+def _worker(rank, world, port, graph, T, result_path, pieces=1):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -77,11 +94,11 @@ def _worker(rank, world, port, graph, T, result_path):
     lrp = rp[lo:hi + 1] - rp[lo]
     lcol = col[rp[lo]:rp[hi]]
     lval = None if val is None else val[rp[lo]:rp[hi]]
-    plan = D.exchange_plan(lrp, starts, rank, world)
+    plan = D.exchange_plan(lrp, starts, rank, world, pieces=pieces)
     shard = OracleShard(lrp, lcol, lval, deg[lo:hi], plan, rank, lo)
-    xT, f = D.power_iterate_sharded(shard, plan, rank, T, seed=3)
+    xT, z = D.power_iterate_sharded(shard, plan, rank, T, seed=3)
     x_all = D.gather_to_rank0(shard.to_original(xT), plan, rank)
-    f_all = D.gather_to_rank0(shard.to_original(f), plan, rank)
+    f_all = D.gather_to_rank0(shard.to_original(shard.local_z(z)), plan, rank)
     if rank == 0:
         np.savez(result_path, x=x_all, f=f_all, starts=starts)
     dist.destroy_process_group()
@@ -97,15 +114,15 @@ def _weighted_graph(n=3000, m=30000, seed=11):
     return g
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_power_iteration_bit_exact(tmp_path, world):
+@pytest.mark.parametrize("world,pieces", [(2, 1), (3, 1), (2, 4), (3, 3)])
+def test_sharded_power_iteration_bit_exact(tmp_path, world, pieces):
     import torch.multiprocessing as mp
 
     g = _weighted_graph()
     graph = (g.row_offsets, g.col_indices.astype(np.int32), g.weights, g.degrees)
     T = 9
     out = str(tmp_path / "res.npz")
-    mp.start_processes(_worker, args=(world, _free_port(), graph, T, out), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), graph, T, out, pieces), nprocs=world,
                        join=True, start_method="spawn")
     res = np.load(out)
     x0 = O.irwin_hall(g.degrees, 3)
@@ -129,13 +146,20 @@ def test_plan_renaming_is_a_bijection():
     rng = np.random.default_rng(1)
     rp = np.concatenate([[0], np.cumsum(rng.integers(1, 300, 5000))])
     starts = D.partition_rows(rp, 4)
-    perms = [D.sell_order(rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]]) for r in range(4)]
-    plan = D.ShardPlan(starts, perms)
-    slots = plan.slot_of
-    assert np.unique(slots).size == slots.size
-    for r in range(4):
-        own = slots[starts[r]:starts[r + 1]]
-        assert own.min() == r * plan.n_max and own.max() < r * plan.n_max + plan.sizes[r]
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(4)]
+    perms = [D.sell_order(x) for x in lrps]
+    for pieces in (1, 3):
+        plan = D.ShardPlan(starts, perms, [D.n_sell_rows(x) for x in lrps], pieces)
+        slots = plan.slot_of
+        assert np.unique(slots).size == slots.size and slots.max() < plan.ncols
+        for r in range(4):
+            b = plan.bounds[r]
+            assert b[0] == 0 and b[-1] == plan.sizes[r]
+            for j in range(pieces):
+                if b[j] < plan.n_sells[r]:
+                    assert b[j] % 32 == 0
+                lo, hi = plan.own(j, r)
+                assert hi - lo == plan.pmax
 
 
 def test_sbm_rows_concatenate_to_sample_sbm():

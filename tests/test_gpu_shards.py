@@ -23,47 +23,49 @@ def _graph(n=5000, m=60000, seed=21):
     return g
 
 
-@pytest.mark.parametrize("world", [1, 3])
-def test_shards_on_one_gpu_bit_exact(world):
+@pytest.mark.parametrize("world,pieces", [(1, 1), (3, 1), (1, 3), (3, 4)])
+def test_shards_on_one_gpu_bit_exact(world, pieces):
     import torch
 
     g = _graph()
     rp, col, val, deg = g.row_offsets, g.col_indices.astype(np.int32), g.weights, g.degrees
     starts = D.partition_rows(rp, world)
-    perms = [D.sell_order(rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]]) for r in range(world)]
-    plan = D.ShardPlan(starts, perms)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(world)]
+    plan = D.ShardPlan(starts, [D.sell_order(x) for x in lrps], [D.n_sell_rows(x) for x in lrps],
+                       pieces)
     shards = []
     for r in range(world):
         lo, hi = int(starts[r]), int(starts[r + 1])
-        lrp = rp[lo:hi + 1] - rp[lo]
-        shards.append(D.CudaShard(lrp, plan.rename(col[rp[lo]:rp[hi]]), val[rp[lo]:rp[hi]],
+        shards.append(D.CudaShard(lrps[r], plan.rename(col[rp[lo]:rp[hi]]), val[rp[lo]:rp[hi]],
                                   deg[lo:hi], plan, r, 0))
     T = 12
     z = [[s.zeros(plan.ncols), s.zeros(plan.ncols)] for s in shards]
     x = [[s.zeros(s.n), s.zeros(s.n)] for s in shards]
     x0 = [s.zeros(s.n) for s in shards]
 
-    def gather(buf_index):
+    def gather(buf_index, j):
+        torch.cuda.synchronize()
         for r in range(world):
-            src = z[r][buf_index][r * plan.n_max:(r + 1) * plan.n_max]
+            lo, hi = plan.own(j, r)
             for q in range(world):
                 if q != r:
-                    z[q][buf_index][r * plan.n_max:(r + 1) * plan.n_max].copy_(src)
+                    z[q][buf_index][lo:hi].copy_(z[r][buf_index][lo:hi])
 
     for r, s in enumerate(shards):
         s.irwin_hall(5, x0[r])
-        s.scale(x0[r], z[r][0])
-    torch.cuda.synchronize()
-    gather(0)
+    for j in range(pieces):
+        for r, s in enumerate(shards):
+            s.scale_piece(j, x0[r], z[r][0])
+        gather(0, j)
     for t in range(T):
         a, b = t & 1, (t & 1) ^ 1
-        for r, s in enumerate(shards):
-            s.step(z[r][a], x0[r] if t == 0 else x[r][a], x[r][b], z[r][b])
-        torch.cuda.synchronize()
-        gather(b)
+        for j in range(pieces):
+            for r, s in enumerate(shards):
+                s.step_piece(j, z[r][a], x0[r] if t == 0 else x[r][a], x[r][b], z[r][b])
+            gather(b, j)
     torch.cuda.synchronize()
     xs = np.concatenate([s.to_original(x[r][T & 1]) for r, s in enumerate(shards)])
-    fs = np.concatenate([s.to_original(z[r][T & 1][r * plan.n_max:]) for r, s in enumerate(shards)])
+    fs = np.concatenate([s.to_original(s.local_z(z[r][T & 1])) for r, s in enumerate(shards)])
     x0_ref = O.irwin_hall(deg, 5)
     x0_dev = np.concatenate([s.to_original(x0[r]) for r, s in enumerate(shards)])
     assert np.array_equal(x0_dev, x0_ref)
@@ -72,3 +74,45 @@ def test_shards_on_one_gpu_bit_exact(world):
     assert np.array_equal(fs, f)
     for s in shards:
         s.close()
+
+
+def _nccl_world1_worker(rank, path, out):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"file://{path}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    g = _graph()
+    rp, col, val, deg = g.row_offsets, g.col_indices.astype(np.int32), g.weights, g.degrees
+    starts = D.partition_rows(rp, 1)
+    plan = D.exchange_plan(rp, starts, 0, 1, pieces=3)
+    shard = D.CudaShard(rp, plan.rename(col), val, deg, plan, 0, 0)
+    runner = D.ShardedPower(shard, plan, 0)
+    runner.sample(5)
+    runner.capture(12)
+    res = []
+    for _ in range(2):  # replay twice: the graph reads x0 and rewrites every buffer
+        xT, z = runner.run(12)
+        torch.cuda.synchronize()
+        res.append((shard.to_original(xT), shard.to_original(shard.local_z(z))))
+    np.savez(out, x1=res[0][0], f1=res[0][1], x2=res[1][0], f2=res[1][1])
+    shard.close()
+    dist.destroy_process_group()
+
+
+def test_nccl_pipeline_cuda_graph_bit_exact(tmp_path):
+    """The NCCL path end to end (world 1, 3 pieces): side-stream all-gathers and the T-step
+    sequence captured in a CUDA graph, replayed twice, bit-exact against the oracle."""
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "r.npz")
+    mp.start_processes(_nccl_world1_worker, args=(str(tmp_path / "store"), out), nprocs=1,
+                       join=True, start_method="spawn")
+    r = np.load(out)
+    g = _graph()
+    x0 = O.irwin_hall(g.degrees, 5)
+    xT, f = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, 12)
+    for i in (1, 2):
+        assert np.array_equal(r[f"x{i}"], xT)
+        assert np.array_equal(r[f"f{i}"], f)
