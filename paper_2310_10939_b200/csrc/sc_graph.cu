@@ -31,6 +31,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <cub/device/device_scan.cuh>
 #include <thread>
 #include <vector>
@@ -281,19 +282,21 @@ __global__ void k_slice_sizes(const int64_t *__restrict__ rp, const int32_t *__r
     }
 }
 
-// one thread per renumbered SELL row: copy its entries column-major into its slice
+// one thread per lane of every slice: copy the renumbered row's entries column-major into
+// its slice; lanes past n_sell in the last slice are all padding (the step kernel still
+// loads their columns, so they must never hold stale indices)
 __global__ void k_fill_sell(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                             const double *__restrict__ val, const int32_t *__restrict__ perm,
                             const int32_t *__restrict__ iperm, const int64_t *__restrict__ slice_ptr,
-                            int64_t n_sell, int64_t col_offset, int64_t n, int rename,
-                            uint32_t *__restrict__ scol, double *__restrict__ sval) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_sell;
+                            int64_t n_sell, int64_t nslices, int64_t col_offset, int64_t n,
+                            int rename, uint32_t *__restrict__ scol, double *__restrict__ sval) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nslices * kSlice;
          p += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t r = perm[p];
         const int64_t s = p / kSlice, lane = p % kSlice;
         const int64_t base = slice_ptr[s];
         const int64_t width = (slice_ptr[s + 1] - base) / kSlice;
-        const int64_t lo = rp[r], len = rp[r + 1] - lo;
+        const int32_t r = p < n_sell ? perm[p] : 0;
+        const int64_t lo = p < n_sell ? rp[r] : 0, len = p < n_sell ? rp[r + 1] - lo : 0;
         for (int64_t t = 0; t < width; ++t) {
             const int64_t dst = base + t * kSlice + lane;
             if (t < len) {
@@ -363,17 +366,118 @@ struct sc_graph {
     int64_t bytes = 0;
     bool l2_window = false;
     double *d_f_orig = nullptr;   // f in original vertex order (for the k-means context)
+    std::vector<std::pair<void *, size_t>> allocs;  // every dmalloc'd buffer (returned to the cache)
 };
 
 namespace sc {
 
+// Device buffers of graph handles come from plain cudaMalloc (persistent buffers live as
+// long as the handle; the stream-ordered pool is used for the construction staging only) and
+// go back to a small process-wide cache on destroy, so a pipeline that builds a graph per
+// call does not pay cudaMalloc/cudaFree (whose device-wide synchronisation and unmapping
+// cost up to hundreds of ms for a multi-GB graph) every time.  A buffer is cached only after
+// the handle's streams are synchronised.  SC_BUFFER_CACHE_MB caps it (default 16384, 0 = off).
+namespace {
+struct CachedBuf {
+    int device;
+    size_t bytes;
+    void *p;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBuf> g_cache;
+size_t g_cache_bytes = 0;
+
+size_t cache_cap() {
+    static size_t cap = [] {
+        const char *e = getenv("SC_BUFFER_CACHE_MB");
+        return (size_t)(e ? atoll(e) : 16384) << 20;
+    }();
+    return cap;
+}
+
+void *cache_take(int device, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_cache.size(); ++i) {
+        const CachedBuf &c = g_cache[i];
+        if (c.device == device && c.bytes >= bytes && c.bytes <= bytes + bytes / 4 + (1u << 20) &&
+            (best < 0 || c.bytes < g_cache[best].bytes))
+            best = i;
+    }
+    if (best < 0) return nullptr;
+    void *p = g_cache[best].p;
+    g_cache_bytes -= g_cache[best].bytes;
+    g_cache.erase(g_cache.begin() + best);
+    return p;
+}
+
+// frees every cached buffer of `device` (all devices if < 0); returns bytes released
+size_t cache_flush(int device) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    size_t freed = 0;
+    for (size_t i = 0; i < g_cache.size();) {
+        if (device < 0 || g_cache[i].device == device) {
+            cudaSetDevice(g_cache[i].device);
+            cudaFree(g_cache[i].p);
+            freed += g_cache[i].bytes;
+            g_cache_bytes -= g_cache[i].bytes;
+            g_cache.erase(g_cache.begin() + i);
+        } else {
+            ++i;
+        }
+    }
+    cudaSetDevice(cur);
+    return freed;
+}
+
+void cache_give(int device, void *p, size_t bytes) {
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        if (bytes <= cache_cap()) {
+            g_cache.push_back({device, bytes, p});
+            g_cache_bytes += bytes;
+            // evict oldest first
+            while (g_cache_bytes > cache_cap() && !g_cache.empty()) {
+                cudaFree(g_cache.front().p);
+                g_cache_bytes -= g_cache.front().bytes;
+                g_cache.erase(g_cache.begin());
+            }
+            return;
+        }
+    }
+    cudaFree(p);
+}
+}  // namespace
+
 static int32_t dmalloc(sc_graph *g, void **p, size_t bytes) {
-    // plain cudaMalloc: persistent buffers live as long as the handle (the stream-ordered
-    // pool is used for the construction staging only)
-    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    bytes = bytes ? bytes : 16;
+    static const bool poison = getenv("SC_DEBUG_POISON") != nullptr;  // read-before-write hunt
+    if (poison) {
+        cudaError_t e = cudaMalloc(p, bytes);
+        if (e != cudaSuccess) return fail(SC_E_OOM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        cudaMemset(*p, 0x7f, bytes);  // out-of-range indices, huge doubles
+        cudaDeviceSynchronize();
+        g->allocs.push_back({*p, bytes});
+        g->bytes += (int64_t)bytes;
+        return SC_OK;
+    }
+    if ((*p = cache_take(g->device, bytes))) {
+        g->allocs.push_back({*p, bytes});
+        g->bytes += (int64_t)bytes;
+        return SC_OK;
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation && cache_flush(g->device)) {
+        cudaGetLastError();
+        e = cudaMalloc(p, bytes);
+    }
     if (e != cudaSuccess)
         return fail(e == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA,
                     "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    g->allocs.push_back({*p, bytes});
     g->bytes += (int64_t)bytes;
     return SC_OK;
 }
@@ -661,9 +765,9 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         return cleanup(st);
     }
     if (g->n_sell)
-        k_fill_sell<<<grid_for(g, g->n_sell, 256), 256, 0, s>>>(
-            t_rp, t_col, t_val, g->d_perm, g->d_iperm, g->d_slice_ptr, g->n_sell, col_offset, n,
-            rename, g->d_col, g->d_val);
+        k_fill_sell<<<grid_for(g, g->nslices * kSlice, 256), 256, 0, s>>>(
+            t_rp, t_col, t_val, g->d_perm, g->d_iperm, g->d_slice_ptr, g->n_sell, g->nslices,
+            col_offset, n, rename, g->d_col, g->d_val);
     if (g->n_wide)
         k_fill_wide<<<(unsigned)g->n_wide, 256, 0, s>>>(t_rp, t_col, t_val, g->d_perm, g->d_iperm,
                                                         g->d_wide_ptr, g->n_sell, g->n_wide,
@@ -854,12 +958,17 @@ void sc_graph_destroy(sc_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     if (g->stream) cudaStreamSynchronize(g->stream);
+    if (g->side) cudaStreamSynchronize(g->side);
     if (g->gexec) cudaGraphExecDestroy(g->gexec);
-    void *ps[] = {g->d_perm, g->d_iperm, g->d_slice_ptr, g->d_col, g->d_val, g->d_wide_ptr,
-                  g->d_wcol, g->d_wval, g->d_deg, g->d_isd, g->d_x0, g->d_x[0], g->d_x[1],
-                  g->d_z[0], g->d_tmp, g->d_f_orig};
-    for (void *p : ps) cudaFree(p);
-    if (g->stream) cudaStreamSynchronize(g->stream);
+    // a sticky error makes the stream query fail: do not recycle buffers of a broken context
+    const bool healthy = !g->stream || cudaStreamQuery(g->stream) == cudaSuccess;
+    for (auto &a : g->allocs) {
+        if (healthy)
+            cache_give(g->device, a.first, a.second);
+        else
+            cudaFree(a.first);
+    }
+    g->allocs.clear();
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);

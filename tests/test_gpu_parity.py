@@ -222,3 +222,17 @@ def test_lloyd_exact_sums_stress(case):
     lab_o, cost_o = O.lloyd(x, k, 77)
     part = lloyd(x[:, None], k, seed=77)
     assert np.array_equal(part.labels, lab_o), case
+
+
+def test_recycled_buffers_partial_last_slice(wg, c1):
+    """Graph buffers are recycled across handles; the lanes past n in the last SELL slice
+    must be padding, not stale column indices of the previous graph (which once read out of
+    bounds).  A bigger weighted graph first, then config 1 (n = 1000: a partial slice)."""
+    for _ in range(2):
+        with DeviceGraph(wg["graph"], keep_weights=True) as dg:
+            dg.set_x0(wg["x0"])
+            dg.power_iterate(3)
+        with DeviceGraph(c1["graph"]) as dg:
+            dg.set_x0(c1["x0"])
+            xT, _ = dg.power_iterate(50, cuda_graph=False)
+            assert np.array_equal(xT, c1["xT"])

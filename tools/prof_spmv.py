@@ -20,7 +20,7 @@ import bench  # noqa: E402
 
 g, _, _ = bench.build_config(cfg)
 print(f"graph n={g.n} nnz={g.nnz} in {time.time()-t:.1f}s", flush=True)
-dg = DeviceGraph(g)
+dg = DeviceGraph(g, keep_weights=weighted)
 dg.sample_irwin_hall(0)
 for rep in range(2):
     dg.power_iterate(T, cuda_graph=False, want_x=False, want_f=False, force_weighted=weighted)
