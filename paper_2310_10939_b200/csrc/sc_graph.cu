@@ -259,6 +259,18 @@ __global__ void k_gather_perm(const double *__restrict__ in, const int32_t *__re
 
 // ---- construction kernels (once per graph) ----------------------------------------------
 
+// flag[0] = 1 if any column index is outside [0, ncols)
+__global__ void k_col_range(const int32_t *__restrict__ col, int64_t nnz, int64_t ncols,
+                            int32_t *__restrict__ flag) {
+    int bad = 0;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = __ldcs(col + j);
+        bad |= (c < 0) | ((int64_t)c >= ncols);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flag[0] = 1;
+}
+
 __global__ void k_inverse_perm(const int32_t *__restrict__ perm, int32_t *__restrict__ iperm,
                                int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -547,31 +559,6 @@ static int64_t sell_order(const int64_t *rp, int64_t n, std::vector<int32_t> &pe
     return n_sell;
 }
 
-// min / max of the column array; the scan is host-memory-bandwidth bound, so large arrays
-// are split over up to 8 threads
-static void col_minmax(const int32_t *col, int64_t nnz, int32_t &mn, int32_t &mx) {
-    mn = mx = 0;
-    if (nnz <= 0) return;
-    auto scan = [col](int64_t lo, int64_t hi, int32_t *omn, int32_t *omx) {
-        int32_t a = col[lo], b = col[lo];
-        for (int64_t j = lo; j < hi; ++j) {
-            a = std::min(a, col[j]);
-            b = std::max(b, col[j]);
-        }
-        *omn = a;
-        *omx = b;
-    };
-    const int nt = nnz > (int64_t(1) << 22) ? 8 : 1;
-    std::vector<int32_t> a(nt), b(nt);
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t)
-        th.emplace_back(scan, nnz * t / nt, nnz * (t + 1) / nt, &a[t], &b[t]);
-    scan(0, nnz / nt, &a[0], &b[0]);
-    for (auto &x : th) x.join();
-    mn = *std::min_element(a.begin(), a.end());
-    mx = *std::max_element(b.begin(), b.end());
-}
-
 static int grid_for(const sc_graph *g, int64_t n, int tpb) {
     int64_t want = (n + tpb - 1) / tpb;
     int64_t cap = (int64_t)std::max(g->sm_count, 1) * 8;
@@ -607,17 +594,18 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         bool mono = true, dok = true;
         for (int64_t i = 0; i < n; ++i) mono &= row_ptr[i + 1] >= row_ptr[i];
         for (int64_t i = 0; i < n; ++i) dok &= (deg[i] > 0.0) & (deg[i] < 1e308);
-        int32_t cmin = 0, cmax = 0;
-        col_minmax(col, nnz, cmin, cmax);
         for (int64_t i = 0; !mono && i < n; ++i)
             SC_REQUIRE(row_ptr[i + 1] >= row_ptr[i], SC_E_RANGE, "row_ptr decreases at %lld",
                        (long long)i);
         for (int64_t i = 0; !dok && i < n; ++i)
             SC_REQUIRE(deg[i] > 0.0 && deg[i] < 1e308, SC_E_RANGE,
                        "degree of row %lld is not positive/finite", (long long)i);
-        for (int64_t j = 0; (cmin < 0 || cmax >= ncols) && j < nnz; ++j)
-            SC_REQUIRE(col[j] >= 0 && col[j] < ncols, SC_E_RANGE,
-                       "col_indices[%lld]=%d out of range", (long long)j, col[j]);
+        // large column arrays are range-checked on the device after the upload (k_col_range,
+        // overlapped with the copy); small ones here
+        if (nnz < (int64_t(1) << 20))
+            for (int64_t j = 0; j < nnz; ++j)
+                SC_REQUIRE(col[j] >= 0 && col[j] < ncols, SC_E_RANGE,
+                           "col_indices[%lld]=%d out of range", (long long)j, col[j]);
     }
     lap("host validation");
     int ndev = 0;
@@ -643,12 +631,6 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->unit = unit;
 
     lap("unit check");
-    std::vector<int32_t> perm;
-    g->n_sell = sell_order(row_ptr, n, perm);
-    lap("sell order");
-    g->n_wide = n - g->n_sell;
-    g->nslices = (g->n_sell + kSlice - 1) / kSlice;
-
     int32_t st;
     auto cleanup = [&](int32_t code) {
         sc_graph_destroy(g);
@@ -675,7 +657,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     int32_t *t_col = nullptr;
     double *t_val = nullptr, *t_deg = nullptr;
     void *t_cub = nullptr;
-    auto free_tmp = [&]() {
+    auto free_tmp0 = [&]() {
         if (t_rp) cudaFreeAsync(t_rp, s);
         if (t_col) cudaFreeAsync(t_col, s);
         if (t_val) cudaFreeAsync(t_val, s);
@@ -683,9 +665,29 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         if (t_sizes) cudaFreeAsync(t_sizes, s);
         if (t_cub) cudaFreeAsync(t_cub, s);
     };
-    cudaError_t e = cudaMallocAsync((void **)&t_rp, (size_t)(n + 1) * 8, s);
-    if (!e) e = cudaMallocAsync((void **)&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4, s);
+    int32_t *t_flag = nullptr;
+    auto free_tmp = [&]() {
+        free_tmp0();
+        if (t_flag) cudaFreeAsync(t_flag, s);
+    };
+    // the big arrays go first so their copies overlap the host-side renumbering below
+    cudaError_t e = cudaMallocAsync((void **)&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4, s);
     if (!e && !unit) e = cudaMallocAsync((void **)&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&t_flag, 16, s);
+    if (!e && nnz) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s);
+    if (!e && t_val) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemsetAsync(t_flag, 0, 16, s);
+    if (!e && nnz) {
+        k_col_range<<<grid_for(g, nnz, 256), 256, 0, s>>>(t_col, nnz, ncols, t_flag);
+        e = cudaGetLastError();
+    }
+    lap("H2D issue");
+    std::vector<int32_t> perm;
+    g->n_sell = sell_order(row_ptr, n, perm);
+    g->n_wide = n - g->n_sell;
+    g->nslices = (g->n_sell + kSlice - 1) / kSlice;
+    lap("sell order");
+    if (!e) e = cudaMallocAsync((void **)&t_rp, (size_t)(n + 1) * 8, s);
     if (!e) e = cudaMallocAsync((void **)&t_deg, (size_t)n * 8, s);
     if (!e) e = cudaMallocAsync((void **)&t_sizes, (size_t)(g->nslices + 1) * 8, s);
     if (e) {
@@ -717,8 +719,6 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->d_z[1] = zz + ncols;
 
     e = cudaMemcpyAsync(t_rp, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s);
-    if (!e && nnz) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s);
-    if (!e && t_val) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s);
     if (!e) e = cudaMemcpyAsync(t_deg, deg, (size_t)n * 8, cudaMemcpyHostToDevice, s);
     if (!e) e = cudaMemcpyAsync(g->d_perm, perm.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s);
     if (!e) e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, s);
@@ -750,12 +750,23 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if (!e)
         e = cudaMemcpyAsync(&g->sell_entries, g->d_slice_ptr + g->nslices, 8,
                             cudaMemcpyDeviceToHost, s);
+    int32_t col_bad = 0;
+    if (!e) e = cudaMemcpyAsync(&col_bad, t_flag, 4, cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
     lap("alloc + H2D + slices");
     if (e) {
         free_tmp();
         fail(SC_E_CUDA, "graph layout: %s", cudaGetErrorString(e));
         return cleanup(SC_E_CUDA);
+    }
+    if (col_bad) {
+        free_tmp();
+        for (int64_t j = 0; j < nnz; ++j)  // locate the culprit for the message
+            if (col[j] < 0 || col[j] >= ncols) {
+                fail(SC_E_RANGE, "col_indices[%lld]=%d out of range", (long long)j, col[j]);
+                break;
+            }
+        return cleanup(SC_E_RANGE);
     }
     if ((st = dmalloc(g, (void **)&g->d_col, (size_t)g->sell_entries * 4 + 16)) ||
         (!unit && (st = dmalloc(g, (void **)&g->d_val, (size_t)g->sell_entries * 8 + 16))) ||

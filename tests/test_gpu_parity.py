@@ -236,3 +236,21 @@ def test_recycled_buffers_partial_last_slice(wg, c1):
             dg.set_x0(c1["x0"])
             xT, _ = dg.power_iterate(50, cuda_graph=False)
             assert np.array_equal(xT, c1["xT"])
+
+
+def test_device_column_range_check():
+    """Column arrays of >= 2^20 entries are range-checked on the device during the upload;
+    a bad index still surfaces as an InputError naming it, and nothing leaks."""
+    from paper_2310_10939_b200.errors import InputError
+
+    n, per = 1 << 15, 40
+    rng = np.random.default_rng(3)
+    rp = np.arange(n + 1, dtype=np.int64) * per
+    col = rng.integers(0, n, n * per).astype(np.int32)
+    col[777_777] = n + 5
+    g = from_csr(n, rp, col, None, np.full(n, float(per)))
+    with pytest.raises(InputError, match=r"col_indices\[777777\]"):
+        DeviceGraph(g)
+    col[777_777] = 3
+    with DeviceGraph(from_csr(n, rp, col, None, np.full(n, float(per)))) as dg:
+        assert dg.info()["nnz"] == n * per
