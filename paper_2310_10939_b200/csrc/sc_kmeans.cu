@@ -236,7 +236,8 @@ __global__ void k_seq_chunkmap(SegView v, SeqWork w, const int64_t *__restrict__
 // prediction is stepped element by element.
 constexpr int kMetaBlk = 256;
 constexpr int kComposeWarps = 4;
-constexpr size_t kComposeSmem = (size_t)kComposeWarps * kMetaBlk * (8 + 8 + 8 + 4);
+constexpr size_t kComposeSmem =
+    (size_t)kComposeWarps * (kMetaBlk * (8 + 8 + 8 + 4) + kSeqChunk * 8);
 
 __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, SeqWork w) {
     extern __shared__ unsigned char cm_raw[];
@@ -248,6 +249,8 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
     double *svm = reinterpret_cast<double *>(cm_raw) + (2 * kComposeWarps + wib) * kMetaBlk;
     int32_t *skp = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(cm_raw) +
                                                3 * kComposeWarps * kMetaBlk) + wib * kMetaBlk;
+    double *sbuf = reinterpret_cast<double *>(cm_raw + (size_t)kComposeWarps * kMetaBlk * 28) +
+                   wib * kSeqChunk;
     const int64_t c0 = v.cofs[s], c1 = v.cofs[s + 1];
     double run = 0.0;
     if (w.neg[s]) {
@@ -257,10 +260,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
             int64_t first;
             const int m = load_chunk(v, s, c, a, first);
             if (lane == 0) w.cstart[c] = run;
-            for (int j = 0; j < m; ++j) {
-                const double x = __shfl_sync(0xffffffffu, a[j % kSeqPerLane], j / kSeqPerLane);
-                run = __dadd_rn(run, x);
-            }
+            warp_step_seq(a, m, run, 0.0, false, sbuf);
         }
         if (lane == 0) w.total[s] = run;
         return;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
             double a[kSeqPerLane];
             int64_t first;
             const int mcount = load_chunk(v, s, c, a, first);
-            warp_step_elements(a, mcount, run, -1.0, false);
+            warp_step_seq(a, mcount, run, 0.0, false, sbuf);
             ++c;
         }
     }
@@ -397,13 +397,14 @@ __global__ void k_kpp_search(SegView v, SeqWork w, int64_t n, int k, int i,
         if (end > target) hi = mid;
         else lo = mid + 1;
     }
+    __shared__ double sbuf[8][kSeqChunk];  // launched with 256 threads
     int64_t idx = n - 1;
     if (lo < c1) {
         double run = w.cstart[lo];
         double a[kSeqPerLane];
         int64_t first;
         const int m = load_chunk(v, r, lo, a, first);
-        const int hit = warp_step_elements(a, m, run, target, true);
+        const int hit = warp_step_seq(a, m, run, target, true, sbuf[(threadIdx.x >> 5) & 7]);
         if (hit >= 0) idx = first - v.seg_off[r] + hit;
     }
     if (lane == 0) chosen[(int64_t)r * k + i] = idx;
@@ -550,45 +551,45 @@ __global__ void k_make_keys(int64_t n, int k, const int32_t *__restrict__ lab,
     }
 }
 
-// segment offsets: seg[t] = first position of key >= t in the sorted keys
-__global__ void k_seg_offsets(int rk, int64_t total, const int32_t *__restrict__ keys,
-                              int64_t *__restrict__ seg) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t > rk) return;
-    int64_t lo = 0, hi = total;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (keys[mid] < t) lo = mid + 1;
-        else hi = mid;
-    }
-    seg[t] = lo;
-}
-
-// chunk offsets of the (restart, cluster) segments: cofs[s] = sum ceil(len/kSeqChunk)
-__global__ void k_chunk_offsets(int S, const int64_t *__restrict__ seg, int64_t *__restrict__ cofs,
-                                int64_t *__restrict__ total) {
-    __shared__ int64_t part[1024];
-    int64_t carry = 0;
-    for (int base = 0; base < S; base += 1024) {
+// Layout of the (slot, cluster) segments of the sorted points, straight from the cluster
+// counts (k_assign / k_repair leave them consistent with the labels): seg = exclusive scan
+// of the counts in (active slot, label) order -- the order of the sort keys -- and cofs the
+// same over ceil(count / kSeqChunk) chunks.  One CTA, 1024 segments per round.
+__global__ void __launch_bounds__(1024) k_seg_layout(int nseg, int k,
+                                                     const int32_t *__restrict__ cnt,
+                                                     const int32_t *__restrict__ act,
+                                                     int64_t *__restrict__ seg,
+                                                     int64_t *__restrict__ cofs,
+                                                     int64_t *__restrict__ total) {
+    __shared__ int64_t pl[1024], pc[1024];
+    int64_t carry_l = 0, carry_c = 0;
+    for (int base = 0; base < nseg; base += 1024) {
         const int i = base + threadIdx.x;
-        const int64_t len = i < S ? seg[i + 1] - seg[i] : 0;
-        part[threadIdx.x] = (len + kSeqChunk - 1) / kSeqChunk;
+        const int64_t len = i < nseg ? cnt[(int64_t)act[i / k] * k + i % k] : 0;
+        const int64_t ch = (len + kSeqChunk - 1) / kSeqChunk;
+        pl[threadIdx.x] = len;
+        pc[threadIdx.x] = ch;
         __syncthreads();
         for (int d = 1; d < 1024; d <<= 1) {
-            const int64_t o = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+            const int64_t ol = threadIdx.x >= d ? pl[threadIdx.x - d] : 0;
+            const int64_t oc = threadIdx.x >= d ? pc[threadIdx.x - d] : 0;
             __syncthreads();
-            part[threadIdx.x] += o;
+            pl[threadIdx.x] += ol;
+            pc[threadIdx.x] += oc;
             __syncthreads();
         }
-        const int64_t incl = part[threadIdx.x];
-        const int64_t mine = (len + kSeqChunk - 1) / kSeqChunk;
-        if (i < S) cofs[i] = carry + incl - mine;
-        carry += part[1023];
+        if (i < nseg) {
+            seg[i] = carry_l + pl[threadIdx.x] - len;
+            cofs[i] = carry_c + pc[threadIdx.x] - ch;
+        }
+        carry_l += pl[1023];
+        carry_c += pc[1023];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        cofs[S] = carry;
-        *total = carry;
+        seg[nseg] = carry_l;
+        cofs[nseg] = carry_c;
+        *total = carry_c;
     }
 }
 
@@ -602,54 +603,135 @@ __global__ void k_seg_means(int nseg, int k, const int64_t *__restrict__ seg,
     cen[(int64_t)act[t / k] * k + t % k] = c > 0 ? __ddiv_rn(total[t], (double)c) : 0.0;
 }
 
-// kmeans_cost in numpy einsum("ij,ij->") order (sc_oracle.c orc_einsum_sumsq): one CTA
-// per (restart, 8192-element buffer) stages the buffer's squared deviations
-// fl(fl(x - c_label)^2) in shared memory with coalesced loads, then two threads run the two
-// SSE lane chains (8 elements per step in the order 6|7, 4|5, 2|3, 0|1, tail with zero fill)
-// out of shared memory at the FP64 add latency.
-__global__ void __launch_bounds__(256) k_cost_buf(const double *__restrict__ x, int64_t n, int k,
-                                                  const int32_t *__restrict__ lab,
-                                                  const double *__restrict__ cen,
-                                                  const int32_t *__restrict__ active, int64_t nbuf,
-                                                  double *__restrict__ part) {
-    extern __shared__ double sqb[];
+// kmeans_cost in numpy einsum("ij,ij->") order (sc_oracle.c orc_einsum_sumsq): one warp
+// per (restart, 8192-element buffer).  The warp stages the squared deviations
+// fl(fl(x - c_label)^2) 256 at a time (coalesced, double-buffered in its shared-memory slot)
+// while lanes 0 and 1 run the two SSE lane chains (8 elements per step in the order 6|7,
+// 4|5, 2|3, 0|1, tail with zero fill) over the previous 256 at the FP64 add latency.  Many
+// small warps instead of one 64 KB CTA per buffer keep every chain of the batch in flight.
+constexpr int kCostWarps = 8;
+constexpr int kCostChunk = 256;
+
+__global__ void __launch_bounds__(32 * kCostWarps) k_cost_buf(
+    const double *__restrict__ x, int64_t n, int k, const int32_t *__restrict__ lab,
+    const double *__restrict__ cen, const int32_t *__restrict__ active, int64_t nbuf,
+    double *__restrict__ part) {
+    __shared__ double sq[kCostWarps][2][kCostChunk];
     const int r = blockIdx.y;
     if (!active[r]) return;
-    const int64_t bufi = blockIdx.x;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t bufi = (int64_t)blockIdx.x * kCostWarps + wib;
+    if (bufi >= nbuf) return;
     const int64_t base = bufi * kEinsumBuf;
     const int m = (int)min((int64_t)kEinsumBuf, n - base);
     const int32_t *lb = lab + (int64_t)r * n + base;
     const double *c = cen + (int64_t)r * k;
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        const double d = __dsub_rn(x[base + j], c[lb[j]]);
-        sqb[j] = __dmul_rn(d, d);
-    }
-    __syncthreads();
-    if (threadIdx.x >= 2) return;
-    const int lane = threadIdx.x;
+    const double *xb0 = x + base;
+    // raw loads of chunk q+2 are issued before the chains of chunk q and the dependent
+    // center lookup of chunk q+1 runs after them, so no lane waits on HBM in between
+    constexpr int PL = kCostChunk / 32;
+    double xa[PL], xb[PL], v[PL];
+    int32_t la[PL], lbv[PL];
+    auto raw = [&](int q, double (&xv)[PL], int32_t (&lv)[PL]) {
+#pragma unroll
+        for (int t = 0; t < PL; ++t) {
+            const int j = q * kCostChunk + t * 32 + lane;
+            xv[t] = j < m ? __ldg(xb0 + j) : 0.0;
+            lv[t] = j < m ? __ldcs(lb + j) : -1;
+        }
+    };
+    auto finish = [&](const double (&xv)[PL], const int32_t (&lv)[PL]) {
+#pragma unroll
+        for (int t = 0; t < PL; ++t) {
+            v[t] = 0.0;
+            if (lv[t] >= 0) {
+                const double d = __dsub_rn(xv[t], c[lv[t]]);
+                v[t] = __dmul_rn(d, d);
+            }
+        }
+    };
+    const int nq = (m + kCostChunk - 1) / kCostChunk;
+    raw(0, xa, la);
+    if (nq > 1) raw(1, xb, lbv);
+    finish(xa, la);
     double acc = 0.0;
-    int i = 0;
-    for (; m - i >= 8; i += 8) {
-        const double p6 = sqb[i + 6 + lane], p4 = sqb[i + 4 + lane], p2 = sqb[i + 2 + lane],
-                     p0 = sqb[i + lane];
-        acc = __dadd_rn(p6, acc);
-        acc = __dadd_rn(p4, acc);
-        acc = __dadd_rn(p2, acc);
-        acc = __dadd_rn(p0, acc);
+    for (int q = 0; q < nq; ++q) {
+        double *cur = sq[wib][q & 1];
+#pragma unroll
+        for (int t = 0; t < PL; ++t) cur[t * 32 + lane] = v[t];
+        __syncwarp();
+        if (q + 2 < nq) raw(q + 2, xa, la);  // chunk q's raw registers are free again
+        if (lane < 2) {
+            const int mm = min(kCostChunk, m - q * kCostChunk);
+            if (mm == kCostChunk) {
+                // full chunk: 32 steps, the next step's four operands are read from shared
+                // memory while the current four are added (the chain is the only latency)
+                double p6 = cur[6 + lane], p4 = cur[4 + lane], p2 = cur[2 + lane], p0 = cur[lane];
+#pragma unroll 4
+                for (int i = 8; i <= kCostChunk; i += 8) {
+                    double n6 = 0.0, n4 = 0.0, n2 = 0.0, n0 = 0.0;
+                    if (i < kCostChunk) {
+                        n6 = cur[i + 6 + lane];
+                        n4 = cur[i + 4 + lane];
+                        n2 = cur[i + 2 + lane];
+                        n0 = cur[i + lane];
+                    }
+                    acc = __dadd_rn(p6, acc);
+                    acc = __dadd_rn(p4, acc);
+                    acc = __dadd_rn(p2, acc);
+                    acc = __dadd_rn(p0, acc);
+                    p6 = n6;
+                    p4 = n4;
+                    p2 = n2;
+                    p0 = n0;
+                }
+            } else {
+                int i = 0;
+                for (; mm - i >= 8; i += 8) {
+                    acc = __dadd_rn(cur[i + 6 + lane], acc);
+                    acc = __dadd_rn(cur[i + 4 + lane], acc);
+                    acc = __dadd_rn(cur[i + 2 + lane], acc);
+                    acc = __dadd_rn(cur[i + lane], acc);
+                }
+                for (; i < mm; i += 2) acc = __dadd_rn(i + lane < mm ? cur[i + lane] : 0.0, acc);
+            }
+        }
+        if (q + 1 < nq) finish(xb, lbv);
+#pragma unroll
+        for (int t = 0; t < PL; ++t) {  // rotate: chunk q+2 becomes "next"
+            const double tx = xa[t];
+            xa[t] = xb[t];
+            xb[t] = tx;
+            const int32_t tl = la[t];
+            la[t] = lbv[t];
+            lbv[t] = tl;
+        }
+        __syncwarp();
     }
-    for (; i < m; i += 2) acc = __dadd_rn(i + lane < m ? sqb[i + lane] : 0.0, acc);
-    part[((int64_t)r * nbuf + bufi) * 2 + lane] = acc;
+    if (lane < 2) part[((int64_t)r * nbuf + bufi) * 2 + lane] = acc;
 }
 
 // buffer totals (l0 + l1) added into the running output in buffer order
+// (the partials are staged in shared memory by the whole CTA first, so the sequential chain
+// runs at the add latency rather than one global-load latency per buffer)
+constexpr int kCombineStage = 2048;  // buffers per staging round (2 partials each)
+
 __global__ void k_cost_combine(int64_t nbuf, const double *__restrict__ part,
                                const int32_t *__restrict__ active, double *__restrict__ cost) {
+    __shared__ double sp[2 * kCombineStage];
     const int r = blockIdx.x;
-    if (threadIdx.x != 0 || !active[r]) return;
+    if (!active[r]) return;
     double out = 0.0;
     const double *p = part + (int64_t)r * nbuf * 2;
-    for (int64_t b = 0; b < nbuf; ++b) out = __dadd_rn(__dadd_rn(p[2 * b], p[2 * b + 1]), out);
-    cost[r] = out;
+    for (int64_t b0 = 0; b0 < nbuf; b0 += kCombineStage) {
+        const int nb = (int)(nbuf - b0 < kCombineStage ? nbuf - b0 : kCombineStage);
+        __syncthreads();
+        for (int t = threadIdx.x; t < 2 * nb; t += blockDim.x) sp[t] = p[2 * b0 + t];
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int b = 0; b < nb; ++b) out = __dadd_rn(__dadd_rn(sp[2 * b], sp[2 * b + 1]), out);
+    }
+    if (threadIdx.x == 0) cost[r] = out;
 }
 
 __global__ void k_gather_centers(const double *__restrict__ x, const int64_t *__restrict__ chosen,
@@ -924,9 +1006,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     if (k > 48 * 1024)
         SC_CUDA(cudaFuncSetAttribute(k_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, k));
     const dim3 ga(grid_1d(km, n, 256) / std::max(1, std::min(R, 8)) + 1, R);
-    const dim3 gc((unsigned)nbuf, R);
-    SC_CUDA(cudaFuncSetAttribute(k_cost_buf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kEinsumBuf * 8));
+    const dim3 gc((unsigned)((nbuf + kCostWarps - 1) / kCostWarps), R);
     SegView vm;
     vm.vals = km->d_vals_alt;
     vm.seg_off = km->d_seg;
@@ -971,9 +1051,9 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         size_t tb = km->cub_bytes;
         SC_CUDA(cub::DeviceRadixSort::SortPairs(km->d_cub, tb, km->d_keys, km->d_keys_alt,
                                                 km->d_vals, km->d_vals_alt, m, 0, end_bit, s));
-        k_seg_offsets<<<(nseg + 1 + 255) / 256, 256, 0, s>>>(nseg, m, km->d_keys_alt, km->d_seg);
+        k_seg_layout<<<1, 1024, 0, s>>>(nseg, k, km->d_cnt, km->d_empty, km->d_seg, km->d_cofs,
+                                        km->d_nchunks);
         if (prof) cudaEventRecord(pe[2], s);
-        k_chunk_offsets<<<1, 1024, 0, s>>>(nseg, km->d_seg, km->d_cofs, km->d_nchunks);
         SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)nseg * 4, s));
         vm.S = nseg;
         const int gwm = grid_1d(km, (m / kSeqChunk + nseg) * 32, 256);
@@ -985,9 +1065,9 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         k_seg_means<<<(nseg + 127) / 128, 128, 0, s>>>(nseg, k, km->d_seg, km->d_total, km->d_empty,
                                                        km->d_cen);
         if (prof) cudaEventRecord(pe[3], s);
-        k_cost_buf<<<gc, 256, kEinsumBuf * 8, s>>>(km->d_x, n, k, km->d_lab[nxt], km->d_cen,
+        k_cost_buf<<<gc, 32 * kCostWarps, 0, s>>>(km->d_x, n, k, km->d_lab[nxt], km->d_cen,
                                                    km->d_active, nbuf, km->d_part);
-        k_cost_combine<<<R, 32, 0, s>>>(nbuf, km->d_part, km->d_active, km->d_cost);
+        k_cost_combine<<<R, 256, 0, s>>>(nbuf, km->d_part, km->d_active, km->d_cost);
         SC_CUDA(cudaGetLastError());
         if (prof) cudaEventRecord(pe[4], s);
         SC_CUDA(cudaMemcpyAsync(cost.data(), km->d_cost, (size_t)R * 8, cudaMemcpyDeviceToHost, s));

@@ -20,9 +20,9 @@
 //   predict    (one warp / segment): approximate chunk starts -> expected binade per chunk
 //   chunkmap   (one warp / chunk): parity map of the whole chunk on that binade's grid
 //   compose    (one warp / segment): walks 32 chunks per step; chunks whose exact start
-//              confirms the prediction advance in O(1), others are stepped element by
-//              element (still 256 elements per warp step).  Emits the exact start of
-//              every chunk and the exact segment total.
+//              confirms the prediction advance in O(1), others are added sequentially by
+//              one lane (warp_step_seq).  Emits the exact start of every chunk and the
+//              exact segment total.
 // Every decision is re-checked in compose against the exact running value, so the
 // prediction only affects speed, never the result.
 #pragma once
@@ -108,82 +108,34 @@ __device__ __forceinline__ PMap warp_exclusive(PMap incl) {
 
 // ---------------------------------------------------------------------------
 // Exact stepping of up to 256 elements held 8 per lane (lane-contiguous), starting from
-// the exact running value s.  Advances s over all n_valid elements.  If `target` >= 0 is
-// given (k-means++ search), stops at the first element whose running sum exceeds target
-// and returns its index (else -1).  Uniform across the warp.
-__device__ __forceinline__ int warp_step_elements(const double (&a)[kSeqPerLane], int n_valid,
-                                                  double &s, double target, bool search) {
+// the exact running value s: the chunk is staged in the warp's shared-memory slot `buf`
+// (kSeqChunk doubles) and lane 0 adds it left to right -- the sequential sum itself, at the
+// FP64 add latency (~2k cycles per chunk).  Used for the few chunks whose binade the
+// prediction could not pin (grid crossings), where a warp-parallel walk would pay one full
+// parity-map scan per crossing.  If `search`, stops at the first element whose running sum
+// exceeds target and returns its index (else -1; s is then the chunk end).  Warp-uniform.
+__device__ __forceinline__ int warp_step_seq(const double (&a)[kSeqPerLane], int n_valid,
+                                             double &s, double target, bool search,
+                                             double *buf) {
     const int lane = threadIdx.x & 31;
-    int pos = 0;
-    while (pos < n_valid) {
-        const Grid g = grid_of(s);
-        const int64_t S0 = (int64_t)to_units(s, g.k);
-        // lane map over its elements >= pos
-        PMap lm = pmap_id();
-        double v[kSeqPerLane];
+    __syncwarp();
 #pragma unroll
-        for (int t = 0; t < kSeqPerLane; ++t) {
-            const int j = lane * kSeqPerLane + t;
-            v[t] = (j >= pos && j < n_valid) ? to_units(a[t], g.k) : 0.0;
-            lm = pmap_then(lm, pmap_elem(v[t]));
-        }
-        const PMap excl = warp_exclusive(warp_scan_pmap(lm));
-        int64_t S = pmap_apply(excl, S0);
-        // walk this lane's elements: first invalid (grid change) or search hit
-        int bad = 1 << 30, hit = 1 << 30;
-#pragma unroll
-        for (int t = 0; t < kSeqPerLane; ++t) {
-            const int j = lane * kSeqPerLane + t;
-            if (j >= pos && j < n_valid && bad == (1 << 30) && hit == (1 << 30)) {
-                if ((double)(g.top - S) < v[t] || !(a[t] >= 0.0) || !isfinite(a[t])) {
-                    bad = j;
-                } else {
-                    S = pmap_apply(pmap_elem(v[t]), S);
-                    if (search && from_units(S, g.k) > target) hit = j;
-                }
+    for (int t = 0; t < kSeqPerLane; ++t) buf[lane * kSeqPerLane + t] = a[t];
+    __syncwarp();
+    double r = s;
+    int hit = -1;
+    if (lane == 0) {
+#pragma unroll 8
+        for (int j = 0; j < n_valid; ++j) {
+            r = __dadd_rn(r, buf[j]);
+            if (search && r > target) {
+                hit = j;
+                break;
             }
         }
-        int first_bad = bad, first_hit = hit;
-#pragma unroll
-        for (int d = 16; d; d >>= 1) {
-            first_bad = min(first_bad, __shfl_xor_sync(0xffffffffu, first_bad, d));
-            first_hit = min(first_hit, __shfl_xor_sync(0xffffffffu, first_hit, d));
-        }
-        if (search && first_hit < first_bad) {
-            // running value right after first_hit, computed by its lane
-            return first_hit;
-        }
-        const int stop = min(first_bad, n_valid);
-        // exact running value just before `stop`: owner lane of element stop-1 recomputes
-        // (cheap: re-walk its elements)
-        {
-            const int64_t Sst = pmap_apply(excl, S0);
-            int64_t Sw = Sst;
-#pragma unroll
-            for (int t = 0; t < kSeqPerLane; ++t) {
-                const int j = lane * kSeqPerLane + t;
-                if (j >= pos && j < stop) Sw = pmap_apply(pmap_elem(v[t]), Sw);
-            }
-            // lane owning element stop-1 (or the lane before the range if stop == pos)
-            const int owner = stop > pos ? (stop - 1) / kSeqPerLane : -1;
-            if (owner >= 0) {
-                const int64_t Sfin = __shfl_sync(0xffffffffu, Sw, owner);
-                s = from_units(Sfin, g.k);
-            }
-        }
-        if (first_bad >= n_valid) return -1;
-        // one real add for the grid-crossing element (owner lane broadcasts the addend)
-        const int ol = first_bad / kSeqPerLane, ot = first_bad % kSeqPerLane;
-        double ab = 0.0;
-#pragma unroll
-        for (int t = 0; t < kSeqPerLane; ++t)
-            if (t == ot) ab = a[t];
-        ab = __shfl_sync(0xffffffffu, ab, ol);
-        s = __dadd_rn(s, ab);
-        if (search && s > target) return first_bad;
-        pos = first_bad + 1;
     }
-    return -1;
+    s = __shfl_sync(0xffffffffu, r, 0);
+    return __shfl_sync(0xffffffffu, hit, 0);
 }
 
 }  // namespace sc
