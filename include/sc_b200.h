@@ -147,6 +147,28 @@ int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t fla
 int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x_out,
                             void *stream);
 
+/* ---- device graph generator (configs too large for the host) ------------ */
+/* Planted-partition graph with the reference SBM's law (generate.py:112-149): k blocks of
+ * n/k consecutive vertices, pairs u < v independent with prob p (same block) / q, isolated
+ * vertices dropped and ids compacted.  Realised on the device with geometric skips over each
+ * row's upper candidates; skip j of row u is word j%4 of Philox4x64-10(key, (j/4+1, u,
+ * 0x5bd1e995, 0)), U = ((raw >> 11) + 1) 2^-53, G = 1 + floor(log(U) * inv_log1m_{p,q})
+ * with inv_log1m_x = 1 / log1p(-x) supplied by the caller and log evaluated with basic
+ * correctly rounded operations only (host oracles reproduce it bit for bit). */
+typedef struct sc_csr sc_csr;
+int32_t sc_generate_sbm(int64_t n, int32_t k, double p, double q, double inv_log1m_p,
+                        double inv_log1m_q, uint64_t key0, uint64_t key1, int32_t device,
+                        sc_csr **out);
+int32_t sc_csr_info(const sc_csr *h, int64_t *n, int64_t *nnz, int64_t *n_generated);
+/* host buffers, each nullable: row_ptr[n+1], col[nnz], deg[n], orig_ids[n] (generated id of
+ * every kept vertex; block = orig_id / (n_generated / k)) */
+int32_t sc_csr_download(const sc_csr *h, int64_t *row_ptr, int32_t *col, double *deg,
+                        int32_t *orig_ids);
+void sc_csr_destroy(sc_csr *h);
+/* graph handle straight from a device-resident CSR (the column array is not copied to the
+ * host; the handle does not keep a reference to h) */
+int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_graph **out);
+
 /* ---- 1-D k-means replica ------------------------------------------------ */
 /* points: host f (n doubles) or, with _from_graph, the f left on the device by the last
  * sc_power_iterate.  restarts batches independent restarts on the device. */

@@ -299,3 +299,81 @@ def canonical_labels(labels: np.ndarray) -> np.ndarray:
     remap = np.empty(labels.max() + 1 if labels.size else 0, dtype=np.int64)
     remap[np.unique(labels)[order]] = np.arange(order.size)
     return remap[labels]
+
+
+# ---------------------------------------------------------------------------
+# the device SBM generator's law, restated (sc_generate.cu; not a reference algorithm -- the
+# reference's per-block-pair streams cannot be replayed at config-5 scale -- so it is pinned
+# by restating the generator's own counter/skip convention in numpy, op for op)
+
+DEVICE_SBM_TAG = 0x5BD1E995
+
+
+def np_sc_log(x: np.ndarray) -> np.ndarray:
+    """sc_generate.cu sc_log: the same IEEE operation sequence (numpy rounds every op)."""
+    x = np.asarray(x, dtype=np.float64)
+    b = x.view(np.uint64)
+    e = ((b >> np.uint64(52)) & np.uint64(0x7FF)).astype(np.int64) - 1023
+    m = ((b & np.uint64(0x000FFFFFFFFFFFFF)) | np.uint64(0x3FF0000000000000)).view(np.float64)
+    big = m > 1.4142135623730951
+    m = np.where(big, m * 0.5, m)
+    e = np.where(big, e + 1, e)
+    t = (m - 1.0) / (m + 1.0)
+    t2 = t * t
+    p = np.full_like(t, 1.0 / 25.0)
+    for d in (23.0, 21.0, 19.0, 17.0, 15.0, 13.0, 11.0, 9.0, 7.0, 5.0, 3.0):
+        p = p * t2 + 1.0 / d
+    p = p * t2 + 1.0
+    return e.astype(np.float64) * 0.6931471805599453 + 2.0 * t * p
+
+
+def device_sbm(n: int, k: int, p: float, q: float, seed: int):
+    """Rows of the device generator's graph, built on the host (small n only).  Returns
+    (row_ptr, col, deg, orig_ids) with isolated vertices dropped and ids compacted."""
+    import math
+
+    key = np.array(np.random.SeedSequence([seed, 9]).generate_state(2, np.uint64))
+    inv_p = 0.0 if p <= 0 else (-0.0 if p >= 1 else 1.0 / math.log1p(-p))
+    inv_q = 0.0 if q <= 0 else (-0.0 if q >= 1 else 1.0 / math.log1p(-q))
+    s = n // k
+    has_p, has_q = p > 0 and s > 1, q > 0 and k > 1
+    us, vs = [], []
+    for u in range(n):
+        bg = np.random.Philox(key=key, counter=[0, u, DEVICE_SBM_TAG, 0])
+        buf, pos = np.empty(0, dtype=np.uint64), 0
+
+        def skip(inv):
+            nonlocal buf, pos
+            if pos == buf.size:
+                buf, pos = bg.random_raw(64), 0
+            raw = buf[pos]
+            pos += 1
+            U = float((int(raw) >> 11) + 1) * 1.1102230246251565e-16
+            g = math.floor(float(np_sc_log(np.array([U]))[0] * inv))
+            return (1 << 62) if g >= 4.0e18 else 1 + g
+
+        hi = (u // s + 1) * s
+        if has_p:
+            v = u + skip(inv_p)
+            while v < hi:
+                us.append(u)
+                vs.append(v)
+                v += skip(inv_p)
+        if has_q:
+            v = hi - 1 + skip(inv_q)
+            while v < n:
+                us.append(u)
+                vs.append(v)
+                v += skip(inv_q)
+    u = np.array(us, dtype=np.int64)
+    v = np.array(vs, dtype=np.int64)
+    r = np.concatenate([u, v])
+    c = np.concatenate([v, u])
+    order = np.lexsort((c, r))
+    r, c = r[order], c[order]
+    deg = np.bincount(r, minlength=n)
+    keep = deg > 0
+    newid = np.cumsum(keep) - 1
+    rp = np.zeros(int(keep.sum()) + 1, dtype=np.int64)
+    np.cumsum(deg[keep], out=rp[1:])
+    return rp, newid[c].astype(np.int32), deg[keep].astype(np.float64), np.flatnonzero(keep)

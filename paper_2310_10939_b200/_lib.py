@@ -46,7 +46,8 @@ EXPORTS = (
     "sc_power_iterate", "sc_shard_step", "sc_shard_scale", "sc_shard_irwin_hall",
     "sc_kmeans_create", "sc_kmeans_create_from_graph", "sc_kmeans_destroy", "sc_kmeans_pp",
     "sc_kmeans_lloyd", "sc_seqsum", "sc_sell_order", "sc_graph_order", "sc_graph_create_ex",
-    "sc_shard_step_range", "sc_shard_scale_range",
+    "sc_shard_step_range", "sc_shard_scale_range", "sc_generate_sbm", "sc_csr_info",
+    "sc_csr_download", "sc_csr_destroy", "sc_graph_create_from_csr",
 )
 
 _lib = None
@@ -90,6 +91,11 @@ def load() -> ctypes.CDLL:
         "sc_shard_step_range": ([P, i64, i64, P, P, P, P, f64, u32, P], i32),
         "sc_shard_scale_range": ([P, i64, i64, P, P, u32, P], i32),
         "sc_graph_order": ([P, P], i32),
+        "sc_generate_sbm": ([i64, i32, f64, f64, f64, f64, u64, u64, i32, PP], i32),
+        "sc_csr_info": ([P, P, P, P], i32),
+        "sc_csr_download": ([P, P, P, P, P], i32),
+        "sc_csr_destroy": ([P], None),
+        "sc_graph_create_from_csr": ([P, u32, PP], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

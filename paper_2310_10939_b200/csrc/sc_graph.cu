@@ -565,10 +565,12 @@ static int grid_for(const sc_graph *g, int64_t n, int tpb) {
     return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
+// col == nullptr with dcol != nullptr: the column array is already on `device` (borrowed,
+// e.g. from sc_generate_sbm) and is neither copied nor freed.
 static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const double *val,
                           const double *deg, int64_t n, int64_t nnz, int64_t ncols,
                           int64_t col_offset, int64_t global_row0, int rename, uint32_t cflags, int32_t device,
-                          sc_graph **out) {
+                          sc_graph **out, const int32_t *dcol = nullptr) {
     SC_REQUIRE(out, SC_E_INVALID, "out is null");
     *out = nullptr;
     const bool prof = getenv("SC_GRAPH_PROFILE") != nullptr;
@@ -580,7 +582,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
                 std::chrono::duration<double, std::milli>(t - tp0).count());
         tp0 = t;
     };
-    SC_REQUIRE(row_ptr && deg && (col || nnz == 0), SC_E_INVALID, "null CSR array");
+    SC_REQUIRE(row_ptr && deg && (col || dcol || nnz == 0), SC_E_INVALID, "null CSR array");
     SC_REQUIRE(n >= 1 && n < (int64_t(1) << 31) - 1, SC_E_INVALID, "n=%lld out of range",
                (long long)n);
     SC_REQUIRE(nnz >= 0 && row_ptr[0] == 0 && row_ptr[n] == nnz, SC_E_RANGE,
@@ -602,7 +604,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
                        "degree of row %lld is not positive/finite", (long long)i);
         // large column arrays are range-checked on the device after the upload (k_col_range,
         // overlapped with the copy); small ones here
-        if (nnz < (int64_t(1) << 20))
+        if (col && nnz < (int64_t(1) << 20))
             for (int64_t j = 0; j < nnz; ++j)
                 SC_REQUIRE(col[j] >= 0 && col[j] < ncols, SC_E_RANGE,
                            "col_indices[%lld]=%d out of range", (long long)j, col[j]);
@@ -659,7 +661,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     void *t_cub = nullptr;
     auto free_tmp0 = [&]() {
         if (t_rp) cudaFreeAsync(t_rp, s);
-        if (t_col) cudaFreeAsync(t_col, s);
+        if (t_col && !dcol) cudaFreeAsync(t_col, s);
         if (t_val) cudaFreeAsync(t_val, s);
         if (t_deg) cudaFreeAsync(t_deg, s);
         if (t_sizes) cudaFreeAsync(t_sizes, s);
@@ -671,10 +673,12 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         if (t_flag) cudaFreeAsync(t_flag, s);
     };
     // the big arrays go first so their copies overlap the host-side renumbering below
-    cudaError_t e = cudaMallocAsync((void **)&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4, s);
+    cudaError_t e = cudaSuccess;
+    if (dcol) t_col = const_cast<int32_t *>(dcol);
+    else e = cudaMallocAsync((void **)&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4, s);
     if (!e && !unit) e = cudaMallocAsync((void **)&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8, s);
     if (!e) e = cudaMallocAsync((void **)&t_flag, 16, s);
-    if (!e && nnz) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s);
+    if (!e && nnz && !dcol) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s);
     if (!e && t_val) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s);
     if (!e) e = cudaMemsetAsync(t_flag, 0, 16, s);
     if (!e && nnz) {
@@ -761,7 +765,8 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     }
     if (col_bad) {
         free_tmp();
-        for (int64_t j = 0; j < nnz; ++j)  // locate the culprit for the message
+        fail(SC_E_RANGE, "col_indices out of range [0, %lld)", (long long)ncols);
+        for (int64_t j = 0; col && j < nnz; ++j)  // locate the culprit for the message
             if (col[j] < 0 || col[j] >= ncols) {
                 fail(SC_E_RANGE, "col_indices[%lld]=%d out of range", (long long)j, col[j]);
                 break;
@@ -916,6 +921,9 @@ static int32_t to_host_original(sc_graph *g, const double *dev, double *host) {
     return SC_OK;
 }
 
+int32_t csr_device_arrays(const sc_csr *h, const int64_t **rp, const int32_t **col,
+                          const double **deg, int32_t *device);  // sc_generate.cu
+
 }  // namespace sc
 
 extern "C" {
@@ -955,6 +963,27 @@ int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double
     // columns arrive already renamed into the global renumbered z space (sc_sell_order)
     return graph_init(row_ptr, col, val, deg, n, nnz, ncols, col_offset, global_row0, 0, 0u, device,
                       out);
+}
+
+int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_graph **out) {
+    SC_REQUIRE(h && out, SC_E_INVALID, "null argument");
+    int64_t n = 0, nnz = 0;
+    int32_t st = sc_csr_info(h, &n, &nnz, nullptr);
+    if (st) return st;
+    const int64_t *d_rp;
+    const int32_t *d_col;
+    const double *d_deg;
+    int32_t device;
+    if ((st = sc::csr_device_arrays(h, &d_rp, &d_col, &d_deg, &device))) return st;
+    SC_CUDA(cudaSetDevice(device));
+    // the renumbering is computed on the host from the row offsets (n + 1 words); the
+    // column array stays on the device
+    std::vector<int64_t> rp((size_t)n + 1);
+    std::vector<double> deg((size_t)n);
+    SC_CUDA(cudaMemcpy(rp.data(), d_rp, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost));
+    SC_CUDA(cudaMemcpy(deg.data(), d_deg, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    return graph_init(rp.data(), nullptr, nullptr, deg.data(), n, nnz, n, 0, 0, 1, create_flags,
+                      device, out, d_col);
 }
 
 int32_t sc_sell_order(const int64_t *row_ptr, int64_t n, int32_t *perm_out) {

@@ -26,6 +26,7 @@ from .graph import Graph, from_csr, from_edges
 TAG_SBM_BLOCK = 4  # generate.py:22
 TAG_DCSBM = 7
 TAG_RGG = 8
+TAG_DEVICE_SBM = 9
 
 
 def rng_for(seed: int, *tags: int) -> np.random.Generator:
@@ -252,3 +253,101 @@ def sample_weighted_rgg(n: int, k: int, seed: int, *, sigma: float = 0.05, knn: 
         planted = planted[mask]
     return SbmSample(graph=g, planted=planted, dropped=dropped,
                      params=SbmParams(n=n, k=1, p=0.0, q=0.0, seed=seed))
+
+
+# ---------------------------------------------------------------------------
+# device generator (sc_generate.cu): the same SBM law, realised on the GPU for sizes the
+# host cannot build (config 5: n = 1e8, ~1.8e9 stored entries)
+
+
+def device_sbm_key(seed: int) -> tuple[int, int]:
+    """Philox key of the device generator: SeedSequence([seed, 9]) (tag 9 unused by the
+    reference, spectral.py:26-29)."""
+    if seed < 0:
+        raise InputError(f"seed must be a nonnegative integer, got {seed}")
+    k = np.random.SeedSequence([seed, TAG_DEVICE_SBM]).generate_state(2, np.uint64)
+    return int(k[0]), int(k[1])
+
+
+def inv_log1m(prob: float) -> float:
+    """1 / log1p(-prob), the geometric-skip scale handed to the generator (-0.0 at prob 1)."""
+    import math
+
+    if prob <= 0.0:
+        return 0.0
+    if prob >= 1.0:
+        return -0.0
+    return 1.0 / math.log1p(-prob)
+
+
+class DeviceCSR:
+    """A CSR generated and kept on one GPU (``sc_csr`` handle)."""
+
+    def __init__(self, params: SbmParams, device: int = 0):
+        import ctypes
+
+        from . import _lib
+
+        L = _lib.require_device()
+        k0, k1 = device_sbm_key(params.seed)
+        h = ctypes.c_void_p()
+        _lib.check(L.sc_generate_sbm(params.n, params.k, params.p, params.q, inv_log1m(params.p),
+                                     inv_log1m(params.q), k0, k1, device, ctypes.byref(h)))
+        self._h, self.params, self.device = h, params, device
+        n, nnz, ng = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(L.sc_csr_info(h, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(ng)))
+        self.n, self.nnz, self.n_generated = n.value, nnz.value, ng.value
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise InputError("device CSR is closed")
+        return self._h
+
+    def download(self, pinned: bool = False) -> SbmSample:
+        """Copy to host arrays (optionally page-locked, for fast re-upload) -> SbmSample with
+        the planted labels of the kept vertices."""
+        from . import _lib
+
+        def empty(count, dtype):
+            if pinned:  # the array's base keeps the page-locked tensor alive
+                import torch
+
+                tdt = {np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}
+                return torch.empty(count, dtype=tdt[dtype], pin_memory=True).numpy()
+            return np.empty(count, dtype=dtype)
+
+        rp, col = empty(self.n + 1, np.int64), empty(self.nnz, np.int32)
+        deg, orig = empty(self.n, np.float64), np.empty(self.n, dtype=np.int32)
+        _lib.check(_lib.load().sc_csr_download(self.handle, _lib.ptr(rp), _lib.ptr(col),
+                                               _lib.ptr(deg), _lib.ptr(orig)))
+        g = Graph(n=self.n, row_offsets=rp, col_indices=col, weights=None, degrees=deg)
+        planted = (orig // self.params.block_size).astype(np.int64)
+        kept = np.zeros(self.n_generated, dtype=bool)
+        kept[orig] = True
+        return SbmSample(graph=g, planted=planted, dropped=list(np.flatnonzero(~kept)),
+                         params=self.params)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            from . import _lib
+
+            _lib.load().sc_csr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def sample_sbm_device(params: SbmParams, device: int = 0, pinned: bool = False) -> SbmSample:
+    with DeviceCSR(params, device) as d:
+        return d.download(pinned=pinned)

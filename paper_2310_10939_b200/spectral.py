@@ -110,6 +110,23 @@ class DeviceGraph:
         self.device = device
         self.last_timing = None
 
+    @classmethod
+    def from_device_csr(cls, csr, keep_weights: bool = False) -> "DeviceGraph":
+        """Graph handle straight from a device-resident CSR (``generate.DeviceCSR``): the
+        column array never visits the host (sc_graph_create_from_csr)."""
+        L = _lib.require_device()
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        _lib.check(L.sc_graph_create_from_csr(csr.handle,
+                                              _lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0,
+                                              ctypes.byref(h)))
+        self._h = h
+        self.graph = None
+        self.n, self.nnz = csr.n, csr.nnz
+        self.device = csr.device
+        self.last_timing = None
+        return self
+
     # -- lifecycle
     def close(self) -> None:
         if getattr(self, "_h", None):

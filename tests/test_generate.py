@@ -75,3 +75,22 @@ def test_rgg_shape():
     g.validate()
     assert g.nnz >= 16 * g.n  # union of 16-NN lists, symmetrised
     assert np.all(g.weights > 0) and np.all(g.weights <= 1.0)
+
+
+def test_device_sbm_law_restatement_statistics():
+    """The numpy restatement of the device generator's law (oracle.device_sbm): edge
+    densities inside / across blocks match p / q within 5 sigma; symmetric CSR."""
+    from oracle import oracle as O
+
+    n, k, p, q = 3000, 3, 0.01, 0.001
+    rp, col, deg, orig = O.device_sbm(n, k, p, q, 11)
+    row = np.repeat(np.arange(orig.size), np.diff(rp))
+    blk_r, blk_c = orig[row] // (n // k), orig[col] // (n // k)
+    s = n // k
+    e_in = np.sum(blk_r == blk_c) / 2
+    e_out = np.sum(blk_r != blk_c) / 2
+    t_in, t_out = k * s * (s - 1) / 2, s * s * k * (k - 1) / 2
+    assert abs(e_in - p * t_in) < 5 * np.sqrt(p * t_in)
+    assert abs(e_out - q * t_out) < 5 * np.sqrt(q * t_out)
+    assert np.array_equal(np.sort(row * n + col), np.sort(col.astype(np.int64) * n + row))
+    assert np.array_equal(deg, np.diff(rp))
