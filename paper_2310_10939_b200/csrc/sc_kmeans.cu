@@ -53,6 +53,9 @@ struct sc_kmeans {
     int32_t *d_start = nullptr;    // [R]
     int32_t *d_degen = nullptr;    // [R]
     double *d_cen = nullptr;       // [R][k]
+    double *d_scen = nullptr;      // [R][k] centers sorted ascending (sorted assignment)
+    int32_t *d_sidx = nullptr;     // [R][k] their original indices
+    double *d_cmax = nullptr;      // [R] max |center|
     int32_t *d_cnt = nullptr;      // [R][k]
     int64_t *d_seg = nullptr;      // [R*k + 1] segment offsets into the sorted arrays
     double *d_part = nullptr;      // [R][nchunks][2] einsum lane partials
@@ -455,6 +458,138 @@ __global__ void k_assign(const double *__restrict__ x, int64_t n, int k,
     if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&changed[r], ch);
 }
 
+// ---- assignment through sorted centers (k >= kSortedMinK) ------------------------------
+// argmin_c d2ref(x, c) is found without evaluating all k centers.  With u = 2^-53 and
+// D(c) = (x - c)^2 exact, d2ref's five roundings give |d2ref - D| <= 3.01 u (|x| + |c|)^2,
+// and Dapprox(c) = fl(fl(x - c)^2) is within 3.01 u D of D and monotone in |x - c| on each
+// side of x.  So every center with Dapprox(c) > Dapprox(c*) + 20 u (|x| + cmax)^2 (c* the
+// nearest neighbour of x among the sorted centers) has d2ref(x, c) > d2ref(x, c*) and cannot
+// be the argmin; the remaining window is contiguous in sorted order and evaluated exactly,
+// ties going to the lowest original index -- the brute-force result, bit for bit.
+constexpr int kSortedMinK = 16;
+constexpr int kSortedMaxK = 4096;
+
+// one CTA per active restart: bitonic sort of (value, original index), and max |c|
+__global__ void __launch_bounds__(1024) k_sort_centers(int k, const double *__restrict__ cen,
+                                                       const int32_t *__restrict__ active,
+                                                       double *__restrict__ scen,
+                                                       int32_t *__restrict__ sidx,
+                                                       double *__restrict__ cmax) {
+    const int r = blockIdx.x;
+    if (!active[r]) return;
+    extern __shared__ unsigned char sort_raw[];
+    __shared__ double red[32];
+    int P = 1;
+    while (P < k) P <<= 1;
+    double *v = reinterpret_cast<double *>(sort_raw);
+    int32_t *ix = reinterpret_cast<int32_t *>(v + P);
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const double c = i < k ? cen[(int64_t)r * k + i] : INFINITY;
+        v[i] = c;
+        ix[i] = i < k ? i : INT32_MAX;
+        if (i < k) mx = fmax(mx, fabs(c));
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool gt = v[i] > v[j] || (v[i] == v[j] && ix[i] > ix[j]);
+                    if (gt == up) {
+                        const double tv = v[i];
+                        v[i] = v[j];
+                        v[j] = tv;
+                        const int32_t ti = ix[i];
+                        ix[i] = ix[j];
+                        ix[j] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        scen[(int64_t)r * k + i] = v[i];
+        sidx[(int64_t)r * k + i] = ix[i];
+    }
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) m = fmax(m, red[w]);
+        cmax[r] = m;
+    }
+}
+
+__global__ void k_assign_sorted(const double *__restrict__ x, int64_t n, int k,
+                                const double *__restrict__ scen, const int32_t *__restrict__ sidx,
+                                const double *__restrict__ cmax_r,
+                                const int32_t *__restrict__ active,
+                                const int32_t *__restrict__ prev, int32_t *__restrict__ lab,
+                                int32_t *__restrict__ cnt, int32_t *__restrict__ changed) {
+    const int r = blockIdx.y;
+    if (!active[r]) return;
+    extern __shared__ unsigned char smem_raw[];
+    double *c = reinterpret_cast<double *>(smem_raw);
+    int32_t *ci = reinterpret_cast<int32_t *>(c + k);
+    int32_t *hist = ci + k;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        c[i] = scen[(int64_t)r * k + i];
+        ci[i] = sidx[(int64_t)r * k + i];
+        hist[i] = 0;
+    }
+    const double cmax = cmax_r[r];
+    __syncthreads();
+    int ch = 0;
+    const int32_t *pv = prev + (int64_t)r * n;
+    int32_t *lb = lab + (int64_t)r * n;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double xj = x[j];
+        // p = first sorted center >= xj
+        int lo = 0, hi = k;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (c[mid] < xj) lo = mid + 1;
+            else hi = mid;
+        }
+        const int p = lo;
+        auto dap = [&](double cv) {
+            const double t = __dsub_rn(xj, cv);
+            return __dmul_rn(t, t);
+        };
+        double dstar = INFINITY;
+        if (p > 0) dstar = dap(c[p - 1]);
+        if (p < k) dstar = fmin(dstar, dap(c[p]));
+        const double m = __dadd_rn(fabs(xj), cmax);
+        const double thr = __dadd_rn(dstar, __dmul_rn(__dmul_rn(m, m), 20.0 * 1.1102230246251565e-16));
+        int bi = INT32_MAX;
+        double bd = INFINITY;
+        auto take = [&](int q) {
+            const double d = d2ref(xj, c[q]);
+            const int id = ci[q];
+            if (d < bd || (d == bd && id < bi)) {
+                bd = d;
+                bi = id;
+            }
+        };
+        for (int q = p - 1; q >= 0 && dap(c[q]) <= thr; --q) take(q);
+        for (int q = p; q < k && dap(c[q]) <= thr; ++q) take(q);
+        lb[j] = bi;
+        ch += (pv[j] != bi);
+        atomicAdd(&hist[bi], 1);
+    }
+    __syncthreads();
+    // hist is indexed by original center index
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+        if (hist[i]) atomicAdd(&cnt[(int64_t)r * k + i], hist[i]);
+    for (int o = 16; o; o >>= 1) ch += __shfl_xor_sync(0xffffffffu, ch, o);
+    if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&changed[r], ch);
+}
+
 // _repair_empty (kmeans.py:151-164), one CTA per restart; returns at once when no
 // cluster is empty (the common case).  Clusters empty after assignment are repaired in
 // increasing order: the first point of maximal own distance moves in, its own distance
@@ -775,6 +910,9 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_start, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_degen, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_cen, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_scen, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_sidx, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_cmax, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_cnt, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_seg, (size_t)S, km->stream))) return st;
     if ((st = grow(&km->d_part, (size_t)R * nbuf * 2, km->stream))) return st;
@@ -882,7 +1020,8 @@ void sc_kmeans_destroy(sc_kmeans *km) {
     if (km->stream) cudaStreamSynchronize(km->stream);
     void *ptrs[] = {km->d_x, km->d_best, km->d_lab[0], km->d_lab[1], km->d_keys, km->d_keys_alt,
                     km->d_vals, km->d_vals_alt, km->d_cub, km->d_chosen, km->d_u,
-                    km->d_start, km->d_degen, km->d_cen, km->d_cnt, km->d_seg, km->d_part,
+                    km->d_start, km->d_degen, km->d_cen, km->d_scen, km->d_sidx, km->d_cmax,
+                    km->d_cnt, km->d_seg, km->d_part,
                     km->d_cost, km->d_changed, km->d_active, km->d_empty, km->d_A,
                     km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
                     km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
@@ -1003,6 +1142,17 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     if (smem_assign > 48 * 1024)
         SC_CUDA(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_assign));
+    const bool sorted_assign = k >= kSortedMinK && k <= kSortedMaxK &&
+                               getenv("SC_KMEANS_BRUTE_ASSIGN") == nullptr;
+    const size_t smem_sorted = (size_t)k * 16;
+    size_t smem_sort = 12;
+    while (smem_sort < (size_t)k * 12) smem_sort <<= 1;  // next power of two of k, x 12 B
+    if (sorted_assign && smem_sorted > 48 * 1024)
+        SC_CUDA(cudaFuncSetAttribute(k_assign_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_sorted));
+    if (sorted_assign)  // (plus 256 B of static shared memory)
+        SC_CUDA(cudaFuncSetAttribute(k_sort_centers, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_sort));
     if (k > 48 * 1024)
         SC_CUDA(cudaFuncSetAttribute(k_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, k));
     const dim3 ga(grid_1d(km, n, 256) / std::max(1, std::min(R, 8)) + 1, R);
@@ -1036,9 +1186,17 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         SC_CUDA(cudaMemsetAsync(km->d_cnt, 0, (size_t)rk * 4, s));
         SC_CUDA(cudaMemsetAsync(km->d_changed, 0, (size_t)R * 4, s));
         if (prof) cudaEventRecord(pe[0], s);
-        k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, k, km->d_cen, km->d_active,
-                                               km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
-                                               km->d_changed);
+        if (sorted_assign) {
+            k_sort_centers<<<R, 1024, smem_sort, s>>>(k, km->d_cen, km->d_active, km->d_scen, km->d_sidx,
+                                              km->d_cmax);
+            k_assign_sorted<<<ga, 256, smem_sorted, s>>>(km->d_x, n, k, km->d_scen, km->d_sidx,
+                                                         km->d_cmax, km->d_active, km->d_lab[cur],
+                                                         km->d_lab[nxt], km->d_cnt, km->d_changed);
+        } else {
+            k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, k, km->d_cen, km->d_active,
+                                                   km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
+                                                   km->d_changed);
+        }
         k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, k, km->d_cen, km->d_active,
                                               km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
                                               km->d_changed, km->d_best);
