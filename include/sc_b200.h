@@ -143,6 +143,21 @@ int32_t sc_shard_scale_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const 
                              double *z_out, uint32_t flags, void *stream);
 int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t flags,
                        void *stream);
+/* ---- fused z exchange over peer memory (NVLink P2P), instead of an all-gather ------- */
+/* sc_shard_buffers: the handle's own z allocation (2*ncols doubles: z0 then z1, zeroed) and
+ * its 64-word flag array.  Ranks export both with sc_ipc_export, import the peers' with
+ * sc_ipc_import, and hand all world bases to sc_shard_set_peers (entries for `rank` ignored).
+ * From then on every z value a step / scale writes into the handle's z allocation is also
+ * stored at the same offset of every peer's allocation from the SpMV epilogue itself, and
+ * sc_shard_barrier (one tiny kernel per step: release/acquire flags at system scope) replaces
+ * the collective.  Results stay bit-identical: rows and their summation order are untouched. */
+int32_t sc_shard_buffers(sc_graph *g, double **z_base, uint32_t **flags);
+int32_t sc_shard_set_peers(sc_graph *g, void *const *z_bases, void *const *flag_bases,
+                           int32_t world, int32_t rank);
+int32_t sc_shard_barrier(sc_graph *g, void *stream);
+int32_t sc_ipc_export(const void *dptr, void *handle_out /* 64 bytes */);
+int32_t sc_ipc_import(const void *handle /* 64 bytes */, int32_t device, void **dptr_out);
+int32_t sc_ipc_release(void *dptr);
 /* x0 for the shard rows (global ids global_row0..), device output */
 int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x_out,
                             void *stream);

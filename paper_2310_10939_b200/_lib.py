@@ -47,7 +47,8 @@ EXPORTS = (
     "sc_kmeans_create", "sc_kmeans_create_from_graph", "sc_kmeans_destroy", "sc_kmeans_pp",
     "sc_kmeans_lloyd", "sc_seqsum", "sc_sell_order", "sc_graph_order", "sc_graph_create_ex",
     "sc_shard_step_range", "sc_shard_scale_range", "sc_generate_sbm", "sc_csr_info",
-    "sc_csr_download", "sc_csr_destroy", "sc_graph_create_from_csr",
+    "sc_csr_download", "sc_csr_destroy", "sc_graph_create_from_csr", "sc_shard_buffers",
+    "sc_shard_set_peers", "sc_shard_barrier", "sc_ipc_export", "sc_ipc_import", "sc_ipc_release",
 )
 
 _lib = None
@@ -96,6 +97,12 @@ def load() -> ctypes.CDLL:
         "sc_csr_download": ([P, P, P, P, P], i32),
         "sc_csr_destroy": ([P], None),
         "sc_graph_create_from_csr": ([P, u32, PP], i32),
+        "sc_shard_buffers": ([P, PP, PP], i32),
+        "sc_shard_set_peers": ([P, P, P, i32, i32], i32),
+        "sc_shard_barrier": ([P, P], i32),
+        "sc_ipc_export": ([P, P], i32),
+        "sc_ipc_import": ([P, i32, PP], i32),
+        "sc_ipc_release": ([P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -33,6 +33,7 @@
 #include <cstring>
 #include <mutex>
 #include <cub/device/device_scan.cuh>
+#include <cuda/atomic>
 #include <thread>
 #include <vector>
 
@@ -87,6 +88,11 @@ struct StepArgs {
     int64_t col_offset;
     int wide_blocks;           // CTAs of the wide-row kernel
     double hs;                 // +0.5 or -0.5
+    // fused exchange (multi-GPU, peer memory over NVLink): every z value written is also
+    // stored at the same offset of each peer's z allocation (peer_base[q] + peer_off + i)
+    double *const *peer_base;
+    int64_t peer_off;
+    int npeer;
 };
 
 template <bool SYM>
@@ -95,7 +101,14 @@ __device__ __forceinline__ void row_epilogue(const StepArgs &a, int64_t r, doubl
     if (SYM) s = __dmul_rn(sc, s);
     const double y = __dadd_rn(__dmul_rn(0.5, xr), __dmul_rn(a.hs, s));
     __stcs(a.x_out + r, y);
-    a.z_out[a.col_offset + r] = SYM ? __dmul_rn(sc, y) : __ddiv_rn(y, sc);
+    const double zv = SYM ? __dmul_rn(sc, y) : __ddiv_rn(y, sc);
+    a.z_out[a.col_offset + r] = zv;
+    for (int q = 0; q < a.npeer; ++q) a.peer_base[q][a.peer_off + a.col_offset + r] = zv;
+}
+
+// make this thread's peer stores visible system-wide before the barrier kernel's flag
+__device__ __forceinline__ void peer_fence(const StepArgs &a) {
+    if (a.npeer) __threadfence_system();
 }
 
 // Wide rows (> kExtreme entries): one warp per row.  The warp gathers 128 products per
@@ -148,6 +161,7 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
         buf1 = tb;
     }
     if (lane == 0) row_epilogue<SYM>(a, r, s, xr, sc);
+    peer_fence(a);
 }
 
 template <bool UNIT, bool SYM>
@@ -203,14 +217,44 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
         }
     }
     if (live) row_epilogue<SYM>(a, r, s, xr, sc);
+    peer_fence(a);
 }
 
 // z[col_offset + i] = x[i] / d[i]   (rw)   or   x[i] * d[i]^-1/2   (sym)
 __global__ void k_scale(const double *__restrict__ x, const double *__restrict__ scale,
-                        double *__restrict__ z, int64_t n, int64_t off, int sym) {
+                        double *__restrict__ z, int64_t n, int64_t off, int sym,
+                        double *const *peer_base = nullptr, int64_t peer_off = 0, int npeer = 0) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        z[off + i] = sym ? __dmul_rn(x[i], scale[i]) : __ddiv_rn(x[i], scale[i]);
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = sym ? __dmul_rn(x[i], scale[i]) : __ddiv_rn(x[i], scale[i]);
+        z[off + i] = v;
+        for (int q = 0; q < npeer; ++q) peer_base[q][peer_off + off + i] = v;
+    }
+    if (npeer) __threadfence_system();
+}
+
+// Cross-GPU barrier of the fused exchange: this rank's epoch counter (flags[kEpochSlot]) is
+// bumped, written into slot `rank` of every peer's flag array (release, system scope), and the
+// kernel waits until every peer has written at least that epoch into our own array (acquire).
+// Launched after each step, it is also what makes the peers' z stores of that step visible.
+constexpr int kMaxWorld = 32;
+constexpr int kEpochSlot = 63;
+
+__global__ void k_peer_barrier(uint32_t *flags, uint32_t *const *peer_flags, int world, int rank) {
+    __shared__ uint32_t e;
+    if (threadIdx.x == 0) {
+        e = flags[kEpochSlot] + 1;
+        flags[kEpochSlot] = e;
+    }
+    __syncthreads();
+    const int q = threadIdx.x;
+    if (q < world && q != rank) {
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_system> out(peer_flags[q][rank]);
+        out.store(e, cuda::memory_order_release);
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_system> in(flags[q]);
+        while (in.load(cuda::memory_order_acquire) < e) __nanosleep(64);
+    }
+    __syncthreads();
 }
 
 // 1/sqrt(d), as numpy's 1.0 / np.sqrt(d) (spectral.py:49)
@@ -379,6 +423,11 @@ struct sc_graph {
     bool l2_window = false;
     double *d_f_orig = nullptr;   // f in original vertex order (for the k-means context)
     std::vector<std::pair<void *, size_t>> allocs;  // every dmalloc'd buffer (returned to the cache)
+    // fused peer exchange (sc_shard_set_peers)
+    uint32_t *d_flags = nullptr;        // 64 words: peer epochs [0, world), own epoch [63]
+    double **d_peer_z = nullptr;        // npeer peer z-allocation bases
+    uint32_t **d_peer_flags = nullptr;  // world peer flag arrays (own slot unused)
+    int npeer = 0, world = 1, rank = 0;
 };
 
 namespace sc {
@@ -837,6 +886,16 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.nslices = g->nslices;
     a.col_offset = g->col_offset;
     a.hs = sign < 0 ? -0.5 : 0.5;
+    a.peer_base = g->d_peer_z;
+    a.npeer = 0;
+    a.peer_off = 0;
+    if (g->npeer) {
+        // the exchange mirrors the handle's own z allocation only
+        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + 2 * g->ncols, SC_E_STATE,
+                   "peer exchange needs z_out inside the handle's z buffers (sc_shard_buffers)");
+        a.npeer = g->npeer;
+        a.peer_off = z_out - g->d_z[0];
+    }
     constexpr int wpb = kStepTPB / 32;
     a.wide_blocks = (int)((a.wide_hi - a.wide_lo + wpb - 1) / wpb);
     const int64_t sblocks = (a.slice_hi - a.slice_lo + wpb - 1) / wpb;
@@ -1175,11 +1234,96 @@ int32_t sc_shard_scale_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const 
     int32_t st;
     if (sym)
         if ((st = ensure_isd(g, s))) return st;
+    int64_t poff = 0;
+    if (g->npeer) {
+        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + 2 * g->ncols, SC_E_STATE,
+                   "peer exchange needs z_out inside the handle's z buffers (sc_shard_buffers)");
+        poff = z_out - g->d_z[0];
+    }
     if (row_hi > row_lo)
         k_scale<<<grid_for(g, row_hi - row_lo, 256), 256, 0, s>>>(
             x + row_lo, (sym ? g->d_isd : g->d_deg) + row_lo, z_out, row_hi - row_lo,
-            g->col_offset + row_lo, sym);
+            g->col_offset + row_lo, sym, g->d_peer_z, poff, g->npeer);
     SC_CUDA(cudaGetLastError());
+    return SC_OK;
+}
+
+int32_t sc_shard_buffers(sc_graph *g, double **z_base, uint32_t **flags) {
+    SC_REQUIRE(g && z_base && flags, SC_E_INVALID, "null argument");
+    SC_CUDA(cudaSetDevice(g->device));
+    if (!g->d_flags) {
+        int32_t st = dmalloc(g, (void **)&g->d_flags, 64 * 4);
+        if (st) return st;
+        SC_CUDA(cudaMemset(g->d_flags, 0, 64 * 4));
+    }
+    *z_base = g->d_z[0];
+    *flags = g->d_flags;
+    return SC_OK;
+}
+
+int32_t sc_shard_set_peers(sc_graph *g, void *const *z_bases, void *const *flag_bases,
+                           int32_t world, int32_t rank) {
+    SC_REQUIRE(g && z_bases && flag_bases, SC_E_INVALID, "null argument");
+    SC_REQUIRE(world >= 1 && world <= kMaxWorld && rank >= 0 && rank < world, SC_E_INVALID,
+               "bad world/rank (%d/%d; at most %d ranks)", world, rank, kMaxWorld);
+    SC_CUDA(cudaSetDevice(g->device));
+    std::vector<double *> pz;
+    std::vector<uint32_t *> pf((size_t)world, nullptr);
+    for (int q = 0; q < world; ++q) {
+        if (q == rank) continue;
+        SC_REQUIRE(z_bases[q] && flag_bases[q], SC_E_INVALID, "null peer pointer for rank %d", q);
+        pz.push_back(static_cast<double *>(z_bases[q]));
+        pf[(size_t)q] = static_cast<uint32_t *>(flag_bases[q]);
+    }
+    if (!g->d_peer_z) {
+        int32_t st;
+        if ((st = dmalloc(g, (void **)&g->d_peer_z, kMaxWorld * sizeof(double *))) ||
+            (st = dmalloc(g, (void **)&g->d_peer_flags, kMaxWorld * sizeof(uint32_t *))))
+            return st;
+    }
+    if (!pz.empty())
+        SC_CUDA(cudaMemcpy(g->d_peer_z, pz.data(), pz.size() * sizeof(double *),
+                           cudaMemcpyHostToDevice));
+    SC_CUDA(cudaMemcpy(g->d_peer_flags, pf.data(), pf.size() * sizeof(uint32_t *),
+                       cudaMemcpyHostToDevice));
+    g->npeer = (int)pz.size();
+    g->world = world;
+    g->rank = rank;
+    return SC_OK;
+}
+
+int32_t sc_shard_barrier(sc_graph *g, void *stream) {
+    SC_REQUIRE(g, SC_E_INVALID, "null graph");
+    if (g->world <= 1) return SC_OK;
+    SC_REQUIRE(g->d_flags, SC_E_STATE, "call sc_shard_buffers before the barrier");
+    SC_CUDA(cudaSetDevice(g->device));
+    k_peer_barrier<<<1, kMaxWorld, 0, (cudaStream_t)stream>>>(g->d_flags, g->d_peer_flags,
+                                                               g->world, g->rank);
+    SC_CUDA(cudaGetLastError());
+    return SC_OK;
+}
+
+int32_t sc_ipc_export(const void *dptr, void *handle_out) {
+    SC_REQUIRE(dptr && handle_out, SC_E_INVALID, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    SC_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(dptr)));
+    std::memcpy(handle_out, &h, 64);
+    return SC_OK;
+}
+
+int32_t sc_ipc_import(const void *handle, int32_t device, void **dptr_out) {
+    SC_REQUIRE(handle && dptr_out, SC_E_INVALID, "null argument");
+    SC_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    SC_CUDA(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return SC_OK;
+}
+
+int32_t sc_ipc_release(void *dptr) {
+    SC_REQUIRE(dptr, SC_E_INVALID, "null argument");
+    SC_CUDA(cudaIpcCloseMemHandle(dptr));
     return SC_OK;
 }
 
@@ -1192,8 +1336,15 @@ int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t fla
     int32_t st;
     if (sym)
         if ((st = ensure_isd(g, s))) return st;
+    int64_t poff = 0;
+    if (g->npeer) {
+        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + 2 * g->ncols, SC_E_STATE,
+                   "peer exchange needs z_out inside the handle's z buffers (sc_shard_buffers)");
+        poff = z_out - g->d_z[0];
+    }
     k_scale<<<grid_for(g, g->n, 256), 256, 0, s>>>(x, sym ? g->d_isd : g->d_deg, z_out, g->n,
-                                                   g->col_offset, sym);
+                                                   g->col_offset, sym, g->d_peer_z, poff,
+                                                   g->npeer);
     SC_CUDA(cudaGetLastError());
     return SC_OK;
 }

@@ -69,6 +69,9 @@ struct sc_kmeans {
     int32_t *d_kpred = nullptr, *d_neg = nullptr, *d_round_on = nullptr, *d_on = nullptr;
     int64_t *d_q0 = nullptr, *d_q1 = nullptr, *d_cofs = nullptr, *d_nchunks = nullptr;
     int64_t *d_segkpp = nullptr;   // [R+1] restart segments over d_best
+    int64_t *d_sq0 = nullptr, *d_sq1 = nullptr;  // super-chunk maps
+    double *d_svmax = nullptr;
+    int32_t *d_skp = nullptr;
 };
 
 namespace sc {
@@ -99,7 +102,14 @@ struct SeqWork {
     double *cstart;   // exact running sum at each chunk start
     int32_t *neg;     // per segment: any negative / non-finite element
     double *total;    // per segment exact total
+    // super-chunks: kSuper consecutive chunks (aligned to the global chunk index) composed
+    // into one map when they all lie in one segment on one predicted grid
+    int64_t *sq0, *sq1;
+    double *svmax;
+    int32_t *skp;     // common predicted grid, or kNoGrid (walk the chunks one by one)
 };
+
+constexpr int kSuper = 32;
 
 __device__ __forceinline__ int seg_of_chunk(const SegView &v, int64_t c) {
     int lo = 0, hi = v.S;  // cofs[lo] <= c < cofs[hi]
@@ -233,6 +243,45 @@ __global__ void k_seq_chunkmap(SegView v, SeqWork w, const int64_t *__restrict__
     }
 }
 
+// one warp per super-chunk: compose its 32 chunk maps (lane = chunk) when they share one
+// segment and one predicted grid
+__global__ void k_seq_superize(SegView v, SeqWork w, const int64_t *__restrict__ pn) {
+    const int64_t nchunks = *pn;
+    const int64_t nsup = (nchunks + kSuper - 1) / kSuper;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t g = wid; g < nsup; g += nw) {
+        const int64_t c = g * kSuper + lane;
+        const bool full = (g + 1) * kSuper <= nchunks;
+        int kp = kNoGrid;
+        PMap m = pmap_id();
+        double vm = 0.0;
+        if (full) {
+            kp = w.kpred[c];
+            m = PMap{w.q0[c], w.q1[c]};
+            vm = w.vmax[c];
+        }
+        int ok = full && kp != kNoGrid;
+        const int kp0 = __shfl_sync(0xffffffffu, kp, 0);
+        ok = __all_sync(0xffffffffu, ok && kp == kp0);
+        if (ok && lane == 0) {
+            const int s0 = seg_of_chunk(v, g * kSuper);
+            ok = seg_on(v, s0) && v.cofs[s0 + 1] >= (g + 1) * kSuper;
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        const PMap tot = warp_scan_pmap(m);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) vm = fmax(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+        if (lane == 31) {
+            w.skp[g] = ok ? kp0 : kNoGrid;
+            w.sq0[g] = tot.i0;
+            w.sq1[g] = tot.i1;
+            w.svmax[g] = vm;
+        }
+    }
+}
+
 // one warp per segment: exact composition of the chunk maps (see sc_seqsum.cuh).  Each
 // warp stages 256 chunks' maps in its slice of shared memory (one memory latency per 256
 // chunks), then advances up to 32 chunks per step; a chunk whose exact start contradicts its
@@ -242,7 +291,8 @@ constexpr int kComposeWarps = 4;
 constexpr size_t kComposeSmem =
     (size_t)kComposeWarps * (kMetaBlk * (8 + 8 + 8 + 4) + kSeqChunk * 8);
 
-__global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, SeqWork w) {
+__global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, SeqWork w,
+                                                                  int want_cstart) {
     extern __shared__ unsigned char cm_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int s = blockIdx.x * kComposeWarps + wib;
@@ -270,6 +320,47 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
     }
     int64_t c = c0, blk = -1, blk_end = -1;
     while (c < c1) {
+        if ((c & (kSuper - 1)) == 0 && c + kSuper <= c1) {
+            // super step: up to 32 super-chunks (1024 chunks) on the current grid at once
+            const Grid g = grid_of(run);
+            const int64_t S0 = (int64_t)to_units(run, g.k);
+            const int64_t G = c / kSuper + lane;
+            const bool valid = (G + 1) * kSuper <= c1;
+            bool ok = false;
+            PMap m = pmap_id();
+            double vmu = 0.0;
+            if (valid && g.top == (int64_t(1) << 53) && w.skp[G] == g.k) {
+                m = PMap{w.sq0[G], w.sq1[G]};
+                vmu = to_units(w.svmax[G], g.k);
+                ok = true;
+            }
+            const PMap excl = warp_exclusive(warp_scan_pmap(m));
+            const int64_t Sl = pmap_apply(excl, S0);
+            if (ok) {
+                const int64_t qmax = max(m.i0, m.i1);
+                ok = (double)(g.top - Sl - qmax) >= vmu && Sl + qmax <= g.top;
+            }
+            const unsigned badm = __ballot_sync(0xffffffffu, valid && !ok);
+            const unsigned valm = __ballot_sync(0xffffffffu, valid);
+            const int Lb = badm ? __ffs(badm) - 1 : 32;
+            const int nadv = min(Lb, __popc(valm));
+            if (want_cstart && lane < nadv) {
+                // exact start of every chunk of this super-chunk (for the k-means++ search)
+                int64_t S = Sl;
+                const int64_t cb = G * kSuper;
+                for (int t = 0; t < kSuper; ++t) {
+                    w.cstart[cb + t] = from_units(S, g.k);
+                    S = pmap_apply(PMap{w.q0[cb + t], w.q1[cb + t]}, S);
+                }
+            }
+            if (nadv > 0) {
+                const int64_t Send = __shfl_sync(0xffffffffu, pmap_apply(m, Sl), nadv - 1);
+                run = from_units(Send, g.k);
+                c += (int64_t)nadv * kSuper;
+                continue;
+            }
+            // the first super-chunk needs the chunk walk (grid change or non-uniform)
+        }
         if (c >= blk_end) {
             blk = c;
             blk_end = min(c + kMetaBlk, c1);
@@ -288,7 +379,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         const Grid g = grid_of(run);
         const int64_t S0 = (int64_t)to_units(run, g.k);
         const int64_t cl = c + lane;
-        const bool valid = cl < blk_end;
+        const bool valid = cl < blk_end && cl < (c / kSuper + 1) * kSuper;
         bool ok = false;
         PMap m = pmap_id();
         double vmu = 0.0;
@@ -308,7 +399,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         const int Lb = badm ? __ffs(badm) - 1 : 32;   // first chunk to step
         const int Le = __popc(valm);                  // valid lanes form a prefix
         const int nadv = min(Lb, Le);
-        if (lane < nadv) w.cstart[cl] = from_units(Sl, g.k);
+        if (want_cstart && lane < nadv) w.cstart[cl] = from_units(Sl, g.k);
         if (nadv > 0) {
             const int64_t Send = __shfl_sync(0xffffffffu, pmap_apply(m, Sl), nadv - 1);
             run = from_units(Send, g.k);
@@ -316,7 +407,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         }
         if (Lb < Le) {
             // step chunk c element by element
-            if (lane == 0) w.cstart[c] = run;
+            if (want_cstart && lane == 0) w.cstart[c] = run;
             double a[kSeqPerLane];
             int64_t first;
             const int mcount = load_chunk(v, s, c, a, first);
@@ -926,6 +1017,10 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_kpred, (size_t)nch, km->stream))) return st;
     if ((st = grow(&km->d_q0, (size_t)nch, km->stream))) return st;
     if ((st = grow(&km->d_q1, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_sq0, (size_t)nch / kSuper + 1, km->stream))) return st;
+    if ((st = grow(&km->d_sq1, (size_t)nch / kSuper + 1, km->stream))) return st;
+    if ((st = grow(&km->d_svmax, (size_t)nch / kSuper + 1, km->stream))) return st;
+    if ((st = grow(&km->d_skp, (size_t)nch / kSuper + 1, km->stream))) return st;
     if ((st = grow(&km->d_total, (size_t)S, km->stream))) return st;
     if ((st = grow(&km->d_neg, (size_t)S, km->stream))) return st;
     if ((st = grow(&km->d_cofs, (size_t)S + 1, km->stream))) return st;
@@ -954,6 +1049,10 @@ static SeqWork seq_work(sc_kmeans *km) {
     w.cstart = km->d_cstart;
     w.neg = km->d_neg;
     w.total = km->d_total;
+    w.sq0 = km->d_sq0;
+    w.sq1 = km->d_sq1;
+    w.svmax = km->d_svmax;
+    w.skp = km->d_skp;
     return w;
 }
 
@@ -1025,6 +1124,7 @@ void sc_kmeans_destroy(sc_kmeans *km) {
                     km->d_cost, km->d_changed, km->d_active, km->d_empty, km->d_A,
                     km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
                     km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
+                    km->d_sq0, km->d_sq1, km->d_svmax, km->d_skp,
                     km->d_segkpp};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, km->stream);
@@ -1099,7 +1199,8 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
         k_seq_summarize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
         k_seq_predict<<<gs, 256, 0, s>>>(v, w);
         k_seq_chunkmap<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
-        k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(v, w);
+        k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
+        k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(v, w, 1);
         k_kpp_search<<<gs, 256, 0, s>>>(v, w, n, k, i, km->d_u, km->d_chosen, km->d_on,
                                          km->d_degen);
     }
@@ -1219,7 +1320,8 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
         k_seq_predict<<<gsm, 256, 0, s>>>(vm, wm);
         k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
-        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(vm, wm);
+        k_seq_superize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
+        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(vm, wm, 0);
         k_seg_means<<<(nseg + 127) / 128, 128, 0, s>>>(nseg, k, km->d_seg, km->d_total, km->d_empty,
                                                        km->d_cen);
         if (prof) cudaEventRecord(pe[3], s);
@@ -1295,7 +1397,9 @@ extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *se
     const int64_t nch = cofs[nseg];
     double *d_vals = nullptr, *d_A = nullptr, *d_vmax = nullptr, *d_cs = nullptr, *d_tot = nullptr;
     int64_t *d_seg = nullptr, *d_cofs = nullptr, *d_q0 = nullptr, *d_q1 = nullptr, *d_nch = nullptr;
-    int32_t *d_kp = nullptr, *d_neg = nullptr;
+    int32_t *d_kp = nullptr, *d_neg = nullptr, *d_skp = nullptr;
+    int64_t *d_sq0 = nullptr, *d_sq1 = nullptr;
+    double *d_svm = nullptr;
     auto al = [](void **p, size_t b) { return cudaMalloc(p, b ? b : 16); };
     cudaError_t e = al((void **)&d_vals, n * 8);
     if (!e) e = al((void **)&d_A, nch * 8);
@@ -1309,6 +1413,10 @@ extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *se
     if (!e) e = al((void **)&d_nch, 8);
     if (!e) e = al((void **)&d_kp, nch * 4);
     if (!e) e = al((void **)&d_neg, nseg * 4);
+    if (!e) e = al((void **)&d_skp, (nch / kSuper + 1) * 4);
+    if (!e) e = al((void **)&d_sq0, (nch / kSuper + 1) * 8);
+    if (!e) e = al((void **)&d_sq1, (nch / kSuper + 1) * 8);
+    if (!e) e = al((void **)&d_svm, (nch / kSuper + 1) * 8);
     if (!e) e = cudaMemcpy(d_vals, vals, n * 8, cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(d_seg, seg_off, (nseg + 1) * 8, cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(d_cofs, cofs.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice);
@@ -1316,18 +1424,20 @@ extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *se
     if (!e) e = cudaMemset(d_neg, 0, nseg * 4);
     if (!e) {
         SegView v{d_vals, d_seg, d_cofs, nseg, nullptr, 1};
-        SeqWork w{d_A, d_vmax, d_kp, d_q0, d_q1, d_cs, d_neg, d_tot};
+        SeqWork w{d_A, d_vmax, d_kp, d_q0, d_q1, d_cs, d_neg, d_tot, d_sq0, d_sq1, d_svm, d_skp};
         const int gw = (int)std::min<int64_t>((nch * 32 + 255) / 256 + 1, 148 * 8);
         const int gs = (nseg * 32 + 255) / 256;
         k_seq_summarize<<<gw, 256>>>(v, w, d_nch);
         k_seq_predict<<<gs, 256>>>(v, w);
         k_seq_chunkmap<<<gw, 256>>>(v, w, d_nch);
-        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem>>>(v, w);
+        k_seq_superize<<<gw, 256>>>(v, w, d_nch);
+        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem>>>(v, w, 1);
         e = cudaDeviceSynchronize();
     }
     if (!e) e = cudaMemcpy(totals, d_tot, nseg * 8, cudaMemcpyDeviceToHost);
     if (!e && chunk_starts) e = cudaMemcpy(chunk_starts, d_cs, nch * 8, cudaMemcpyDeviceToHost);
-    void *ps[] = {d_vals, d_A, d_vmax, d_cs, d_tot, d_seg, d_cofs, d_q0, d_q1, d_nch, d_kp, d_neg};
+    void *ps[] = {d_vals, d_A, d_vmax, d_cs, d_tot, d_seg, d_cofs, d_q0, d_q1, d_nch, d_kp, d_neg,
+                  d_skp, d_sq0, d_sq1, d_svm};
     for (void *p : ps) cudaFree(p);
     SC_CUDA(e);
     return SC_OK;

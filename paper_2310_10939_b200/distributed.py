@@ -235,12 +235,103 @@ class CudaShard:
             parts.append(z_full[lo:lo + int(b[j + 1] - b[j])].cpu().numpy())
         return np.concatenate(parts)
 
+    def z_views(self):
+        """(z0, z1) torch views over the handle's own z allocation, and its flag array address
+        (the buffers the fused peer exchange mirrors, sc_shard_buffers)."""
+        zb, fl = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(_lib.load().sc_shard_buffers(self.h, ctypes.byref(zb), ctypes.byref(fl)))
+        nc = self.plan.ncols
+        z0 = _device_view(zb.value, nc, self.device)
+        z1 = _device_view(zb.value + 8 * nc, nc, self.device)
+        return z0, z1, zb.value, fl.value
+
     def to_original(self, v_local):
         """renumbered local vector (tensor or array) -> array in original local order"""
         v = v_local.cpu().numpy() if hasattr(v_local, "cpu") else np.asarray(v_local)
         out = np.empty(self.n)
         out[self.plan.perms[self.rank]] = v[: self.n]
         return out
+
+
+def _device_view(ptr: int, count: int, device: int):
+    """Zero-copy float64 torch tensor over device memory owned by the library
+    (__cuda_array_interface__ import)."""
+    import torch
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_Cai(), device=torch.device("cuda", device))
+
+
+class P2PComm:
+    """Fused exchange: the step kernels store every z value straight into the peers' z
+    allocations over NVLink (sc_shard_set_peers), so there is nothing to gather; ``finish``
+    launches the system-scope flag barrier that ends a step.  ``link`` exchanges CUDA IPC
+    handles with the other ranks; ``link_local`` wires shards living in one process (the
+    single-GPU emulation used by the tests, where the host serialises the steps instead of
+    a barrier)."""
+
+    def __init__(self, shard, plan: ShardPlan, rank: int):
+        import torch
+
+        self.torch = torch
+        self.shard, self.plan, self.rank = shard, plan, rank
+        self.z0, self.z1, self.zbase, self.flags = shard.z_views()
+        self._opened = []
+        self.barrier = True
+
+    def link(self, group=None):
+        import torch.distributed as dist
+
+        L = _lib.load()
+        world = self.plan.world
+        hz, hf = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+        _lib.check(L.sc_ipc_export(ctypes.c_void_p(self.zbase), hz))
+        _lib.check(L.sc_ipc_export(ctypes.c_void_p(self.flags), hf))
+        handles = [None] * world
+        dist.all_gather_object(handles, (hz.raw, hf.raw), group=group)
+        zs, fs = [], []
+        for q, (a, b) in enumerate(handles):
+            if q == self.rank:
+                zs.append(self.zbase)
+                fs.append(self.flags)
+                continue
+            pz, pf = ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.check(L.sc_ipc_import(a, self.shard.device, ctypes.byref(pz)))
+            _lib.check(L.sc_ipc_import(b, self.shard.device, ctypes.byref(pf)))
+            self._opened += [pz.value, pf.value]
+            zs.append(pz.value)
+            fs.append(pf.value)
+        self._set(zs, fs)
+
+    @staticmethod
+    def link_local(comms):
+        zs = [c.zbase for c in comms]
+        fs = [c.flags for c in comms]
+        for c in comms:
+            c._set(zs, fs)
+            c.barrier = False
+
+    def _set(self, zs, fs):
+        arr = ctypes.c_void_p * len(zs)
+        _lib.check(_lib.load().sc_shard_set_peers(self.shard.h, arr(*zs), arr(*fs), len(zs),
+                                                  self.rank))
+
+    def gather_piece(self, z_full, j):
+        pass  # the SpMV epilogue already stored this piece into every peer
+
+    def finish(self):
+        if self.barrier:
+            stream = self.torch.cuda.current_stream().cuda_stream
+            _lib.check(_lib.load().sc_shard_barrier(self.shard.h, ctypes.c_void_p(stream)))
+
+    def close(self):
+        L = _lib.load()
+        for p in self._opened:
+            L.sc_ipc_release(ctypes.c_void_p(p))
+        self._opened = []
 
 
 class PieceComm:
@@ -287,12 +378,16 @@ class ShardedPower:
     issuing 2*P launches per step."""
 
     def __init__(self, shard, plan: ShardPlan, rank: int, *, sign: float = 1.0,
-                 sym: bool = False, group=None):
+                 sym: bool = False, group=None, comm=None):
         self.shard, self.plan, self.rank = shard, plan, rank
         self.sign, self.sym = sign, sym
         n = int(plan.sizes[rank])
-        self.comm = PieceComm(plan, rank, group)
-        self.z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
+        if comm is None:
+            self.comm = PieceComm(plan, rank, group)
+            self.z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
+        else:  # fused peer exchange: z lives in the handle's mirrored allocation
+            self.comm = comm
+            self.z = [comm.z0, comm.z1]
         self.x = [shard.zeros(n), shard.zeros(n)]
         self.x0 = shard.zeros(n)
         self.graph = None
@@ -319,8 +414,8 @@ class ShardedPower:
         """Record T steps (from the current x0 buffer) into a CUDA graph; NCCL only."""
         import torch
 
-        if not self.comm.nccl:
-            raise InputError("CUDA-graph capture needs the NCCL backend")
+        if not getattr(self.comm, "nccl", True):
+            raise InputError("CUDA-graph capture needs the NCCL backend or the peer exchange")
         self._enqueue(T)  # warm: communicator and side-stream setup outside the capture
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -381,7 +476,8 @@ def bench_main(args, metric: str, unit: str):
     params = SbmParams(n=world * n_loc, k=10 * world, p=40 / (10**5 - 1),
                        q=4 / (world * n_loc - 10**5), seed=0)
     T = 100
-    pieces = int(getattr(args, "pieces", 0) or (4 if world > 1 else 1))
+    p2p = getattr(args, "comm", "nccl") == "p2p"
+    pieces = 1 if p2p else int(getattr(args, "pieces", 0) or (4 if world > 1 else 1))
     starts = np.arange(world + 1, dtype=np.int64) * n_loc
     rp, col, deg, iso = sbm_rows(params, int(starts[rank]), int(starts[rank + 1]))
     iso_t = torch.tensor([iso], device="cuda")
@@ -394,7 +490,11 @@ def bench_main(args, metric: str, unit: str):
     dist.all_reduce(nnz_t)
     nnz_total = int(nnz_t.item())
     stream = torch.cuda.current_stream()
-    runner = ShardedPower(shard, plan, rank)
+    comm = None
+    if p2p:
+        comm = P2PComm(shard, plan, rank)
+        comm.link()
+    runner = ShardedPower(shard, plan, rank, comm=comm)
     use_graph = not getattr(args, "no_graph", False)
 
     def one_step():
@@ -420,14 +520,14 @@ def bench_main(args, metric: str, unit: str):
     tot_ms = float(ms.item())
     # the all-gathers alone (NVLink): T steps x P pieces
     zbuf = shard.zeros(plan.ncols)
-    comm = PieceComm(plan, rank)
+    agc = PieceComm(plan, rank)
     torch.cuda.synchronize()
     dist.barrier()
     e0.record(stream)
     for _ in range(T):
         for j in range(plan.pieces):
-            comm.gather_piece(zbuf, j)
-        comm.finish()
+            agc.gather_piece(zbuf, j)
+        agc.finish()
     e1.record(stream)
     torch.cuda.synchronize()
     ag = torch.tensor([e0.elapsed_time(e1) / T], device="cuda", dtype=torch.float64)
@@ -442,14 +542,20 @@ def bench_main(args, metric: str, unit: str):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config2 block per GPU (SBM n={params.n}, k={params.k})",
                        "n_per_gpu": n_loc, "nnz_total": nnz_total, "T": T, "pieces": plan.pieces,
-                       "cuda_graph": use_graph,
-                       "parallelism": f"row-block shards x{world}, pipelined NCCL all-gather "
-                                      f"of z ({plan.pieces} pieces per step)"},
+                       "cuda_graph": use_graph, "comm": "p2p" if p2p else "nccl",
+                       "parallelism": (f"row-block shards x{world}, z stored into the peers' "
+                                       "buffers by the SpMV epilogue + flag barrier"
+                                       if p2p else
+                                       f"row-block shards x{world}, pipelined NCCL all-gather "
+                                       f"of z ({plan.pieces} pieces per step)")},
             "allgather": {"ms_per_step": ag_ms, "recv_bytes_per_gpu": recv_bytes,
                           "gbs_per_gpu": recv_bytes / (ag_ms / 1e3) / 1e9 if world > 1 else 0.0},
-            "gpu_launches": args.steps * (1 + T * plan.pieces + plan.pieces),
+            "gpu_launches": args.steps * (1 + (T + 1) * plan.pieces
+                                          + ((T + 1) if p2p and world > 1 else 0)),
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     shard.close()
     dist.destroy_process_group()
 

@@ -116,3 +116,69 @@ def test_nccl_pipeline_cuda_graph_bit_exact(tmp_path):
     for i in (1, 2):
         assert np.array_equal(r[f"x{i}"], xT)
         assert np.array_equal(r[f"f{i}"], f)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_peer_exchange_emulated_on_one_gpu(world):
+    """The fused exchange (SpMV epilogue stores every z value into the peers' z allocations,
+    sc_shard_set_peers): W shards in one process on one GPU, wired with each other's
+    buffers; the host serialises the shards' steps on one stream (no cross-kernel waiting, so
+    the barrier kernel is not used).  Bit-exact against the single-graph oracle."""
+    import torch
+
+    g = _graph()
+    rp, col, val, deg = g.row_offsets, g.col_indices.astype(np.int32), g.weights, g.degrees
+    starts = D.partition_rows(rp, world)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(world)]
+    plan = D.ShardPlan(starts, [D.sell_order(x) for x in lrps], [D.n_sell_rows(x) for x in lrps])
+    shards = []
+    for r in range(world):
+        lo, hi = int(starts[r]), int(starts[r + 1])
+        shards.append(D.CudaShard(lrps[r], plan.rename(col[rp[lo]:rp[hi]]), val[rp[lo]:rp[hi]],
+                                  deg[lo:hi], plan, r, 0))
+    comms = [D.P2PComm(s, plan, r) for r, s in enumerate(shards)]
+    D.P2PComm.link_local(comms)
+    runners = [D.ShardedPower(s, plan, r, comm=c) for r, (s, c) in enumerate(zip(shards, comms))]
+    T = 11
+    for rn in runners:
+        rn.sample(5)
+    for r, rn in enumerate(runners):
+        rn.shard.scale_piece(0, rn.x0, rn.z[0])
+    torch.cuda.synchronize()
+    for t in range(T):
+        a, b = t & 1, (t & 1) ^ 1
+        for rn in runners:
+            rn.shard.step_piece(0, rn.z[a], rn.x0 if t == 0 else rn.x[a], rn.x[b], rn.z[b])
+        torch.cuda.synchronize()
+    xs = np.concatenate([rn.shard.to_original(rn.x[T & 1]) for rn in runners])
+    fs = np.concatenate([rn.shard.to_original(rn.shard.local_z(rn.z[T & 1])) for rn in runners])
+    # every rank holds the whole z space
+    for rn in runners[1:]:
+        assert np.array_equal(rn.z[T & 1].cpu().numpy(), runners[0].z[T & 1].cpu().numpy())
+    x0 = O.irwin_hall(deg, 5)
+    xT, f = O.power_iterate(rp, col, val, deg, x0, T)
+    assert np.array_equal(xs, xT)
+    assert np.array_equal(fs, f)
+    for s in shards:
+        s.close()
+
+
+def test_peer_exchange_requires_own_buffers():
+    """With peers set, a z_out outside the handle's mirrored allocation is refused."""
+    from paper_2310_10939_b200.errors import SpeclusterError
+
+    g = _graph(n=600, m=5000)
+    rp, col, val, deg = g.row_offsets, g.col_indices.astype(np.int32), g.weights, g.degrees
+    starts = D.partition_rows(rp, 2)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(2)]
+    plan = D.ShardPlan(starts, [D.sell_order(x) for x in lrps], [D.n_sell_rows(x) for x in lrps])
+    shards = [D.CudaShard(lrps[r], plan.rename(col[rp[int(starts[r])]:rp[int(starts[r + 1])]]),
+                          val[rp[int(starts[r])]:rp[int(starts[r + 1])]],
+                          deg[int(starts[r]):int(starts[r + 1])], plan, r, 0) for r in range(2)]
+    comms = [D.P2PComm(s, plan, r) for r, s in enumerate(shards)]
+    D.P2PComm.link_local(comms)
+    x = shards[0].zeros(shards[0].n)
+    with pytest.raises(SpeclusterError, match="z buffers"):
+        shards[0].scale_piece(0, x, shards[0].zeros(plan.ncols))
+    for s in shards:
+        s.close()
