@@ -211,6 +211,21 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t restarts, const int64_
 int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *seg_off, int32_t device,
                   double *totals, double *chunk_starts);
 
+/* ---- evaluation metrics (metrics.py:36-201 of the reference) -------------------------- */
+/* sums_out[q] = np.add.at(zeros(nkeys), keys, vals)[q] bit for bit (stable device sort by key,
+ * then the exact sequential sums above); counts_out (nullable) = occurrences of every key.
+ * Used for part volumes, the matched-volume intersections and the cut weights. */
+int32_t sc_keyed_sums(const int32_t *keys, const double *vals, int64_t m, int32_t nkeys,
+                      int32_t device, double *sums_out, int64_t *counts_out);
+/* cut_out[c] = sum of the weights (1.0 if w is NULL) of the CSR entries (r, col) with
+ * labels[r] = c != labels[col], added in CSR order (np.add.at, metrics.py:143-146) */
+int32_t sc_cut_sums(const int64_t *row_ptr, const int32_t *col, const double *w,
+                    const int64_t *labels, int64_t n, int64_t nnz, int32_t k, int32_t device,
+                    double *cut_out);
+/* counts_out[a * kb + b] = #{i : la[i] = a, lb[i] = b} (the contingency table) */
+int32_t sc_contingency(const int64_t *la, const int64_t *lb, int64_t n, int32_t ka, int32_t kb,
+                       int32_t device, int64_t *counts_out);
+
 #ifdef __cplusplus
 }
 #endif

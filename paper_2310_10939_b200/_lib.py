@@ -49,6 +49,7 @@ EXPORTS = (
     "sc_shard_step_range", "sc_shard_scale_range", "sc_generate_sbm", "sc_csr_info",
     "sc_csr_download", "sc_csr_destroy", "sc_graph_create_from_csr", "sc_shard_buffers",
     "sc_shard_set_peers", "sc_shard_barrier", "sc_ipc_export", "sc_ipc_import", "sc_ipc_release",
+    "sc_keyed_sums", "sc_contingency", "sc_cut_sums",
 )
 
 _lib = None
@@ -103,6 +104,9 @@ def load() -> ctypes.CDLL:
         "sc_ipc_export": ([P, P], i32),
         "sc_ipc_import": ([P, i32, PP], i32),
         "sc_ipc_release": ([P], i32),
+        "sc_keyed_sums": ([P, P, i64, i32, i32, P, P], i32),
+        "sc_contingency": ([P, P, i64, i32, i32, i32, P], i32),
+        "sc_cut_sums": ([P, P, P, P, i64, i64, i32, i32, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -21,6 +21,8 @@
 #include <chrono>
 #include <cmath>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cstring>
 #include <vector>
 
 #include "sc_common.cuh"
@@ -1384,25 +1386,26 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
 
 }  // extern "C"
 
-extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *seg_off,
-                             int32_t device, double *totals, double *chunk_starts) {
-    SC_REQUIRE(vals && seg_off && totals && nseg >= 1, SC_E_INVALID, "null argument");
-    for (int s = 0; s < nseg; ++s)
-        SC_REQUIRE(seg_off[s + 1] >= seg_off[s], SC_E_RANGE, "segment offsets decrease");
-    SC_CUDA(cudaSetDevice(device));
-    const int64_t n = seg_off[nseg];
+namespace sc {
+// exact sequential sums of the nseg segments of device array d_vals (host segment offsets):
+// the seqsum pipeline of the k-means replica run once, synchronously, on the current device
+static int32_t seqsum_device(const double *d_vals, int32_t nseg, const int64_t *seg_off,
+                             double *totals, double *chunk_starts) {
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     std::vector<int64_t> cofs(nseg + 1, 0);
     for (int s = 0; s < nseg; ++s)
         cofs[s + 1] = cofs[s] + (seg_off[s + 1] - seg_off[s] + kSeqChunk - 1) / kSeqChunk;
     const int64_t nch = cofs[nseg];
-    double *d_vals = nullptr, *d_A = nullptr, *d_vmax = nullptr, *d_cs = nullptr, *d_tot = nullptr;
+    double *d_A = nullptr, *d_vmax = nullptr, *d_cs = nullptr, *d_tot = nullptr;
     int64_t *d_seg = nullptr, *d_cofs = nullptr, *d_q0 = nullptr, *d_q1 = nullptr, *d_nch = nullptr;
     int32_t *d_kp = nullptr, *d_neg = nullptr, *d_skp = nullptr;
     int64_t *d_sq0 = nullptr, *d_sq1 = nullptr;
     double *d_svm = nullptr;
     auto al = [](void **p, size_t b) { return cudaMalloc(p, b ? b : 16); };
-    cudaError_t e = al((void **)&d_vals, n * 8);
-    if (!e) e = al((void **)&d_A, nch * 8);
+    const size_t nsup = (size_t)nch / kSuper + 1;
+    cudaError_t e = al((void **)&d_A, nch * 8);
     if (!e) e = al((void **)&d_vmax, nch * 8);
     if (!e) e = al((void **)&d_cs, nch * 8);
     if (!e) e = al((void **)&d_tot, nseg * 8);
@@ -1413,11 +1416,10 @@ extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *se
     if (!e) e = al((void **)&d_nch, 8);
     if (!e) e = al((void **)&d_kp, nch * 4);
     if (!e) e = al((void **)&d_neg, nseg * 4);
-    if (!e) e = al((void **)&d_skp, (nch / kSuper + 1) * 4);
-    if (!e) e = al((void **)&d_sq0, (nch / kSuper + 1) * 8);
-    if (!e) e = al((void **)&d_sq1, (nch / kSuper + 1) * 8);
-    if (!e) e = al((void **)&d_svm, (nch / kSuper + 1) * 8);
-    if (!e) e = cudaMemcpy(d_vals, vals, n * 8, cudaMemcpyHostToDevice);
+    if (!e) e = al((void **)&d_skp, nsup * 4);
+    if (!e) e = al((void **)&d_sq0, nsup * 8);
+    if (!e) e = al((void **)&d_sq1, nsup * 8);
+    if (!e) e = al((void **)&d_svm, nsup * 8);
     if (!e) e = cudaMemcpy(d_seg, seg_off, (nseg + 1) * 8, cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(d_cofs, cofs.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(d_nch, &nch, 8, cudaMemcpyHostToDevice);
@@ -1425,20 +1427,241 @@ extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *se
     if (!e) {
         SegView v{d_vals, d_seg, d_cofs, nseg, nullptr, 1};
         SeqWork w{d_A, d_vmax, d_kp, d_q0, d_q1, d_cs, d_neg, d_tot, d_sq0, d_sq1, d_svm, d_skp};
-        const int gw = (int)std::min<int64_t>((nch * 32 + 255) / 256 + 1, 148 * 8);
+        const int gw = (int)std::min<int64_t>((nch * 32 + 255) / 256 + 1, (int64_t)sms * 8);
         const int gs = (nseg * 32 + 255) / 256;
         k_seq_summarize<<<gw, 256>>>(v, w, d_nch);
         k_seq_predict<<<gs, 256>>>(v, w);
         k_seq_chunkmap<<<gw, 256>>>(v, w, d_nch);
         k_seq_superize<<<gw, 256>>>(v, w, d_nch);
-        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem>>>(v, w, 1);
+        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem>>>(
+            v, w, chunk_starts != nullptr);
         e = cudaDeviceSynchronize();
     }
     if (!e) e = cudaMemcpy(totals, d_tot, nseg * 8, cudaMemcpyDeviceToHost);
     if (!e && chunk_starts) e = cudaMemcpy(chunk_starts, d_cs, nch * 8, cudaMemcpyDeviceToHost);
-    void *ps[] = {d_vals, d_A, d_vmax, d_cs, d_tot, d_seg, d_cofs, d_q0, d_q1, d_nch, d_kp, d_neg,
+    void *ps[] = {d_A, d_vmax, d_cs, d_tot, d_seg, d_cofs, d_q0, d_q1, d_nch, d_kp, d_neg,
                   d_skp, d_sq0, d_sq1, d_svm};
     for (void *p : ps) cudaFree(p);
     SC_CUDA(e);
+    return SC_OK;
+}
+
+// histograms; out-of-range keys are not counted (the totals then disagree with m / n and
+// the caller reports the input error)
+__global__ void k_key_hist(const int32_t *__restrict__ keys, int64_t m, int32_t nkeys,
+                           int64_t *__restrict__ cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t q = keys[i];
+        if (q >= 0 && q < nkeys) atomicAdd(reinterpret_cast<unsigned long long *>(cnt + q), 1ull);
+    }
+}
+
+__global__ void k_pair_hist(const int64_t *__restrict__ a, const int64_t *__restrict__ b, int64_t n,
+                            int64_t ka, int64_t kb, int64_t *__restrict__ cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = a[i], y = b[i];
+        if (x >= 0 && x < ka && y >= 0 && y < kb)
+            atomicAdd(reinterpret_cast<unsigned long long *>(cnt + x * kb + y), 1ull);
+    }
+}
+}  // namespace sc
+
+extern "C" int32_t sc_seqsum(const double *vals, int32_t nseg, const int64_t *seg_off,
+                             int32_t device, double *totals, double *chunk_starts) {
+    using namespace sc;
+    SC_REQUIRE(vals && seg_off && totals && nseg >= 1, SC_E_INVALID, "null argument");
+    for (int s = 0; s < nseg; ++s)
+        SC_REQUIRE(seg_off[s + 1] >= seg_off[s], SC_E_RANGE, "segment offsets decrease");
+    SC_CUDA(cudaSetDevice(device));
+    const int64_t n = seg_off[nseg];
+    double *d_vals = nullptr;
+    SC_CUDA(cudaMalloc((void **)&d_vals, n ? n * 8 : 16));
+    cudaError_t e = cudaMemcpy(d_vals, vals, n * 8, cudaMemcpyHostToDevice);
+    if (e) {
+        cudaFree(d_vals);
+        SC_CUDA(e);
+    }
+    const int32_t st = seqsum_device(d_vals, nseg, seg_off, totals, chunk_starts);
+    cudaFree(d_vals);
+    return st;
+}
+
+namespace sc {
+// np.add.at over device arrays (dk, dv are consumed as sort input)
+static int32_t keyed_sums_device(int32_t *dk, double *dv, int64_t m, int32_t nkeys,
+                                 double *sums_out, int64_t *counts_out) {
+    int32_t *dk2 = nullptr;
+    double *dv2 = nullptr;
+    int64_t *dc = nullptr;
+    void *tmp = nullptr;
+    size_t tb = 0;
+    int end_bit = 1;
+    while ((1ll << end_bit) < (long long)nkeys) ++end_bit;
+    std::vector<int64_t> cnt((size_t)nkeys), seg((size_t)nkeys + 1, 0);
+    cudaError_t e = cudaMalloc((void **)&dk2, m ? m * 4 : 16);
+    if (!e) e = cudaMalloc((void **)&dv2, m ? m * 8 : 16);
+    if (!e) e = cudaMalloc((void **)&dc, (size_t)nkeys * 8);
+    if (!e) e = cudaMemset(dc, 0, (size_t)nkeys * 8);
+    if (!e && m) {
+        k_key_hist<<<1184, 256>>>(dk, m, nkeys, dc);
+        e = cudaGetLastError();
+    }
+    if (!e) e = cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dk2, dv, dv2, (int)m, 0, end_bit);
+    if (!e) e = cudaMalloc(&tmp, tb ? tb : 16);
+    if (!e) e = cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dk2, dv, dv2, (int)m, 0, end_bit);
+    if (!e) e = cudaMemcpy(cnt.data(), dc, (size_t)nkeys * 8, cudaMemcpyDeviceToHost);
+    int32_t st = SC_OK;
+    if (!e) {
+        for (int32_t q = 0; q < nkeys; ++q) seg[(size_t)q + 1] = seg[(size_t)q] + cnt[(size_t)q];
+        if (seg[(size_t)nkeys] != m) {
+            st = fail(SC_E_RANGE, "keys must lie in [0, %d)", nkeys);
+        } else {
+            st = seqsum_device(dv2, nkeys, seg.data(), sums_out, nullptr);
+            if (counts_out) std::memcpy(counts_out, cnt.data(), (size_t)nkeys * 8);
+        }
+    }
+    for (void *p : {(void *)dk2, (void *)dv2, (void *)dc, tmp}) cudaFree(p);
+    SC_CUDA(e);
+    return st;
+}
+
+// crossing entries of the CSR (label[row] != label[col]) in CSR order: key = label[row],
+// val = weight (1.0 if w is null); non-crossing entries get key -1
+__global__ void k_cut_keys(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           const double *__restrict__ w, const int64_t *__restrict__ lab, int64_t n,
+                           int32_t *__restrict__ keys, double *__restrict__ vals) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lr = lab[r];
+        for (int64_t j = rp[r]; j < rp[r + 1]; ++j) {
+            const bool cross = lab[col[j]] != lr;
+            keys[j] = cross ? (int32_t)lr : -1;
+            vals[j] = w ? w[j] : 1.0;
+        }
+    }
+}
+
+struct NonNeg {
+    __device__ bool operator()(const int32_t &k) const { return k >= 0; }
+};
+
+__global__ void k_flags_from_keys(const int32_t *__restrict__ keys, int64_t m,
+                                  int32_t *__restrict__ flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flags[i] = keys[i] >= 0;
+}
+}  // namespace sc
+
+// np.add.at(out, keys, vals) for out = zeros(nkeys): stable sort by key on the device, then
+// every key's values summed left to right in input order (the exact np.add.at rounding).
+extern "C" int32_t sc_keyed_sums(const int32_t *keys, const double *vals, int64_t m,
+                                 int32_t nkeys, int32_t device, double *sums_out,
+                                 int64_t *counts_out) {
+    using namespace sc;
+    SC_REQUIRE(keys && vals && sums_out && nkeys >= 1 && m >= 0 && m < (int64_t(1) << 31),
+               SC_E_INVALID, "bad argument");
+    SC_CUDA(cudaSetDevice(device));
+    int32_t *dk = nullptr;
+    double *dv = nullptr;
+    cudaError_t e = cudaMalloc((void **)&dk, m ? m * 4 : 16);
+    if (!e) e = cudaMalloc((void **)&dv, m ? m * 8 : 16);
+    if (!e && m) e = cudaMemcpy(dk, keys, m * 4, cudaMemcpyHostToDevice);
+    if (!e && m) e = cudaMemcpy(dv, vals, m * 8, cudaMemcpyHostToDevice);
+    int32_t st = SC_OK;
+    if (!e) st = keyed_sums_device(dk, dv, m, nkeys, sums_out, counts_out);
+    cudaFree(dk);
+    cudaFree(dv);
+    SC_CUDA(e);
+    return st;
+}
+
+// cut weight of every part: np.add.at(cut, labels[src[crossing]], w[crossing]) with the
+// crossing entries in CSR order (partition_conductances, metrics.py:143-146)
+extern "C" int32_t sc_cut_sums(const int64_t *row_ptr, const int32_t *col, const double *w,
+                               const int64_t *labels, int64_t n, int64_t nnz, int32_t k,
+                               int32_t device, double *cut_out) {
+    using namespace sc;
+    SC_REQUIRE(row_ptr && (col || nnz == 0) && labels && cut_out && n >= 1 && k >= 1 &&
+                   nnz < (int64_t(1) << 31),
+               SC_E_INVALID, "bad argument");
+    for (int64_t i = 0; i < n; ++i)
+        SC_REQUIRE(labels[i] >= 0 && labels[i] < k, SC_E_RANGE, "label %lld of vertex %lld "
+                   "outside [0, %d)", (long long)labels[i], (long long)i, k);
+    SC_CUDA(cudaSetDevice(device));
+    int64_t *drp = nullptr, *dlab = nullptr;
+    int32_t *dcol = nullptr, *dkeys = nullptr, *dk = nullptr, *dnsel = nullptr;
+    double *dw = nullptr, *dvals = nullptr, *dv = nullptr;
+    void *tmp = nullptr;
+    size_t tb = 0;
+    cudaError_t e = cudaMalloc((void **)&drp, (n + 1) * 8);
+    if (!e) e = cudaMalloc((void **)&dlab, n * 8);
+    if (!e) e = cudaMalloc((void **)&dcol, nnz ? nnz * 4 : 16);
+    if (!e && w) e = cudaMalloc((void **)&dw, nnz ? nnz * 8 : 16);
+    if (!e) e = cudaMalloc((void **)&dkeys, nnz ? nnz * 4 : 16);
+    if (!e) e = cudaMalloc((void **)&dvals, nnz ? nnz * 8 : 16);
+    if (!e) e = cudaMalloc((void **)&dk, nnz ? nnz * 4 : 16);
+    if (!e) e = cudaMalloc((void **)&dv, nnz ? nnz * 8 : 16);
+    if (!e) e = cudaMalloc((void **)&dnsel, 16);
+    if (!e) e = cudaMemcpy(drp, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(dlab, labels, n * 8, cudaMemcpyHostToDevice);
+    if (!e && nnz) e = cudaMemcpy(dcol, col, nnz * 4, cudaMemcpyHostToDevice);
+    if (!e && w && nnz) e = cudaMemcpy(dw, w, nnz * 8, cudaMemcpyHostToDevice);
+    if (!e) {
+        k_cut_keys<<<1184, 256>>>(drp, dcol, dw, dlab, n, dkeys, dvals);
+        e = cudaGetLastError();
+    }
+    // order-preserving compaction of the crossing entries (keys >= 0), values alongside
+    if (!e) e = cub::DeviceSelect::If(nullptr, tb, dkeys, dk, dnsel, (int)nnz, NonNeg());
+    size_t tb2 = 0;
+    if (!e) e = cub::DeviceSelect::Flagged(nullptr, tb2, dvals, dkeys, dv, dnsel, (int)nnz);
+    if (!e) e = cudaMalloc(&tmp, std::max(std::max(tb, tb2), (size_t)16));
+    int32_t nsel = 0;
+    // values first (flags = keys >= 0 computed from a copy of keys as 0/1), then keys
+    if (!e) {
+        k_flags_from_keys<<<1184, 256>>>(dkeys, nnz, dk);
+        e = cudaGetLastError();
+    }
+    if (!e) e = cub::DeviceSelect::Flagged(tmp, tb2, dvals, dk, dv, dnsel, (int)nnz);
+    if (!e) e = cub::DeviceSelect::If(tmp, tb, dkeys, dk, dnsel, (int)nnz, NonNeg());
+    if (!e) e = cudaMemcpy(&nsel, dnsel, 4, cudaMemcpyDeviceToHost);
+    int32_t st = SC_OK;
+    if (!e) st = keyed_sums_device(dk, dv, nsel, k, cut_out, nullptr);
+    for (void *p : {(void *)drp, (void *)dlab, (void *)dcol, (void *)dw, (void *)dkeys,
+                    (void *)dvals, (void *)dk, (void *)dv, (void *)dnsel, tmp})
+        cudaFree(p);
+    SC_CUDA(e);
+    return st;
+}
+
+// contingency counts[a][b] of two labelings (exact integer counts)
+extern "C" int32_t sc_contingency(const int64_t *la, const int64_t *lb, int64_t n, int32_t ka,
+                                  int32_t kb, int32_t device, int64_t *counts_out) {
+    using namespace sc;
+    SC_REQUIRE(la && lb && counts_out && n >= 0 && ka >= 1 && kb >= 1, SC_E_INVALID,
+               "bad argument");
+    SC_CUDA(cudaSetDevice(device));
+    int64_t *da = nullptr, *db = nullptr, *dc = nullptr;
+    const size_t cells = (size_t)ka * kb;
+    cudaError_t e = cudaMalloc((void **)&da, n ? n * 8 : 16);
+    if (!e) e = cudaMalloc((void **)&db, n ? n * 8 : 16);
+    if (!e) e = cudaMalloc((void **)&dc, cells * 8);
+    if (!e && n) e = cudaMemcpy(da, la, n * 8, cudaMemcpyHostToDevice);
+    if (!e && n) e = cudaMemcpy(db, lb, n * 8, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemset(dc, 0, cells * 8);
+    if (!e && n) {
+        k_pair_hist<<<1184, 256>>>(da, db, n, ka, kb, dc);
+        e = cudaGetLastError();
+    }
+    if (!e) e = cudaMemcpy(counts_out, dc, cells * 8, cudaMemcpyDeviceToHost);
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dc);
+    SC_CUDA(e);
+    int64_t tot = 0;
+    for (size_t c = 0; c < cells; ++c) tot += counts_out[c];
+    SC_REQUIRE(tot == n, SC_E_RANGE, "labels must lie in [0, %d) x [0, %d)", ka, kb);
     return SC_OK;
 }
