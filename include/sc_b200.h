@@ -127,6 +127,14 @@ int32_t sc_set_x0(sc_graph *g, const double *x0_host);
 int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, double *xT_out,
                          double *f_out, sc_timing *t_out);
 
+/* Block power method for the reference's pm_log_k mode (pipeline.py:144-147): T steps of
+ * the signless operator M = (I + D^-1/2 A D^-1/2) / 2 on an (n, L) block x0 (host,
+ * row-major, original vertex order, 1 <= L <= 16), every column bit-identical to
+ * power_method(SignlessLaplacianOp(g), x0, T) (spectral.py:87-102).  raw_out = M^T x0,
+ * scaled_out = raw * d^-1/2 per row (pipeline.py:157); both host (n, L), nullable. */
+int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *x0,
+                               double *raw_out, double *scaled_out, sc_timing *t_out);
+
 /* ---- device-pointer shard step (multi-GPU composition) ------------------ */
 /* One iteration on a shard using caller-owned device buffers, launched on `stream` (a
  * cudaStream_t; 0 = the legacy default stream), all buffers in renumbered order:

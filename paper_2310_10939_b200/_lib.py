@@ -49,7 +49,7 @@ EXPORTS = (
     "sc_shard_step_range", "sc_shard_scale_range", "sc_generate_sbm", "sc_csr_info",
     "sc_csr_download", "sc_csr_destroy", "sc_graph_create_from_csr", "sc_shard_buffers",
     "sc_shard_set_peers", "sc_shard_barrier", "sc_ipc_export", "sc_ipc_import", "sc_ipc_release",
-    "sc_keyed_sums", "sc_contingency", "sc_cut_sums",
+    "sc_keyed_sums", "sc_contingency", "sc_cut_sums", "sc_power_iterate_block",
 )
 
 _lib = None
@@ -107,6 +107,7 @@ def load() -> ctypes.CDLL:
         "sc_keyed_sums": ([P, P, i64, i32, i32, P, P], i32),
         "sc_contingency": ([P, P, i64, i32, i32, i32, P], i32),
         "sc_cut_sums": ([P, P, P, P, i64, i64, i32, i32, P], i32),
+        "sc_power_iterate_block": ([P, i32, i32, P, P, P, ctypes.POINTER(Timing)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -220,6 +220,143 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
     peer_fence(a);
 }
 
+// ---- block power method: L columns at once (pm_log_k, spectral.py:52-57 on an (n, L)
+// block).  scipy's csr_matvecs adds, per row and per stored entry, a_ij * x_jk to every
+// column k in turn, so each column sees exactly the single-vector summation order; here a
+// lane owns a row and keeps L accumulators, and the gathered vector z = d^-1/2 x is stored
+// row-major [n][L] so one gather brings a row's L values (one or a few sectors) instead of
+// L scattered ones.
+struct BlkArgs {
+    const int64_t *slice_ptr;
+    const uint32_t *col;
+    const double *val;
+    const int64_t *wide_ptr;
+    const uint32_t *wcol;
+    const double *wval;
+    const double *isd;  // d^-1/2, renumbered
+    const double *x_in, *z_in;
+    double *x_out, *z_out;
+    int64_t n_sell, nslices, n_wide;
+};
+
+template <int L>
+__device__ __forceinline__ void blk_epilogue(const BlkArgs &a, int64_t r, const double (&acc)[L],
+                                             const double (&xr)[L], double sc) {
+#pragma unroll
+    for (int q = 0; q < L; ++q) {
+        const double y = __dadd_rn(__dmul_rn(0.5, xr[q]), __dmul_rn(0.5, __dmul_rn(sc, acc[q])));
+        a.x_out[r * L + q] = y;
+        a.z_out[r * L + q] = __dmul_rn(sc, y);
+    }
+}
+
+template <int L, bool UNIT>
+__global__ void __launch_bounds__(kStepTPB) k_blk_step(BlkArgs a) {
+    constexpr int U = L <= 2 ? 4 : 2;  // entries in flight per lane
+    const int lane = threadIdx.x & 31;
+    const int64_t sl = (int64_t)blockIdx.x * (kStepTPB / 32) + (threadIdx.x >> 5);
+    if (sl >= a.nslices) return;
+    const int64_t r = sl * kSlice + lane;
+    const bool live = r < a.n_sell;
+    double xr[L], acc[L];
+    double sc = 1.0;
+#pragma unroll
+    for (int q = 0; q < L; ++q) {
+        acc[q] = 0.0;
+        xr[q] = live ? a.x_in[r * L + q] : 0.0;
+    }
+    if (live) sc = a.isd[r];
+    const int64_t base = a.slice_ptr[sl];
+    const int width = (int)((a.slice_ptr[sl + 1] - base) >> 5);
+    const uint32_t *cp = a.col + base + lane;
+    const double *vp = UNIT ? nullptr : a.val + base + lane;
+    for (int t = 0; t < width; t += U) {
+        uint32_t c[U];
+        double v[U][L], w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            c[u] = t + u < width ? __ldcs(cp + (int64_t)(t + u) * kSlice) : kPad;
+            w[u] = (!UNIT && c[u] != kPad) ? __ldcs(vp + (int64_t)(t + u) * kSlice) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < L; ++q)
+                v[u][q] = c[u] != kPad ? __ldg(a.z_in + (int64_t)c[u] * L + q) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (c[u] != kPad)
+#pragma unroll
+                for (int q = 0; q < L; ++q)
+                    acc[q] = __dadd_rn(acc[q], UNIT ? v[u][q] : __dmul_rn(w[u], v[u][q]));
+    }
+    if (live) blk_epilogue<L>(a, r, acc, xr, sc);
+}
+
+// wide rows: one warp per row; 32 entries per batch are gathered (lane = entry) into the
+// warp's shared-memory slot, lanes 0..L-1 then fold them in order for their column while the
+// next batch's gathers are in flight
+template <int L, bool UNIT>
+__global__ void __launch_bounds__(kStepTPB) k_blk_wide(BlkArgs a) {
+    __shared__ double wb[kStepTPB / 32][32][L];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t w = (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
+    if (w >= a.n_wide) return;
+    const int64_t r = a.n_sell + w;
+    const int64_t lo = a.wide_ptr[w], hi = a.wide_ptr[w + 1];
+    double v[L];
+    auto gather = [&](int64_t j) {
+#pragma unroll
+        for (int q = 0; q < L; ++q) v[q] = 0.0;
+        if (j < hi) {
+            const int64_t c = __ldcs(a.wcol + j);
+            const double wt = UNIT ? 1.0 : __ldcs(a.wval + j);
+#pragma unroll
+            for (int q = 0; q < L; ++q) {
+                const double z = __ldg(a.z_in + c * L + q);
+                v[q] = UNIT ? z : __dmul_rn(wt, z);
+            }
+        }
+    };
+    double acc = 0.0;
+    gather(lo + lane);
+    for (int64_t b = lo; b < hi; b += 32) {
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < L; ++q) wb[warp][lane][q] = v[q];
+        __syncwarp();
+        if (b + 32 < hi) gather(b + 32 + lane);
+        if (lane < L) {
+            const int m = (int)(hi - b < 32 ? hi - b : 32);
+            for (int e = 0; e < m; ++e) acc = __dadd_rn(acc, wb[warp][e][lane]);
+        }
+    }
+    // lane q holds column q's sum; lanes 0..L-1 finish their column
+    if (lane < L) {
+        const double sc = a.isd[r], xr = a.x_in[r * L + lane];
+        const double y = __dadd_rn(__dmul_rn(0.5, xr), __dmul_rn(0.5, __dmul_rn(sc, acc)));
+        a.x_out[r * L + lane] = y;
+        a.z_out[r * L + lane] = __dmul_rn(sc, y);
+    }
+}
+
+// out[i*L + q] = in[idx[i]*L + q] (row permutation of an [n][L] block), and z = s * x rows
+__global__ void k_gather_rows(const double *__restrict__ in, const int32_t *__restrict__ idx,
+                              double *__restrict__ out, int64_t n, int L) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * L;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / L, q = t - i * L;
+        out[t] = in[(int64_t)idx[i] * L + q];
+    }
+}
+
+__global__ void k_scale_rows(const double *__restrict__ x, const double *__restrict__ s,
+                             double *__restrict__ z, int64_t n, int L) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * L;
+         t += (int64_t)gridDim.x * blockDim.x)
+        z[t] = __dmul_rn(s[t / L], x[t]);
+}
+
 // z[col_offset + i] = x[i] / d[i]   (rw)   or   x[i] * d[i]^-1/2   (sym)
 __global__ void k_scale(const double *__restrict__ x, const double *__restrict__ scale,
                         double *__restrict__ z, int64_t n, int64_t off, int sym,
@@ -1192,6 +1329,124 @@ int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, do
         t_out->d2h_ms = std::chrono::duration<double, std::milli>(h1 - h0).count();
     }
     return SC_OK;
+}
+
+}  // extern "C"
+
+namespace sc {
+template <int L>
+static void launch_blk(const sc_graph *g, const BlkArgs &a, cudaStream_t s) {
+    constexpr int wpb = kStepTPB / 32;
+    if (g->n_wide) {
+        cudaEventRecord(g->ev_fork, s);
+        cudaStreamWaitEvent(g->side, g->ev_fork, 0);
+        const unsigned wb = (unsigned)((g->n_wide + wpb - 1) / wpb);
+        if (g->unit) k_blk_wide<L, true><<<wb, kStepTPB, 0, g->side>>>(a);
+        else k_blk_wide<L, false><<<wb, kStepTPB, 0, g->side>>>(a);
+    }
+    if (g->nslices) {
+        const unsigned sb = (unsigned)((g->nslices + wpb - 1) / wpb);
+        if (g->unit) k_blk_step<L, true><<<sb, kStepTPB, 0, s>>>(a);
+        else k_blk_step<L, false><<<sb, kStepTPB, 0, s>>>(a);
+    }
+    if (g->n_wide) {
+        cudaEventRecord(g->ev_join, g->side);
+        cudaStreamWaitEvent(s, g->ev_join, 0);
+    }
+}
+
+template <int... Ls>
+struct BlkDispatch;
+template <>
+struct BlkDispatch<> {
+    static bool run(int, const sc_graph *, const BlkArgs &, cudaStream_t) { return false; }
+};
+template <int L0, int... Ls>
+struct BlkDispatch<L0, Ls...> {
+    static bool run(int L, const sc_graph *g, const BlkArgs &a, cudaStream_t s) {
+        if (L == L0) {
+            launch_blk<L0>(g, a, s);
+            return true;
+        }
+        return BlkDispatch<Ls...>::run(L, g, a, s);
+    }
+};
+using BlkAll = BlkDispatch<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>;
+constexpr int kMaxBlockCols = 16;
+}  // namespace sc
+
+extern "C" {
+
+int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *x0,
+                               double *raw_out, double *scaled_out, sc_timing *t_out) {
+    using namespace sc;
+    SC_REQUIRE(g && x0, SC_E_INVALID, "null argument");
+    SC_REQUIRE(T >= 0, SC_E_INVALID, "power method step count must be >= 0, got %d", T);
+    SC_REQUIRE(L >= 1 && L <= kMaxBlockCols, SC_E_INVALID, "block width %d outside [1, %d]", L,
+               kMaxBlockCols);
+    SC_REQUIRE(g->ncols == g->n, SC_E_STATE, "block power method needs a whole graph");
+    SC_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = g->stream;
+    int32_t st;
+    if ((st = ensure_isd(g, s))) return st;
+    const int64_t n = g->n, nl = n * L;
+    double *buf = nullptr;  // x0, x[2], z[2], staging: 6 [n][L] blocks
+    SC_CUDA(cudaMallocAsync((void **)&buf, (size_t)nl * 6 * 8, s));
+    double *bx0 = buf, *bx[2] = {buf + nl, buf + 2 * nl}, *bz[2] = {buf + 3 * nl, buf + 4 * nl};
+    double *stage = buf + 5 * nl;
+    auto done = [&](int32_t code) {
+        cudaFreeAsync(buf, s);
+        cudaStreamSynchronize(s);
+        return code;
+    };
+    cudaError_t e = cudaMemcpyAsync(stage, x0, (size_t)nl * 8, cudaMemcpyHostToDevice, s);
+    if (e) return done(fail(SC_E_CUDA, "block upload: %s", cudaGetErrorString(e)));
+    const int gr = grid_for(g, nl, 256);
+    k_gather_rows<<<gr, 256, 0, s>>>(stage, g->d_perm, bx0, n, L);  // original -> renumbered
+    k_scale_rows<<<gr, 256, 0, s>>>(bx0, g->d_isd, bz[0], n, L);
+    cudaEventRecord(g->ev0, s);
+    BlkArgs a;
+    a.slice_ptr = g->d_slice_ptr;
+    a.col = g->d_col;
+    a.val = g->d_val;
+    a.wide_ptr = g->d_wide_ptr;
+    a.wcol = g->d_wcol;
+    a.wval = g->d_wval;
+    a.isd = g->d_isd;
+    a.n_sell = g->n_sell;
+    a.nslices = g->nslices;
+    a.n_wide = g->n_wide;
+    for (int32_t t = 0; t < T; ++t) {
+        const int in = t & 1, out = in ^ 1;
+        a.x_in = t == 0 ? bx0 : bx[in];
+        a.z_in = bz[in];
+        a.x_out = bx[out];
+        a.z_out = bz[out];
+        BlkAll::run(L, g, a, s);
+    }
+    cudaEventRecord(g->ev1, s);
+    e = cudaGetLastError();
+    if (!e) e = cudaEventSynchronize(g->ev1);
+    if (e) return done(fail(SC_E_CUDA, "block power method: %s", cudaGetErrorString(e)));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g->ev0, g->ev1);
+    const double *xr = T == 0 ? bx0 : bx[T & 1];
+    const double *zr = bz[T & 1];  // = d^-1/2 x_T: the scaled embedding (pipeline.py:157)
+    for (int pass = 0; pass < 2; ++pass) {
+        double *host = pass ? scaled_out : raw_out;
+        if (!host) continue;
+        k_gather_rows<<<gr, 256, 0, s>>>(pass ? zr : xr, g->d_iperm, stage, n, L);
+        e = cudaMemcpyAsync(host, stage, (size_t)nl * 8, cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e) return done(fail(SC_E_CUDA, "block download: %s", cudaGetErrorString(e)));
+    }
+    if (t_out) {
+        t_out->power_ms = ms;
+        t_out->kernel_ms = T ? ms / T : 0.0;
+        t_out->sample_ms = 0.0;
+        t_out->d2h_ms = 0.0;
+    }
+    return done(SC_OK);
 }
 
 int32_t sc_shard_step(sc_graph *g, const double *z_in, const double *x_in, double *x_out,

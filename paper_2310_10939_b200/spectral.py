@@ -189,6 +189,23 @@ class DeviceGraph:
                             "d2h_ms": tm.d2h_ms}
         return xT, f
 
+    def power_iterate_block(self, x0: np.ndarray, t: int, *, want_raw: bool = True):
+        """t steps of the signless operator on an (n, L) block (pm_log_k's embedding,
+        pipeline.py:144-147); returns (raw = M^t x0, scaled = raw * d^-1/2)."""
+        x = np.ascontiguousarray(x0, dtype=np.float64)
+        if x.ndim != 2 or x.shape[0] != self.n:
+            raise InputError(f"block must be ({self.n}, L), got {x.shape}")
+        if t < 0:
+            raise InputError(f"power method step count must be >= 0, got {t}")
+        raw = np.empty_like(x) if want_raw else None
+        scaled = np.empty_like(x)
+        tm = _lib.Timing()
+        _lib.check(_lib.load().sc_power_iterate_block(self.handle, int(t), x.shape[1], _lib.ptr(x),
+                                                       _lib.ptr(raw), _lib.ptr(scaled),
+                                                       ctypes.byref(tm)))
+        self.last_timing = {"power_ms": tm.power_ms, "kernel_ms": tm.kernel_ms}
+        return raw, scaled
+
 
 class _DeviceOp:
     """Operator protocol of spectral.py:52-59/71-79 (``.n``, ``.matvec``) backed by a
@@ -210,6 +227,8 @@ class _DeviceOp:
             self.dev.set_x0(x0)
             xT, _ = self.dev.power_iterate(t, sign=self.sign, sym=self._sym, want_f=False)
             return xT
+        if self._sym and self.sign == 1.0 and 1 <= x0.shape[1] <= 16:
+            return self.dev.power_iterate_block(x0, t)[0]  # all columns in one pass
         cols = [self.power(x0[:, i], t) for i in range(x0.shape[1])]
         return np.stack(cols, axis=1)
 
@@ -250,6 +269,20 @@ def power_method(op, x0: np.ndarray, t: int) -> np.ndarray:
         return x
     raise InputError(f"cannot interpret {type(op).__name__} as a device operator; wrap the "
                      "graph in RandomWalkOp or SignlessLaplacianOp")
+
+
+TAG_GAUSSIAN_COLUMN = 1  # spectral.py:28
+
+
+def sample_gaussian_vectors(n: int, l: int, seed: int) -> EmbeddingMatrix:
+    """Algorithm 2's start block (spectral.py:183-195): column i is
+    rng_for(seed, 1, i).standard_normal(n) -- the same numpy calls, so the same bits."""
+    if n < 1 or l < 1:
+        raise InputError(f"need n >= 1 and l >= 1, got n={n}, l={l}")
+    data = np.empty((n, l), dtype=np.float64)
+    for i in range(l):
+        data[:, i] = rng_for(seed, TAG_GAUSSIAN_COLUMN, i).standard_normal(n)
+    return EmbeddingMatrix(data=data, scaled=False, seed=seed)
 
 
 def sample_irwin_hall(graph, seed: int, device: int = 0) -> EmbeddingMatrix:
