@@ -198,6 +198,12 @@ int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_grap
 int32_t sc_kmeans_create(const double *points_host, int64_t n, int32_t device,
                          sc_kmeans **out);
 int32_t sc_kmeans_create_from_graph(sc_graph *g, sc_kmeans **out);
+/* points of dimension l (host, [n][l] row-major; 1 <= l <= 64).  Everything above applies;
+ * distances are (sum x^2 - 2 sum x c) + sum c^2 with left-to-right sums (the reference uses
+ * BLAS for the middle term, so for l > 1 labels match it up to exact distance ties), means
+ * and cost keep the reference's np.add.at / einsum order per coordinate. */
+int32_t sc_kmeans_create_nd(const double *points_host, int64_t n, int32_t l, int32_t device,
+                            sc_kmeans **out);
 void sc_kmeans_destroy(sc_kmeans *km);
 /* k-means++ seeding for `restarts` restarts at once.  chosen[r*k + i] (in/out);
  * rounds start_round[r]..k-1 are run with uniforms[r*(k-1) + i-1] as round i's

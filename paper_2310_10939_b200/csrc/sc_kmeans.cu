@@ -38,7 +38,9 @@ struct sc_kmeans {
     int device = 0;
     int sm_count = 148;
     int64_t n = 0;
+    int l = 1;                     // point dimension; d_x is [n][l] row-major
     double *d_x = nullptr;
+    int32_t *d_idx = nullptr, *d_idx_alt = nullptr;  // [R*n] sort payload when l > 1
     cudaStream_t stream = nullptr;
     // workspaces (grown on demand)
     int cap_r = 0, cap_k = 0;
@@ -79,6 +81,24 @@ struct sc_kmeans {
 namespace sc {
 
 constexpr int kEinsumBuf = 8192;  // numpy nditer buffer size (elements)
+
+// _sq_dists_to for one point / one center of dimension l (kmeans.py:106-113):
+// (sum x^2 - 2 sum x*c) + sum c^2, clipped at 0, each sum left to right, every operation
+// separately rounded.  For l = 1 it equals d2ref bit for bit (2.0*(x*c) == (2x)*c).  The
+// reference evaluates the middle term with BLAS (dgemm/dgemv), whose summation order is
+// CPU-specific, so for l > 1 labels agree with the reference up to exact ties only.
+__device__ __forceinline__ double d2nd(const double *__restrict__ x, const double *__restrict__ c,
+                                       int l) {
+    if (l == 1) return d2ref(x[0], c[0]);
+    double xx = 0.0, xc = 0.0, cc = 0.0;
+    for (int q = 0; q < l; ++q) {
+        xx = __dadd_rn(xx, __dmul_rn(x[q], x[q]));
+        xc = __dadd_rn(xc, __dmul_rn(x[q], c[q]));
+        cc = __dadd_rn(cc, __dmul_rn(c[q], c[q]));
+    }
+    const double v = __dadd_rn(__dsub_rn(xx, __dmul_rn(2.0, xc)), cc);
+    return v < 0.0 ? 0.0 : v;
+}
 
 // ---------------------------------------------------------------------------
 // Segmented exact sequential sums (sc_seqsum.cuh) over a batch of segments.
@@ -424,7 +444,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
 // k-means++
 
 // best[r][j] = min over chosen[r][0..start_r-1] of d2(x_j, x[chosen])
-__global__ void k_kpp_init(const double *__restrict__ x, int64_t n, int k,
+__global__ void k_kpp_init(const double *__restrict__ x, int64_t n, int l, int k,
                            const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
                            const int32_t *__restrict__ on, double *__restrict__ best) {
     const int r = blockIdx.y;
@@ -434,24 +454,24 @@ __global__ void k_kpp_init(const double *__restrict__ x, int64_t n, int k,
     const int64_t *ch = chosen + (int64_t)r * k;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x) {
-        const double xj = x[j];
-        double v = d2ref(xj, x[ch[0]]);
-        for (int i = 1; i < s; ++i) v = fmin(v, d2ref(xj, x[ch[i]]));
+        const double *xj = x + j * l;
+        double v = d2nd(xj, x + ch[0] * l, l);
+        for (int i = 1; i < s; ++i) v = fmin(v, d2nd(xj, x + ch[i] * l, l));
         b[j] = v;
     }
 }
 
 // best = min(best, d2(x, x[chosen[r][i-1]])) when round i-1 was picked in this call
-__global__ void k_kpp_update(const double *__restrict__ x, int64_t n, int k, int i,
+__global__ void k_kpp_update(const double *__restrict__ x, int64_t n, int l, int k, int i,
                              const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
                              const int32_t *__restrict__ on, double *__restrict__ best) {
     const int r = blockIdx.y;
     if (!on[r] || i - 1 < start[r]) return;
-    const double c = x[chosen[(int64_t)r * k + i - 1]];
+    const double *c = x + chosen[(int64_t)r * k + i - 1] * l;
     double *b = best + (int64_t)r * n;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x) {
-        const double v = d2ref(x[j], c);
+        const double v = d2nd(x + j * l, c, l);
         if (v < b[j]) b[j] = v;
     }
 }
@@ -510,7 +530,7 @@ __global__ void k_kpp_search(SegView v, SeqWork w, int64_t n, int k, int i,
 // Lloyd
 
 // assignment: labels, counts, changed vs previous labels
-__global__ void k_assign(const double *__restrict__ x, int64_t n, int k,
+__global__ void k_assign(const double *__restrict__ x, int64_t n, int l, int k,
                          const double *__restrict__ cen, const int32_t *__restrict__ active,
                          const int32_t *__restrict__ prev, int32_t *__restrict__ lab,
                          int32_t *__restrict__ cnt, int32_t *__restrict__ changed) {
@@ -518,22 +538,20 @@ __global__ void k_assign(const double *__restrict__ x, int64_t n, int k,
     if (!active[r]) return;
     extern __shared__ unsigned char smem_raw[];
     double *c = reinterpret_cast<double *>(smem_raw);
-    int32_t *hist = reinterpret_cast<int32_t *>(c + k);
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
-        c[i] = cen[(int64_t)r * k + i];
-        hist[i] = 0;
-    }
+    int32_t *hist = reinterpret_cast<int32_t *>(c + (size_t)k * l);
+    for (int i = threadIdx.x; i < k * l; i += blockDim.x) c[i] = cen[(int64_t)r * k * l + i];
+    for (int i = threadIdx.x; i < k; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     int ch = 0;
     const int32_t *pv = prev + (int64_t)r * n;
     int32_t *lb = lab + (int64_t)r * n;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x) {
-        const double xj = x[j];
+        const double *xj = x + j * l;
         int bi = 0;
-        double bd = d2ref(xj, c[0]);
+        double bd = d2nd(xj, c, l);
         for (int q = 1; q < k; ++q) {
-            const double d = d2ref(xj, c[q]);
+            const double d = d2nd(xj, c + (size_t)q * l, l);
             if (d < bd) {
                 bd = d;
                 bi = q;
@@ -687,7 +705,8 @@ __global__ void k_assign_sorted(const double *__restrict__ x, int64_t n, int k,
 // cluster is empty (the common case).  Clusters empty after assignment are repaired in
 // increasing order: the first point of maximal own distance moves in, its own distance
 // becomes 0.  Then counts and the changed-label count of the restart are recomputed.
-__global__ void __launch_bounds__(1024) k_repair(const double *__restrict__ x, int64_t n, int k,
+__global__ void __launch_bounds__(1024) k_repair(const double *__restrict__ x, int64_t n, int l,
+                                                 int k,
                                                  const double *__restrict__ cen,
                                                  const int32_t *__restrict__ active,
                                                  const int32_t *__restrict__ prev,
@@ -711,9 +730,10 @@ __global__ void __launch_bounds__(1024) k_repair(const double *__restrict__ x, i
     __syncthreads();
     if (!has) return;
     int32_t *lb = lab + (int64_t)r * n;
-    const double *cc = cen + (int64_t)r * k;
+    const double *cc = cen + (int64_t)r * k * l;
     double *own = own_all + (int64_t)r * n;
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) own[j] = d2ref(x[j], cc[lb[j]]);
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
+        own[j] = d2nd(x + j * l, cc + (int64_t)lb[j] * l, l);
     __syncthreads();
     for (int e = 0; e < k; ++e) {
         if (!was_empty[e]) continue;
@@ -779,6 +799,26 @@ __global__ void k_make_keys(int64_t n, int k, const int32_t *__restrict__ lab,
     }
 }
 
+// l > 1: the sort carries the point index; each coordinate is gathered in sorted order
+__global__ void k_make_keys_idx(int64_t n, int k, const int32_t *__restrict__ lab,
+                                const int32_t *__restrict__ act, int nact,
+                                int32_t *__restrict__ keys, int32_t *__restrict__ idx) {
+    const int64_t tot = (int64_t)nact * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / n, j = t - s * n;
+        keys[t] = (int32_t)(s * k + lab[(int64_t)act[s] * n + j]);
+        idx[t] = (int32_t)j;
+    }
+}
+
+__global__ void k_gather_coord(const double *__restrict__ x, const int32_t *__restrict__ idx,
+                               int64_t m, int l, int q, double *__restrict__ vals) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m;
+         t += (int64_t)gridDim.x * blockDim.x)
+        vals[t] = x[(int64_t)idx[t] * l + q];
+}
+
 // Layout of the (slot, cluster) segments of the sorted points, straight from the cluster
 // counts (k_assign / k_repair leave them consistent with the labels): seg = exclusive scan
 // of the counts in (active slot, label) order -- the order of the sort keys -- and cofs the
@@ -822,13 +862,13 @@ __global__ void __launch_bounds__(1024) k_seg_layout(int nseg, int k,
 }
 
 // means = ordered sum / count (cluster_means, kmeans.py:86-93); empty clusters keep 0
-__global__ void k_seg_means(int nseg, int k, const int64_t *__restrict__ seg,
+__global__ void k_seg_means(int nseg, int k, int l, int q, const int64_t *__restrict__ seg,
                             const double *__restrict__ total, const int32_t *__restrict__ act,
                             double *__restrict__ cen) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nseg) return;
     const int64_t c = seg[t + 1] - seg[t];
-    cen[(int64_t)act[t / k] * k + t % k] = c > 0 ? __ddiv_rn(total[t], (double)c) : 0.0;
+    cen[((int64_t)act[t / k] * k + t % k) * l + q] = c > 0 ? __ddiv_rn(total[t], (double)c) : 0.0;
 }
 
 // kmeans_cost in numpy einsum("ij,ij->") order (sc_oracle.c orc_einsum_sumsq): one warp
@@ -840,8 +880,10 @@ __global__ void k_seg_means(int nseg, int k, const int64_t *__restrict__ seg,
 constexpr int kCostWarps = 8;
 constexpr int kCostChunk = 256;
 
+// (points of dimension l: the buffers run over the n*l coordinates in C order, as numpy's
+// nditer does for the (n, l) operands)
 __global__ void __launch_bounds__(32 * kCostWarps) k_cost_buf(
-    const double *__restrict__ x, int64_t n, int k, const int32_t *__restrict__ lab,
+    const double *__restrict__ x, int64_t n, int l, int k, const int32_t *__restrict__ lab,
     const double *__restrict__ cen, const int32_t *__restrict__ active, int64_t nbuf,
     double *__restrict__ part) {
     __shared__ double sq[kCostWarps][2][kCostChunk];
@@ -850,10 +892,10 @@ __global__ void __launch_bounds__(32 * kCostWarps) k_cost_buf(
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t bufi = (int64_t)blockIdx.x * kCostWarps + wib;
     if (bufi >= nbuf) return;
-    const int64_t base = bufi * kEinsumBuf;
-    const int m = (int)min((int64_t)kEinsumBuf, n - base);
-    const int32_t *lb = lab + (int64_t)r * n + base;
-    const double *c = cen + (int64_t)r * k;
+    const int64_t base = bufi * kEinsumBuf, nl = n * l;
+    const int m = (int)min((int64_t)kEinsumBuf, nl - base);
+    const int32_t *lr = lab + (int64_t)r * n;
+    const double *c = cen + (int64_t)r * k * l;
     const double *xb0 = x + base;
     // raw loads of chunk q+2 are issued before the chains of chunk q and the dependent
     // center lookup of chunk q+1 runs after them, so no lane waits on HBM in between
@@ -864,8 +906,9 @@ __global__ void __launch_bounds__(32 * kCostWarps) k_cost_buf(
 #pragma unroll
         for (int t = 0; t < PL; ++t) {
             const int j = q * kCostChunk + t * 32 + lane;
+            const int64_t e = base + j;
             xv[t] = j < m ? __ldg(xb0 + j) : 0.0;
-            lv[t] = j < m ? __ldcs(lb + j) : -1;
+            lv[t] = j >= m ? -1 : (l == 1 ? __ldcs(lr + e) : lr[e / l] * l + (int)(e % l));
         }
     };
     auto finish = [&](const double (&xv)[PL], const int32_t (&lv)[PL]) {
@@ -963,9 +1006,9 @@ __global__ void k_cost_combine(int64_t nbuf, const double *__restrict__ part,
 }
 
 __global__ void k_gather_centers(const double *__restrict__ x, const int64_t *__restrict__ chosen,
-                                 int rk, double *__restrict__ cen) {
+                                 int rk, int l, double *__restrict__ cen) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < rk) cen[t] = x[chosen[t]];
+    if (t < rk * l) cen[t] = x[chosen[t / l] * l + t % l];
 }
 
 template <typename T>
@@ -986,7 +1029,7 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     R = std::max(R, km->cap_r);
     k = std::max(k, km->cap_k);
     const int64_t n = km->n;
-    const int64_t nbuf = (n + kEinsumBuf - 1) / kEinsumBuf;
+    const int64_t nbuf = (n * km->l + kEinsumBuf - 1) / kEinsumBuf;
     // chunks: kpp uses R * ceil(n/C); Lloyd's R*k segments need at most R*n/C + R*k
     const int64_t nch = (int64_t)R * ((n + kSeqChunk - 1) / kSeqChunk) + (int64_t)R * k + 1;
     const int64_t S = (int64_t)R * k + 1;
@@ -1002,7 +1045,11 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_u, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_start, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_degen, (size_t)R, km->stream))) return st;
-    if ((st = grow(&km->d_cen, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_cen, (size_t)R * k * km->l, km->stream))) return st;
+    if (km->l > 1) {
+        if ((st = grow(&km->d_idx, (size_t)R * n, km->stream))) return st;
+        if ((st = grow(&km->d_idx_alt, (size_t)R * n, km->stream))) return st;
+    }
     if ((st = grow(&km->d_scen, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_sidx, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_cmax, (size_t)R, km->stream))) return st;
@@ -1030,9 +1077,12 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_round_on, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_on, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_segkpp, (size_t)R + 1, km->stream))) return st;
-    size_t need = 0;
+    size_t need = 0, need2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, need, km->d_keys, km->d_keys_alt, km->d_vals,
                                     km->d_vals_alt, (int64_t)R * n, 0, 31, km->stream);
+    cub::DeviceRadixSort::SortPairs(nullptr, need2, km->d_keys, km->d_keys_alt, km->d_idx,
+                                    km->d_idx_alt, (int64_t)R * n, 0, 31, km->stream);
+    need = std::max(need, need2);
     if ((st = grow((unsigned char **)&km->d_cub, need, km->stream))) return st;
     km->cub_bytes = need;
     km->cap_r = R;
@@ -1063,10 +1113,11 @@ static int grid_1d(const sc_kmeans *km, int64_t work, int tpb) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)km->sm_count * 8));
 }
 
-static int32_t km_init(int device, int64_t n, sc_kmeans **out) {
+static int32_t km_init(int device, int64_t n, int l, sc_kmeans **out) {
     sc_kmeans *km = new sc_kmeans();
     km->device = device;
     km->n = n;
+    km->l = l;
     cudaDeviceGetAttribute(&km->sm_count, cudaDevAttrMultiProcessorCount, device);
     // keep freed workspace memory in the device pool across contexts (repeated clusterings)
     cudaMemPool_t pool;
@@ -1075,7 +1126,7 @@ static int32_t km_init(int device, int64_t n, sc_kmeans **out) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaError_t e = cudaStreamCreateWithFlags(&km->stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMallocAsync((void **)&km->d_x, (size_t)n * 8, km->stream);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&km->d_x, (size_t)n * l * 8, km->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(km->stream);
     if (e != cudaSuccess) {
         sc_kmeans_destroy(km);
@@ -1091,17 +1142,24 @@ using namespace sc;
 
 extern "C" {
 
-int32_t sc_kmeans_create(const double *points_host, int64_t n, int32_t device,
-                         sc_kmeans **out) {
+int32_t sc_kmeans_create_nd(const double *points_host, int64_t n, int32_t l, int32_t device,
+                            sc_kmeans **out) {
     SC_REQUIRE(out && points_host, SC_E_INVALID, "null argument");
     SC_REQUIRE(n >= 1, SC_E_INVALID, "need n >= 1 points");
-    for (int64_t i = 0; i < n; ++i)
+    SC_REQUIRE(l >= 1 && l <= 64, SC_E_INVALID, "point dimension %d outside [1, 64]", l);
+    SC_REQUIRE(n < (int64_t(1) << 31), SC_E_INVALID, "n too large");
+    for (int64_t i = 0; i < n * l; ++i)
         SC_REQUIRE(std::isfinite(points_host[i]), SC_E_INVALID, "points contain NaN or Inf");
     SC_CUDA(cudaSetDevice(device));
-    int32_t st = km_init(device, n, out);
+    int32_t st = km_init(device, n, l, out);
     if (st) return st;
-    SC_CUDA(cudaMemcpy((*out)->d_x, points_host, (size_t)n * 8, cudaMemcpyHostToDevice));
+    SC_CUDA(cudaMemcpy((*out)->d_x, points_host, (size_t)n * l * 8, cudaMemcpyHostToDevice));
     return SC_OK;
+}
+
+int32_t sc_kmeans_create(const double *points_host, int64_t n, int32_t device,
+                         sc_kmeans **out) {
+    return sc_kmeans_create_nd(points_host, n, 1, device, out);
 }
 
 int32_t sc_kmeans_create_from_graph(sc_graph *g, sc_kmeans **out) {
@@ -1109,7 +1167,7 @@ int32_t sc_kmeans_create_from_graph(sc_graph *g, sc_kmeans **out) {
     const double *f = graph_f_device(g);
     SC_REQUIRE(f, SC_E_STATE, "graph has no embedding yet: call sc_power_iterate first");
     SC_CUDA(cudaSetDevice(graph_device(g)));
-    int32_t st = km_init(graph_device(g), graph_n(g), out);
+    int32_t st = km_init(graph_device(g), graph_n(g), 1, out);
     if (st) return st;
     SC_CUDA(cudaMemcpy((*out)->d_x, f, (size_t)graph_n(g) * 8, cudaMemcpyDeviceToDevice));
     return SC_OK;
@@ -1126,7 +1184,7 @@ void sc_kmeans_destroy(sc_kmeans *km) {
                     km->d_cost, km->d_changed, km->d_active, km->d_empty, km->d_A,
                     km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
                     km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
-                    km->d_sq0, km->d_sq1, km->d_svmax, km->d_skp,
+                    km->d_sq0, km->d_sq1, km->d_svmax, km->d_skp, km->d_idx, km->d_idx_alt,
                     km->d_segkpp};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, km->stream);
@@ -1191,10 +1249,11 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     const dim3 g2(grid_1d(km, n, 256) / std::max(1, std::min(R, 8)) + 1, R);
     const int gw = grid_1d(km, nch * 32, 256);
     const int gs = (R * 32 + 255) / 256;
-    k_kpp_init<<<g2, 256, 0, s>>>(km->d_x, n, k, km->d_chosen, km->d_start, km->d_on, km->d_best);
+    k_kpp_init<<<g2, 256, 0, s>>>(km->d_x, n, km->l, k, km->d_chosen, km->d_start, km->d_on,
+                                  km->d_best);
     SC_CUDA(cudaGetLastError());
     for (int i = smin; i < k; ++i) {
-        k_kpp_update<<<g2, 256, 0, s>>>(km->d_x, n, k, i, km->d_chosen, km->d_start, km->d_on,
+        k_kpp_update<<<g2, 256, 0, s>>>(km->d_x, n, km->l, k, i, km->d_chosen, km->d_start, km->d_on,
                                          km->d_best);
         k_kpp_round_on<<<(R + 127) / 128, 128, 0, s>>>(R, i, km->d_start, km->d_on,
                                                        km->d_round_on, km->d_neg);
@@ -1229,10 +1288,11 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     auto t0 = std::chrono::steady_clock::now();
     cudaStream_t s = km->stream;
     const int64_t n = km->n;
-    const int64_t nbuf = (n + kEinsumBuf - 1) / kEinsumBuf;
+    const int l = km->l;
+    const int64_t nbuf = (n * l + kEinsumBuf - 1) / kEinsumBuf;
     const int rk = R * k;
     SC_CUDA(cudaMemcpyAsync(km->d_chosen, chosen, (size_t)rk * 8, cudaMemcpyHostToDevice, s));
-    k_gather_centers<<<(rk + 255) / 256, 256, 0, s>>>(km->d_x, km->d_chosen, rk, km->d_cen);
+    k_gather_centers<<<(rk * l + 255) / 256, 256, 0, s>>>(km->d_x, km->d_chosen, rk, l, km->d_cen);
     // labels start at zero (kmeans.py:195)
     SC_CUDA(cudaMemsetAsync(km->d_lab[0], 0, (size_t)R * n * 4, s));
     std::vector<int32_t> active(R, 1), changed(R), iters(R, 0), final_buf(R, 0);
@@ -1240,12 +1300,12 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     int cur = 0;  // d_lab[cur] = labels of the previous iteration
     int end_bit = 1;
     while ((1ll << end_bit) < (long long)rk) ++end_bit;
-    const size_t smem_assign = (size_t)k * 12;
+    const size_t smem_assign = (size_t)k * (8 * l + 4);
     SC_REQUIRE(smem_assign <= 200 * 1024, SC_E_INVALID, "k=%d too large for the assign kernel", k);
     if (smem_assign > 48 * 1024)
         SC_CUDA(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_assign));
-    const bool sorted_assign = k >= kSortedMinK && k <= kSortedMaxK &&
+    const bool sorted_assign = l == 1 && k >= kSortedMinK && k <= kSortedMaxK &&
                                getenv("SC_KMEANS_BRUTE_ASSIGN") == nullptr;
     const size_t smem_sorted = (size_t)k * 16;
     size_t smem_sort = 12;
@@ -1296,38 +1356,51 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                                          km->d_cmax, km->d_active, km->d_lab[cur],
                                                          km->d_lab[nxt], km->d_cnt, km->d_changed);
         } else {
-            k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, k, km->d_cen, km->d_active,
+            k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, l, k, km->d_cen, km->d_active,
                                                    km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
                                                    km->d_changed);
         }
-        k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, k, km->d_cen, km->d_active,
+        k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, l, k, km->d_cen, km->d_active,
                                               km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
                                               km->d_changed, km->d_best);
         // np.add.at order: stable radix sort of the active restarts' points on
         // (slot, label) keeps point-index order inside every cluster; then exact ordered sums
         if (prof) cudaEventRecord(pe[1], s);
         const int64_t m = (int64_t)nact * n;
-        k_make_keys<<<grid_1d(km, m, 256), 256, 0, s>>>(n, k, km->d_lab[nxt], km->d_empty, nact,
-                                                         km->d_keys, km->d_vals, km->d_x);
         size_t tb = km->cub_bytes;
-        SC_CUDA(cub::DeviceRadixSort::SortPairs(km->d_cub, tb, km->d_keys, km->d_keys_alt,
-                                                km->d_vals, km->d_vals_alt, m, 0, end_bit, s));
+        if (l == 1) {
+            k_make_keys<<<grid_1d(km, m, 256), 256, 0, s>>>(n, k, km->d_lab[nxt], km->d_empty,
+                                                             nact, km->d_keys, km->d_vals, km->d_x);
+            SC_CUDA(cub::DeviceRadixSort::SortPairs(km->d_cub, tb, km->d_keys, km->d_keys_alt,
+                                                    km->d_vals, km->d_vals_alt, m, 0, end_bit, s));
+        } else {
+            k_make_keys_idx<<<grid_1d(km, m, 256), 256, 0, s>>>(n, k, km->d_lab[nxt], km->d_empty,
+                                                                 nact, km->d_keys, km->d_idx);
+            SC_CUDA(cub::DeviceRadixSort::SortPairs(km->d_cub, tb, km->d_keys, km->d_keys_alt,
+                                                    km->d_idx, km->d_idx_alt, m, 0, end_bit, s));
+        }
         k_seg_layout<<<1, 1024, 0, s>>>(nseg, k, km->d_cnt, km->d_empty, km->d_seg, km->d_cofs,
                                         km->d_nchunks);
         if (prof) cudaEventRecord(pe[2], s);
-        SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)nseg * 4, s));
         vm.S = nseg;
         const int gwm = grid_1d(km, (m / kSeqChunk + nseg) * 32, 256);
         const int gsm = (nseg * 32 + 255) / 256;
-        k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
-        k_seq_predict<<<gsm, 256, 0, s>>>(vm, wm);
-        k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
-        k_seq_superize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
-        k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(vm, wm, 0);
-        k_seg_means<<<(nseg + 127) / 128, 128, 0, s>>>(nseg, k, km->d_seg, km->d_total, km->d_empty,
-                                                       km->d_cen);
+        for (int q = 0; q < l; ++q) {  // np.add.at over each coordinate column
+            if (l > 1)
+                k_gather_coord<<<grid_1d(km, m, 256), 256, 0, s>>>(km->d_x, km->d_idx_alt, m, l, q,
+                                                                    km->d_vals_alt);
+            SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)nseg * 4, s));
+            k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
+            k_seq_predict<<<gsm, 256, 0, s>>>(vm, wm);
+            k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
+            k_seq_superize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
+            k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
+                            kComposeSmem, s>>>(vm, wm, 0);
+            k_seg_means<<<(nseg + 127) / 128, 128, 0, s>>>(nseg, k, l, q, km->d_seg, km->d_total,
+                                                           km->d_empty, km->d_cen);
+        }
         if (prof) cudaEventRecord(pe[3], s);
-        k_cost_buf<<<gc, 32 * kCostWarps, 0, s>>>(km->d_x, n, k, km->d_lab[nxt], km->d_cen,
+        k_cost_buf<<<gc, 32 * kCostWarps, 0, s>>>(km->d_x, n, l, k, km->d_lab[nxt], km->d_cen,
                                                    km->d_active, nbuf, km->d_part);
         k_cost_combine<<<R, 256, 0, s>>>(nbuf, km->d_part, km->d_active, km->d_cost);
         SC_CUDA(cudaGetLastError());

@@ -10,8 +10,10 @@ Mirrors specluster/kmeans.py:
                                   ``integers(n)`` then one ``random()`` per round, or
                                   ``integers(#unchosen)`` in the all-weights-zero round.
 The data work (distances, cumulative sums, assignment, repair, ordered means, einsum-
-order cost) runs in libsc_b200.so (csrc/sc_kmeans.cu).  Only 1-D point sets (the one-
-vector embedding) are supported; wider embeddings are outside the B200 path.
+order cost) runs in libsc_b200.so (csrc/sc_kmeans.cu).  1-D point sets (the one-vector
+embedding) are replicated bit for bit; d-dimensional ones (pm_log_k embeddings) use the same
+kernels with d-dimensional distances, whose middle term the reference evaluates with BLAS
+(CPU-specific order), so there labels agree with the reference up to exact distance ties.
 """
 
 from __future__ import annotations
@@ -88,9 +90,10 @@ class KMeans1D:
             _lib.check(L.sc_kmeans_create_from_graph(graph.handle, ctypes.byref(h)))
             self.n = graph.n
         else:
-            x = _as_1d(points)
-            _lib.check(L.sc_kmeans_create(_lib.ptr(x), x.size, device, ctypes.byref(h)))
-            self.n = x.size
+            x = _as_2d(points)
+            _lib.check(L.sc_kmeans_create_nd(_lib.ptr(x), x.shape[0], x.shape[1], device,
+                                             ctypes.byref(h)))
+            self.n = x.shape[0]
         self._h = h
         self.last = {}
 
@@ -186,20 +189,30 @@ def _nth_unchosen(taken_sorted: np.ndarray, m: int) -> int:
     return int(idx)
 
 
-def _as_1d(points) -> np.ndarray:
+def _as_2d(points) -> np.ndarray:
     if isinstance(points, np.ndarray) and points.ndim == 1:
         points = points[:, None]
     c = points.coords if isinstance(points, PointSet) else PointSet(np.asarray(points)).coords
+    if c.shape[1] > 64:
+        raise InputError(f"point dimension {c.shape[1]} exceeds the device limit of 64")
+    return np.ascontiguousarray(c)
+
+
+def _as_1d(points) -> np.ndarray:
+    c = _as_2d(points)
     if c.shape[1] != 1:
-        raise InputError(f"the B200 k-means path clusters 1-D embeddings; got d={c.shape[1]}")
+        raise InputError(f"expected 1-D points, got d={c.shape[1]}")
     return np.ascontiguousarray(c[:, 0])
+
+
+KMeans = KMeans1D  # the context handles any dimension; the name is kept for callers
 
 
 def lloyd(points, k: int, seed: int, max_iters: int = 100, tol: float = 1e-6,
           restarts: int = 10) -> Partition:
     """Restarted Lloyd from k-means++ seeds, best cost kept (kmeans.py:167-215)."""
-    x = _as_1d(points)
-    if not 1 <= k <= x.size:
-        raise InputError(f"need 1 <= k <= n, got k={k}, n={x.size}")
+    x = _as_2d(points)
+    if not 1 <= k <= x.shape[0]:
+        raise InputError(f"need 1 <= k <= n, got k={k}, n={x.shape[0]}")
     with KMeans1D(x) as km:
         return km.lloyd(k, seed, max_iters=max_iters, tol=tol, restarts=restarts)

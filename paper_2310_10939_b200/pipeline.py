@@ -10,8 +10,11 @@ in ``MODES``: ``"one_vector"`` -- the method of PAPER.md:12-253:
     labels = lloyd(f, k, seed=_kmeans_seed(seed))   (bit-exact GPU replica)
 
 Timings keep the reference keys {embed, scale, kmeans, total} in milliseconds
-(pipeline.py:163-168).  The Algorithm-2 modes (pm_log_k, pm_k, eigs_*) are the
-reference's other embeddings and are outside this B200 path: they raise InputError.
+(pipeline.py:163-168).  ``"pm_log_k"`` (the reference's default Algorithm-2 embedding,
+pipeline.py:144-147) also runs on the device: the reference's own Gaussian start block
+(host numpy, same calls), the block power method of the signless operator (bit-exact,
+csrc sc_power_iterate_block), the d^-1/2 row scaling fused into the last step, and the
+d-dimensional k-means.  pm_k and the eigs_* modes raise InputError.
 """
 
 from __future__ import annotations
@@ -25,10 +28,10 @@ import numpy as np
 from .errors import InputError
 from .graph import as_graph
 from .kmeans import KMeans1D, Partition
-from .spectral import DeviceGraph, EmbeddingMatrix
+from .spectral import DeviceGraph, EmbeddingMatrix, sample_gaussian_vectors
 
 MODES = ("pm_log_k", "pm_k", "eigs_k", "eigs_log_k", "one_vector")
-DEVICE_MODES = ("one_vector",)
+DEVICE_MODES = ("one_vector", "pm_log_k")
 
 _TAG_KMEANS = 2  # pipeline.py:47
 
@@ -125,6 +128,8 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
     if params.k > n:
         raise InputError(f"k={params.k} exceeds the vertex count n={n}")
     steps = params.num_steps(n)
+    if params.mode == "pm_log_k":
+        return _pm_log_k(graph, params, steps, device_graph)
     t_start = time.perf_counter()
     dev = device_graph if device_graph is not None else DeviceGraph(graph, params.device)
     try:
@@ -159,3 +164,38 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
     dt["kmeans_best_restart"] = km_info.get("best_restart")
     return PipelineResult(partition=part, embedding=embedding, timings=timings,
                           mode=params.mode, l=1, t=steps, x_T=x_t, device_timings=dt)
+
+
+def _pm_log_k(graph, params: SpectralParams, steps: int, device_graph) -> PipelineResult:
+    """pipeline.py:140-178 for mode pm_log_k, on the device."""
+    n = graph.n
+    cols = params.num_columns(n)
+    if cols > n:
+        raise InputError(f"embedding width l={cols} exceeds n={n}")
+    if cols > 16:
+        raise InputError(f"the device block power method handles l <= 16 columns, got {cols}")
+    t_start = time.perf_counter()
+    dev = device_graph if device_graph is not None else DeviceGraph(graph, params.device)
+    try:
+        t0 = time.perf_counter()
+        x0 = sample_gaussian_vectors(n, cols, params.seed).data
+        _, scaled = dev.power_iterate_block(x0, steps, want_raw=False)
+        t1 = time.perf_counter()
+        embedding = EmbeddingMatrix(data=scaled, scaled=True, seed=params.seed)
+        t2 = time.perf_counter()
+        with KMeans1D(scaled, device=params.device) as km:
+            part = km.lloyd(params.k, _kmeans_seed(params.seed), max_iters=params.max_iters,
+                            tol=params.tol, restarts=params.restarts)
+            km_info = dict(km.last)
+        t3 = time.perf_counter()
+    finally:
+        if device_graph is None:
+            dev.close()
+    timings = {"embed": (t1 - t0) * 1e3, "scale": (t2 - t1) * 1e3, "kmeans": (t3 - t2) * 1e3,
+               "total": (t3 - t0) * 1e3}
+    dt = dict(dev.last_timing or {})
+    dt["upload_ms"] = (t0 - t_start) * 1e3
+    dt["kmeans_costs"] = km_info.get("costs")
+    dt["kmeans_iters"] = km_info.get("iters")
+    return PipelineResult(partition=part, embedding=embedding, timings=timings,
+                          mode=params.mode, l=cols, t=steps, device_timings=dt)

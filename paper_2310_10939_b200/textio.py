@@ -115,7 +115,8 @@ def save_labels(labels, path, header_comments: Sequence[str] = ()) -> None:
         fh.write("".join(f"{v}\n" for v in lab.tolist()))
 
 
-def save_embedding(data: np.ndarray, path, *, scaled: bool, seed: int) -> None:
+def save_embedding(data: np.ndarray, path, *, scaled: bool, seed: int,
+                   generator: str | None = None) -> None:
     """Header + one comma-separated row per vertex at 17 significant digits."""
     d = np.asarray(data, dtype=np.float64)
     if d.ndim == 1:
@@ -123,7 +124,7 @@ def save_embedding(data: np.ndarray, path, *, scaled: bool, seed: int) -> None:
     with open(path, "w", encoding="utf-8") as fh:
         fh.write(f"{_EMBEDDING_MAGIC} n={d.shape[0]} l={d.shape[1]} "
                  f"scaled={1 if scaled else 0} seed={seed}\n")
-        fh.write(f"# generator={GENERATOR_NAME} numpy={np.__version__}\n")
+        fh.write(f"# generator={generator or GENERATOR_NAME} numpy={np.__version__}\n")
         if d.shape[1] == 1:
             fh.write("".join(f"{v:.17g}\n" for v in d[:, 0].tolist()))
         else:

@@ -47,6 +47,16 @@ def main():
     g, _ = from_edges(n, u[keep], v[keep], 0.25 + rng.random(keep.sum()), drop_isolated=True)
     assert np.diff(g.row_offsets).max() > 256
     run(g, 100, 3, out, "wide", l=7)
+    # the reference's whole pm_log_k pipeline (labels through its BLAS-based k-means)
+    from specluster.pipeline import fast_spectral_cluster
+    r = fast_spectral_cluster(s.graph, SpectralParams(k=5, seed=0))
+    out["c1_pipeline_labels"] = r.partition.labels
+    out["c1_pipeline_embedding"] = r.embedding.data
+    s2 = sample_sbm(SbmParams(n=20000, k=8, p=0.01, q=0.0005, seed=2))
+    r2 = fast_spectral_cluster(s2.graph, SpectralParams(k=8, seed=2))
+    out.update({"sbm8_rp": s2.graph.row_offsets, "sbm8_col": s2.graph.col_indices,
+                "sbm8_deg": s2.graph.degrees, "sbm8_labels": r2.partition.labels,
+                "sbm8_embedding": r2.embedding.data})
     np.savez_compressed(os.path.join(HERE, "block.npz"), **out)
     print({k: out[k].shape for k in out if k.endswith("_raw")}, int(out["c1_t"]))
 

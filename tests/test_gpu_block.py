@@ -28,3 +28,26 @@ def test_block_power_method_bit_exact(name):
         assert np.array_equal(SignlessLaplacianOp(dg).power(x0, int(G["t"])), G["raw"])
         raw0, _ = dg.power_iterate_block(x0, 0)
         assert np.array_equal(raw0, x0)
+
+
+@pytest.mark.parametrize("case", ["c1", "sbm8"])
+def test_pm_log_k_pipeline_against_reference(case):
+    """The whole pm_log_k pipeline: the embedding handed to k-means is bit-identical to the
+    reference's; the labels come from the d-dimensional device k-means (same seeding draws,
+    same np.add.at means and einsum cost; distances in our order instead of BLAS's), which
+    must reproduce the reference's partition on these instances."""
+    from oracle import oracle as O
+    from paper_2310_10939_b200 import SpectralParams, fast_spectral_cluster
+
+    if case == "c1":
+        g = from_csr(len(GOLD["c1_deg"]), GOLD["c1_rp"], GOLD["c1_col"], None, GOLD["c1_deg"])
+        k, seed = 5, 0
+    else:
+        g = from_csr(len(GOLD["sbm8_deg"]), GOLD["sbm8_rp"], GOLD["sbm8_col"], None,
+                     GOLD["sbm8_deg"])
+        k, seed = 8, 2
+    res = fast_spectral_cluster(g, SpectralParams(k=k, seed=seed, mode="pm_log_k"))
+    assert np.array_equal(res.embedding.data, GOLD[f"{case}_pipeline_embedding"
+                                                   if case == "c1" else "sbm8_embedding"])
+    ref = GOLD["c1_pipeline_labels" if case == "c1" else "sbm8_labels"]
+    assert np.array_equal(O.canonical_labels(res.partition.labels), O.canonical_labels(ref))

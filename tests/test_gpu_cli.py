@@ -25,6 +25,7 @@ def test_cluster_config1_matches_reference_and_is_byte_deterministic(tmp_path):
     for run in range(2):
         o = tmp_path / f"run{run}"
         assert cli.main(["cluster", "--graph", str(tmp_path / "g.tsv"), "--k", "5", "--t", "50",
+                         "--mode", "one_vector",
                          "--seed", "0", "--out", str(o)]) == 0
         outs.append(o)
     lab = load_labels(outs[0] / "labels.txt", expected_n=g.n)

@@ -82,10 +82,16 @@ def test_params_semantics():
     assert _kmeans_seed(0) == 3141116543
 
 
-def test_algorithm2_modes_are_outside_the_path():
+def test_unsupported_algorithm2_modes_are_refused():
+    """pm_k and the eigensolver modes are outside the device path (pm_log_k is on it);
+    the block width of pm_log_k is bounded by the device kernel."""
     g, _ = from_edges(4, [0, 1, 2], [1, 2, 3])
+    for mode in ("pm_k", "eigs_k", "eigs_log_k"):
+        with pytest.raises(InputError):
+            fast_spectral_cluster(g, SpectralParams(k=2, mode=mode))
+    g, _ = from_edges(40, list(range(39)), list(range(1, 40)))
     with pytest.raises(InputError):
-        fast_spectral_cluster(g, SpectralParams(k=2, mode="pm_log_k"))
+        fast_spectral_cluster(g, SpectralParams(k=2, l=17, mode="pm_log_k"))
 
 
 def test_k_exceeds_n():
