@@ -26,6 +26,8 @@
 #include <vector>
 
 #include "sc_common.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 #include "sc_seqsum.cuh"
 
 namespace sc {
@@ -60,6 +62,11 @@ struct sc_kmeans {
     double *d_scen = nullptr;      // [R][k] centers sorted ascending (sorted assignment)
     int32_t *d_sidx = nullptr;     // [R][k] their original indices
     double *d_cmax = nullptr;      // [R] max |center|
+    int32_t *d_elist = nullptr;    // [R][k] empty clusters (cooperative repair)
+    int32_t *d_mlist = nullptr;    // [R]
+    double *d_pval = nullptr;      // [R][grid] partial argmax
+    int64_t *d_pidx = nullptr;
+    int coop_grid = 0;
     int32_t *d_cnt = nullptr;      // [R][k]
     int64_t *d_seg = nullptr;      // [R*k + 1] segment offsets into the sorted arrays
     double *d_part = nullptr;      // [R][nchunks][2] einsum lane partials
@@ -569,6 +576,151 @@ __global__ void k_assign(const double *__restrict__ x, int64_t n, int l, int k,
     if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&changed[r], ch);
 }
 
+// _repair_empty for all restarts with one cooperative grid (used when n is large): the
+// per-empty-cluster argmax over the n own-distances is a grid-wide reduction instead of one
+// CTA's scan, so a repair costs ~n/(SMs x bandwidth) instead of n/(one SM).  Same semantics
+// as k_repair: clusters empty after assignment, in increasing order, each takes the first
+// point of maximal own distance, whose own distance then becomes 0; counts and the
+// changed-label count are recomputed for the repaired restarts.
+constexpr int kRepairTPB = 512;
+constexpr int64_t kCoopRepairMinN = 200000;  // below this one CTA per restart is cheaper
+constexpr int kRepairMaxK = 16384;           // shared-memory histogram bins
+
+__global__ void __launch_bounds__(kRepairTPB) k_repair_coop(
+    const double *__restrict__ x, int64_t n, int l, int k, const double *__restrict__ cen,
+    const int32_t *__restrict__ active, const int32_t *__restrict__ prev, int32_t *__restrict__ lab,
+    int32_t *__restrict__ cnt, int32_t *__restrict__ changed, double *__restrict__ own_all,
+    int32_t *__restrict__ elist, int32_t *__restrict__ mlist, double *__restrict__ pval,
+    int64_t *__restrict__ pidx, int R) {
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, b = blockIdx.x;
+    __shared__ int base;
+    __shared__ double sv[kRepairTPB / 32];
+    __shared__ int64_t si[kRepairTPB / 32];
+    // phase 0: ordered list of the empty clusters of every active restart
+    for (int r = b; r < R; r += G) {
+        if (threadIdx.x == 0) base = 0;
+        __syncthreads();
+        if (active[r]) {
+            for (int c0 = 0; c0 < k; c0 += blockDim.x) {
+                const int c = c0 + threadIdx.x;
+                const bool e = c < k && cnt[(int64_t)r * k + c] == 0;
+                // block-ordered compaction: warp ballots, then warps in order
+                const unsigned bal = __ballot_sync(0xffffffffu, e);
+                __shared__ int wcnt[kRepairTPB / 32];
+                if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = __popc(bal);
+                __syncthreads();
+                int off = base;
+                for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) off += wcnt[w];
+                if (e) elist[(int64_t)r * k + off + __popc(bal & ((1u << (threadIdx.x & 31)) - 1))] = c;
+                __syncthreads();
+                if (threadIdx.x == 0)
+                    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) base += wcnt[w];
+                __syncthreads();
+            }
+        }
+        if (threadIdx.x == 0) mlist[r] = active[r] ? base : 0;
+        __syncthreads();
+    }
+    grid.sync();
+    int mm = 0;
+    for (int r = 0; r < R; ++r) mm = max(mm, mlist[r]);
+    if (mm == 0) return;  // uniform across the grid
+    // phase 1: own distances of the restarts that repair
+    const int64_t tid = (int64_t)b * blockDim.x + threadIdx.x, nth = (int64_t)G * blockDim.x;
+    for (int64_t t = tid; t < (int64_t)R * n; t += nth) {
+        const int r = (int)(t / n);
+        if (mlist[r] == 0) continue;
+        const int64_t j = t - (int64_t)r * n;
+        own_all[t] = d2nd(x + j * l, cen + ((int64_t)r * k + lab[t]) * l, l);
+    }
+    grid.sync();
+    for (int i = 0; i < mm; ++i) {
+        // phase A: per-block partial argmax (value desc, index asc) for every repairing restart
+        for (int r = 0; r < R; ++r) {
+            if (i >= mlist[r]) continue;
+            const double *own = own_all + (int64_t)r * n;
+            double bv = -1.0;
+            int64_t bj = n;
+            for (int64_t j = tid; j < n; j += nth) {
+                const double v = own[j];
+                if (v > bv) {
+                    bv = v;
+                    bj = j;
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int64_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                if (ov > bv || (ov == bv && oj < bj)) {
+                    bv = ov;
+                    bj = oj;
+                }
+            }
+            if ((threadIdx.x & 31) == 0) {
+                sv[threadIdx.x >> 5] = bv;
+                si[threadIdx.x >> 5] = bj;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+                    if (sv[w] > sv[0] || (sv[w] == sv[0] && si[w] < si[0])) {
+                        sv[0] = sv[w];
+                        si[0] = si[w];
+                    }
+                pval[(int64_t)r * G + b] = sv[0];
+                pidx[(int64_t)r * G + b] = si[0];
+            }
+            __syncthreads();
+        }
+        grid.sync();
+        // phase B: one thread per repairing restart combines the partials and moves the point
+        if (b == 0)
+            for (int r = threadIdx.x; r < R; r += blockDim.x) {
+                if (i >= mlist[r]) continue;
+                double bv = -1.0;
+                int64_t bj = n;
+                for (int q = 0; q < G; ++q) {
+                    const double v = pval[(int64_t)r * G + q];
+                    const int64_t j = pidx[(int64_t)r * G + q];
+                    if (v > bv || (v == bv && j < bj)) {
+                        bv = v;
+                        bj = j;
+                    }
+                }
+                lab[(int64_t)r * n + bj] = elist[(int64_t)r * k + i];
+                own_all[(int64_t)r * n + bj] = 0.0;
+            }
+        grid.sync();
+    }
+    // phase C: recount the repaired restarts
+    for (int64_t t = tid; t < (int64_t)R * k; t += nth)
+        if (mlist[t / k]) cnt[t] = 0;
+    if (b == 0)
+        for (int r = threadIdx.x; r < R; r += blockDim.x)
+            if (mlist[r]) changed[r] = 0;
+    grid.sync();
+    // block-local histograms in shared memory (k bins), one global add per bin per block
+    extern __shared__ int32_t hist[];
+    for (int r = 0; r < R; ++r) {
+        if (mlist[r] == 0) continue;
+        for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+        __syncthreads();
+        int ch = 0;
+        for (int64_t j = tid; j < n; j += nth) {
+            const int32_t lb = lab[(int64_t)r * n + j];
+            atomicAdd(&hist[lb], 1);
+            ch += lb != prev[(int64_t)r * n + j];
+        }
+        for (int o = 16; o; o >>= 1) ch += __shfl_xor_sync(0xffffffffu, ch, o);
+        if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&changed[r], ch);
+        __syncthreads();
+        for (int c = threadIdx.x; c < k; c += blockDim.x)
+            if (hist[c]) atomicAdd(&cnt[(int64_t)r * k + c], hist[c]);
+        __syncthreads();
+    }
+}
+
 // ---- assignment through sorted centers (k >= kSortedMinK) ------------------------------
 // argmin_c d2ref(x, c) is found without evaluating all k centers.  With u = 2^-53 and
 // D(c) = (x - c)^2 exact, d2ref's five roundings give |d2ref - D| <= 3.01 u (|x| + |c|)^2,
@@ -1053,6 +1205,18 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_scen, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_sidx, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_cmax, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_elist, (size_t)R * k, km->stream))) return st;
+    if ((st = grow(&km->d_mlist, (size_t)R, km->stream))) return st;
+    if (!km->coop_grid) {
+        int per = 0;
+        cudaFuncSetAttribute(k_repair_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kRepairMaxK * 4);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_repair_coop, kRepairTPB,
+                                                      kRepairMaxK * 4);
+        km->coop_grid = std::max(1, per) * km->sm_count;
+    }
+    if ((st = grow(&km->d_pval, (size_t)R * km->coop_grid, km->stream))) return st;
+    if ((st = grow(&km->d_pidx, (size_t)R * km->coop_grid, km->stream))) return st;
     if ((st = grow(&km->d_cnt, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_seg, (size_t)S, km->stream))) return st;
     if ((st = grow(&km->d_part, (size_t)R * nbuf * 2, km->stream))) return st;
@@ -1185,6 +1349,7 @@ void sc_kmeans_destroy(sc_kmeans *km) {
                     km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
                     km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
                     km->d_sq0, km->d_sq1, km->d_svmax, km->d_skp, km->d_idx, km->d_idx_alt,
+                    km->d_elist, km->d_mlist, km->d_pval, km->d_pidx,
                     km->d_segkpp};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, km->stream);
@@ -1360,12 +1525,42 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                                    km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
                                                    km->d_changed);
         }
-        k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, l, k, km->d_cen, km->d_active,
-                                              km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
-                                              km->d_changed, km->d_best);
+        if (n >= kCoopRepairMinN && k <= kRepairMaxK && getenv("SC_KMEANS_CTA_REPAIR") == nullptr) {
+            const double *a_x = km->d_x, *a_cen = km->d_cen;
+            const int32_t *a_act = km->d_active, *a_prev = km->d_lab[cur];
+            int32_t *a_lab = km->d_lab[nxt], *a_cnt = km->d_cnt, *a_ch = km->d_changed;
+            double *a_own = km->d_best, *a_pv = km->d_pval;
+            int32_t *a_el = km->d_elist, *a_ml = km->d_mlist;
+            int64_t *a_pi = km->d_pidx;
+            int64_t a_n = n;
+            int a_l = l, a_k = k, a_R = R;
+            void *args[] = {&a_x, &a_n, &a_l, &a_k, &a_cen, &a_act, &a_prev, &a_lab, &a_cnt,
+                            &a_ch, &a_own, &a_el, &a_ml, &a_pv, &a_pi, &a_R};
+            SC_CUDA(cudaLaunchCooperativeKernel((const void *)k_repair_coop, km->coop_grid,
+                                                kRepairTPB, args, (size_t)k * 4, s));
+        } else {
+            k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, l, k, km->d_cen, km->d_active,
+                                                  km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
+                                                  km->d_changed, km->d_best);
+        }
         // np.add.at order: stable radix sort of the active restarts' points on
         // (slot, label) keeps point-index order inside every cluster; then exact ordered sums
         if (prof) cudaEventRecord(pe[1], s);
+        if (prof && n >= kCoopRepairMinN && k <= kRepairMaxK &&
+            getenv("SC_KMEANS_CTA_REPAIR") == nullptr) {
+            std::vector<int32_t> ml(R);
+            cudaMemcpyAsync(ml.data(), km->d_mlist, (size_t)R * 4, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            float ms_a = 0.f;
+            cudaEventElapsedTime(&ms_a, pe[0], pe[1]);
+            int mx = 0, tot = 0;
+            for (int r = 0; r < R; ++r) {
+                mx = std::max(mx, ml[r]);
+                tot += ml[r];
+            }
+            fprintf(stderr, "[sc_kmeans_lloyd] it %d: empty clusters max %d total %d, "
+                    "assign+repair %.3f ms\n", it, mx, tot, ms_a);
+        }
         const int64_t m = (int64_t)nact * n;
         size_t tb = km->cub_bytes;
         if (l == 1) {

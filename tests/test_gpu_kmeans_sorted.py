@@ -30,3 +30,21 @@ def test_sorted_assignment_matches_bruteforce(name, x, k):
         part = km.lloyd(k, 11, restarts=2)
     lab, _ = O.lloyd(x, k, 11, restarts=2)
     assert np.array_equal(part.labels, lab)
+
+
+def test_cooperative_repair_matches_oracle():
+    """n >= 200k takes the grid-wide (cooperative) empty-cluster repair; heavy duplication
+    with k above the number of distinct values forces degenerate seeding rounds and repeated
+    repairs, including the all-zero-distance argmax corner.  Labels vs the C oracle."""
+    rng = np.random.default_rng(7)
+    vals = rng.random(60)
+    x = vals[rng.integers(0, 60, 300_000)]
+    with KMeans1D(x) as km:
+        part = km.lloyd(90, 3, restarts=2, max_iters=6)
+    lab, _ = O.lloyd(x, 90, 3, restarts=2, max_iters=6)
+    assert np.array_equal(part.labels, lab)
+    x2 = np.concatenate([rng.random(250_000), np.full(50_000, 0.5)])
+    with KMeans1D(x2) as km:
+        part = km.lloyd(40, 5, restarts=3, max_iters=8)
+    lab, _ = O.lloyd(x2, 40, 5, restarts=3, max_iters=8)
+    assert np.array_equal(part.labels, lab)
