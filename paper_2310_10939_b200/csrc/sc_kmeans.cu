@@ -207,12 +207,27 @@ __global__ void k_seq_summarize(SegView v, SeqWork w, const int64_t *__restrict_
 // one warp per segment: approximate chunk starts -> predicted grid per chunk.  Chunk data
 // are read 256 at a time (8 independent loads per lane) so the walk pays one memory latency
 // per 256 chunks.
-__global__ void k_seq_predict(SegView v, SeqWork w) {
-    const int lane = threadIdx.x & 31;
-    const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+constexpr int kPredictWarps = 8;
+
+// one CTA per segment: each warp takes a contiguous share of the segment's chunks, the
+// warps' approximate totals are scanned in shared memory, then every warp walks its share
+// from its carry (approximate prefixes: they only steer the prediction, compose re-checks)
+__global__ void __launch_bounds__(32 * kPredictWarps) k_seq_predict(SegView v, SeqWork w) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int s = blockIdx.x;
     if (s >= v.S || !seg_on(v, s)) return;
-    const int64_t c0 = v.cofs[s], c1 = v.cofs[s + 1];
+    const int64_t c0s = v.cofs[s], c1s = v.cofs[s + 1];
+    const int64_t per = ((c1s - c0s + kPredictWarps - 1) / kPredictWarps + 31) / 32 * 32;
+    const int64_t c0 = min(c1s, c0s + wid * per), c1 = min(c1s, c0 + per);
+    __shared__ double part[kPredictWarps];
+    double tot = 0.0;
+    for (int64_t c = c0 + lane; c < c1; c += 32) tot += w.A[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) part[wid] = tot;
+    __syncthreads();
     double carry = 0.0;
+    for (int q = 0; q < wid; ++q) carry += part[q];
     const double lo_f = 1.0 - 1.0 / 1048576.0, hi_f = 1.0 + 1.0 / 1048576.0;
     for (int64_t blk = c0; blk < c1; blk += 256) {
         double A[8], V[8];
@@ -374,12 +389,22 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
             const int Lb = badm ? __ffs(badm) - 1 : 32;
             const int nadv = min(Lb, __popc(valm));
             if (want_cstart && lane < nadv) {
-                // exact start of every chunk of this super-chunk (for the k-means++ search)
+                // exact start of every chunk of this super-chunk (for the k-means++ search);
+                // the chunk maps are fetched 8 at a time so a step pays 4 memory latencies
                 int64_t S = Sl;
                 const int64_t cb = G * kSuper;
-                for (int t = 0; t < kSuper; ++t) {
-                    w.cstart[cb + t] = from_units(S, g.k);
-                    S = pmap_apply(PMap{w.q0[cb + t], w.q1[cb + t]}, S);
+                for (int t0 = 0; t0 < kSuper; t0 += 8) {
+                    int64_t a0[8], a1[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        a0[u] = w.q0[cb + t0 + u];
+                        a1[u] = w.q1[cb + t0 + u];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        w.cstart[cb + t0 + u] = from_units(S, g.k);
+                        S = pmap_apply(PMap{a0[u], a1[u]}, S);
+                    }
                 }
             }
             if (nadv > 0) {
@@ -480,6 +505,58 @@ __global__ void k_kpp_update(const double *__restrict__ x, int64_t n, int l, int
          j += (int64_t)gridDim.x * blockDim.x) {
         const double v = d2nd(x + j * l, c, l);
         if (v < b[j]) b[j] = v;
+    }
+}
+
+// k-means++ round i, fused with the seqsum summary of the D^2 weights: one warp per
+// 256-weight chunk lowers best[] by the distance to the center chosen in round i-1 (when
+// this restart has one) and records the chunk's approximate sum and max for the prediction
+// (k_seq_summarize's output), so the weights are read once per round instead of twice
+__global__ void k_kpp_update_sum(const double *__restrict__ x, int64_t n, int l, int k, int i,
+                                 const int64_t *__restrict__ chosen,
+                                 const int32_t *__restrict__ start, const int32_t *__restrict__ on,
+                                 const int32_t *__restrict__ round_on, double *__restrict__ best,
+                                 SeqWork w, int64_t cps, int R) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = wid; c < (int64_t)R * cps; c += nw) {
+        const int r = (int)(c / cps);
+        if (!round_on[r]) continue;
+        const bool upd = on[r] && i - 1 >= start[r];
+        const double *cn = upd ? x + chosen[(int64_t)r * k + i - 1] * l : nullptr;
+        double *b = best + (int64_t)r * n;
+        const int64_t j0 = (c - (int64_t)r * cps) * kSeqChunk + lane * kSeqPerLane;
+        double sum = 0.0, mx = 0.0;
+        int bad = 0;
+#pragma unroll
+        for (int t = 0; t < kSeqPerLane; ++t) {
+            const int64_t j = j0 + t;
+            if (j < n) {
+                double v = b[j];
+                if (upd) {
+                    const double d = d2nd(x + j * l, cn, l);
+                    if (d < v) {
+                        v = d;
+                        b[j] = v;
+                    }
+                }
+                sum += v;
+                mx = fmax(mx, v);
+                bad |= !(v >= 0.0) || !isfinite(v);
+            }
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+        }
+        if (lane == 0) {
+            w.A[c] = sum;
+            w.vmax[c] = mx;
+            if (bad) w.neg[r] = 1;
+        }
     }
 }
 
@@ -1418,12 +1495,11 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
                                   km->d_best);
     SC_CUDA(cudaGetLastError());
     for (int i = smin; i < k; ++i) {
-        k_kpp_update<<<g2, 256, 0, s>>>(km->d_x, n, km->l, k, i, km->d_chosen, km->d_start, km->d_on,
-                                         km->d_best);
         k_kpp_round_on<<<(R + 127) / 128, 128, 0, s>>>(R, i, km->d_start, km->d_on,
                                                        km->d_round_on, km->d_neg);
-        k_seq_summarize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
-        k_seq_predict<<<gs, 256, 0, s>>>(v, w);
+        k_kpp_update_sum<<<gw, 256, 0, s>>>(km->d_x, n, km->l, k, i, km->d_chosen, km->d_start,
+                                            km->d_on, km->d_round_on, km->d_best, w, cps, R);
+        k_seq_predict<<<R, 32 * kPredictWarps, 0, s>>>(v, w);
         k_seq_chunkmap<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
         k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
         k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(v, w, 1);
@@ -1586,7 +1662,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                                                     km->d_vals_alt);
             SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)nseg * 4, s));
             k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
-            k_seq_predict<<<gsm, 256, 0, s>>>(vm, wm);
+            k_seq_predict<<<nseg, 32 * kPredictWarps, 0, s>>>(vm, wm);
             k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
             k_seq_superize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
             k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
@@ -1698,7 +1774,7 @@ static int32_t seqsum_device(const double *d_vals, int32_t nseg, const int64_t *
         const int gw = (int)std::min<int64_t>((nch * 32 + 255) / 256 + 1, (int64_t)sms * 8);
         const int gs = (nseg * 32 + 255) / 256;
         k_seq_summarize<<<gw, 256>>>(v, w, d_nch);
-        k_seq_predict<<<gs, 256>>>(v, w);
+        k_seq_predict<<<nseg, 32 * kPredictWarps>>>(v, w);
         k_seq_chunkmap<<<gw, 256>>>(v, w, d_nch);
         k_seq_superize<<<gw, 256>>>(v, w, d_nch);
         k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem>>>(
