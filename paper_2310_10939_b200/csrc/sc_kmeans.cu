@@ -44,6 +44,12 @@ struct sc_kmeans {
     double *d_x = nullptr;
     int32_t *d_idx = nullptr, *d_idx_alt = nullptr;  // [R*n] sort payload when l > 1
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;  // Lloyd: cost of iteration it beside main(it+1)
+    cudaEvent_t ev_main = nullptr, ev_cost = nullptr;
+    double *h_cost = nullptr;        // pinned [2][R]
+    int32_t *h_changed = nullptr;    // pinned [2][R]
+    int32_t *h_act = nullptr;        // pinned [2][2R]: active flags + compacted list per parity
+    int cap_host_r = 0;
     // workspaces (grown on demand)
     int cap_r = 0, cap_k = 0;
     double *d_best = nullptr;      // [R][n] k-means++ D^2 weights
@@ -1274,7 +1280,7 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_u, (size_t)R * k, km->stream))) return st;
     if ((st = grow(&km->d_start, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_degen, (size_t)R, km->stream))) return st;
-    if ((st = grow(&km->d_cen, (size_t)R * k * km->l, km->stream))) return st;
+    if ((st = grow(&km->d_cen, (size_t)2 * R * k * km->l, km->stream))) return st;
     if (km->l > 1) {
         if ((st = grow(&km->d_idx, (size_t)R * n, km->stream))) return st;
         if ((st = grow(&km->d_idx_alt, (size_t)R * n, km->stream))) return st;
@@ -1298,8 +1304,29 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_seg, (size_t)S, km->stream))) return st;
     if ((st = grow(&km->d_part, (size_t)R * nbuf * 2, km->stream))) return st;
     if ((st = grow(&km->d_cost, (size_t)R, km->stream))) return st;
-    if ((st = grow(&km->d_changed, (size_t)R, km->stream))) return st;
-    if ((st = grow(&km->d_active, (size_t)R, km->stream))) return st;
+    if ((st = grow(&km->d_changed, (size_t)2 * R, km->stream))) return st;
+    if ((st = grow(&km->d_active, (size_t)2 * R, km->stream))) return st;
+    if (R > km->cap_host_r) {
+        // page-locked result/flag slots live in a per-thread arena that outlives the
+        // context (cudaMallocHost/cudaFreeHost per clustering would cost milliseconds)
+        thread_local struct Arena {
+            unsigned char *p = nullptr;
+            size_t bytes = 0;
+        } arena;
+        const size_t need = (size_t)R * (16 + 8 + 16);
+        if (arena.bytes < need) {
+            if (arena.p) cudaFreeHost(arena.p);
+            arena.p = nullptr;
+            arena.bytes = 0;
+            if (cudaMallocHost((void **)&arena.p, need) != cudaSuccess)
+                return fail(SC_E_OOM, "pinned host buffers");
+            arena.bytes = need;
+        }
+        km->h_cost = reinterpret_cast<double *>(arena.p);
+        km->h_changed = reinterpret_cast<int32_t *>(arena.p + (size_t)R * 16);
+        km->h_act = reinterpret_cast<int32_t *>(arena.p + (size_t)R * 24);
+        km->cap_host_r = R;
+    }
     if ((st = grow(&km->d_empty, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_A, (size_t)nch, km->stream))) return st;
     if ((st = grow(&km->d_vmax, (size_t)nch, km->stream))) return st;
@@ -1367,6 +1394,9 @@ static int32_t km_init(int device, int64_t n, int l, sc_kmeans **out) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaError_t e = cudaStreamCreateWithFlags(&km->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&km->stream2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&km->ev_main, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&km->ev_cost, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&km->d_x, (size_t)n * l * 8, km->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(km->stream);
     if (e != cudaSuccess) {
@@ -1428,12 +1458,16 @@ void sc_kmeans_destroy(sc_kmeans *km) {
                     km->d_sq0, km->d_sq1, km->d_svmax, km->d_skp, km->d_idx, km->d_idx_alt,
                     km->d_elist, km->d_mlist, km->d_pval, km->d_pidx,
                     km->d_segkpp};
+    if (km->stream2) cudaStreamSynchronize(km->stream2);
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, km->stream);
     if (km->stream) {
         cudaStreamSynchronize(km->stream);
         cudaStreamDestroy(km->stream);
     }
+    if (km->stream2) cudaStreamDestroy(km->stream2);
+    if (km->ev_main) cudaEventDestroy(km->ev_main);
+    if (km->ev_cost) cudaEventDestroy(km->ev_cost);
     delete km;
 }
 
@@ -1574,37 +1608,51 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     double pacc[4] = {0, 0, 0, 0};
     if (prof)
         for (auto &ev : pe) cudaEventCreate(&ev);
-    for (int it = 0; it < max_iters; ++it) {
+    // Iteration it: "main" (assign, repair, sort, ordered sums, means) on stream s, then the
+    // einsum cost on stream s2.  While the host waits for cost(it) to decide which restarts
+    // stop, main(it+1) already runs speculatively for every restart still active at it (a
+    // restart that stops at it simply ignores its iteration it+1), so the cost chain and
+    // the host round trip overlap the next iteration.  Double-buffered per parity of it:
+    // centers (assign reads cen[it&1], means write cen[(it+1)&1]), active flags, changed
+    // counts, host result slots.
+    cudaStream_t s2 = km->stream2;
+    auto cen_buf = [&](int i) { return km->d_cen + (size_t)(i & 1) * rk * l; };
+    auto act_buf = [&](int i) { return km->d_active + (i & 1) * R; };
+    auto chg_buf = [&](int i) { return km->d_changed + (i & 1) * R; };
+    auto launch_main = [&](int it, const std::vector<int32_t> &actv, int cur_lab) -> int32_t {
+        // pinned staging (a pageable copy would make the host wait for the stream)
+        int32_t *hflags = km->h_act + (size_t)(it & 1) * 2 * R, *hlist = hflags + R;
         int nact = 0;
-        for (int r = 0; r < R; ++r) nact += active[r];
-        if (!nact) break;
-        const int nxt = cur ^ 1;
-        std::vector<int32_t> act;
-        for (int r = 0; r < R; ++r)
-            if (active[r]) act.push_back(r);
+        for (int r = 0; r < R; ++r) {
+            hflags[r] = actv[r];
+            if (actv[r]) hlist[nact++] = r;
+        }
+        const int nxt = cur_lab ^ 1;
         const int nseg = nact * k;
         int end_bit = 1;
         while ((1ll << end_bit) < (long long)nseg) ++end_bit;
-        SC_CUDA(cudaMemcpyAsync(km->d_active, active.data(), (size_t)R * 4, cudaMemcpyHostToDevice, s));
-        SC_CUDA(cudaMemcpyAsync(km->d_empty, act.data(), (size_t)nact * 4, cudaMemcpyHostToDevice, s));
+        int32_t *d_act = act_buf(it), *d_chg = chg_buf(it);
+        double *cen_in = cen_buf(it), *cen_out = cen_buf(it + 1);
+        SC_CUDA(cudaMemcpyAsync(d_act, hflags, (size_t)R * 4, cudaMemcpyHostToDevice, s));
+        SC_CUDA(cudaMemcpyAsync(km->d_empty, hlist, (size_t)nact * 4, cudaMemcpyHostToDevice, s));
         SC_CUDA(cudaMemsetAsync(km->d_cnt, 0, (size_t)rk * 4, s));
-        SC_CUDA(cudaMemsetAsync(km->d_changed, 0, (size_t)R * 4, s));
+        SC_CUDA(cudaMemsetAsync(d_chg, 0, (size_t)R * 4, s));
         if (prof) cudaEventRecord(pe[0], s);
         if (sorted_assign) {
-            k_sort_centers<<<R, 1024, smem_sort, s>>>(k, km->d_cen, km->d_active, km->d_scen, km->d_sidx,
-                                              km->d_cmax);
+            k_sort_centers<<<R, 1024, smem_sort, s>>>(k, cen_in, d_act, km->d_scen, km->d_sidx,
+                                                      km->d_cmax);
             k_assign_sorted<<<ga, 256, smem_sorted, s>>>(km->d_x, n, k, km->d_scen, km->d_sidx,
-                                                         km->d_cmax, km->d_active, km->d_lab[cur],
-                                                         km->d_lab[nxt], km->d_cnt, km->d_changed);
+                                                         km->d_cmax, d_act, km->d_lab[cur_lab],
+                                                         km->d_lab[nxt], km->d_cnt, d_chg);
         } else {
-            k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, l, k, km->d_cen, km->d_active,
-                                                   km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
-                                                   km->d_changed);
+            k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, l, k, cen_in, d_act,
+                                                   km->d_lab[cur_lab], km->d_lab[nxt], km->d_cnt,
+                                                   d_chg);
         }
         if (n >= kCoopRepairMinN && k <= kRepairMaxK && getenv("SC_KMEANS_CTA_REPAIR") == nullptr) {
-            const double *a_x = km->d_x, *a_cen = km->d_cen;
-            const int32_t *a_act = km->d_active, *a_prev = km->d_lab[cur];
-            int32_t *a_lab = km->d_lab[nxt], *a_cnt = km->d_cnt, *a_ch = km->d_changed;
+            const double *a_x = km->d_x, *a_cen = cen_in;
+            const int32_t *a_act = d_act, *a_prev = km->d_lab[cur_lab];
+            int32_t *a_lab = km->d_lab[nxt], *a_cnt = km->d_cnt, *a_ch = d_chg;
             double *a_own = km->d_best, *a_pv = km->d_pval;
             int32_t *a_el = km->d_elist, *a_ml = km->d_mlist;
             int64_t *a_pi = km->d_pidx;
@@ -1615,28 +1663,13 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             SC_CUDA(cudaLaunchCooperativeKernel((const void *)k_repair_coop, km->coop_grid,
                                                 kRepairTPB, args, (size_t)k * 4, s));
         } else {
-            k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, l, k, km->d_cen, km->d_active,
-                                                  km->d_lab[cur], km->d_lab[nxt], km->d_cnt,
-                                                  km->d_changed, km->d_best);
+            k_repair<<<R, 1024, (size_t)k, s>>>(km->d_x, n, l, k, cen_in, d_act,
+                                                  km->d_lab[cur_lab], km->d_lab[nxt], km->d_cnt,
+                                                  d_chg, km->d_best);
         }
         // np.add.at order: stable radix sort of the active restarts' points on
         // (slot, label) keeps point-index order inside every cluster; then exact ordered sums
         if (prof) cudaEventRecord(pe[1], s);
-        if (prof && n >= kCoopRepairMinN && k <= kRepairMaxK &&
-            getenv("SC_KMEANS_CTA_REPAIR") == nullptr) {
-            std::vector<int32_t> ml(R);
-            cudaMemcpyAsync(ml.data(), km->d_mlist, (size_t)R * 4, cudaMemcpyDeviceToHost, s);
-            cudaStreamSynchronize(s);
-            float ms_a = 0.f;
-            cudaEventElapsedTime(&ms_a, pe[0], pe[1]);
-            int mx = 0, tot = 0;
-            for (int r = 0; r < R; ++r) {
-                mx = std::max(mx, ml[r]);
-                tot += ml[r];
-            }
-            fprintf(stderr, "[sc_kmeans_lloyd] it %d: empty clusters max %d total %d, "
-                    "assign+repair %.3f ms\n", it, mx, tot, ms_a);
-        }
         const int64_t m = (int64_t)nact * n;
         size_t tb = km->cub_bytes;
         if (l == 1) {
@@ -1655,7 +1688,6 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         if (prof) cudaEventRecord(pe[2], s);
         vm.S = nseg;
         const int gwm = grid_1d(km, (m / kSeqChunk + nseg) * 32, 256);
-        const int gsm = (nseg * 32 + 255) / 256;
         for (int q = 0; q < l; ++q) {  // np.add.at over each coordinate column
             if (l > 1)
                 k_gather_coord<<<grid_1d(km, m, 256), 256, 0, s>>>(km->d_x, km->d_idx_alt, m, l, q,
@@ -1668,37 +1700,67 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
                             kComposeSmem, s>>>(vm, wm, 0);
             k_seg_means<<<(nseg + 127) / 128, 128, 0, s>>>(nseg, k, l, q, km->d_seg, km->d_total,
-                                                           km->d_empty, km->d_cen);
+                                                           km->d_empty, cen_out);
         }
         if (prof) cudaEventRecord(pe[3], s);
-        k_cost_buf<<<gc, 32 * kCostWarps, 0, s>>>(km->d_x, n, l, k, km->d_lab[nxt], km->d_cen,
-                                                   km->d_active, nbuf, km->d_part);
-        k_cost_combine<<<R, 256, 0, s>>>(nbuf, km->d_part, km->d_active, km->d_cost);
         SC_CUDA(cudaGetLastError());
-        if (prof) cudaEventRecord(pe[4], s);
-        SC_CUDA(cudaMemcpyAsync(cost.data(), km->d_cost, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
-        SC_CUDA(cudaMemcpyAsync(changed.data(), km->d_changed, (size_t)R * 4, cudaMemcpyDeviceToHost, s));
-        SC_CUDA(cudaStreamSynchronize(s));
+        return SC_OK;
+    };
+    // cost of iteration it (labels d_lab[lab_buf], centers cen[(it+1)&1]) on s2 after main(it)
+    auto launch_cost = [&](int it, int lab_buf) -> int32_t {
+        SC_CUDA(cudaEventRecord(km->ev_main, s));
+        SC_CUDA(cudaStreamWaitEvent(s2, km->ev_main, 0));
+        k_cost_buf<<<gc, 32 * kCostWarps, 0, s2>>>(km->d_x, n, l, k, km->d_lab[lab_buf],
+                                                    cen_buf(it + 1), act_buf(it), nbuf, km->d_part);
+        k_cost_combine<<<R, 256, 0, s2>>>(nbuf, km->d_part, act_buf(it), km->d_cost);
+        SC_CUDA(cudaGetLastError());
+        if (prof) cudaEventRecord(pe[4], s2);
+        SC_CUDA(cudaMemcpyAsync(km->h_cost + (it & 1) * R, km->d_cost, (size_t)R * 8,
+                                cudaMemcpyDeviceToHost, s2));
+        SC_CUDA(cudaMemcpyAsync(km->h_changed + (it & 1) * R, chg_buf(it), (size_t)R * 4,
+                                cudaMemcpyDeviceToHost, s2));
+        SC_CUDA(cudaEventRecord(km->ev_cost, s2));
+        return SC_OK;
+    };
+    const bool speculate = getenv("SC_KMEANS_NO_SPECULATION") == nullptr;
+    double wait_ms = 0.0;
+    if ((st = launch_main(0, active, cur))) return st;
+    for (int it = 0; it < max_iters; ++it) {
+        const int nxt = cur ^ 1;
+        if ((st = launch_cost(it, nxt))) return st;
+        const bool spec = speculate && it + 1 < max_iters;
+        if (spec && (st = launch_main(it + 1, active, nxt))) return st;
+        auto w0 = std::chrono::steady_clock::now();
+        SC_CUDA(cudaEventSynchronize(km->ev_cost));
+        wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
         if (prof)
             for (int q = 0; q < 4; ++q) {
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, pe[q], pe[q + 1]);
                 pacc[q] += ms;
             }
+        const double *hc = km->h_cost + (it & 1) * R;
+        const int32_t *hch = km->h_changed + (it & 1) * R;
+        int nact = 0;
         for (int r = 0; r < R; ++r) {
             if (!active[r]) continue;
             // kmeans.py:202-210, in the same double arithmetic
             const bool fin = std::isfinite(prev[r]);
-            const bool unchanged = changed[r] == 0 && fin;
-            const double c = cost[r];
+            const bool unchanged = hch[r] == 0 && fin;
+            const double c = hc[r];
             const bool small_gain = fin && (prev[r] - c <= tol * std::max(prev[r], 1e-300));
             prev[r] = c;
             iters[r] += 1;
             final_buf[r] = nxt;
             if (unchanged || small_gain) active[r] = 0;
+            nact += active[r];
         }
         cur = nxt;
+        if (!nact) break;
+        if (!speculate && it + 1 < max_iters && (st = launch_main(it + 1, active, cur))) return st;
     }
+    if (prof) fprintf(stderr, "[sc_kmeans_lloyd] host waited %.3f ms for the iteration results\n", wait_ms);
+    SC_CUDA(cudaStreamSynchronize(s));  // a speculative iteration may still be running
     if (prof) {
         fprintf(stderr, "[sc_kmeans_lloyd] assign+repair %.3f ms, sort %.3f ms, ordered sums %.3f ms, cost %.3f ms\n",
                 pacc[0], pacc[1], pacc[2], pacc[3]);
