@@ -239,6 +239,14 @@ struct BlkArgs {
     int64_t n_sell, nslices, n_wide;
 };
 
+// 256-bit read-only load (sm_100: LDG.E.ENL2.256), p 32-byte aligned
+__device__ __forceinline__ void ld_nc_v4(const double *p, double &a, double &b, double &c,
+                                         double &d) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+                 : "l"(p));
+}
+
 template <int L>
 __device__ __forceinline__ void blk_epilogue(const BlkArgs &a, int64_t r, const double (&acc)[L],
                                              const double (&xr)[L], double sc) {
@@ -252,7 +260,7 @@ __device__ __forceinline__ void blk_epilogue(const BlkArgs &a, int64_t r, const 
 
 template <int L, bool UNIT>
 __global__ void __launch_bounds__(kStepTPB) k_blk_step(BlkArgs a) {
-    constexpr int U = L <= 2 ? 4 : 2;  // entries in flight per lane
+    constexpr int U = L <= 4 ? 4 : 2;  // entries in flight per lane
     const int lane = threadIdx.x & 31;
     const int64_t sl = (int64_t)blockIdx.x * (kStepTPB / 32) + (threadIdx.x >> 5);
     if (sl >= a.nslices) return;
@@ -281,8 +289,11 @@ __global__ void __launch_bounds__(kStepTPB) k_blk_step(BlkArgs a) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int q = 0; q < L; ++q)
-                v[u][q] = c[u] != kPad ? __ldg(a.z_in + (int64_t)c[u] * L + q) : 0.0;
+            for (int q = 0; q < L; q += 4) {  // one 32-byte load per 4 columns (L % 4 == 0)
+                if (c[u] != kPad) ld_nc_v4(a.z_in + (int64_t)c[u] * L + q, v[u][q], v[u][q + 1],
+                                            v[u][q + 2], v[u][q + 3]);
+                else v[u][q] = v[u][q + 1] = v[u][q + 2] = v[u][q + 3] = 0.0;
+            }
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (c[u] != kPad)
@@ -312,9 +323,13 @@ __global__ void __launch_bounds__(kStepTPB) k_blk_wide(BlkArgs a) {
             const int64_t c = __ldcs(a.wcol + j);
             const double wt = UNIT ? 1.0 : __ldcs(a.wval + j);
 #pragma unroll
-            for (int q = 0; q < L; ++q) {
-                const double z = __ldg(a.z_in + c * L + q);
-                v[q] = UNIT ? z : __dmul_rn(wt, z);
+            for (int q = 0; q < L; q += 4) {
+                double z0, z1, z2, z3;
+                ld_nc_v4(a.z_in + c * L + q, z0, z1, z2, z3);
+                v[q] = UNIT ? z0 : __dmul_rn(wt, z0);
+                v[q + 1] = UNIT ? z1 : __dmul_rn(wt, z1);
+                v[q + 2] = UNIT ? z2 : __dmul_rn(wt, z2);
+                v[q + 3] = UNIT ? z3 : __dmul_rn(wt, z3);
             }
         }
     };
@@ -340,13 +355,14 @@ __global__ void __launch_bounds__(kStepTPB) k_blk_wide(BlkArgs a) {
     }
 }
 
-// out[i*L + q] = in[idx[i]*L + q] (row permutation of an [n][L] block), and z = s * x rows
+// out[i*lo + q] = in[idx[i]*li + q] for q < L (row permutation of an [n][L] block between
+// row strides li and lo; columns L..lo-1 of out are zero-filled), and z = s * x rows
 __global__ void k_gather_rows(const double *__restrict__ in, const int32_t *__restrict__ idx,
-                              double *__restrict__ out, int64_t n, int L) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * L;
+                              double *__restrict__ out, int64_t n, int L, int li, int lo) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * lo;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / L, q = t - i * L;
-        out[t] = in[(int64_t)idx[i] * L + q];
+        const int64_t i = t / lo, q = t - i * lo;
+        out[t] = q < L ? in[(int64_t)idx[i] * li + q] : 0.0;
     }
 }
 
@@ -1371,7 +1387,7 @@ struct BlkDispatch<L0, Ls...> {
         return BlkDispatch<Ls...>::run(L, g, a, s);
     }
 };
-using BlkAll = BlkDispatch<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>;
+using BlkAll = BlkDispatch<4, 8, 12, 16>;  // padded widths (32-byte rows)
 constexpr int kMaxBlockCols = 16;
 }  // namespace sc
 
@@ -1389,8 +1405,11 @@ int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *
     cudaStream_t s = g->stream;
     int32_t st;
     if ((st = ensure_isd(g, s))) return st;
-    const int64_t n = g->n, nl = n * L;
-    double *buf = nullptr;  // x0, x[2], z[2], staging: 6 [n][L] blocks
+    // columns padded to a multiple of 4 so every row is 32-byte aligned and one 256-bit
+    // load fetches four of a neighbour's values; the zero padding columns stay zero
+    const int LP = (L + 3) / 4 * 4;
+    const int64_t n = g->n, nl = n * LP;
+    double *buf = nullptr;  // x0, x[2], z[2], staging: 6 [n][LP] blocks
     SC_CUDA(cudaMallocAsync((void **)&buf, (size_t)nl * 6 * 8, s));
     double *bx0 = buf, *bx[2] = {buf + nl, buf + 2 * nl}, *bz[2] = {buf + 3 * nl, buf + 4 * nl};
     double *stage = buf + 5 * nl;
@@ -1399,11 +1418,11 @@ int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *
         cudaStreamSynchronize(s);
         return code;
     };
-    cudaError_t e = cudaMemcpyAsync(stage, x0, (size_t)nl * 8, cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaMemcpyAsync(stage, x0, (size_t)n * L * 8, cudaMemcpyHostToDevice, s);
     if (e) return done(fail(SC_E_CUDA, "block upload: %s", cudaGetErrorString(e)));
     const int gr = grid_for(g, nl, 256);
-    k_gather_rows<<<gr, 256, 0, s>>>(stage, g->d_perm, bx0, n, L);  // original -> renumbered
-    k_scale_rows<<<gr, 256, 0, s>>>(bx0, g->d_isd, bz[0], n, L);
+    k_gather_rows<<<gr, 256, 0, s>>>(stage, g->d_perm, bx0, n, L, L, LP);  // original -> renumbered
+    k_scale_rows<<<gr, 256, 0, s>>>(bx0, g->d_isd, bz[0], n, LP);
     cudaEventRecord(g->ev0, s);
     BlkArgs a;
     a.slice_ptr = g->d_slice_ptr;
@@ -1422,7 +1441,7 @@ int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *
         a.z_in = bz[in];
         a.x_out = bx[out];
         a.z_out = bz[out];
-        BlkAll::run(L, g, a, s);
+        BlkAll::run(LP, g, a, s);
     }
     cudaEventRecord(g->ev1, s);
     e = cudaGetLastError();
@@ -1435,8 +1454,8 @@ int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *
     for (int pass = 0; pass < 2; ++pass) {
         double *host = pass ? scaled_out : raw_out;
         if (!host) continue;
-        k_gather_rows<<<gr, 256, 0, s>>>(pass ? zr : xr, g->d_iperm, stage, n, L);
-        e = cudaMemcpyAsync(host, stage, (size_t)nl * 8, cudaMemcpyDeviceToHost, s);
+        k_gather_rows<<<gr, 256, 0, s>>>(pass ? zr : xr, g->d_iperm, stage, n, L, LP, L);
+        e = cudaMemcpyAsync(host, stage, (size_t)n * L * 8, cudaMemcpyDeviceToHost, s);
         if (!e) e = cudaStreamSynchronize(s);
         if (e) return done(fail(SC_E_CUDA, "block download: %s", cudaGetErrorString(e)));
     }
