@@ -499,20 +499,6 @@ __global__ void k_kpp_init(const double *__restrict__ x, int64_t n, int l, int k
     }
 }
 
-// best = min(best, d2(x, x[chosen[r][i-1]])) when round i-1 was picked in this call
-__global__ void k_kpp_update(const double *__restrict__ x, int64_t n, int l, int k, int i,
-                             const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
-                             const int32_t *__restrict__ on, double *__restrict__ best) {
-    const int r = blockIdx.y;
-    if (!on[r] || i - 1 < start[r]) return;
-    const double *c = x + chosen[(int64_t)r * k + i - 1] * l;
-    double *b = best + (int64_t)r * n;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        const double v = d2nd(x + j * l, c, l);
-        if (v < b[j]) b[j] = v;
-    }
-}
 
 // k-means++ round i, fused with the seqsum summary of the D^2 weights: one warp per
 // 256-weight chunk lowers best[] by the distance to the center chosen in round i-1 (when
