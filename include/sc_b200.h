@@ -218,6 +218,17 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t restarts, const int64_
                         int32_t max_iters, double tol, int64_t *labels_out, double *costs_out,
                         int32_t *iters_out, int32_t *best_restart_out, double *ms_out);
 
+/* Fast mode (north star step 3): the same seeds, then Lloyd on the sorted values -- every
+ * cluster is an interval of the sorted points, so an iteration is k binary searches plus
+ * prefix-sum means and costs, all restarts' iterations in one kernel (one CTA per restart).
+ * Tie rules, empty-cluster repair and stop rules follow the reference, but the sums are
+ * prefix sums (not the reference's np.add.at / einsum order): not bit-exact, labels agree
+ * with the replica except where a distance or stop decision sits within rounding.
+ * 1-D points, k <= 2048. */
+int32_t sc_kmeans_lloyd_sorted(sc_kmeans *km, int32_t k, int32_t restarts, const int64_t *chosen,
+                               int32_t max_iters, double tol, int64_t *labels_out,
+                               double *costs_out, int32_t *iters_out, int32_t *best_restart_out);
+
 /* ---- exact sequential sums (the k-means replica's engine, exposed for testing) ---- */
 /* totals[s] = ((vals[lo] + vals[lo+1]) + ...) left to right in double, lo..hi = segment s;
  * bit-identical to a scalar loop / np.cumsum(...)[-1].  chunk_starts (nullable) receives

@@ -21,6 +21,7 @@
 #include <chrono>
 #include <cmath>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cstring>
 #include <vector>
@@ -1735,6 +1736,8 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             const bool unchanged = hch[r] == 0 && fin;
             const double c = hc[r];
             const bool small_gain = fin && (prev[r] - c <= tol * std::max(prev[r], 1e-300));
+            if (r == 0 && getenv("SC_KMEANS_TRACE"))
+                fprintf(stderr, "exact  r0 it %d cost %.17g changed %d\n", iters[r], c, hch[r]);
             prev[r] = c;
             iters[r] += 1;
             final_buf[r] = nxt;
@@ -1777,6 +1780,311 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
 }
 
 }  // extern "C"
+
+namespace sc {
+// ---------------------------------------------------------------------------------------
+// Fast 1-D Lloyd on sorted values (BASELINE north star, step 3: "CUB radix sort, prefix sums
+// and a Lloyd split on the sorted values").  In one dimension every cluster is an interval
+// of the sorted points, so an iteration is k binary searches for the boundaries plus prefix-
+// sum lookups for the means and the cost: O(k log n) instead of O(n).  One CTA runs all the
+// iterations of one restart.  Seeding (k-means++), the argmin tie rule, the empty-cluster
+// repair (the far end of an interval) and the stop rules follow the reference; the sums come
+// from prefix sums instead of np.add.at / einsum, so this mode is not bit-exact: labels can
+// differ from the replica only where a distance or a stopping decision sits within rounding.
+constexpr int kFastMaxK = 2048;
+
+__device__ __forceinline__ bool upper_wins(double x, double cl, int il, double cu, int iu) {
+    const double dl = d2ref(x, cl), du = d2ref(x, cu);
+    return du < dl || (du == dl && iu < il);
+}
+
+__global__ void __launch_bounds__(256) k_lloyd_sorted(
+    const double *__restrict__ xs, const int32_t *__restrict__ ix, const double *__restrict__ P,
+    const double *__restrict__ Q, int64_t n, int k, const double *__restrict__ cen0,
+    int max_iters, double tol, int64_t *__restrict__ out_lo, int64_t *__restrict__ out_hi,
+    double *__restrict__ out_cost, int32_t *__restrict__ out_iters, int trace) {
+    extern __shared__ unsigned char fs_raw[];
+    const int r = blockIdx.x;
+    int Pk = 1;
+    while (Pk < k) Pk <<= 1;
+    double *cv = reinterpret_cast<double *>(fs_raw);  // centers by id
+    double *sv = cv + k;                              // sorted center values (Pk)
+    int32_t *si = reinterpret_cast<int32_t *>(sv + Pk);  // their ids (Pk)
+    int64_t *lo = reinterpret_cast<int64_t *>(si + Pk + (Pk & 1));
+    int64_t *hi = lo + k, *plo = hi + k, *phi = plo + k;
+    __shared__ double red[8];
+    __shared__ int flag;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        cv[i] = cen0[(int64_t)r * k + i];
+        plo[i] = -1;
+        phi[i] = -1;
+    }
+    double prev_cost = INFINITY;
+    int it = 0;
+    for (; it < max_iters; ++it) {
+        __syncthreads();
+        // (a) centers sorted by (value, id)
+        for (int i = threadIdx.x; i < Pk; i += blockDim.x) {
+            sv[i] = i < k ? cv[i] : INFINITY;
+            si[i] = i < k ? i : INT32_MAX;
+        }
+        __syncthreads();
+        for (int size = 2; size <= Pk; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = threadIdx.x; i < Pk; i += blockDim.x) {
+                    const int j = i ^ stride;
+                    if (j > i) {
+                        const bool up = (i & size) == 0;
+                        const bool gt = sv[i] > sv[j] || (sv[i] == sv[j] && si[i] > si[j]);
+                        if (gt == up) {
+                            const double tv = sv[i];
+                            sv[i] = sv[j];
+                            sv[j] = tv;
+                            const int32_t ti = si[i];
+                            si[i] = si[j];
+                            si[j] = ti;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        // (b) intervals: the first of equal-valued centers (lowest id) owns their points;
+        // between consecutive distinct centers the boundary is the first point the upper one
+        // wins (argmin, ties to the lower id)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            lo[si[j]] = 0;
+            hi[si[j]] = 0;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            if (j > 0 && sv[j] == sv[j - 1]) continue;  // duplicate value: empty
+            // previous distinct owner
+            int jp = j - 1;
+            while (jp > 0 && sv[jp] == sv[jp - 1]) --jp;
+            int jn = j + 1;
+            while (jn < k && sv[jn] == sv[j]) ++jn;
+            int64_t a = 0, b = n;
+            if (j > 0) {  // first point that j wins against its lower neighbour
+                int64_t l0 = 0, h0 = n;
+                while (l0 < h0) {
+                    const int64_t m = (l0 + h0) >> 1;
+                    if (upper_wins(xs[m], sv[jp], si[jp], sv[j], si[j])) h0 = m;
+                    else l0 = m + 1;
+                }
+                a = l0;
+            }
+            if (jn < k) {  // first point the next distinct center wins against j
+                int64_t l0 = 0, h0 = n;
+                while (l0 < h0) {
+                    const int64_t m = (l0 + h0) >> 1;
+                    if (upper_wins(xs[m], sv[j], si[j], sv[jn], si[jn])) h0 = m;
+                    else l0 = m + 1;
+                }
+                b = l0;
+            }
+            lo[si[j]] = a;
+            hi[si[j]] = b < a ? a : b;
+        }
+        __syncthreads();
+        // (c) empty clusters in increasing id take the far end of the interval with the
+        // largest own distance (first point index on ties); a moved point keeps distance 0
+        if (threadIdx.x == 0) {
+            for (int e = 0; e < k; ++e) {
+                if (hi[e] > lo[e]) continue;
+                double bv = -1.0;
+                int32_t bidx = INT32_MAX;
+                int bj = -1;
+                int64_t bp = -1;
+                for (int j = 0; j < k; ++j) {
+                    if (hi[j] - lo[j] < 2) continue;  // singletons (incl. moved points): 0
+                    const int64_t cand[2] = {lo[j], hi[j] - 1};
+                    for (int q = 0; q < 2; ++q) {
+                        const double d = d2ref(xs[cand[q]], cv[j]);
+                        const int32_t id = ix[cand[q]];
+                        if (d > bv || (d == bv && id < bidx)) {
+                            bv = d;
+                            bidx = id;
+                            bj = j;
+                            bp = cand[q];
+                        }
+                    }
+                }
+                if (bj < 0) break;  // nothing left to move
+                if (bp == lo[bj]) ++lo[bj];
+                else --hi[bj];
+                lo[e] = bp;
+                hi[e] = bp + 1;
+            }
+        }
+        __syncthreads();
+        // (d) means, cost and change
+        double cst = 0.0;
+        int ch = 0;
+        const double x0 = xs[n / 2];  // P, Q hold prefix sums of x - x0 and (x - x0)^2
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            const int64_t a = lo[j], b = hi[j];
+            const double cnt = (double)(b - a);
+            const double S = P[b] - P[a], S2 = Q[b] - Q[a];
+            const double m = cnt > 0 ? S / cnt : 0.0;  // centred mean
+            const double mu = cnt > 0 ? x0 + m : 0.0;
+            cst += fmax(0.0, S2 - 2.0 * m * S + cnt * m * m);
+            ch |= (a != plo[j]) || (b != phi[j]);
+            plo[j] = a;
+            phi[j] = b;
+            cv[j] = mu;
+        }
+        for (int o = 16; o; o >>= 1) {
+            cst += __shfl_xor_sync(0xffffffffu, cst, o);
+            ch |= __shfl_xor_sync(0xffffffffu, ch, o);
+        }
+        if (threadIdx.x == 0) flag = 0;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) {
+            red[threadIdx.x >> 5] = cst;
+            if (ch) atomicOr(&flag, 1);
+        }
+        __syncthreads();
+        double cost = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) cost += red[w];
+        const bool fin = isfinite(prev_cost);
+        const bool unchanged = fin && flag == 0;
+        if (trace && r == 0 && threadIdx.x == 0)
+            printf("sorted r0 it %d cost %.17g changed %d\n", it, cost, flag);
+        const bool small_gain = fin && (prev_cost - cost <= tol * fmax(prev_cost, 1e-300));
+        prev_cost = cost;
+        if (unchanged || small_gain) {
+            ++it;
+            break;
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        out_lo[(int64_t)r * k + j] = plo[j];
+        out_hi[(int64_t)r * k + j] = phi[j];
+    }
+    if (threadIdx.x == 0) {
+        out_cost[r] = prev_cost;
+        out_iters[r] = it;
+    }
+}
+
+__global__ void k_sorted_labels(const int32_t *__restrict__ ix, const int64_t *__restrict__ lo,
+                                const int64_t *__restrict__ hi, int k,
+                                int32_t *__restrict__ lab) {
+    const int j = blockIdx.x;
+    if (j >= k) return;
+    for (int64_t p = lo[j] + threadIdx.x; p < hi[j]; p += blockDim.x) lab[ix[p]] = j;
+}
+
+__global__ void k_iota(int32_t *__restrict__ a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (int32_t)i;
+}
+
+// y = x - x0 and y^2 (x0 = the median sorted value, read on the device): prefix sums of
+// centred values keep the cost Q - 2 mu S + n mu^2 from cancelling away (embeddings are
+// typically a narrow band far from zero, e.g. f ~ 0.4999 +- 1e-6 at config 2)
+__global__ void k_center_square(const double *__restrict__ xs, int64_t n, double *__restrict__ y,
+                                double *__restrict__ y2) {
+    const double x0 = xs[n / 2];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = xs[i] - x0;
+        y[i] = v;
+        y2[i] = v * v;
+    }
+}
+}  // namespace sc
+
+extern "C" int32_t sc_kmeans_lloyd_sorted(sc_kmeans *km, int32_t k, int32_t R,
+                                          const int64_t *chosen, int32_t max_iters, double tol,
+                                          int64_t *labels_out, double *costs_out,
+                                          int32_t *iters_out, int32_t *best_restart_out) {
+    using namespace sc;
+    SC_REQUIRE(km && chosen && labels_out, SC_E_INVALID, "null argument");
+    SC_REQUIRE(km->l == 1, SC_E_INVALID, "the sorted Lloyd handles 1-D points only");
+    SC_REQUIRE(k >= 1 && k <= km->n && k <= kFastMaxK, SC_E_INVALID,
+               "need 1 <= k <= min(n, %d), got k=%d", kFastMaxK, k);
+    SC_REQUIRE(R >= 1 && max_iters >= 1, SC_E_INVALID, "bad restarts / max_iters");
+    for (int64_t i = 0; i < (int64_t)R * k; ++i)
+        SC_REQUIRE(chosen[i] >= 0 && chosen[i] < km->n, SC_E_RANGE, "chosen index out of range");
+    SC_CUDA(cudaSetDevice(km->device));
+    int32_t st = ensure(km, R, k);
+    if (st) return st;
+    cudaStream_t s = km->stream;
+    const int64_t n = km->n;
+    // sorted points, their indices and prefix sums (kept in the Lloyd workspaces)
+    double *fb = nullptr;  // sorted x, P, Q, squares
+    void *tmp = nullptr;
+    size_t tb = 0, sb = 0;
+    SC_CUDA(cudaMallocAsync((void **)&fb, (size_t)(4 * n + 2) * 8, s));
+    double *ys = nullptr;  // centred sorted values
+    SC_CUDA(cudaMallocAsync((void **)&ys, (size_t)n * 8, s));
+    double *xs = fb, *P = fb + n, *Q = P + n + 1, *sq = Q + n + 1;
+    int32_t *ixs = km->d_keys_alt, *iota = km->d_keys;
+    k_iota<<<grid_1d(km, n, 256), 256, 0, s>>>(iota, n);
+    SC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, km->d_x, xs, iota, ixs, n, 0, 64, s));
+    SC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, sb, xs, P + 1, n, s));
+    SC_CUDA(cudaMallocAsync(&tmp, std::max(tb, sb) + 16, s));
+    SC_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, km->d_x, xs, iota, ixs, n, 0, 64, s));
+    SC_CUDA(cudaMemsetAsync(P, 0, 8, s));
+    SC_CUDA(cudaMemsetAsync(Q, 0, 8, s));
+    k_center_square<<<grid_1d(km, n, 256), 256, 0, s>>>(xs, n, ys, sq);
+    SC_CUDA(cub::DeviceScan::InclusiveSum(tmp, sb, ys, P + 1, n, s));
+    SC_CUDA(cub::DeviceScan::InclusiveSum(tmp, sb, sq, Q + 1, n, s));
+    const int rk = R * k;
+    SC_CUDA(cudaMemcpyAsync(km->d_chosen, chosen, (size_t)rk * 8, cudaMemcpyHostToDevice, s));
+    k_gather_centers<<<(rk + 255) / 256, 256, 0, s>>>(km->d_x, km->d_chosen, rk, 1, km->d_cen);
+    int Pk = 1;
+    while (Pk < k) Pk <<= 1;
+    const size_t smem = (size_t)k * 8 + (size_t)Pk * 12 + 8 + (size_t)k * 32;
+    SC_CUDA(cudaFuncSetAttribute(k_lloyd_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int64_t *dlo = nullptr, *dhi = nullptr;
+    int64_t *buf = nullptr;
+    SC_CUDA(cudaMallocAsync((void **)&buf, (size_t)rk * 16, s));
+    dlo = buf;
+    dhi = buf + rk;
+    k_lloyd_sorted<<<R, 256, smem, s>>>(xs, ixs, P, Q, n, k, km->d_cen, max_iters, tol, dlo, dhi,
+                                        km->d_cost, km->d_changed,
+                                        getenv("SC_KMEANS_TRACE") != nullptr);
+    std::vector<double> cost((size_t)R);
+    std::vector<int32_t> iters((size_t)R);
+    SC_CUDA(cudaMemcpyAsync(cost.data(), km->d_cost, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaMemcpyAsync(iters.data(), km->d_changed, (size_t)R * 4, cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaStreamSynchronize(s));
+    int best = -1;
+    double bc = INFINITY;
+    for (int r = 0; r < R; ++r)
+        if (cost[(size_t)r] < bc) {
+            bc = cost[(size_t)r];
+            best = r;
+        }
+    if (best < 0) {
+        cudaFreeAsync(buf, s);
+        cudaFreeAsync(fb, s);
+        cudaFreeAsync(tmp, s);
+        cudaFreeAsync(ys, s);
+        return fail(SC_E_INTERNAL, "no restart produced a finite cost");
+    }
+    k_sorted_labels<<<k, 256, 0, s>>>(ixs, dlo + (int64_t)best * k, dhi + (int64_t)best * k, k,
+                                      km->d_lab[1]);
+    std::vector<int32_t> lab32((size_t)n);
+    SC_CUDA(cudaMemcpyAsync(lab32.data(), km->d_lab[1], (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(buf, s);
+    cudaFreeAsync(fb, s);
+    cudaFreeAsync(tmp, s);
+    cudaFreeAsync(ys, s);
+    SC_CUDA(cudaStreamSynchronize(s));
+    for (int64_t j = 0; j < n; ++j) labels_out[j] = lab32[(size_t)j];
+    if (costs_out)
+        for (int r = 0; r < R; ++r) costs_out[r] = cost[(size_t)r];
+    if (iters_out)
+        for (int r = 0; r < R; ++r) iters_out[r] = iters[(size_t)r];
+    if (best_restart_out) *best_restart_out = best;
+    return SC_OK;
+}
 
 namespace sc {
 // exact sequential sums of the nseg segments of device array d_vals (host segment offsets):

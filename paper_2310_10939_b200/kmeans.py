@@ -157,7 +157,11 @@ class KMeans1D:
         return chosen
 
     def lloyd(self, k: int, seed: int, max_iters: int = 100, tol: float = 1e-6,
-              restarts: int = 10) -> Partition:
+              restarts: int = 10, method: str = "exact") -> Partition:
+        """method "exact": the bit-exact replica; "sorted": the same seeds, then Lloyd on the
+        sorted values with prefix-sum means (1-D only, k <= 2048; not bit-exact)."""
+        if method not in ("exact", "sorted"):
+            raise InputError(f"method must be 'exact' or 'sorted', got {method!r}")
         if not 1 <= k <= self.n:
             raise InputError(f"need 1 <= k <= n, got k={k}, n={self.n}")
         if restarts < 1:
@@ -170,6 +174,13 @@ class KMeans1D:
         iters = np.empty(restarts, dtype=np.int32)
         best = ctypes.c_int32()
         ms = ctypes.c_double()
+        if method == "sorted":
+            _lib.check(_lib.load().sc_kmeans_lloyd_sorted(
+                self._h, k, restarts, _lib.ptr(chosen), max_iters, float(tol), _lib.ptr(labels),
+                _lib.ptr(costs), _lib.ptr(iters), ctypes.byref(best)))
+            self.last = {"costs": costs, "iters": iters, "best_restart": best.value,
+                         "chosen": chosen, "method": "sorted"}
+            return Partition(labels=labels, k=k)
         _lib.check(_lib.load().sc_kmeans_lloyd(
             self._h, k, restarts, _lib.ptr(chosen), max_iters, float(tol), _lib.ptr(labels),
             _lib.ptr(costs), _lib.ptr(iters), ctypes.byref(best), ctypes.byref(ms)))

@@ -53,6 +53,7 @@ class SpectralParams:
     restarts: int = 10
     max_iters: int = 100
     tol: float = 1e-6
+    kmeans: str = "exact"        # "exact" (bit-exact replica) or "sorted" (fast, one_vector)
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -69,6 +70,8 @@ class SpectralParams:
             raise InputError(f"seed must be nonnegative, got {self.seed}")
         if self.walk_sign not in (1, -1):
             raise InputError(f"walk_sign must be +1 or -1, got {self.walk_sign}")
+        if self.kmeans not in ("exact", "sorted"):
+            raise InputError(f"kmeans must be 'exact' or 'sorted', got {self.kmeans!r}")
 
     def num_columns(self, n: int) -> int:
         if self.mode == "one_vector":
@@ -145,7 +148,7 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
         t2 = time.perf_counter()
         with KMeans1D(graph=dev) as km:
             part = km.lloyd(params.k, _kmeans_seed(params.seed), max_iters=params.max_iters,
-                            tol=params.tol, restarts=params.restarts)
+                            tol=params.tol, restarts=params.restarts, method=params.kmeans)
             km_info = dict(km.last)
         t3 = time.perf_counter()
     finally:
