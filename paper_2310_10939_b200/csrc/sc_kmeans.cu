@@ -1021,6 +1021,72 @@ __global__ void k_make_keys(int64_t n, int k, const int32_t *__restrict__ lab,
     }
 }
 
+// ---- stable counting sort of the points by (slot, label) for small key counts ----------
+// Replaces key construction + radix sort when nseg <= kCsMaxKeys: a tile histogram pass, an
+// exclusive scan of the (key, tile) counts, and a scatter that ranks equal keys in point
+// order inside the tile (warp match + per-warp running counters), so the output is exactly
+// the stable sort's (np.add.at order preserved).
+constexpr int kCsTile = 4096, kCsWarps = 8, kCsMaxKeys = 1024;
+
+__device__ __forceinline__ int cs_key(int64_t t, int64_t n, int k, const int32_t *lab,
+                                      const int32_t *act) {
+    const int64_t s = t / n, j = t - s * n;
+    return (int)(s * k + lab[(int64_t)act[s] * n + j]);
+}
+
+__global__ void __launch_bounds__(32 * kCsWarps) k_cs_hist(int64_t m, int64_t n, int k,
+                                                           const int32_t *__restrict__ lab,
+                                                           const int32_t *__restrict__ act,
+                                                           int nseg, int ntiles,
+                                                           int32_t *__restrict__ bh) {
+    extern __shared__ int32_t cs_h[];
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x) cs_h[q] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kCsTile;
+    for (int64_t t = t0 + threadIdx.x; t < min(m, t0 + kCsTile); t += blockDim.x)
+        atomicAdd(&cs_h[cs_key(t, n, k, lab, act)], 1);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x)
+        bh[(int64_t)q * ntiles + blockIdx.x] = cs_h[q];
+}
+
+__global__ void __launch_bounds__(32 * kCsWarps) k_cs_scatter(
+    int64_t m, int64_t n, int k, const int32_t *__restrict__ lab, const int32_t *__restrict__ act,
+    int nseg, int ntiles, const int32_t *__restrict__ off, const double *__restrict__ x,
+    double *__restrict__ out) {
+    extern __shared__ int32_t cs_s[];  // [kCsWarps][nseg] counts, then running positions
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t *run = cs_s + w * nseg;
+    for (int q = threadIdx.x; q < kCsWarps * nseg; q += blockDim.x) cs_s[q] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kCsTile;
+    constexpr int SUB = kCsTile / kCsWarps;
+    const int64_t s0 = t0 + (int64_t)w * SUB, s1 = min(m, s0 + SUB);
+    for (int64_t t = s0 + lane; t < s1; t += 32) atomicAdd(&run[cs_key(t, n, k, lab, act)], 1);
+    __syncthreads();
+    // exclusive prefix over warps per key, plus the tile's global offset
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x) {
+        int acc = off[(int64_t)q * ntiles + blockIdx.x];
+        for (int ww = 0; ww < kCsWarps; ++ww) {
+            const int c = cs_s[ww * nseg + q];
+            cs_s[ww * nseg + q] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    for (int64_t b = s0; b < s1; b += 32) {
+        const int64_t t = b + lane;
+        const bool ok = t < s1;
+        const int key = ok ? cs_key(t, n, k, lab, act) : -1 - lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int rank = __popc(peers & ((1u << lane) - 1));
+        if (ok) out[run[key] + rank] = x[t - (t / n) * n];
+        __syncwarp();
+        if (ok && rank == 0) run[key] += __popc(peers);  // leader: lowest lane of the group
+        __syncwarp();
+    }
+}
+
 // l > 1: the sort carries the point index; each coordinate is gathered in sorted order
 __global__ void k_make_keys_idx(int64_t n, int k, const int32_t *__restrict__ lab,
                                 const int32_t *__restrict__ act, int nact,
@@ -1338,6 +1404,10 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     cub::DeviceRadixSort::SortPairs(nullptr, need2, km->d_keys, km->d_keys_alt, km->d_idx,
                                     km->d_idx_alt, (int64_t)R * n, 0, 31, km->stream);
     need = std::max(need, need2);
+    size_t need3 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need3, km->d_keys, km->d_keys_alt, (int64_t)R * n,
+                                  km->stream);
+    need = std::max(need, need3);
     if ((st = grow((unsigned char **)&km->d_cub, need, km->stream))) return st;
     km->cub_bytes = need;
     km->cap_r = R;
@@ -1567,7 +1637,9 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     if (smem_assign > 48 * 1024)
         SC_CUDA(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_assign));
-    const bool sorted_assign = l == 1 && k >= kSortedMinK && k <= kSortedMaxK &&
+    const char *smk = getenv("SC_KMEANS_SORTED_MIN_K");
+    const int sorted_min_k = smk ? atoi(smk) : kSortedMinK;
+    const bool sorted_assign = l == 1 && k >= sorted_min_k && k <= kSortedMaxK &&
                                getenv("SC_KMEANS_BRUTE_ASSIGN") == nullptr;
     const size_t smem_sorted = (size_t)k * 16;
     size_t smem_sort = 12;
@@ -1606,7 +1678,28 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     auto cen_buf = [&](int i) { return km->d_cen + (size_t)(i & 1) * rk * l; };
     auto act_buf = [&](int i) { return km->d_active + (i & 1) * R; };
     auto chg_buf = [&](int i) { return km->d_changed + (i & 1) * R; };
+    const bool tl = getenv("SC_KMEANS_TIMELINE") != nullptr;
+    std::vector<cudaEvent_t> tl_ev;
+    std::vector<double> tl_host;
+    cudaEvent_t tl0 = nullptr;
+    auto host_ms = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+            .count();
+    };
+    auto tl_mark = [&](cudaStream_t st_) {
+        if (!tl) return;
+        cudaEvent_t e_;
+        cudaEventCreate(&e_);
+        cudaEventRecord(e_, st_);
+        tl_ev.push_back(e_);
+        tl_host.push_back(host_ms());
+    };
+    if (tl) {
+        cudaEventCreate(&tl0);
+        cudaEventRecord(tl0, s);
+    }
     auto launch_main = [&](int it, const std::vector<int32_t> &actv, int cur_lab) -> int32_t {
+        tl_mark(s);
         // pinned staging (a pageable copy would make the host wait for the stream)
         int32_t *hflags = km->h_act + (size_t)(it & 1) * 2 * R, *hlist = hflags + R;
         int nact = 0;
@@ -1659,7 +1752,18 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         if (prof) cudaEventRecord(pe[1], s);
         const int64_t m = (int64_t)nact * n;
         size_t tb = km->cub_bytes;
-        if (l == 1) {
+        if (l == 1 && nseg <= kCsMaxKeys && getenv("SC_KMEANS_RADIX_SORT") == nullptr) {
+            const int ntiles = (int)((m + kCsTile - 1) / kCsTile);
+            int32_t *bh = km->d_keys, *boff = km->d_keys_alt;  // nseg * ntiles <= m ints each
+            k_cs_hist<<<ntiles, 32 * kCsWarps, (size_t)nseg * 4, s>>>(
+                m, n, k, km->d_lab[nxt], km->d_empty, nseg, ntiles, bh);
+            size_t sb = km->cub_bytes;
+            SC_CUDA(cub::DeviceScan::ExclusiveSum(km->d_cub, sb, bh, boff, (int64_t)nseg * ntiles,
+                                                  s));
+            k_cs_scatter<<<ntiles, 32 * kCsWarps, (size_t)nseg * kCsWarps * 4, s>>>(
+                m, n, k, km->d_lab[nxt], km->d_empty, nseg, ntiles, boff, km->d_x,
+                km->d_vals_alt);
+        } else if (l == 1) {
             k_make_keys<<<grid_1d(km, m, 256), 256, 0, s>>>(n, k, km->d_lab[nxt], km->d_empty,
                                                              nact, km->d_keys, km->d_vals, km->d_x);
             SC_CUDA(cub::DeviceRadixSort::SortPairs(km->d_cub, tb, km->d_keys, km->d_keys_alt,
@@ -1690,6 +1794,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                                            km->d_empty, cen_out);
         }
         if (prof) cudaEventRecord(pe[3], s);
+        tl_mark(s);
         SC_CUDA(cudaGetLastError());
         return SC_OK;
     };
@@ -1707,6 +1812,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         SC_CUDA(cudaMemcpyAsync(km->h_changed + (it & 1) * R, chg_buf(it), (size_t)R * 4,
                                 cudaMemcpyDeviceToHost, s2));
         SC_CUDA(cudaEventRecord(km->ev_cost, s2));
+        tl_mark(s2);
         return SC_OK;
     };
     const bool speculate = getenv("SC_KMEANS_NO_SPECULATION") == nullptr;
@@ -1749,6 +1855,19 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         if (!speculate && it + 1 < max_iters && (st = launch_main(it + 1, active, cur))) return st;
     }
     if (prof) fprintf(stderr, "[sc_kmeans_lloyd] host waited %.3f ms for the iteration results\n", wait_ms);
+    if (tl) {
+        cudaDeviceSynchronize();
+        // records come in the order main-start, main-end, cost-end per launch; print device
+        // time (ms since the first record) and the host time each was enqueued
+        for (size_t q = 0; q < tl_ev.size() && q < 60; ++q) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl0, tl_ev[q]);
+            fprintf(stderr, "[timeline] %2zu dev %8.3f ms  host-enqueue %8.3f ms\n", q, ms,
+                    tl_host[q]);
+        }
+        for (auto e_ : tl_ev) cudaEventDestroy(e_);
+        cudaEventDestroy(tl0);
+    }
     SC_CUDA(cudaStreamSynchronize(s));  // a speculative iteration may still be running
     if (prof) {
         fprintf(stderr, "[sc_kmeans_lloyd] assign+repair %.3f ms, sort %.3f ms, ordered sums %.3f ms, cost %.3f ms\n",
