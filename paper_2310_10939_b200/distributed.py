@@ -28,6 +28,7 @@ from __future__ import annotations
 import ctypes
 import json
 import os
+import sys
 
 import numpy as np
 
@@ -503,7 +504,18 @@ def bench_main(args, metric: str, unit: str):
 
     runner.sample(0)
     if use_graph:
-        runner.capture(T)
+        # every rank must take the same path: capture, agree on success, else launch per step
+        ok = torch.tensor([1], device="cuda", dtype=torch.int32)
+        try:
+            runner.capture(T)
+        except Exception as exc:  # noqa: BLE001 -- e.g. a NCCL build that cannot be captured
+            print(f"[rank {rank}] CUDA-graph capture failed ({exc}); launching per step",
+                  file=sys.stderr, flush=True)
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            runner.graph = None
+            use_graph = False
     for _ in range(max(args.warmup, 3)):
         one_step()
     torch.cuda.synchronize()
