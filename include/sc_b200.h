@@ -93,6 +93,9 @@ int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double
 /* As sc_graph_create; create_flags: SC_CREATE_KEEP_WEIGHTS keeps an all-ones weight array on
  * the device (the weighted kernel then streams it) instead of eliding it. */
 #define SC_CREATE_KEEP_WEIGHTS 0x1u
+/* store the weights as fp32 (8 -> 4 bytes per entry; products still formed in fp64): the
+ * optional fp32-value variant, agreeing with fp64 within 1e-5 relative (not bit-exact) */
+#define SC_CREATE_FP32_VALUES 0x2u
 int32_t sc_graph_create_ex(const int64_t *row_ptr, const int32_t *col, const double *val,
                            const double *deg, int64_t n, int64_t nnz, int32_t device,
                            uint32_t create_flags, sc_graph **out);

@@ -93,6 +93,8 @@ struct StepArgs {
     double *const *peer_base;
     int64_t peer_off;
     int npeer;
+    const float *val32;   // fp32 weights (SC_CREATE_FP32_VALUES), SELL / wide layouts
+    const float *wval32;
 };
 
 template <bool SYM>
@@ -116,7 +118,7 @@ __device__ __forceinline__ void peer_fence(const StepArgs &a) {
 // (the scipy order) while the next 128 gathers are already in flight.
 constexpr int kWideBatch = 128;
 
-template <bool UNIT, bool SYM>
+template <bool UNIT, bool SYM, bool F32 = false>
 __global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
     __shared__ double wbuf[kStepTPB / 32][2][kWideBatch];
     const int lane = threadIdx.x & 31;
@@ -134,7 +136,8 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
             p[q] = 0.0;
             if (j < hi) {
                 const double zv = __ldg(a.z_in + __ldcs(a.wcol + j));
-                p[q] = UNIT ? zv : __dmul_rn(__ldcs(a.wval + j), zv);
+                const double wv = UNIT ? 1.0 : F32 ? (double)__ldcs(a.wval32 + j) : __ldcs(a.wval + j);
+                p[q] = UNIT ? zv : __dmul_rn(wv, zv);
             }
         }
     };
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
     peer_fence(a);
 }
 
-template <bool UNIT, bool SYM>
+template <bool UNIT, bool SYM, bool F32 = false>
 __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -181,7 +184,8 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
     const int64_t base = a.slice_ptr[sl];
     const int width = (int)((a.slice_ptr[sl + 1] - base) >> 5);
     const uint32_t *cp = a.col + base + lane;
-    const double *vp = UNIT ? nullptr : a.val + base + lane;
+    const double *vp = (UNIT || F32) ? nullptr : a.val + base + lane;
+    const float *vp32 = F32 ? a.val32 + base + lane : nullptr;
     // Software pipeline: batch i+1's column indices are loaded while batch i's z values
     // (and weights, which do not depend on the indices) are fetched and added, so a slice
     // pays about one memory latency per batch; the last batch is predicated, not peeled.
@@ -205,7 +209,10 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
             p[q] = 0.0;
             if (c[q] != kPad) {
                 const double zv = __ldg(a.z_in + c[q]);
-                p[q] = UNIT ? zv : __dmul_rn(__ldcs(vp + (int64_t)(t + q) * kSlice), zv);
+                const double wv = UNIT ? 1.0
+                                  : F32 ? (double)__ldcs(vp32 + (int64_t)(t + q) * kSlice)
+                                        : __ldcs(vp + (int64_t)(t + q) * kSlice);
+                p[q] = UNIT ? zv : __dmul_rn(wv, zv);
             }
         }
 #pragma unroll
@@ -498,7 +505,8 @@ __global__ void k_fill_sell(const int64_t *__restrict__ rp, const int32_t *__res
                             const double *__restrict__ val, const int32_t *__restrict__ perm,
                             const int32_t *__restrict__ iperm, const int64_t *__restrict__ slice_ptr,
                             int64_t n_sell, int64_t nslices, int64_t col_offset, int64_t n,
-                            int rename, uint32_t *__restrict__ scol, double *__restrict__ sval) {
+                            int rename, uint32_t *__restrict__ scol, double *__restrict__ sval,
+                            float *__restrict__ sval32) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nslices * kSlice;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = p / kSlice, lane = p % kSlice;
@@ -514,9 +522,11 @@ __global__ void k_fill_sell(const int64_t *__restrict__ rp, const int32_t *__res
                     c = col_offset + iperm[c - col_offset];
                 scol[dst] = (uint32_t)c;
                 if (sval) sval[dst] = val[lo + t];
+                if (sval32) sval32[dst] = __double2float_rn(val[lo + t]);
             } else {
                 scol[dst] = kPad;
                 if (sval) sval[dst] = 0.0;
+                if (sval32) sval32[dst] = 0.0f;
             }
         }
     }
@@ -526,7 +536,8 @@ __global__ void k_fill_wide(const int64_t *__restrict__ rp, const int32_t *__res
                             const double *__restrict__ val, const int32_t *__restrict__ perm,
                             const int32_t *__restrict__ iperm, const int64_t *__restrict__ wide_ptr,
                             int64_t n_sell, int64_t n_wide, int64_t col_offset, int64_t n,
-                            int rename, uint32_t *__restrict__ wcol, double *__restrict__ wval) {
+                            int rename, uint32_t *__restrict__ wcol, double *__restrict__ wval,
+                            float *__restrict__ wval32) {
     const int64_t w = blockIdx.x;
     if (w >= n_wide) return;
     const int32_t r = perm[n_sell + w];
@@ -536,6 +547,7 @@ __global__ void k_fill_wide(const int64_t *__restrict__ rp, const int32_t *__res
         if (rename && c >= col_offset && c < col_offset + n) c = col_offset + iperm[c - col_offset];
         wcol[dst + t] = (uint32_t)c;
         if (wval) wval[dst + t] = val[lo + t];
+        if (wval32) wval32[dst + t] = __double2float_rn(val[lo + t]);
     }
 }
 
@@ -575,6 +587,8 @@ struct sc_graph {
     int64_t bytes = 0;
     bool l2_window = false;
     double *d_f_orig = nullptr;   // f in original vertex order (for the k-means context)
+    bool f32 = false;             // weights stored as fp32 (SC_CREATE_FP32_VALUES)
+    float *d_val32 = nullptr, *d_wval32 = nullptr;
     std::vector<std::pair<void *, size_t>> allocs;  // every dmalloc'd buffer (returned to the cache)
     // fused peer exchange (sc_shard_set_peers)
     uint32_t *d_flags = nullptr;        // 64 words: peer epochs [0, world), own epoch [63]
@@ -833,6 +847,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         if (cflags & SC_CREATE_KEEP_WEIGHTS) unit = false;
     }
     g->unit = unit;
+    g->f32 = !unit && (cflags & SC_CREATE_FP32_VALUES);
 
     lap("unit check");
     int32_t st;
@@ -976,20 +991,25 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         return cleanup(SC_E_RANGE);
     }
     if ((st = dmalloc(g, (void **)&g->d_col, (size_t)g->sell_entries * 4 + 16)) ||
-        (!unit && (st = dmalloc(g, (void **)&g->d_val, (size_t)g->sell_entries * 8 + 16))) ||
+        (!unit && !g->f32 &&
+         (st = dmalloc(g, (void **)&g->d_val, (size_t)g->sell_entries * 8 + 16))) ||
+        (g->f32 && (st = dmalloc(g, (void **)&g->d_val32, (size_t)g->sell_entries * 4 + 16))) ||
         (st = dmalloc(g, (void **)&g->d_wcol, (size_t)wptr.back() * 4 + 16)) ||
-        (!unit && (st = dmalloc(g, (void **)&g->d_wval, (size_t)wptr.back() * 8 + 16)))) {
+        (!unit && !g->f32 &&
+         (st = dmalloc(g, (void **)&g->d_wval, (size_t)wptr.back() * 8 + 16))) ||
+        (g->f32 && (st = dmalloc(g, (void **)&g->d_wval32, (size_t)wptr.back() * 4 + 16)))) {
         free_tmp();
         return cleanup(st);
     }
     if (g->n_sell)
         k_fill_sell<<<grid_for(g, g->nslices * kSlice, 256), 256, 0, s>>>(
             t_rp, t_col, t_val, g->d_perm, g->d_iperm, g->d_slice_ptr, g->n_sell, g->nslices,
-            col_offset, n, rename, g->d_col, g->d_val);
+            col_offset, n, rename, g->d_col, g->d_val, g->d_val32);
     if (g->n_wide)
         k_fill_wide<<<(unsigned)g->n_wide, 256, 0, s>>>(t_rp, t_col, t_val, g->d_perm, g->d_iperm,
                                                         g->d_wide_ptr, g->n_sell, g->n_wide,
-                                                        col_offset, n, rename, g->d_wcol, g->d_wval);
+                                                        col_offset, n, rename, g->d_wcol, g->d_wval,
+                                                        g->d_wval32);
     e = cudaGetLastError();
     if (!e) e = cudaStreamSynchronize(s);
     free_tmp();
@@ -1029,6 +1049,8 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.wide_ptr = g->d_wide_ptr;
     a.wcol = g->d_wcol;
     a.wval = g->d_wval;
+    a.val32 = g->d_val32;
+    a.wval32 = g->d_wval32;
     a.scale = sym ? g->d_isd : g->d_deg;
     a.x_in = x_in;
     a.z_in = z_in;
@@ -1061,6 +1083,9 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
         if (g->unit) {
             if (sym) k_rw_wide<true, true><<<wg, kStepTPB, 0, g->side>>>(a);
             else k_rw_wide<true, false><<<wg, kStepTPB, 0, g->side>>>(a);
+        } else if (g->f32) {
+            if (sym) k_rw_wide<false, true, true><<<wg, kStepTPB, 0, g->side>>>(a);
+            else k_rw_wide<false, false, true><<<wg, kStepTPB, 0, g->side>>>(a);
         } else {
             if (sym) k_rw_wide<false, true><<<wg, kStepTPB, 0, g->side>>>(a);
             else k_rw_wide<false, false><<<wg, kStepTPB, 0, g->side>>>(a);
@@ -1071,6 +1096,9 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
         if (g->unit) {
             if (sym) k_rw_step<true, true><<<grid, kStepTPB, 0, s>>>(a);
             else k_rw_step<true, false><<<grid, kStepTPB, 0, s>>>(a);
+        } else if (g->f32) {
+            if (sym) k_rw_step<false, true, true><<<grid, kStepTPB, 0, s>>>(a);
+            else k_rw_step<false, false, true><<<grid, kStepTPB, 0, s>>>(a);
         } else {
             if (sym) k_rw_step<false, true><<<grid, kStepTPB, 0, s>>>(a);
             else k_rw_step<false, false><<<grid, kStepTPB, 0, s>>>(a);
@@ -1401,6 +1429,7 @@ int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *
     SC_REQUIRE(L >= 1 && L <= kMaxBlockCols, SC_E_INVALID, "block width %d outside [1, %d]", L,
                kMaxBlockCols);
     SC_REQUIRE(g->ncols == g->n, SC_E_STATE, "block power method needs a whole graph");
+    SC_REQUIRE(!g->f32, SC_E_STATE, "block power method needs fp64 weights (no SC_CREATE_FP32_VALUES)");
     SC_CUDA(cudaSetDevice(g->device));
     cudaStream_t s = g->stream;
     int32_t st;

@@ -84,7 +84,11 @@ class DeviceGraph:
     """Owns an ``sc_graph`` handle: the CSR uploaded once to one GPU (graph.py:28-45
     layout; degrees copied verbatim, never recomputed)."""
 
-    def __init__(self, graph, device: int = 0, keep_weights: bool = False):
+    def __init__(self, graph, device: int = 0, keep_weights: bool = False,
+                 fp32_values: bool = False):
+        """``fp32_values``: store the weights as fp32 (the optional fp32-value variant:
+        half the weight bytes, results within 1e-5 relative of fp64; unit-weight graphs are
+        unaffected)."""
         g = as_graph(graph)
         _check_shapes(g)  # content (ranges, monotonicity, degrees) is validated by the C-ABI
         L = _lib.require_device()
@@ -104,7 +108,8 @@ class DeviceGraph:
         h = ctypes.c_void_p()
         _lib.check(L.sc_graph_create_ex(_lib.ptr(self._rp), _lib.ptr(self._col), _lib.ptr(w),
                                         _lib.ptr(self._deg), g.n, g.nnz, device,
-                                        _lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0,
+                                        (_lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0)
+                                        | (_lib.SC_CREATE_FP32_VALUES if fp32_values else 0),
                                         ctypes.byref(h)))
         self._h = h
         self.device = device

@@ -69,3 +69,21 @@ def test_all_rows_wide():
     with DeviceGraph(g) as dg:
         assert dg.info()["long_rows"] == n
     _check_pipeline(g, 3, 12)
+
+
+def test_fp32_value_variant_within_tolerance():
+    """SC_CREATE_FP32_VALUES: weights stored as fp32 (products and sums still fp64); x_T and
+    f agree with the fp64 oracle within 1e-5 relative (the north star's bound for this
+    optional variant), on a weighted graph with wide rows and T = 200."""
+    from paper_2310_10939_b200.generate import sample_dcsbm
+
+    g = sample_dcsbm(200_000, 20, seed=4).graph
+    x0 = O.irwin_hall(g.degrees, 2)
+    with DeviceGraph(g, fp32_values=True) as dg:
+        dg.set_x0(x0)
+        xT, f = dg.power_iterate(200)
+        assert dg.info()["long_rows"] > 0
+    xo, fo = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, 200)
+    assert np.max(np.abs(xT - xo) / np.abs(xo)) < 1e-5
+    assert np.max(np.abs(f - fo) / np.abs(fo)) < 1e-5
+    assert not np.array_equal(xT, xo)  # it really is the reduced-precision variant
