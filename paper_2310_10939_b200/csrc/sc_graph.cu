@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda/atomic>
 #include <thread>
@@ -463,6 +464,73 @@ __global__ void k_gather_perm(const double *__restrict__ in, const int32_t *__re
 
 // ---- construction kernels (once per graph) ----------------------------------------------
 
+// Row checks on the device: stats[2] = first row whose offsets decrease, stats[3] = first
+// row with a non-positive / non-finite degree (n if none); for the renumbering:
+// stats[0] = rows with <= kSellMax entries, stats[1] = their entries, stats[4] = max length
+__global__ void k_validate_rows(const int64_t *__restrict__ rp, const double *__restrict__ deg,
+                                int64_t n, int32_t *__restrict__ flag,
+                                int64_t *__restrict__ stats) {
+    __shared__ unsigned long long sc, ss, smx, sbad, sdeg;
+    if (threadIdx.x == 0) {
+        sc = ss = smx = 0;
+        sbad = sdeg = (unsigned long long)n;
+    }
+    __syncthreads();
+    unsigned long long c = 0, sm = 0, mx = 0, bad = n, bdeg = n;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = rp[r + 1] - rp[r];
+        if (len < 0 && (unsigned long long)r < bad) bad = r;
+        const double d = deg[r];
+        if (!(d > 0.0 && d < 1e308) && (unsigned long long)r < bdeg) bdeg = r;
+        if (len >= 0 && len <= kSellMax) {
+            ++c;
+            sm += len;
+            if ((unsigned long long)len > mx) mx = len;
+        }
+    }
+    atomicAdd(&sc, c);
+    atomicAdd(&ss, sm);
+    atomicMax(&smx, mx);
+    atomicMin(&sbad, bad);
+    atomicMin(&sdeg, bdeg);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(stats + 0), sc);
+        atomicAdd(reinterpret_cast<unsigned long long *>(stats + 1), ss);
+        atomicMax(reinterpret_cast<unsigned long long *>(stats + 4), smx);
+        // stats[2], [3] start at 0: store n - (first bad) so that 0 means "none"... use min
+        // on a biased value instead: first = n - max(n - bad)
+        atomicMax(reinterpret_cast<unsigned long long *>(stats + 5), (unsigned long long)n - sbad);
+        atomicMax(reinterpret_cast<unsigned long long *>(stats + 6), (unsigned long long)n - sdeg);
+    }
+}
+
+__global__ void k_finish_stats(int64_t *stats, int64_t n) {
+    stats[2] = n - stats[5];
+    stats[3] = n - stats[6];
+}
+
+// sort key of the SELL renumbering: (window, kSellMax - length); wide rows after every window
+__global__ void k_sell_keys(const int64_t *__restrict__ rp, int64_t n, int64_t sigma, int64_t nwin,
+                            uint32_t *__restrict__ keys, int32_t *__restrict__ iota) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = rp[r + 1] - rp[r];
+        keys[r] = len <= kSellMax ? (uint32_t)((r / sigma) * 512 + (kSellMax - len))
+                                  : (uint32_t)(nwin * 512);
+        iota[r] = (int32_t)r;
+    }
+}
+
+// lengths of the wide rows (renumbered order), with a trailing 0 for the exclusive scan
+__global__ void k_wide_lens(const int64_t *__restrict__ rp, const int32_t *__restrict__ wperm,
+                            int64_t n_wide, int64_t *__restrict__ len) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= n_wide;
+         w += (int64_t)gridDim.x * blockDim.x)
+        len[w] = w < n_wide ? rp[wperm[w] + 1] - rp[wperm[w]] : 0;
+}
+
 // flag[0] = 1 if any column index is outside [0, ncols)
 __global__ void k_col_range(const int32_t *__restrict__ col, int64_t nnz, int64_t ncols,
                             int32_t *__restrict__ flag) {
@@ -807,24 +875,20 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
                    col_offset + n <= ncols,
                SC_E_RANGE, "bad z-space geometry ncols=%lld col_offset=%lld", (long long)ncols,
                (long long)col_offset);
-    {
-        // branch-free scans (vectorised by the compiler); locate the culprit only on failure
-        bool mono = true, dok = true;
-        for (int64_t i = 0; i < n; ++i) mono &= row_ptr[i + 1] >= row_ptr[i];
-        for (int64_t i = 0; i < n; ++i) dok &= (deg[i] > 0.0) & (deg[i] < 1e308);
-        for (int64_t i = 0; !mono && i < n; ++i)
+    // large inputs are validated on the device (k_validate_rows for the row offsets and
+    // degrees, k_col_range for the columns, overlapped with their copy); small ones here
+    if (n < (int64_t(1) << 16)) {
+        for (int64_t i = 0; i < n; ++i)
             SC_REQUIRE(row_ptr[i + 1] >= row_ptr[i], SC_E_RANGE, "row_ptr decreases at %lld",
                        (long long)i);
-        for (int64_t i = 0; !dok && i < n; ++i)
+        for (int64_t i = 0; i < n; ++i)
             SC_REQUIRE(deg[i] > 0.0 && deg[i] < 1e308, SC_E_RANGE,
                        "degree of row %lld is not positive/finite", (long long)i);
-        // large column arrays are range-checked on the device after the upload (k_col_range,
-        // overlapped with the copy); small ones here
-        if (col && nnz < (int64_t(1) << 20))
-            for (int64_t j = 0; j < nnz; ++j)
-                SC_REQUIRE(col[j] >= 0 && col[j] < ncols, SC_E_RANGE,
-                           "col_indices[%lld]=%d out of range", (long long)j, col[j]);
     }
+    if (col && nnz < (int64_t(1) << 20))
+        for (int64_t j = 0; j < nnz; ++j)
+            SC_REQUIRE(col[j] >= 0 && col[j] < ncols, SC_E_RANGE,
+                       "col_indices[%lld]=%d out of range", (long long)j, col[j]);
     lap("host validation");
     int ndev = 0;
     SC_CUDA(cudaGetDeviceCount(&ndev));
@@ -870,53 +934,101 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         fail(SC_E_CUDA, "stream/event creation failed");
         return cleanup(SC_E_CUDA);
     }
-    cudaStream_t s = g->stream;
-    // staging: the original CSR on the device, freed once the SELL layout is built
-    int64_t *t_rp = nullptr, *t_sizes = nullptr;
-    int32_t *t_col = nullptr;
+    cudaStream_t s = g->stream, s2 = g->side;
+    // staging: the original CSR on the device, freed once the SELL layout is built.  The
+    // column / weight copies run on the side stream while the main stream validates the rows
+    // and builds the renumbering from the row offsets (all on the device).
+    int64_t *t_rp = nullptr, *t_sizes = nullptr, *t_stats = nullptr, *t_wlen = nullptr;
+    int32_t *t_col = nullptr, *t_flag = nullptr;
+    uint32_t *t_keys = nullptr, *t_keys2 = nullptr;
+    int32_t *t_iota = nullptr;
     double *t_val = nullptr, *t_deg = nullptr;
     void *t_cub = nullptr;
-    auto free_tmp0 = [&]() {
-        if (t_rp) cudaFreeAsync(t_rp, s);
-        if (t_col && !dcol) cudaFreeAsync(t_col, s);
-        if (t_val) cudaFreeAsync(t_val, s);
-        if (t_deg) cudaFreeAsync(t_deg, s);
-        if (t_sizes) cudaFreeAsync(t_sizes, s);
-        if (t_cub) cudaFreeAsync(t_cub, s);
-    };
-    int32_t *t_flag = nullptr;
+    size_t cub_cap = 0;
     auto free_tmp = [&]() {
-        free_tmp0();
-        if (t_flag) cudaFreeAsync(t_flag, s);
+        for (void *p_ : {(void *)t_rp, (void *)t_sizes, (void *)t_stats, (void *)t_wlen,
+                         (void *)t_flag, (void *)t_keys, (void *)t_keys2, (void *)t_iota,
+                         (void *)t_val, (void *)t_deg, t_cub})
+            if (p_) cudaFreeAsync(p_, s);
+        if (t_col && !dcol) cudaFreeAsync(t_col, s);
     };
-    // the big arrays go first so their copies overlap the host-side renumbering below
+    auto need_cub = [&](size_t bytes) -> cudaError_t {
+        if (bytes <= cub_cap) return cudaSuccess;
+        if (t_cub) cudaFreeAsync(t_cub, s);
+        cub_cap = bytes;
+        return cudaMallocAsync(&t_cub, bytes, s);
+    };
+    auto bail = [&](cudaError_t err, const char *what) {
+        cudaStreamSynchronize(s2);
+        free_tmp();
+        fail(err == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA, "%s: %s", what,
+             cudaGetErrorString(err));
+        return cleanup(err == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA);
+    };
     cudaError_t e = cudaSuccess;
     if (dcol) t_col = const_cast<int32_t *>(dcol);
     else e = cudaMallocAsync((void **)&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4, s);
     if (!e && !unit) e = cudaMallocAsync((void **)&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8, s);
-    if (!e) e = cudaMallocAsync((void **)&t_flag, 16, s);
-    if (!e && nnz && !dcol) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s);
-    if (!e && t_val) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemsetAsync(t_flag, 0, 16, s);
-    if (!e && nnz) {
-        k_col_range<<<grid_for(g, nnz, 256), 256, 0, s>>>(t_col, nnz, ncols, t_flag);
-        e = cudaGetLastError();
-    }
-    lap("H2D issue");
-    std::vector<int32_t> perm;
-    g->n_sell = sell_order(row_ptr, n, perm);
-    g->n_wide = n - g->n_sell;
-    g->nslices = (g->n_sell + kSlice - 1) / kSlice;
-    lap("sell order");
     if (!e) e = cudaMallocAsync((void **)&t_rp, (size_t)(n + 1) * 8, s);
     if (!e) e = cudaMallocAsync((void **)&t_deg, (size_t)n * 8, s);
-    if (!e) e = cudaMallocAsync((void **)&t_sizes, (size_t)(g->nslices + 1) * 8, s);
-    if (e) {
-        free_tmp();
-        fail(e == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA, "staging allocation: %s",
-             cudaGetErrorString(e));
-        return cleanup(SC_E_OOM);
+    if (!e) e = cudaMallocAsync((void **)&t_flag, 64, s);
+    if (!e) e = cudaMallocAsync((void **)&t_stats, 64, s);
+    // row offsets and degrees first (they gate the renumbering), then the big arrays
+    if (!e) e = cudaMemcpyAsync(t_rp, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(t_deg, deg, (size_t)n * 8, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaEventRecord(g->ev_fork, s);  // allocations done -> side stream may copy
+    if (!e) e = cudaStreamWaitEvent(s2, g->ev_fork, 0);
+    if (!e && nnz && !dcol) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s2);
+    if (!e && t_val) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s2);
+    if (!e) e = cudaMemsetAsync(t_flag, 0, 64, s);
+    if (!e && nnz) {
+        // flag[0]: any column index out of range (side stream, right after the copy)
+        k_col_range<<<grid_for(g, nnz, 256), 256, 0, s2>>>(t_col, nnz, ncols, t_flag);
+        e = cudaGetLastError();
     }
+    if (!e) e = cudaEventRecord(g->ev_join, s2);
+    if (!e) e = cudaMemsetAsync(t_stats, 0, 64, s);
+    if (!e) {
+        k_validate_rows<<<grid_for(g, n, 256), 256, 0, s>>>(t_rp, t_deg, n, t_flag, t_stats);
+        k_finish_stats<<<1, 1, 0, s>>>(t_stats, n);
+        e = cudaGetLastError();
+    }
+    int64_t hst[8] = {0};
+    int32_t hfl[4] = {0};
+    if (!e) e = cudaMemcpyAsync(hst, t_stats, 64, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaMemcpyAsync(hfl, t_flag, 16, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) return bail(e, "graph upload");
+    lap("H2D + row validation");
+    if (hst[2] < n) {  // hst[2] = first row whose offsets decrease (n if none)
+        cudaStreamSynchronize(s2);
+        free_tmp();
+        fail(SC_E_RANGE, "row_ptr decreases at %lld", (long long)hst[2]);
+        return cleanup(SC_E_RANGE);
+    }
+    if (hst[3] < n) {  // first row with a non-positive / non-finite degree
+        cudaStreamSynchronize(s2);
+        free_tmp();
+        fail(SC_E_RANGE, "degree of row %lld is not positive/finite", (long long)hst[3]);
+        return cleanup(SC_E_RANGE);
+    }
+    // the SELL renumbering (see sell_order): windows of kSigma rows, or one global window
+    // for heavy-tailed lengths (max > 4 x mean among rows <= kSellMax), rows sorted by
+    // decreasing length inside a window (stable), wide rows last in their original order
+    const int64_t cnt_rows = hst[0], sum_len = hst[1], max_len = hst[4];
+    const int64_t sigma = (cnt_rows && max_len * cnt_rows > 4 * sum_len) ? n : kSigma;
+    g->n_sell = cnt_rows;
+    g->n_wide = n - g->n_sell;
+    g->nslices = (g->n_sell + kSlice - 1) / kSlice;
+    const int64_t nwin = (n + sigma - 1) / sigma;
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) <= (nwin + 1) * 512) ++end_bit;
+    if (!e) e = cudaMallocAsync((void **)&t_keys, (size_t)n * 4, s);
+    if (!e) e = cudaMallocAsync((void **)&t_keys2, (size_t)n * 4, s);
+    if (!e) e = cudaMallocAsync((void **)&t_iota, (size_t)n * 4, s);
+    if (!e) e = cudaMallocAsync((void **)&t_sizes, (size_t)(g->nslices + 1) * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&t_wlen, (size_t)(g->n_wide + 1) * 8, s);
+    if (e) return bail(e, "staging allocation");
     if ((st = dmalloc(g, (void **)&g->d_perm, (size_t)n * 4)) ||
         (st = dmalloc(g, (void **)&g->d_iperm, (size_t)n * 4)) ||
         (st = dmalloc(g, (void **)&g->d_slice_ptr, (size_t)(g->nslices + 1) * 8)) ||
@@ -927,59 +1039,59 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         (st = dmalloc(g, (void **)&g->d_x[1], (size_t)n * 8)) ||
         (st = dmalloc(g, (void **)&g->d_tmp, (size_t)n * 8)) ||
         (st = dmalloc(g, (void **)&g->d_f_orig, (size_t)n * 8))) {
+        cudaStreamSynchronize(s2);
         free_tmp();
         return cleanup(st);
     }
     // both z buffers in one allocation so one L2 access-policy window covers them
     double *zz = nullptr;
     if ((st = dmalloc(g, (void **)&zz, (size_t)ncols * 16))) {
+        cudaStreamSynchronize(s2);
         free_tmp();
         return cleanup(st);
     }
     g->d_z[0] = zz;
     g->d_z[1] = zz + ncols;
-
-    e = cudaMemcpyAsync(t_rp, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemcpyAsync(t_deg, deg, (size_t)n * 8, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemcpyAsync(g->d_perm, perm.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, s);
-    // wide-row offsets (host: few rows)
-    std::vector<int64_t> wptr((size_t)g->n_wide + 1, 0);
-    for (int64_t w = 0; w < g->n_wide; ++w) {
-        const int32_t r = perm[(size_t)(g->n_sell + w)];
-        wptr[(size_t)w + 1] = wptr[(size_t)w] + (row_ptr[r + 1] - row_ptr[r]);
+    e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, s);
+    size_t cb = 0, cb2 = 0;
+    if (!e) {
+        k_sell_keys<<<grid_for(g, n, 256), 256, 0, s>>>(t_rp, n, sigma, nwin, t_keys, t_iota);
+        e = cudaGetLastError();
     }
-    if (!e)
-        e = cudaMemcpyAsync(g->d_wide_ptr, wptr.data(), wptr.size() * 8, cudaMemcpyHostToDevice, s);
+    if (!e) e = cub::DeviceRadixSort::SortPairs(nullptr, cb, t_keys, t_keys2, t_iota, g->d_perm,
+                                                n, 0, end_bit, s);
+    if (!e) e = cub::DeviceScan::ExclusiveSum(nullptr, cb2, t_sizes, g->d_slice_ptr,
+                                              g->nslices + 1, s);
+    if (!e) e = need_cub(std::max(std::max(cb, cb2), (size_t)16));
+    if (!e) e = cub::DeviceRadixSort::SortPairs(t_cub, cb, t_keys, t_keys2, t_iota, g->d_perm,
+                                                n, 0, end_bit, s);
     if (!e) {
         k_inverse_perm<<<grid_for(g, n, 256), 256, 0, s>>>(g->d_perm, g->d_iperm, n);
         k_gather_perm<<<grid_for(g, n, 256), 256, 0, s>>>(t_deg, g->d_perm, g->d_deg, n);
         if (g->nslices)
             k_slice_sizes<<<grid_for(g, g->nslices, 256), 256, 0, s>>>(t_rp, g->d_perm, g->n_sell,
                                                                        g->nslices, t_sizes);
+        k_wide_lens<<<grid_for(g, g->n_wide + 1, 256), 256, 0, s>>>(t_rp, g->d_perm + g->n_sell,
+                                                                    g->n_wide, t_wlen);
         e = cudaGetLastError();
     }
     if (!e) e = cudaMemsetAsync(t_sizes + g->nslices, 0, 8, s);
-    size_t cub_bytes = 0;
-    if (!e)
-        e = cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, t_sizes, g->d_slice_ptr,
-                                          g->nslices + 1, s);
-    if (!e) e = cudaMallocAsync(&t_cub, std::max<size_t>(cub_bytes, 16), s);
-    if (!e)
-        e = cub::DeviceScan::ExclusiveSum(t_cub, cub_bytes, t_sizes, g->d_slice_ptr,
-                                          g->nslices + 1, s);
-    if (!e)
-        e = cudaMemcpyAsync(&g->sell_entries, g->d_slice_ptr + g->nslices, 8,
-                            cudaMemcpyDeviceToHost, s);
+    if (!e) e = cub::DeviceScan::ExclusiveSum(t_cub, cb2, t_sizes, g->d_slice_ptr,
+                                              g->nslices + 1, s);
+    size_t cb3 = 0;
+    if (!e) e = cub::DeviceScan::ExclusiveSum(nullptr, cb3, t_wlen, g->d_wide_ptr, g->n_wide + 1, s);
+    if (!e) e = need_cub(cb3);
+    if (!e) e = cub::DeviceScan::ExclusiveSum(t_cub, cb3, t_wlen, g->d_wide_ptr, g->n_wide + 1, s);
+    int64_t wide_total = 0;
+    if (!e) e = cudaMemcpyAsync(&g->sell_entries, g->d_slice_ptr + g->nslices, 8,
+                                cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaMemcpyAsync(&wide_total, g->d_wide_ptr + g->n_wide, 8, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamWaitEvent(s, g->ev_join, 0);  // columns copied and range-checked
     int32_t col_bad = 0;
     if (!e) e = cudaMemcpyAsync(&col_bad, t_flag, 4, cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
-    lap("alloc + H2D + slices");
-    if (e) {
-        free_tmp();
-        fail(SC_E_CUDA, "graph layout: %s", cudaGetErrorString(e));
-        return cleanup(SC_E_CUDA);
-    }
+    lap("renumbering + slices");
+    if (e) return bail(e, "graph layout");
     if (col_bad) {
         free_tmp();
         fail(SC_E_RANGE, "col_indices out of range [0, %lld)", (long long)ncols);
@@ -994,10 +1106,10 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         (!unit && !g->f32 &&
          (st = dmalloc(g, (void **)&g->d_val, (size_t)g->sell_entries * 8 + 16))) ||
         (g->f32 && (st = dmalloc(g, (void **)&g->d_val32, (size_t)g->sell_entries * 4 + 16))) ||
-        (st = dmalloc(g, (void **)&g->d_wcol, (size_t)wptr.back() * 4 + 16)) ||
+        (st = dmalloc(g, (void **)&g->d_wcol, (size_t)wide_total * 4 + 16)) ||
         (!unit && !g->f32 &&
-         (st = dmalloc(g, (void **)&g->d_wval, (size_t)wptr.back() * 8 + 16))) ||
-        (g->f32 && (st = dmalloc(g, (void **)&g->d_wval32, (size_t)wptr.back() * 4 + 16)))) {
+         (st = dmalloc(g, (void **)&g->d_wval, (size_t)wide_total * 8 + 16))) ||
+        (g->f32 && (st = dmalloc(g, (void **)&g->d_wval32, (size_t)wide_total * 4 + 16)))) {
         free_tmp();
         return cleanup(st);
     }

@@ -87,3 +87,52 @@ def test_fp32_value_variant_within_tolerance():
     assert np.max(np.abs(xT - xo) / np.abs(xo)) < 1e-5
     assert np.max(np.abs(f - fo) / np.abs(fo)) < 1e-5
     assert not np.array_equal(xT, xo)  # it really is the reduced-precision variant
+
+
+@pytest.mark.parametrize("kind", ["sbm", "heavy_tail", "wide"])
+def test_device_renumbering_equals_host_sell_order(kind):
+    """The graph handle builds its SELL renumbering on the device; multi-GPU plans rename
+    columns with the host sc_sell_order -- the two must agree exactly."""
+    import ctypes
+
+    from paper_2310_10939_b200 import _lib
+    from paper_2310_10939_b200.distributed import sell_order
+    from paper_2310_10939_b200.generate import SbmParams, sample_dcsbm, sample_sbm
+
+    if kind == "sbm":
+        g = sample_sbm(SbmParams(n=20000, k=4, p=0.004, q=0.0004, seed=1)).graph
+    elif kind == "heavy_tail":
+        g = sample_dcsbm(50_000, 10, seed=3).graph
+    else:
+        n = 3000
+        iu, iv = np.triu_indices(300, 1)
+        rng = np.random.default_rng(5)
+        u = np.concatenate([iu, rng.integers(300, n, 9000)])
+        v = np.concatenate([iv, rng.integers(300, n, 9000)])
+        keep = u != v
+        g, _ = from_edges(n, u[keep], v[keep], drop_isolated=True)
+    with DeviceGraph(g) as dg:
+        perm = np.empty(g.n, dtype=np.int32)
+        _lib.check(_lib.load().sc_graph_order(dg.handle, _lib.ptr(perm)))
+    assert np.array_equal(perm, sell_order(g.row_offsets))
+
+
+def test_invalid_rows_rejected_on_device():
+    """row_ptr / degree errors are detected by the device validation with the same messages."""
+    from paper_2310_10939_b200 import from_csr
+    from paper_2310_10939_b200.errors import InputError
+
+    n = 1 << 21  # above the host-validation threshold
+    rp = np.arange(n + 1, dtype=np.int64)
+    col = ((np.arange(n) + 1) % n).astype(np.int32)
+    deg = np.ones(n)
+    rp_bad = rp.copy()
+    rp_bad[777] = rp_bad[779]  # row 777 ends before it starts
+    with pytest.raises(InputError, match="row_ptr decreases at 777"):
+        DeviceGraph(from_csr(n, rp_bad, col, None, deg))
+    deg_bad = deg.copy()
+    deg_bad[123456] = 0.0
+    with pytest.raises(InputError, match="degree of row 123456"):
+        DeviceGraph(from_csr(n, rp, col, None, deg_bad))
+    with DeviceGraph(from_csr(n, rp, col, None, deg)) as dg:
+        assert dg.info()["n"] == n
