@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="sharded path: issue every launch from the host (no CUDA graph)")
     ap.add_argument("--pieces", type=int, default=0,
-                    help="sharded path: SpMV/all-gather pieces per step (0 = 4 if N > 1 else 1)")
+                    help="sharded path: SpMV/all-gather pieces per step (0 = 2 if N >= 8 else 1)")
     return ap.parse_args()
 
 

@@ -478,7 +478,12 @@ def bench_main(args, metric: str, unit: str):
                        q=4 / (world * n_loc - 10**5), seed=0)
     T = 100
     p2p = getattr(args, "comm", "nccl") == "p2p"
-    pieces = 1 if p2p else int(getattr(args, "pieces", 0) or (4 if world > 1 else 1))
+    # Splitting a step into P pieces costs ~12 us per extra piece on one B200 (smaller grids,
+    # one more collective) and hides up to (P-1)/P of the all-gather, which moves
+    # (W-1) * 8 MB per GPU per step (~12 us at W = 2, ~80 us at W = 8 over NVLink): only
+    # worth it for the widest runs.
+    default_pieces = 2 if world >= 8 else 1
+    pieces = 1 if p2p else int(getattr(args, "pieces", 0) or default_pieces)
     starts = np.arange(world + 1, dtype=np.int64) * n_loc
     rp, col, deg, iso = sbm_rows(params, int(starts[rank]), int(starts[rank + 1]))
     iso_t = torch.tensor([iso], device="cuda")
