@@ -96,6 +96,10 @@ int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double
 /* store the weights as fp32 (8 -> 4 bytes per entry; products still formed in fp64): the
  * optional fp32-value variant, agreeing with fp64 within 1e-5 relative (not bit-exact) */
 #define SC_CREATE_FP32_VALUES 0x2u
+/* locality pre-order: vertices renumbered by a multi-source BFS (regions of ~4096 vertices
+ * around every 4096th vertex, by level) before the SELL layout, for graphs whose ids carry no
+ * locality; exact (only where z values live changes), whole graphs only */
+#define SC_CREATE_REORDER_BFS 0x4u
 int32_t sc_graph_create_ex(const int64_t *row_ptr, const int32_t *col, const double *val,
                            const double *deg, int64_t n, int64_t nnz, int32_t device,
                            uint32_t create_flags, sc_graph **out);

@@ -24,6 +24,7 @@ SC_L2_PERSIST = 0x4
 SC_FORCE_WEIGHTED = 0x8
 SC_CREATE_KEEP_WEIGHTS = 0x1
 SC_CREATE_FP32_VALUES = 0x2
+SC_CREATE_REORDER_BFS = 0x4
 
 
 class GraphInfo(ctypes.Structure):

@@ -523,6 +523,84 @@ __global__ void k_sell_keys(const int64_t *__restrict__ rp, int64_t n, int64_t s
     }
 }
 
+// ---- optional locality-preserving pre-order (SC_CREATE_REORDER_BFS) ----------------------
+// Multi-source breadth-first search from every kBfsStride-th vertex: each vertex joins the
+// region of the first seed to reach it; vertices are then ordered by (region, level), so a
+// region -- a ball of ~kBfsStride vertices -- is contiguous in the new numbering and the rows
+// of a slice gather from a small window of z.  Renumbering changes where z values live, never
+// the order of a row's products, so results stay bit-identical.
+constexpr int64_t kBfsStride = 4096;
+
+__global__ void k_bfs_init(int64_t n, int32_t *__restrict__ region, int32_t *__restrict__ lev,
+                           int32_t *__restrict__ cur) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const bool seed = v % kBfsStride == 0;
+        region[v] = seed ? (int32_t)(v / kBfsStride) : -1;
+        lev[v] = seed ? 0 : -1;
+        if (seed) cur[v / kBfsStride] = (int32_t)v;
+    }
+}
+
+// one warp per frontier vertex, lanes over its neighbours (coalesced column reads); claimed
+// vertices are appended with one warp-aggregated atomic per batch
+__global__ void k_bfs_expand(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                             int32_t *__restrict__ region, int32_t *__restrict__ lev,
+                             const int32_t *__restrict__ cur, int32_t ncur, int32_t *__restrict__ nxt,
+                             int32_t *__restrict__ nnxt, int32_t level) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < ncur;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t v = cur[i], rv = region[v];
+        const int64_t lo = rp[v], hi = rp[v + 1];
+        for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+            const int64_t j = j0 + lane;
+            bool won = false;
+            int32_t u = 0;
+            if (j < hi) {
+                u = col[j];
+                won = region[u] == -1 && atomicCAS(&region[u], -1, rv) == -1;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, won);
+            if (m) {
+                int32_t base = 0;
+                if (lane == 0) base = atomicAdd(nnxt, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (won) {
+                    lev[u] = level + 1;
+                    nxt[base + __popc(m & ((1u << lane) - 1))] = u;
+                }
+            }
+        }
+    }
+}
+
+// key (region, level); vertices no seed reached keep their original order after all regions
+__global__ void k_bfs_keys(int64_t n, const int32_t *__restrict__ region,
+                           const int32_t *__restrict__ lev, int64_t nseeds,
+                           uint64_t *__restrict__ keys, int32_t *__restrict__ iota) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t rg = region[v] >= 0 ? region[v] : nseeds + v / kBfsStride;
+        keys[v] = ((uint64_t)rg << 20) | (uint64_t)(lev[v] >= 0 ? min(lev[v], (1 << 20) - 1) : 0);
+        iota[v] = (int32_t)v;
+    }
+}
+
+// SELL keys over a pre-order: position p holds original row ord[p]
+__global__ void k_sell_keys_ord(const int64_t *__restrict__ rp, const int32_t *__restrict__ ord,
+                                int64_t n, int64_t sigma, int64_t nwin,
+                                uint32_t *__restrict__ keys, int32_t *__restrict__ payload) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = ord[p];
+        const int64_t len = rp[r + 1] - rp[r];
+        keys[p] = len <= kSellMax ? (uint32_t)((p / sigma) * 512 + (kSellMax - len))
+                                  : (uint32_t)(nwin * 512);
+        payload[p] = r;
+    }
+}
+
 // lengths of the wide rows (renumbered order), with a trailing 0 for the exclusive scan
 __global__ void k_wide_lens(const int64_t *__restrict__ rp, const int32_t *__restrict__ wperm,
                             int64_t n_wide, int64_t *__restrict__ len) {
@@ -656,6 +734,7 @@ struct sc_graph {
     bool l2_window = false;
     double *d_f_orig = nullptr;   // f in original vertex order (for the k-means context)
     bool f32 = false;             // weights stored as fp32 (SC_CREATE_FP32_VALUES)
+    int64_t bfs_sigma = 0, bfs_nwin = 0;  // SELL window parameters for the BFS pre-order
     float *d_val32 = nullptr, *d_wval32 = nullptr;
     std::vector<std::pair<void *, size_t>> allocs;  // every dmalloc'd buffer (returned to the cache)
     // fused peer exchange (sc_shard_set_peers)
@@ -849,6 +928,63 @@ static int grid_for(const sc_graph *g, int64_t n, int tpb) {
     return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
+// Builds the SELL sort keys over a BFS pre-order into keys / payload (see k_bfs_*); waits
+// for the column upload (ev_join) first.
+static cudaError_t reorder_bfs(sc_graph *g, cudaStream_t s, const int64_t *rp, const int32_t *col,
+                               int64_t n, uint32_t *keys_out, int32_t *payload_out, bool prof) {
+    const int64_t nseeds = (n + kBfsStride - 1) / kBfsStride;
+    int32_t *region = nullptr, *lev = nullptr, *q0 = nullptr, *q1 = nullptr, *cnt = nullptr,
+            *ord = nullptr, *iota = nullptr, *ordv = nullptr;
+    uint64_t *k64 = nullptr, *k64b = nullptr;
+    void *tmp = nullptr;
+    cudaError_t e = cudaStreamWaitEvent(s, g->ev_join, 0);
+    for (auto pp : {(void **)&region, (void **)&lev, (void **)&q0, (void **)&q1, (void **)&ord,
+                    (void **)&iota, (void **)&ordv})
+        if (!e) e = cudaMallocAsync(pp, (size_t)n * 4, s);
+    if (!e) e = cudaMallocAsync((void **)&cnt, 16, s);
+    if (!e) e = cudaMallocAsync((void **)&k64, (size_t)n * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&k64b, (size_t)n * 8, s);
+    if (!e) {
+        k_bfs_init<<<grid_for(g, n, 256), 256, 0, s>>>(n, region, lev, q0);
+        e = cudaGetLastError();
+    }
+    int32_t ncur = (int32_t)nseeds, level = 0;
+    while (!e && ncur > 0) {
+        e = cudaMemsetAsync(cnt, 0, 4, s);
+        if (!e) {
+            k_bfs_expand<<<grid_for(g, (int64_t)ncur * 32, 256), 256, 0, s>>>(
+                rp, col, region, lev, q0, ncur, q1, cnt, level);
+            e = cudaGetLastError();
+        }
+        if (!e) e = cudaMemcpyAsync(&ncur, cnt, 4, cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        std::swap(q0, q1);
+        ++level;
+    }
+    if (prof) fprintf(stderr, "[sc_graph_create] BFS: %lld seeds, %d levels\n",
+                      (long long)nseeds, level);
+    size_t tb = 0;
+    int end_bit = 21;
+    while ((int64_t(1) << (end_bit - 20)) <= 2 * nseeds + 1) ++end_bit;
+    if (!e) {
+        k_bfs_keys<<<grid_for(g, n, 256), 256, 0, s>>>(n, region, lev, nseeds, k64, iota);
+        e = cudaGetLastError();
+    }
+    if (!e) e = cub::DeviceRadixSort::SortPairs(nullptr, tb, k64, k64b, iota, ord, n, 0, end_bit, s);
+    if (!e) e = cudaMallocAsync(&tmp, tb + 16, s);
+    if (!e) e = cub::DeviceRadixSort::SortPairs(tmp, tb, k64, k64b, iota, ord, n, 0, end_bit, s);
+    if (!e) {
+        // the SELL keys are then built over the BFS positions (the caller sorts them)
+        k_sell_keys_ord<<<grid_for(g, n, 256), 256, 0, s>>>(rp, ord, n, g->bfs_sigma, g->bfs_nwin,
+                                                            keys_out, payload_out);
+        e = cudaGetLastError();
+    }
+    for (void *p_ : {(void *)region, (void *)lev, (void *)q0, (void *)q1, (void *)cnt, (void *)ord,
+                     (void *)iota, (void *)ordv, (void *)k64, (void *)k64b, tmp})
+        if (p_) cudaFreeAsync(p_, s);
+    return e;
+}
+
 // col == nullptr with dcol != nullptr: the column array is already on `device` (borrowed,
 // e.g. from sc_generate_sbm) and is neither copied nor freed.
 static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const double *val,
@@ -867,6 +1003,8 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         tp0 = t;
     };
     SC_REQUIRE(row_ptr && deg && (col || dcol || nnz == 0), SC_E_INVALID, "null CSR array");
+    SC_REQUIRE(!(cflags & SC_CREATE_REORDER_BFS) || rename, SC_E_INVALID,
+               "the BFS pre-order applies to whole graphs (shards keep the plan's order)");
     SC_REQUIRE(n >= 1 && n < (int64_t(1) << 31) - 1, SC_E_INVALID, "n=%lld out of range",
                (long long)n);
     SC_REQUIRE(nnz >= 0 && row_ptr[0] == 0 && row_ptr[n] == nnz, SC_E_RANGE,
@@ -1021,6 +1159,9 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->n_wide = n - g->n_sell;
     g->nslices = (g->n_sell + kSlice - 1) / kSlice;
     const int64_t nwin = (n + sigma - 1) / sigma;
+    g->bfs_sigma = sigma;
+    g->bfs_nwin = nwin;
+
     int end_bit = 1;
     while ((int64_t(1) << end_bit) <= (nwin + 1) * 512) ++end_bit;
     if (!e) e = cudaMallocAsync((void **)&t_keys, (size_t)n * 4, s);
@@ -1054,7 +1195,12 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->d_z[1] = zz + ncols;
     e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, s);
     size_t cb = 0, cb2 = 0;
-    if (!e) {
+    // (a heavy-tailed graph is sorted by length globally, which would undo any pre-order)
+    if (!e && (cflags & SC_CREATE_REORDER_BFS) && sigma < n) {
+        // locality pre-order from a multi-source BFS (needs the columns on the device)
+        e = reorder_bfs(g, s, t_rp, t_col, n, t_keys, t_iota, prof);
+        lap("BFS pre-order");
+    } else if (!e) {
         k_sell_keys<<<grid_for(g, n, 256), 256, 0, s>>>(t_rp, n, sigma, nwin, t_keys, t_iota);
         e = cudaGetLastError();
     }

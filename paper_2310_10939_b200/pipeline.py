@@ -54,6 +54,7 @@ class SpectralParams:
     max_iters: int = 100
     tol: float = 1e-6
     kmeans: str = "exact"        # "exact" (bit-exact replica) or "sorted" (fast, one_vector)
+    reorder: str | None = "auto"  # device-layout pre-order: "auto", "bfs" or None (exact)
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -134,7 +135,8 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
     if params.mode == "pm_log_k":
         return _pm_log_k(graph, params, steps, device_graph)
     t_start = time.perf_counter()
-    dev = device_graph if device_graph is not None else DeviceGraph(graph, params.device)
+    dev = device_graph if device_graph is not None else DeviceGraph(graph, params.device,
+                                                                    reorder=params.reorder)
     try:
         t0 = time.perf_counter()
         if params.x0 is not None:

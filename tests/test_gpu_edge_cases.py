@@ -136,3 +136,28 @@ def test_invalid_rows_rejected_on_device():
         DeviceGraph(from_csr(n, rp, col, None, deg_bad))
     with DeviceGraph(from_csr(n, rp, col, None, deg)) as dg:
         assert dg.info()["n"] == n
+
+
+def test_bfs_reorder_is_exact():
+    """The BFS locality pre-order only moves where z values live: x_T, f and the labels are
+    bit-identical to the default layout and to the oracle (weighted, hubs, several components)."""
+    rng = np.random.default_rng(8)
+    n = 30000
+    u, v = rng.integers(0, n, 150000), rng.integers(0, n, 150000)
+    u = np.concatenate([u, np.zeros(600, int)])
+    v = np.concatenate([v, rng.integers(1, n, 600)])
+    keep = u != v
+    g, _ = from_edges(n, u[keep], v[keep], 0.5 + rng.random(keep.sum()), drop_isolated=True)
+    x0 = O.irwin_hall(g.degrees, 1)
+    out = []
+    for reorder in (None, "bfs"):
+        with DeviceGraph(g, reorder=reorder) as dg:
+            dg.set_x0(x0)
+            out.append(dg.power_iterate(40))
+    xo, fo = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, 40)
+    for xT, f in out:
+        assert np.array_equal(xT, xo) and np.array_equal(f, fo)
+    r = fast_spectral_cluster(g, SpectralParams(k=6, t=40, mode="one_vector", seed=1,
+                                                reorder="bfs"))
+    lab, _ = O.lloyd(r.embedding.data[:, 0], 6, O.kmeans_seed(1))
+    assert np.array_equal(r.partition.labels, lab)
