@@ -289,8 +289,9 @@ def run_b200(args):
 
     g, T, k = build_config(args.config)
     unit = g.unit_weights() and not args.weighted
-    dev = DeviceGraph(g, keep_weights=args.weighted)
+    dev = DeviceGraph(g, keep_weights=args.weighted, reorder="auto")  # as fast_spectral_cluster
     info = dev.info()
+    dev_reorder = dev.reorder or "none"
     dev.sample_irwin_hall(0)
     times, clocks = time_power(dev, T, args.steps, args.warmup, clocks=True)
     tot_ms = sum(times)
@@ -303,7 +304,7 @@ def run_b200(args):
     # the north-star byte formula nnz*(idx+val) applies to this one
     weighted = None
     if unit and not args.no_weighted_probe:
-        with DeviceGraph(g, keep_weights=True) as dw:
+        with DeviceGraph(g, keep_weights=True, reorder="auto") as dw:
             iw = dw.info()
             dw.sample_irwin_hall(0)
             wt, _ = time_power(dw, T, max(3, args.steps // 2), 2)
@@ -352,6 +353,7 @@ def run_b200(args):
         "config": {"workload": f"config{args.config}",
                    "graph": GRAPH_DESC.get(args.config, "synthetic"),
                    "n": n, "nnz": g.nnz, "T": T, "k": k, "unit_weight_kernel": unit,
+                   "layout_preorder": dev_reorder,
                    "l2": "inputs larger than L2 (CSR streamed per iteration >= 0.2 GB)",
                    "parallelism": "single GPU"},
         "roofline": roofline,

@@ -157,6 +157,7 @@ class DeviceGraph:
                                               ctypes.byref(h)))
         self._h = h
         self.graph = None
+        self.reorder = None
         self.n, self.nnz = csr.n, csr.nnz
         self.device = csr.device
         self.last_timing = None
