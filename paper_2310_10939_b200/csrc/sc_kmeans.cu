@@ -136,7 +136,7 @@ struct SeqWork {
     int32_t *kpred;   // predicted grid exponent per chunk (kNoGrid = step it)
     int64_t *q0, *q1; // chunk parity map
     double *cstart;   // exact running sum at each chunk start
-    int32_t *neg;     // per segment: any negative / non-finite element
+    int32_t *neg;     // per segment flags: 1 negative, 2 positive, 4 non-finite element
     double *total;    // per segment exact total
     // super-chunks: kSuper consecutive chunks (aligned to the global chunk index) composed
     // into one map when they all lie in one segment on one predicted grid
@@ -188,25 +188,25 @@ __global__ void k_seq_summarize(SegView v, SeqWork w, const int64_t *__restrict_
         int64_t first;
         const int m = load_chunk(v, s, c, a, first);
         double sum = 0.0, mx = 0.0;
-        int bad = 0;
+        int fl = 0;
 #pragma unroll
         for (int t = 0; t < kSeqPerLane; ++t) {
             if (lane * kSeqPerLane + t < m) {
                 sum += a[t];
                 mx = fmax(mx, a[t]);
-                bad |= !(a[t] >= 0.0) || !isfinite(a[t]);
+                fl |= (a[t] < 0.0) | ((a[t] > 0.0) << 1) | ((!isfinite(a[t])) << 2);
             }
         }
 #pragma unroll
         for (int d = 16; d; d >>= 1) {
             sum += __shfl_xor_sync(0xffffffffu, sum, d);
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-            bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+            fl |= __shfl_xor_sync(0xffffffffu, fl, d);
         }
         if (lane == 0) {
             w.A[c] = sum;
             w.vmax[c] = mx;
-            if (bad) w.neg[s] = 1;
+            if (fl) atomicOr(&w.neg[s], fl);
         }
     }
 }
@@ -214,6 +214,43 @@ __global__ void k_seq_summarize(SegView v, SeqWork w, const int64_t *__restrict_
 // one warp per segment: approximate chunk starts -> predicted grid per chunk.  Chunk data
 // are read 256 at a time (8 independent loads per lane) so the walk pays one memory latency
 // per 256 chunks.
+// A segment whose elements are all <= 0 is summed as the negation of its negated elements
+// (round-to-nearest-even is symmetric: fl(-x + -y) = -fl(x + y)), so it takes the fast
+// path too; only mixed-sign or non-finite segments are added element by element.
+__device__ __forceinline__ bool seg_slow(int f) { return (f & 4) || ((f & 1) && (f & 2)); }
+__device__ __forceinline__ bool seg_flipped(int f) { return !seg_slow(f) && (f & 1); }
+
+// one warp per chunk of a flipped segment: negate its elements in place and re-summarise
+__global__ void k_seq_flip(SegView v, SeqWork w, const int64_t *__restrict__ pn) {
+    const int64_t nchunks = *pn;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double *vals = const_cast<double *>(v.vals);
+    for (int64_t c = wid; c < nchunks; c += nw) {
+        const int s = seg_of_chunk(v, c);
+        if (!seg_on(v, s) || !seg_flipped(w.neg[s])) continue;
+        const int64_t lo = v.seg_off[s] + (c - v.cofs[s]) * kSeqChunk;
+        const int64_t hi = min(lo + kSeqChunk, v.seg_off[s + 1]);
+        double sum = 0.0, mx = 0.0;
+        for (int64_t j = lo + lane; j < hi; j += 32) {
+            const double a = -vals[j];
+            vals[j] = a;
+            sum += a;
+            mx = fmax(mx, a);
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        }
+        if (lane == 0) {
+            w.A[c] = sum;
+            w.vmax[c] = mx;
+        }
+    }
+}
+
 constexpr int kPredictWarps = 8;
 
 // one CTA per segment: each warp takes a contiguous share of the segment's chunks, the
@@ -357,8 +394,10 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
                    wib * kSeqChunk;
     const int64_t c0 = v.cofs[s], c1 = v.cofs[s + 1];
     double run = 0.0;
-    if (w.neg[s]) {
-        // a segment with negative (or non-finite) elements: plain sequential sum
+    const int sflags = w.neg[s];
+    const double sgn = seg_flipped(sflags) ? -1.0 : 1.0;  // flipped: negated elements
+    if (seg_slow(sflags)) {
+        // mixed signs or non-finite elements: plain sequential sum
         for (int64_t c = c0; c < c1; ++c) {
             double a[kSeqPerLane];
             int64_t first;
@@ -409,7 +448,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        w.cstart[cb + t0 + u] = from_units(S, g.k);
+                        w.cstart[cb + t0 + u] = sgn * from_units(S, g.k);
                         S = pmap_apply(PMap{a0[u], a1[u]}, S);
                     }
                 }
@@ -460,7 +499,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         const int Lb = badm ? __ffs(badm) - 1 : 32;   // first chunk to step
         const int Le = __popc(valm);                  // valid lanes form a prefix
         const int nadv = min(Lb, Le);
-        if (want_cstart && lane < nadv) w.cstart[cl] = from_units(Sl, g.k);
+        if (want_cstart && lane < nadv) w.cstart[cl] = sgn * from_units(Sl, g.k);
         if (nadv > 0) {
             const int64_t Send = __shfl_sync(0xffffffffu, pmap_apply(m, Sl), nadv - 1);
             run = from_units(Send, g.k);
@@ -468,7 +507,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         }
         if (Lb < Le) {
             // step chunk c element by element
-            if (want_cstart && lane == 0) w.cstart[c] = run;
+            if (want_cstart && lane == 0) w.cstart[c] = sgn * run;
             double a[kSeqPerLane];
             int64_t first;
             const int mcount = load_chunk(v, s, c, a, first);
@@ -476,7 +515,7 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
             ++c;
         }
     }
-    if (lane == 0) w.total[s] = run;
+    if (lane == 0) w.total[s] = sgn * run;
 }
 
 // ---------------------------------------------------------------------------
@@ -548,7 +587,7 @@ __global__ void k_kpp_update_sum(const double *__restrict__ x, int64_t n, int l,
         if (lane == 0) {
             w.A[c] = sum;
             w.vmax[c] = mx;
-            if (bad) w.neg[r] = 1;
+            if (bad) w.neg[r] = 4;
         }
     }
 }
@@ -1785,6 +1824,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
                                                                     km->d_vals_alt);
             SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)nseg * 4, s));
             k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
+            k_seq_flip<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
             k_seq_predict<<<nseg, 32 * kPredictWarps, 0, s>>>(vm, wm);
             k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
             k_seq_superize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
@@ -2249,6 +2289,7 @@ static int32_t seqsum_device(const double *d_vals, int32_t nseg, const int64_t *
         const int gw = (int)std::min<int64_t>((nch * 32 + 255) / 256 + 1, (int64_t)sms * 8);
         const int gs = (nseg * 32 + 255) / 256;
         k_seq_summarize<<<gw, 256>>>(v, w, d_nch);
+        k_seq_flip<<<gw, 256>>>(v, w, d_nch);
         k_seq_predict<<<nseg, 32 * kPredictWarps>>>(v, w);
         k_seq_chunkmap<<<gw, 256>>>(v, w, d_nch);
         k_seq_superize<<<gw, 256>>>(v, w, d_nch);

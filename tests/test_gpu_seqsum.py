@@ -56,3 +56,31 @@ def test_seqsum_segments_and_negatives():
     tot, _ = run(a, offs)
     ref = np.array([np.cumsum(a[offs[i]:offs[i + 1]])[-1] for i in range(len(offs) - 1)])
     assert np.array_equal(tot, ref)
+
+
+@pytest.mark.parametrize("name", ["uniform", "wide", "dyadic", "spiky", "above_2p53"])
+def test_seqsum_all_nonpositive_segments(name):
+    """Segments whose elements are all <= 0 are summed as negated nonnegative sums (the
+    rounding is symmetric); totals and chunk starts must still equal np.cumsum's."""
+    a = -cases()[name]
+    a[::97] = -0.0
+    tot, cs = run(a, [0, a.size])
+    cum = np.concatenate([[0.0], np.cumsum(a)])
+    assert tot[0] == cum[-1]
+    starts = cum[np.arange(0, a.size, 256)]
+    assert np.array_equal(cs[: starts.size], starts)
+
+
+def test_seqsum_mixed_sign_segments_batch():
+    """Many segments: nonnegative, nonpositive and mixed-sign ones side by side."""
+    rng = np.random.default_rng(9)
+    a = np.exp(rng.normal(0, 6, 300000))
+    offs = [0] + np.sort(rng.choice(np.arange(1, a.size), 199, replace=False)).tolist() + [a.size]
+    for i in range(0, 200, 3):  # every third segment all negative
+        a[offs[i]:offs[i + 1]] *= -1.0
+    for i in range(1, 200, 7):  # some mixed
+        a[offs[i]:offs[i + 1]:5] *= -1.0
+    tot, _ = run(a, offs)
+    ref = np.array([np.cumsum(a[offs[i]:offs[i + 1]])[-1] if offs[i + 1] > offs[i] else 0.0
+                    for i in range(len(offs) - 1)])
+    assert np.array_equal(tot, ref)
