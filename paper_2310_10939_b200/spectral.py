@@ -316,8 +316,18 @@ def sample_gaussian_vectors(n: int, l: int, seed: int) -> EmbeddingMatrix:
     if n < 1 or l < 1:
         raise InputError(f"need n >= 1 and l >= 1, got n={n}, l={l}")
     data = np.empty((n, l), dtype=np.float64)
-    for i in range(l):
+
+    def column(i):
         data[:, i] = rng_for(seed, TAG_GAUSSIAN_COLUMN, i).standard_normal(n)
+
+    if l > 1 and n >= 100_000:  # independent streams: fill the columns concurrently
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(min(l, 8)) as ex:
+            list(ex.map(column, range(l)))
+    else:
+        for i in range(l):
+            column(i)
     return EmbeddingMatrix(data=data, scaled=False, seed=seed)
 
 
