@@ -111,6 +111,10 @@ int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double
                         int64_t col_offset, int64_t global_row0, int32_t device,
                         sc_graph **out);
 void sc_graph_destroy(sc_graph *g);
+/* Destroyed handles return their device buffers to a process-wide cache (reused by the next
+ * handle; capped by SC_BUFFER_CACHE_MB, default 16384).  This frees the cached buffers of
+ * `device` (all devices if < 0) and returns the bytes released. */
+int64_t sc_release_cached_memory(int32_t device);
 int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *out);
 /* The device layout renumbers rows (SELL-32-sigma: length-sorted inside 4096-row windows,
  * rows longer than 256 last).  sc_sell_order returns that permutation for a row_ptr

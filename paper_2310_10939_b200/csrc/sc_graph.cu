@@ -1484,6 +1484,11 @@ int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_grap
                       device, out, d_col);
 }
 
+int64_t sc_release_cached_memory(int32_t device) {
+    // device < 0: every device
+    return (int64_t)sc::cache_flush(device);
+}
+
 int32_t sc_sell_order(const int64_t *row_ptr, int64_t n, int32_t *perm_out) {
     SC_REQUIRE(row_ptr && perm_out && n >= 1, SC_E_INVALID, "null argument");
     std::vector<int32_t> perm;

@@ -336,3 +336,9 @@ def sample_irwin_hall(graph, seed: int, device: int = 0) -> EmbeddingMatrix:
     dev = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
     x0 = dev.sample_irwin_hall(seed, return_host=True)
     return EmbeddingMatrix(data=x0[:, None], scaled=False, seed=seed)
+
+
+def release_device_memory(device: int = -1) -> int:
+    """Free the device buffers that destroyed graphs left in the library's reuse cache
+    (all devices by default); returns the bytes released."""
+    return int(_lib.load().sc_release_cached_memory(int(device)))

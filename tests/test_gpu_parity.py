@@ -254,3 +254,14 @@ def test_device_column_range_check():
     col[777_777] = 3
     with DeviceGraph(from_csr(n, rp, col, None, np.full(n, float(per)))) as dg:
         assert dg.info()["nnz"] == n * per
+
+
+def test_release_cached_device_memory(c1):
+    """Destroyed handles park their buffers in the reuse cache; release_device_memory frees
+    them (and a second call finds nothing)."""
+    from paper_2310_10939_b200.spectral import release_device_memory
+
+    with DeviceGraph(c1["graph"]) as dg:
+        dg.sample_irwin_hall(0)
+    assert release_device_memory() > 0
+    assert release_device_memory() == 0
