@@ -1856,6 +1856,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         return SC_OK;
     };
     const bool speculate = getenv("SC_KMEANS_NO_SPECULATION") == nullptr;
+    const bool trace = getenv("SC_KMEANS_TRACE") != nullptr;
     double wait_ms = 0.0;
     if ((st = launch_main(0, active, cur))) return st;
     for (int it = 0; it < max_iters; ++it) {
@@ -1882,7 +1883,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             const bool unchanged = hch[r] == 0 && fin;
             const double c = hc[r];
             const bool small_gain = fin && (prev[r] - c <= tol * std::max(prev[r], 1e-300));
-            if (r == 0 && getenv("SC_KMEANS_TRACE"))
+            if (r == 0 && trace)
                 fprintf(stderr, "exact  r0 it %d cost %.17g changed %d\n", iters[r], c, hch[r]);
             prev[r] = c;
             iters[r] += 1;
