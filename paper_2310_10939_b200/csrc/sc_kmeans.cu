@@ -685,6 +685,64 @@ __global__ void k_assign(const double *__restrict__ x, int64_t n, int l, int k,
     if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&changed[r], ch);
 }
 
+// l == 1: the point is loaded once and the k centers come from shared memory; each point's
+// work is k (sub, mul, compare) -- the generic kernel re-read x from global per center.  Two
+// points per thread keep two independent compare chains in flight.
+__global__ void __launch_bounds__(256) k_assign1(const double *__restrict__ x, int64_t n, int k,
+                                                 const double *__restrict__ cen,
+                                                 const int32_t *__restrict__ active,
+                                                 const int32_t *__restrict__ prev,
+                                                 int32_t *__restrict__ lab, int32_t *__restrict__ cnt,
+                                                 int32_t *__restrict__ changed) {
+    const int r = blockIdx.y;
+    if (!active[r]) return;
+    extern __shared__ unsigned char smem_raw[];
+    double *c = reinterpret_cast<double *>(smem_raw);
+    int32_t *hist = reinterpret_cast<int32_t *>(c + k);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        c[i] = cen[(int64_t)r * k + i];
+        hist[i] = 0;
+    }
+    __syncthreads();
+    int ch = 0;
+    const int32_t *pv = prev + (int64_t)r * n;
+    int32_t *lb = lab + (int64_t)r * n;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += 2 * stride) {
+        const int64_t j2 = j + stride;
+        const bool two = j2 < n;
+        const double xa = __ldg(x + j), xb = two ? __ldg(x + j2) : 0.0;
+        const int32_t pa = __ldcs(pv + j), pb = two ? __ldcs(pv + j2) : 0;
+        int ba = 0, bb = 0;
+        double da = d2ref(xa, c[0]), db = d2ref(xb, c[0]);
+        for (int q = 1; q < k; ++q) {
+            const double cq = c[q];
+            const double ea = d2ref(xa, cq), eb = d2ref(xb, cq);
+            if (ea < da) {
+                da = ea;
+                ba = q;
+            }
+            if (eb < db) {
+                db = eb;
+                bb = q;
+            }
+        }
+        __stcs(lb + j, ba);
+        ch += (pa != ba);
+        atomicAdd(&hist[ba], 1);
+        if (two) {
+            __stcs(lb + j2, bb);
+            ch += (pb != bb);
+            atomicAdd(&hist[bb], 1);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+        if (hist[i]) atomicAdd(&cnt[(int64_t)r * k + i], hist[i]);
+    for (int o = 16; o; o >>= 1) ch += __shfl_xor_sync(0xffffffffu, ch, o);
+    if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&changed[r], ch);
+}
+
 // _repair_empty for all restarts with one cooperative grid (used when n is large): the
 // per-empty-cluster argmax over the n own-distances is a grid-wide reduction instead of one
 // CTA's scan, so a repair costs ~n/(SMs x bandwidth) instead of n/(one SM).  Same semantics
@@ -1067,9 +1125,26 @@ __global__ void k_make_keys(int64_t n, int k, const int32_t *__restrict__ lab,
 // the stable sort's (np.add.at order preserved).
 constexpr int kCsTile = 4096, kCsWarps = 8, kCsMaxKeys = 1024;
 
-__device__ __forceinline__ int cs_key(int64_t t, int64_t n, int k, const int32_t *lab,
-                                      const int32_t *act) {
-    const int64_t s = t / n, j = t - s * n;
+// Slot of element t of a tile [t0, t0 + kCsTile): the tile's slots are s0, s0 + 1, ... with
+// boundaries edge, edge + n, ...; walking them replaces a 64-bit division per element (a tile
+// spans one or two slots whenever n >= kCsTile).
+struct CsSlot {
+    int64_t s0, edge;
+    __device__ CsSlot(int64_t t0, int64_t n) : s0(t0 / n), edge((t0 / n + 1) * n) {}
+    __device__ __forceinline__ int64_t slot(int64_t t, int64_t n) const {
+        int64_t s = s0, e = edge;
+        while (t >= e) {
+            ++s;
+            e += n;
+        }
+        return s;
+    }
+};
+
+__device__ __forceinline__ int cs_key(const CsSlot &sl, int64_t t, int64_t n, int k,
+                                      const int32_t *lab, const int32_t *act, int64_t *jout = nullptr) {
+    const int64_t s = sl.slot(t, n), j = t - s * n;
+    if (jout) *jout = j;
     return (int)(s * k + lab[(int64_t)act[s] * n + j]);
 }
 
@@ -1082,8 +1157,9 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs_hist(int64_t m, int64_t n,
     for (int q = threadIdx.x; q < nseg; q += blockDim.x) cs_h[q] = 0;
     __syncthreads();
     const int64_t t0 = (int64_t)blockIdx.x * kCsTile;
+    const CsSlot sl(t0, n);
     for (int64_t t = t0 + threadIdx.x; t < min(m, t0 + kCsTile); t += blockDim.x)
-        atomicAdd(&cs_h[cs_key(t, n, k, lab, act)], 1);
+        atomicAdd(&cs_h[cs_key(sl, t, n, k, lab, act)], 1);
     __syncthreads();
     for (int q = threadIdx.x; q < nseg; q += blockDim.x)
         bh[(int64_t)q * ntiles + blockIdx.x] = cs_h[q];
@@ -1101,7 +1177,8 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs_scatter(
     const int64_t t0 = (int64_t)blockIdx.x * kCsTile;
     constexpr int SUB = kCsTile / kCsWarps;
     const int64_t s0 = t0 + (int64_t)w * SUB, s1 = min(m, s0 + SUB);
-    for (int64_t t = s0 + lane; t < s1; t += 32) atomicAdd(&run[cs_key(t, n, k, lab, act)], 1);
+    const CsSlot sl(t0, n);
+    for (int64_t t = s0 + lane; t < s1; t += 32) atomicAdd(&run[cs_key(sl, t, n, k, lab, act)], 1);
     __syncthreads();
     // exclusive prefix over warps per key, plus the tile's global offset
     for (int q = threadIdx.x; q < nseg; q += blockDim.x) {
@@ -1116,10 +1193,11 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs_scatter(
     for (int64_t b = s0; b < s1; b += 32) {
         const int64_t t = b + lane;
         const bool ok = t < s1;
-        const int key = ok ? cs_key(t, n, k, lab, act) : -1 - lane;
+        int64_t j = 0;
+        const int key = ok ? cs_key(sl, t, n, k, lab, act, &j) : -1 - lane;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
         const int rank = __popc(peers & ((1u << lane) - 1));
-        if (ok) out[run[key] + rank] = x[t - (t / n) * n];
+        if (ok) out[run[key] + rank] = x[j];
         __syncwarp();
         if (ok && rank == 0) run[key] += __popc(peers);  // leader: lowest lane of the group
         __syncwarp();
@@ -1673,9 +1751,12 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     while ((1ll << end_bit) < (long long)rk) ++end_bit;
     const size_t smem_assign = (size_t)k * (8 * l + 4);
     SC_REQUIRE(smem_assign <= 200 * 1024, SC_E_INVALID, "k=%d too large for the assign kernel", k);
-    if (smem_assign > 48 * 1024)
+    if (smem_assign > 48 * 1024) {
         SC_CUDA(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_assign));
+        SC_CUDA(cudaFuncSetAttribute(k_assign1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_assign));
+    }
     const char *smk = getenv("SC_KMEANS_SORTED_MIN_K");
     const int sorted_min_k = smk ? atoi(smk) : kSortedMinK;
     const bool sorted_assign = l == 1 && k >= sorted_min_k && k <= kSortedMaxK &&
@@ -1763,6 +1844,9 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             k_assign_sorted<<<ga, 256, smem_sorted, s>>>(km->d_x, n, k, km->d_scen, km->d_sidx,
                                                          km->d_cmax, d_act, km->d_lab[cur_lab],
                                                          km->d_lab[nxt], km->d_cnt, d_chg);
+        } else if (l == 1) {
+            k_assign1<<<ga, 256, smem_assign, s>>>(km->d_x, n, k, cen_in, d_act, km->d_lab[cur_lab],
+                                                    km->d_lab[nxt], km->d_cnt, d_chg);
         } else {
             k_assign<<<ga, 256, smem_assign, s>>>(km->d_x, n, l, k, cen_in, d_act,
                                                    km->d_lab[cur_lab], km->d_lab[nxt], km->d_cnt,
