@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--no-weighted-probe", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-block sharded (torch.distributed) path even at N=1")
-    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
-                    help="sharded path: NCCL all-gathers, or z stored into the peers' buffers "
-                         "by the SpMV epilogue (CUDA IPC + flag barrier)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p", "halo"],
+                    help="sharded path: NCCL all-gathers, z stored into the peers' buffers "
+                         "by the SpMV epilogue (CUDA IPC + flag barrier), or a halo exchange "
+                         "(only referenced entries, NCCL send/recv)")
     ap.add_argument("--no-graph", action="store_true",
                     help="sharded path: issue every launch from the host (no CUDA graph)")
     ap.add_argument("--pieces", type=int, default=0,

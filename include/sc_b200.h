@@ -177,6 +177,14 @@ int32_t sc_shard_barrier(sc_graph *g, void *stream);
 int32_t sc_ipc_export(const void *dptr, void *handle_out /* 64 bytes */);
 int32_t sc_ipc_import(const void *handle /* 64 bytes */, int32_t device, void **dptr_out);
 int32_t sc_ipc_release(void *dptr);
+/* ---- halo exchange (only the z entries a peer references) -------------------------- */
+/* dst[i] = src[idx[i]] for i < count (device pointers, on `stream`): packs the own z
+ * entries a peer's rows reference into a contiguous send buffer.  Paired with a shard whose
+ * columns are renamed into [own rows | halo entries grouped by owner], the exchange moves
+ * only those entries (ncclSend/ncclRecv) instead of all-gathering z; bit-exact, since no row
+ * or summation order changes. */
+int32_t sc_gather_f64(const double *src, const int32_t *idx, int64_t count, double *dst,
+                      void *stream);
 /* x0 for the shard rows (global ids global_row0..), device output */
 int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x_out,
                             void *stream);

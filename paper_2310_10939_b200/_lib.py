@@ -53,6 +53,7 @@ EXPORTS = (
     "sc_shard_set_peers", "sc_shard_barrier", "sc_ipc_export", "sc_ipc_import", "sc_ipc_release",
     "sc_keyed_sums", "sc_contingency", "sc_cut_sums", "sc_power_iterate_block",
     "sc_kmeans_create_nd", "sc_kmeans_lloyd_sorted", "sc_release_cached_memory",
+    "sc_gather_f64",
 )
 
 _lib = None
@@ -114,6 +115,7 @@ def load() -> ctypes.CDLL:
         "sc_kmeans_create_nd": ([P, i64, i32, i32, PP], i32),
         "sc_kmeans_lloyd_sorted": ([P, i32, i32, P, i32, f64, P, P, P, P], i32),
         "sc_release_cached_memory": ([i32], i64),
+        "sc_gather_f64": ([P, P, i64, P, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -1424,6 +1424,14 @@ int32_t csr_device_arrays(const sc_csr *h, const int64_t **rp, const int32_t **c
 
 }  // namespace sc
 
+// halo pack: dst[i] = src[idx[i]]
+__global__ void k_gather_f64(const double *__restrict__ src, const int32_t *__restrict__ idx,
+                             int64_t count, double *__restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[__ldg(idx + i)];
+}
+
 extern "C" {
 
 int32_t sc_version(void) { return 2; }
@@ -1855,6 +1863,17 @@ int32_t sc_shard_set_peers(sc_graph *g, void *const *z_bases, void *const *flag_
     g->npeer = (int)pz.size();
     g->world = world;
     g->rank = rank;
+    return SC_OK;
+}
+
+int32_t sc_gather_f64(const double *src, const int32_t *idx, int64_t count, double *dst,
+                      void *stream) {
+    SC_REQUIRE(count >= 0, SC_E_INVALID, "negative count");
+    if (count == 0) return SC_OK;
+    SC_REQUIRE(src && idx && dst, SC_E_INVALID, "null argument");
+    const int blocks = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
+    k_gather_f64<<<blocks, 256, 0, (cudaStream_t)stream>>>(src, idx, count, dst);
+    SC_CUDA(cudaGetLastError());
     return SC_OK;
 }
 

@@ -149,6 +149,126 @@ def exchange_plan(local_row_ptr: np.ndarray, starts: np.ndarray, rank: int, worl
     return ShardPlan(starts, perms, n_sells, pieces)
 
 
+class HaloPlan:
+    """z space of one rank for the halo exchange (SURVEY §8(e) option 2): the rank's own rows
+    in renumbered order (slots [0, n)), then the remote entries its rows reference, grouped by
+    owner rank and sorted by global id.  Per step every rank sends each peer only the own
+    entries that peer references (``send_idx``, local renumbered slots, in the peer's halo
+    order) -- at config 5 on 8 GPUs ~19 M entries per GPU instead of the 87.5 M an all-gather
+    delivers.  Columns are only renamed, never reordered, so results stay bit-identical.
+
+    Exposes the ShardPlan attributes CudaShard uses (one piece)."""
+
+    def __init__(self, starts, rank, perm, n_sell, halo_ids, send_idx):
+        self.starts = np.asarray(starts, dtype=np.int64)
+        self.world = self.starts.size - 1
+        self.sizes = np.diff(self.starts)
+        self.n_global = int(self.starts[-1])
+        self.rank = rank
+        n = int(self.sizes[rank])
+        self.n = n
+        self.perms = [None] * self.world
+        self.perms[rank] = np.asarray(perm, dtype=np.int32)
+        self.n_sells = [0] * self.world
+        self.n_sells[rank] = int(n_sell)
+        self.pieces = 1
+        self.bounds = [np.array([0, int(sz)], dtype=np.int64) for sz in self.sizes]
+        self.halo_ids = [np.asarray(h, dtype=np.int64) for h in halo_ids]  # per owner
+        self.send_idx = [np.asarray(h, dtype=np.int32) for h in send_idx]  # per peer
+        cnt = np.array([h.size for h in self.halo_ids], dtype=np.int64)
+        self.halo_off = n + np.concatenate([[0], np.cumsum(cnt)])  # owner q: [off[q], off[q+1])
+        self.n_halo = int(cnt.sum())
+        self.pmax = n
+        self.n_max = int(self.sizes.max())
+        inv = np.empty(n, dtype=np.int64)
+        inv[self.perms[rank]] = np.arange(n, dtype=np.int64)
+        self._inv = inv
+        self._halo_all = (np.concatenate(self.halo_ids) if self.halo_ids
+                          else np.empty(0, dtype=np.int64))
+
+    @property
+    def ncols(self) -> int:
+        return self.n + self.n_halo
+
+    def own(self, j: int, rank: int) -> tuple[int, int]:
+        return 0, self.n
+
+    def rename(self, col_global: np.ndarray) -> np.ndarray:
+        c = np.asarray(col_global, dtype=np.int64)
+        lo, hi = int(self.starts[self.rank]), int(self.starts[self.rank + 1])
+        out = np.empty(c.size, dtype=np.int64)
+        mine = (c >= lo) & (c < hi)
+        out[mine] = self._inv[c[mine] - lo]
+        # halo ids are sorted within each owner and owners are ordered by id range, so the
+        # concatenation is globally sorted
+        out[~mine] = self.n + np.searchsorted(self._halo_all, c[~mine])
+        return out.astype(np.int32)
+
+
+def halo_plans_local(local_row_ptrs, local_cols_global, starts) -> list:
+    """All ranks' HaloPlans computed in one process (single-GPU emulation and tests): the
+    same lists exchange_halo_plan builds with point-to-point messages."""
+    starts = np.asarray(starts, dtype=np.int64)
+    world = starts.size - 1
+    perms, halos = [], []
+    for r in range(world):
+        lo, hi = int(starts[r]), int(starts[r + 1])
+        col = np.asarray(local_cols_global[r], dtype=np.int64)
+        remote = np.unique(col[(col < lo) | (col >= hi)])
+        owner = np.searchsorted(starts, remote, side="right") - 1
+        halos.append([remote[owner == q] for q in range(world)])
+        perms.append(sell_order(local_row_ptrs[r]))
+    plans = []
+    for r in range(world):
+        lo, hi = int(starts[r]), int(starts[r + 1])
+        inv = np.empty(hi - lo, dtype=np.int64)
+        inv[perms[r]] = np.arange(hi - lo, dtype=np.int64)
+        send = [np.empty(0, dtype=np.int32) if q == r else inv[halos[q][r] - lo].astype(np.int32)
+                for q in range(world)]
+        plans.append(HaloPlan(starts, r, perms[r], n_sell_rows(local_row_ptrs[r]), halos[r], send))
+    return plans
+
+
+def exchange_halo_plan(local_row_ptr: np.ndarray, local_col_global: np.ndarray,
+                       starts: np.ndarray, rank: int, world: int, group=None) -> HaloPlan:
+    """Every rank lists the remote vertices its rows reference (per owner), sends each owner
+    its list and receives the lists the peers need from it, translated to its renumbered
+    local slots."""
+    import torch
+    import torch.distributed as dist
+
+    starts = np.asarray(starts, dtype=np.int64)
+    lo, hi = int(starts[rank]), int(starts[rank + 1])
+    perm = sell_order(local_row_ptr)
+    n_sell = n_sell_rows(local_row_ptr)
+    col = np.asarray(local_col_global, dtype=np.int64)
+    remote = np.unique(col[(col < lo) | (col >= hi)])
+    owner = np.searchsorted(starts, remote, side="right") - 1
+    halo_ids = [remote[owner == q] for q in range(world)]
+    dev = _group_device(group)
+    cnt = torch.tensor([h.size for h in halo_ids], dtype=torch.int64, device=dev)
+    all_cnt = [torch.empty(world, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(all_cnt, cnt, group=group)
+    need_from_me = [int(all_cnt[q][rank].item()) for q in range(world)]  # peer q asks me
+    ops, recv = [], [None] * world
+    for q in range(world):
+        if q == rank:
+            continue
+        if halo_ids[q].size:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(halo_ids[q]).to(dev), q, group))
+        if need_from_me[q]:
+            recv[q] = torch.empty(need_from_me[q], dtype=torch.int64, device=dev)
+            ops.append(dist.P2POp(dist.irecv, recv[q], q, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    inv = np.empty(hi - lo, dtype=np.int64)
+    inv[perm] = np.arange(hi - lo, dtype=np.int64)
+    send_idx = [np.empty(0, dtype=np.int32) if recv[q] is None
+                else inv[recv[q].cpu().numpy() - lo].astype(np.int32) for q in range(world)]
+    return HaloPlan(starts, rank, perm, n_sell, halo_ids, send_idx)
+
+
 def _group_device(group):
     import torch
     import torch.distributed as dist
@@ -226,6 +346,12 @@ class CudaShard:
             self.h, int(b[j]), int(b[j + 1]), ctypes.c_void_p(z_in.data_ptr()),
             ctypes.c_void_p(x_in.data_ptr()), ctypes.c_void_p(x_out.data_ptr()),
             self._zout(z_out, j), float(sign), _lib.SC_SYM_VARIANT if sym else 0, self._stream()))
+
+    def pack(self, z_full, idx, out):
+        """out[i] = z_full[idx[i]] (idx: int32 device tensor) -- the halo send buffer"""
+        _lib.check(_lib.load().sc_gather_f64(ctypes.c_void_p(z_full.data_ptr()),
+                                             ctypes.c_void_p(idx.data_ptr()), int(idx.numel()),
+                                             ctypes.c_void_p(out.data_ptr()), self._stream()))
 
     def local_z(self, z_full):
         """this rank's z entries (renumbered local order) as a host array"""
@@ -372,6 +498,49 @@ class PieceComm:
             self.torch.cuda.current_stream().wait_stream(self.side)
 
 
+class HaloComm:
+    """Halo exchange per step (SURVEY §8(e) option 2): pack the own z entries each peer
+    references (sc_gather_f64) and move them with one batch of point-to-point sends/receives
+    straight into the peers' halo slots.  Pieces are not used (one exchange per step)."""
+
+    def __init__(self, shard, plan: HaloPlan, rank: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.shard, self.plan, self.rank, self.group = shard, plan, rank, group
+        self.nccl = dist.get_backend(group) == "nccl"
+        dev = _group_device(group)
+        self.peers = [q for q in range(plan.world) if q != rank and
+                      (plan.send_idx[q].size or plan.halo_ids[q].size)]
+        self.idx = {q: torch.from_numpy(plan.send_idx[q]).to(dev) for q in self.peers}
+        self.sbuf = {q: torch.empty(plan.send_idx[q].size, dtype=torch.float64, device=dev)
+                     for q in self.peers}
+
+    def gather_piece(self, z_full, j):
+        dist, plan = self.dist, self.plan
+        ops = []
+        for q in self.peers:
+            if self.sbuf[q].numel():
+                self.shard.pack(z_full, self.idx[q], self.sbuf[q])
+                ops.append(dist.P2POp(dist.isend, self.sbuf[q], q, self.group))
+            a, b = int(plan.halo_off[q]), int(plan.halo_off[q + 1])
+            if b > a:
+                ops.append(dist.P2POp(dist.irecv, z_full[a:b], q, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def finish(self):
+        pass
+
+    def recv_bytes(self) -> int:
+        return 8 * self.plan.n_halo
+
+    def close(self):
+        pass
+
+
 class ShardedPower:
     """T pipelined steps over a shard with buffers allocated once.  With NCCL the whole
     T-step sequence (per-piece SpMVs, side-stream all-gathers and their event fork/joins) can
@@ -386,9 +555,12 @@ class ShardedPower:
         if comm is None:
             self.comm = PieceComm(plan, rank, group)
             self.z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
-        else:  # fused peer exchange: z lives in the handle's mirrored allocation
+        elif hasattr(comm, "z0"):  # fused peer exchange: z lives in the mirrored allocation
             self.comm = comm
             self.z = [comm.z0, comm.z1]
+        else:  # halo exchange
+            self.comm = comm
+            self.z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
         self.x = [shard.zeros(n), shard.zeros(n)]
         self.x0 = shard.zeros(n)
         self.graph = None
@@ -478,19 +650,23 @@ def bench_main(args, metric: str, unit: str):
                        q=4 / (world * n_loc - 10**5), seed=0)
     T = 100
     p2p = getattr(args, "comm", "nccl") == "p2p"
+    halo = getattr(args, "comm", "nccl") == "halo"
     # Splitting a step into P pieces costs ~12 us per extra piece on one B200 (smaller grids,
     # one more collective) and hides up to (P-1)/P of the all-gather, which moves
     # (W-1) * 8 MB per GPU per step (~12 us at W = 2, ~80 us at W = 8 over NVLink): only
     # worth it for the widest runs.
     default_pieces = 2 if world >= 8 else 1
-    pieces = 1 if p2p else int(getattr(args, "pieces", 0) or default_pieces)
+    pieces = 1 if (p2p or halo) else int(getattr(args, "pieces", 0) or default_pieces)
     starts = np.arange(world + 1, dtype=np.int64) * n_loc
     rp, col, deg, iso = sbm_rows(params, int(starts[rank]), int(starts[rank + 1]))
     iso_t = torch.tensor([iso], device="cuda")
     dist.all_reduce(iso_t)
     if int(iso_t.item()):
         raise InputError("isolated vertices in the scaling graph; choose another seed")
-    plan = exchange_plan(rp, starts, rank, world, pieces=pieces)
+    if halo:
+        plan = exchange_halo_plan(rp, col, starts, rank, world)
+    else:
+        plan = exchange_plan(rp, starts, rank, world, pieces=pieces)
     shard = CudaShard(rp, plan.rename(col), None, deg, plan, rank, local)
     nnz_t = torch.tensor([int(rp[-1])], device="cuda", dtype=torch.int64)
     dist.all_reduce(nnz_t)
@@ -500,6 +676,8 @@ def bench_main(args, metric: str, unit: str):
     if p2p:
         comm = P2PComm(shard, plan, rank)
         comm.link()
+    elif halo:
+        comm = HaloComm(shard, plan, rank)
     runner = ShardedPower(shard, plan, rank, comm=comm)
     use_graph = not getattr(args, "no_graph", False)
 
@@ -535,9 +713,9 @@ def bench_main(args, metric: str, unit: str):
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     tot_ms = float(ms.item())
-    # the all-gathers alone (NVLink): T steps x P pieces
+    # the exchange alone (NVLink): T steps x P pieces
     zbuf = shard.zeros(plan.ncols)
-    agc = PieceComm(plan, rank)
+    agc = comm if halo else PieceComm(plan, rank)
     torch.cuda.synchronize()
     dist.barrier()
     e0.record(stream)
@@ -550,7 +728,7 @@ def bench_main(args, metric: str, unit: str):
     ag = torch.tensor([e0.elapsed_time(e1) / T], device="cuda", dtype=torch.float64)
     dist.all_reduce(ag, op=dist.ReduceOp.MAX)
     ag_ms = float(ag.item())
-    recv_bytes = (world - 1) * plan.pieces * plan.pmax * 8
+    recv_bytes = comm.recv_bytes() if halo else (world - 1) * plan.pieces * plan.pmax * 8
     if rank == 0:
         value = nnz_total * T * args.steps / (tot_ms / 1e3) / 1e9
         line = {
@@ -559,16 +737,24 @@ def bench_main(args, metric: str, unit: str):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config2 block per GPU (SBM n={params.n}, k={params.k})",
                        "n_per_gpu": n_loc, "nnz_total": nnz_total, "T": T, "pieces": plan.pieces,
-                       "cuda_graph": use_graph, "comm": "p2p" if p2p else "nccl",
+                       "cuda_graph": use_graph,
+                       "comm": "p2p" if p2p else "halo" if halo else "nccl",
                        "parallelism": (f"row-block shards x{world}, z stored into the peers' "
                                        "buffers by the SpMV epilogue + flag barrier"
                                        if p2p else
+                                       f"row-block shards x{world}, halo exchange (packed "
+                                       "referenced entries, NCCL send/recv)"
+                                       if halo else
                                        f"row-block shards x{world}, pipelined NCCL all-gather "
                                        f"of z ({plan.pieces} pieces per step)")},
-            "allgather": {"ms_per_step": ag_ms, "recv_bytes_per_gpu": recv_bytes,
-                          "gbs_per_gpu": recv_bytes / (ag_ms / 1e3) / 1e9 if world > 1 else 0.0},
+            "exchange": {"kind": "halo send/recv" if halo else "all-gather",
+                         "ms_per_step": ag_ms, "recv_bytes_per_gpu": recv_bytes,
+                         "gbs_per_gpu": recv_bytes / (ag_ms / 1e3) / 1e9 if world > 1 else 0.0},
             "gpu_launches": args.steps * (1 + (T + 1) * plan.pieces
-                                          + ((T + 1) if p2p and world > 1 else 0)),
+                                          + ((T + 1) if p2p and world > 1 else 0)
+                                          + ((T + 1) * sum(1 for q in comm.peers
+                                                           if comm.sbuf[q].numel())
+                                             if halo else 0)),
         }
         print(json.dumps(line), flush=True)
     if comm is not None:

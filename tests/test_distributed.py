@@ -60,6 +60,9 @@ class OracleShard:
         x_out[lo:hi] = self.torch.from_numpy(y)
         z_out[o:o + hi - lo] = self.torch.from_numpy(zo)
 
+    def pack(self, z_full, idx, out):
+        out.copy_(z_full[idx.long()])
+
     def local_z(self, z_full):
         parts = []
         for j in range(self.plan.pieces):
@@ -102,6 +105,68 @@ def _worker(rank, world, port, graph, T, result_path, pieces=1):
     if rank == 0:
         np.savez(result_path, x=x_all, f=f_all, starts=starts)
     dist.destroy_process_group()
+
+
+def _halo_worker(rank, world, port, graph, T, result_path):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rp, col, val, deg = graph
+    starts = D.partition_rows(rp, world)
+    lo, hi = int(starts[rank]), int(starts[rank + 1])
+    lrp = rp[lo:hi + 1] - rp[lo]
+    lcol = col[rp[lo]:rp[hi]]
+    lval = None if val is None else val[rp[lo]:rp[hi]]
+    plan = D.exchange_halo_plan(lrp, lcol, starts, rank, world)
+    shard = OracleShard(lrp, lcol, lval, deg[lo:hi], plan, rank, lo)
+    runner = D.ShardedPower(shard, plan, rank, comm=D.HaloComm(shard, plan, rank))
+    runner.sample(3)
+    xT, z = runner.run(T)
+    x_all = D.gather_to_rank0(shard.to_original(xT), plan, rank)
+    f_all = D.gather_to_rank0(shard.to_original(shard.local_z(z)), plan, rank)
+    if rank == 0:
+        np.savez(result_path, x=x_all, f=f_all, halo=plan.n_halo, ncols=plan.ncols)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_power_iteration_bit_exact(tmp_path, world):
+    """Halo exchange (only referenced remote z entries move, point to point) is bit-exact."""
+    import torch.multiprocessing as mp
+
+    g = _weighted_graph()
+    graph = (g.row_offsets, g.col_indices.astype(np.int32), g.weights, g.degrees)
+    T = 9
+    out = str(tmp_path / "halo.npz")
+    mp.start_processes(_halo_worker, args=(world, _free_port(), graph, T, out), nprocs=world,
+                       join=True, start_method="spawn")
+    res = np.load(out)
+    x0 = O.irwin_hall(g.degrees, 3)
+    xT, f = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, T)
+    assert np.array_equal(res["x"], xT)
+    assert np.array_equal(res["f"], f)
+    assert 0 < int(res["halo"]) < g.n
+
+
+def test_halo_plans_local_match_distributed_lists():
+    """halo_plans_local: every rank's send list is exactly the peer's halo request, in order."""
+    g = _weighted_graph(n=2000, m=15000, seed=5)
+    rp, col = g.row_offsets, g.col_indices.astype(np.int64)
+    starts = D.partition_rows(rp, 3)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(3)]
+    lcols = [col[rp[starts[r]]:rp[starts[r + 1]]] for r in range(3)]
+    plans = D.halo_plans_local(lrps, lcols, starts)
+    for r, pl in enumerate(plans):
+        ren = pl.rename(lcols[r])
+        assert ren.min() >= 0 and ren.max() < pl.ncols
+        for q in range(3):
+            if q == r:
+                continue
+            # the ids q sends to r, mapped back through q's renumbering, are r's halo ids from q
+            sent = plans[q].perms[q][plans[q].send_idx[r]] + starts[q]
+            assert np.array_equal(sent, pl.halo_ids[q])
 
 
 def _weighted_graph(n=3000, m=30000, seed=11):

@@ -76,6 +76,56 @@ def test_shards_on_one_gpu_bit_exact(world, pieces):
         s.close()
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_halo_shards_on_one_gpu_bit_exact(world):
+    """Halo layout (own rows + referenced remote entries) on the CUDA shard kernels, the
+    exchange emulated by sc_gather_f64 packs copied into the peers' halo slots."""
+    import torch
+
+    g = _graph()
+    rp, col, val, deg = g.row_offsets, g.col_indices.astype(np.int32), g.weights, g.degrees
+    starts = D.partition_rows(rp, world)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(world)]
+    lcols = [col[rp[starts[r]]:rp[starts[r + 1]]] for r in range(world)]
+    plans = D.halo_plans_local(lrps, lcols, starts)
+    shards = [D.CudaShard(lrps[r], plans[r].rename(lcols[r]), val[rp[starts[r]]:rp[starts[r + 1]]],
+                          deg[starts[r]:starts[r + 1]], plans[r], r, 0) for r in range(world)]
+    z = [[s.zeros(plans[r].ncols), s.zeros(plans[r].ncols)] for r, s in enumerate(shards)]
+    x = [[s.zeros(s.n), s.zeros(s.n)] for s in shards]
+    x0 = [s.zeros(s.n) for s in shards]
+    idx = [[torch.from_numpy(plans[q].send_idx[r]).cuda() for r in range(world)] for q in range(world)]
+
+    def exchange(b):
+        for r in range(world):
+            for q in range(world):
+                if q == r or idx[q][r].numel() == 0:
+                    continue
+                buf = shards[q].zeros(idx[q][r].numel())
+                shards[q].pack(z[q][b], idx[q][r], buf)
+                a, e = int(plans[r].halo_off[q]), int(plans[r].halo_off[q + 1])
+                z[r][b][a:e].copy_(buf)
+        torch.cuda.synchronize()
+
+    T = 12
+    for r, s in enumerate(shards):
+        s.irwin_hall(5, x0[r])
+        s.scale_piece(0, x0[r], z[r][0])
+    exchange(0)
+    for t in range(T):
+        a, b = t & 1, (t & 1) ^ 1
+        for r, s in enumerate(shards):
+            s.step_piece(0, z[r][a], x0[r] if t == 0 else x[r][a], x[r][b], z[r][b])
+        exchange(b)
+    xs = np.concatenate([s.to_original(x[r][T & 1]) for r, s in enumerate(shards)])
+    fs = np.concatenate([s.to_original(s.local_z(z[r][T & 1])) for r, s in enumerate(shards)])
+    xT, f = O.power_iterate(rp, col, val, deg, O.irwin_hall(deg, 5), T)
+    assert np.array_equal(xs, xT)
+    assert np.array_equal(fs, f)
+    assert all(p.n_halo <= p.n_global - p.n for p in plans)  # never more than an all-gather
+    for s in shards:
+        s.close()
+
+
 def _nccl_world1_worker(rank, path, out):
     import torch
     import torch.distributed as dist
