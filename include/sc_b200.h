@@ -53,6 +53,7 @@ extern "C" {
 #define SC_NO_CUDA_GRAPH 0x2u  /* launch T kernels instead of replaying a captured graph */
 #define SC_L2_PERSIST 0x4u     /* pin the gathered z vector in L2 (access-policy window) */
 #define SC_FORCE_WEIGHTED 0x8u /* use the weighted kernel even if all weights are 1.0 */
+#define SC_FORCE_SELL 0x10u    /* use the SELL kernel even if the handle has a panel layout */
 
 typedef struct sc_graph sc_graph;
 typedef struct sc_kmeans sc_kmeans;
@@ -70,6 +71,8 @@ typedef struct sc_graph_info {
     int32_t device;
     int32_t sm_count;
     int64_t stored_entries; /* SELL-32 entries incl. padding (+ wide-row entries excluded) */
+    int64_t panel_groups;   /* column-panel layout: stages (0 = no panel layout) */
+    int64_t panel_bytes;    /* column-panel layout: bytes streamed per step */
 } sc_graph_info;
 
 typedef struct sc_timing {
@@ -100,6 +103,11 @@ int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double
  * around every 4096th vertex, by level) before the SELL layout, for graphs whose ids carry no
  * locality; exact (only where z values live changes), whole graphs only */
 #define SC_CREATE_REORDER_BFS 0x4u
+/* column-panel layout in addition to SELL (unit weights, no rows > 256 entries, whole graphs):
+ * each 3392-row block's heavily referenced 8192-column ranges are staged in shared memory
+ * and gathered there, the rest from L2; bit-identical results.  Declined silently when the
+ * graph does not qualify (sc_graph_info.panel_groups == 0). */
+#define SC_CREATE_PANELS 0x8u
 int32_t sc_graph_create_ex(const int64_t *row_ptr, const int32_t *col, const double *val,
                            const double *deg, int64_t n, int64_t nnz, int32_t device,
                            uint32_t create_flags, sc_graph **out);

@@ -22,9 +22,11 @@ SC_SYM_VARIANT = 0x1
 SC_NO_CUDA_GRAPH = 0x2
 SC_L2_PERSIST = 0x4
 SC_FORCE_WEIGHTED = 0x8
+SC_FORCE_SELL = 0x10
 SC_CREATE_KEEP_WEIGHTS = 0x1
 SC_CREATE_FP32_VALUES = 0x2
 SC_CREATE_REORDER_BFS = 0x4
+SC_CREATE_PANELS = 0x8
 
 
 class GraphInfo(ctypes.Structure):
@@ -34,6 +36,7 @@ class GraphInfo(ctypes.Structure):
         ("unit_weights", ctypes.c_int32), ("rp64", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
         ("device", ctypes.c_int32), ("sm_count", ctypes.c_int32),
         ("stored_entries", ctypes.c_int64),
+        ("panel_groups", ctypes.c_int64), ("panel_bytes", ctypes.c_int64),
     ]
 
 

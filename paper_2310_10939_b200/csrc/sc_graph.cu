@@ -701,6 +701,10 @@ __global__ void k_fill_wide(const int64_t *__restrict__ rp, const int32_t *__res
 
 using namespace sc;
 
+namespace sc {
+struct PanGroup;
+}
+
 struct sc_graph {
     int device = 0;
     int sm_count = 0;
@@ -742,6 +746,13 @@ struct sc_graph {
     double **d_peer_z = nullptr;        // npeer peer z-allocation bases
     uint32_t **d_peer_flags = nullptr;  // world peer flag arrays (own slot unused)
     int npeer = 0, world = 1, rank = 0;
+    // column-panel layout (sc_panel.cuh; SC_CREATE_PANELS), used for whole-graph steps
+    int pan_ctas = 0, pan_slot = 0, pan_groups = 0, pan_rpc = 0;
+    int64_t pan_bytes = 0;
+    int32_t *d_pan_blk = nullptr;
+    sc::PanGroup *d_pan_grp = nullptr;
+    uint8_t *d_pan_stream = nullptr;
+    int64_t zstride = 0;  // d_z[1] - d_z[0] (ncols, rounded up to 32 for whole graphs)
 };
 
 namespace sc {
@@ -985,6 +996,8 @@ static cudaError_t reorder_bfs(sc_graph *g, cudaStream_t s, const int64_t *rp, c
     return e;
 }
 
+#include "sc_panel.cuh"  // (inside namespace sc)
+
 // col == nullptr with dcol != nullptr: the column array is already on `device` (borrowed,
 // e.g. from sc_generate_sbm) and is neither copied nor freed.
 static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const double *val,
@@ -1186,14 +1199,18 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     }
     // both z buffers in one allocation so one L2 access-policy window covers them
     double *zz = nullptr;
-    if ((st = dmalloc(g, (void **)&zz, (size_t)ncols * 16))) {
+    // whole graphs: z[1] 256-byte aligned (bulk copies of panels need 16-byte alignment), a
+    // zero slot z[ncols] in both buffers (padding target of the panel layout), and 64 bytes of
+    // slack after z[1] (the last panel copy is rounded up to 16 bytes)
+    g->zstride = rename ? (ncols + 32) & ~(int64_t)31 : ncols;
+    if ((st = dmalloc(g, (void **)&zz, (size_t)g->zstride * 16 + 64))) {
         cudaStreamSynchronize(s2);
         free_tmp();
         return cleanup(st);
     }
     g->d_z[0] = zz;
-    g->d_z[1] = zz + ncols;
-    e = cudaMemsetAsync(zz, 0, (size_t)ncols * 16, s);
+    g->d_z[1] = zz + g->zstride;
+    e = cudaMemsetAsync(zz, 0, (size_t)g->zstride * 16 + 64, s);
     size_t cb = 0, cb2 = 0;
     // (a heavy-tailed graph is sorted by length globally, which would undo any pre-order)
     if (!e && (cflags & SC_CREATE_REORDER_BFS) && sigma < n) {
@@ -1276,6 +1293,10 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         fail(SC_E_CUDA, "graph layout: %s", cudaGetErrorString(e));
         return cleanup(SC_E_CUDA);
     }
+    if ((cflags & SC_CREATE_PANELS) && rename) {
+        if ((st = build_panels(g, prof))) return cleanup(st);
+        lap("panel layout");
+    }
     *out = g;
     return SC_OK;
 }
@@ -1295,6 +1316,9 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
                            cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = -1) {
     const bool sym = flags & SC_SYM_VARIANT;
     if (row_hi < 0) row_hi = g->n;
+    // whole-graph steps use the column-panel layout when the handle has one
+    const bool panel = g->pan_ctas && !(flags & SC_FORCE_SELL) && row_lo == 0 && row_hi == g->n &&
+                       g->npeer == 0;
     StepArgs a;
     a.slice_lo = std::min(row_lo, g->n_sell) / kSlice;
     a.slice_hi = (std::min(row_hi, g->n_sell) + kSlice - 1) / kSlice;
@@ -1328,6 +1352,10 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
                    "peer exchange needs z_out inside the handle's z buffers (sc_shard_buffers)");
         a.npeer = g->npeer;
         a.peer_off = z_out - g->d_z[0];
+    }
+    if (panel) {
+        SC_CUDA(launch_panel_step(g, a, sym, s));
+        return SC_OK;
     }
     constexpr int wpb = kStepTPB / 32;
     a.wide_blocks = (int)((a.wide_hi - a.wide_lo + wpb - 1) / wpb);
@@ -1393,7 +1421,7 @@ static void set_l2_window(sc_graph *g, bool on) {
         int maxwin = 0, maxpersist = 0;
         cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
         cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
-        size_t bytes = (size_t)g->ncols * 16;
+        size_t bytes = (size_t)g->zstride * 16;
         size_t win = std::min<size_t>(bytes, (size_t)maxwin);
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, maxpersist));
         attr.accessPolicyWindow.base_ptr = g->d_z[0];
@@ -1545,6 +1573,8 @@ int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *o) {
     o->device_bytes = g->bytes;
     o->device = g->device;
     o->sm_count = g->sm_count;
+    o->panel_groups = g->pan_ctas ? g->pan_groups : 0;
+    o->panel_bytes = g->pan_ctas ? g->pan_bytes : 0;
     o->stored_entries = g->sell_entries;
     return SC_OK;
 }

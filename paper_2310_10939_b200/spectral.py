@@ -108,8 +108,11 @@ class DeviceGraph:
     layout; degrees copied verbatim, never recomputed)."""
 
     def __init__(self, graph, device: int = 0, keep_weights: bool = False,
-                 fp32_values: bool = False, reorder: str | None = None):
-        """``fp32_values``: store the weights as fp32 (the optional fp32-value variant:
+                 fp32_values: bool = False, reorder: str | None = None, panels: bool = False):
+        """``panels``: also build the column-panel layout (sc_panel.cuh; unit weights and rows
+        of <= 256 entries only, declined silently otherwise -- see ``info()['panel_groups']``);
+        whole-graph steps then stage heavily referenced column ranges in shared memory.
+        ``fp32_values``: store the weights as fp32 (the optional fp32-value variant:
         half the weight bytes, results within 1e-5 relative of fp64; unit-weight graphs are
         unaffected).  ``reorder="bfs"``: renumber the vertices by a multi-source BFS before the
         SELL layout (locality for graphs whose ids carry none; results unchanged)."""
@@ -139,21 +142,23 @@ class DeviceGraph:
                                         _lib.ptr(self._deg), g.n, g.nnz, device,
                                         (_lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0)
                                         | (_lib.SC_CREATE_FP32_VALUES if fp32_values else 0)
-                                        | (_lib.SC_CREATE_REORDER_BFS if reorder == "bfs" else 0),
+                                        | (_lib.SC_CREATE_REORDER_BFS if reorder == "bfs" else 0)
+                                        | (_lib.SC_CREATE_PANELS if panels else 0),
                                         ctypes.byref(h)))
         self._h = h
         self.device = device
         self.last_timing = None
 
     @classmethod
-    def from_device_csr(cls, csr, keep_weights: bool = False) -> "DeviceGraph":
+    def from_device_csr(cls, csr, keep_weights: bool = False, panels: bool = False) -> "DeviceGraph":
         """Graph handle straight from a device-resident CSR (``generate.DeviceCSR``): the
         column array never visits the host (sc_graph_create_from_csr)."""
         L = _lib.require_device()
         self = cls.__new__(cls)
         h = ctypes.c_void_p()
         _lib.check(L.sc_graph_create_from_csr(csr.handle,
-                                              _lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0,
+                                              (_lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0)
+                                              | (_lib.SC_CREATE_PANELS if panels else 0),
                                               ctypes.byref(h)))
         self._h = h
         self.graph = None
@@ -210,12 +215,14 @@ class DeviceGraph:
     # -- power iteration
     def power_iterate(self, t: int, *, sign: float = 1.0, sym: bool = False,
                       want_x: bool = True, want_f: bool = True, cuda_graph: bool = True,
-                      l2_persist: bool = False, force_weighted: bool = False):
+                      l2_persist: bool = False, force_weighted: bool = False,
+                      force_sell: bool = False):
         if t < 0:
             raise InputError(f"power method step count must be >= 0, got {t}")
         flags = ((_lib.SC_SYM_VARIANT if sym else 0) | (0 if cuda_graph else _lib.SC_NO_CUDA_GRAPH)
                  | (_lib.SC_L2_PERSIST if l2_persist else 0)
-                 | (_lib.SC_FORCE_WEIGHTED if force_weighted else 0))
+                 | (_lib.SC_FORCE_WEIGHTED if force_weighted else 0)
+                 | (_lib.SC_FORCE_SELL if force_sell else 0))
         xT = np.empty(self.n) if want_x else None
         f = np.empty(self.n) if want_f else None
         tm = _lib.Timing()

@@ -1,5 +1,5 @@
 """Profiling driver: config-2 power iteration without CUDA graphs (so ncu sees each
-kernel launch), a few iterations.  Usage: python tools/prof_spmv.py [T] [--weighted] [--cfg N]"""
+kernel launch), a few iterations.  Usage: python tools/prof_spmv.py [T] [--weighted] [--panels] [--cfg N]"""
 import os
 import sys
 import time
@@ -12,6 +12,7 @@ from paper_2310_10939_b200.generate import config_sbm, sample_sbm  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 4
 weighted = "--weighted" in sys.argv
+panels = "--panels" in sys.argv
 cfg = 2
 if "--cfg" in sys.argv:
     cfg = int(sys.argv[sys.argv.index("--cfg") + 1])
@@ -20,7 +21,7 @@ import bench  # noqa: E402
 
 g, _, _ = bench.build_config(cfg)
 print(f"graph n={g.n} nnz={g.nnz} in {time.time()-t:.1f}s", flush=True)
-dg = DeviceGraph(g, keep_weights=weighted)
+dg = DeviceGraph(g, keep_weights=weighted, panels=panels)
 dg.sample_irwin_hall(0)
 for rep in range(2):
     dg.power_iterate(T, cuda_graph=False, want_x=False, want_f=False, force_weighted=weighted)
