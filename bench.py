@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--weighted", action="store_true",
                     help="force the weighted kernel (reads val even for unit weights)")
     ap.add_argument("--no-weighted-probe", action="store_true")
+    ap.add_argument("--sell", action="store_true",
+                    help="measure the SELL kernel even where the column-panel layout applies")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-block sharded (torch.distributed) path even at N=1")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p", "halo"],
@@ -145,14 +147,14 @@ def peak_hbm():
     return 6650.0, "fallback"
 
 
-def traffic_from_profiles(cfg: int, unit: bool):
+def traffic_from_profiles(cfg: int, unit: bool, layout: str = "sell"):
     """dram bytes per launch of the SpMV kernel from the committed ncu summary (or None)."""
     p = os.path.join(ROOT, "profiles", "spmv_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
         d = json.load(fh)
-    return d.get(f"c{cfg}_{'unit' if unit else 'weighted'}")
+    return d.get(f"c{cfg}_{'unit' if unit else 'weighted'}" + ("_panels" if layout == "panels" else ""))
 
 
 def cpu_path_step(g, T, k, threads):
@@ -252,6 +254,8 @@ def roofline_for(g, info, kernel_ms, reads_val: bool):
     alg = nnz * idx_val + 16 * n
     stored = int(info.get("stored_entries") or nnz)
     compulsory = stored * idx_val + n * (8 + 8 + 8 + 8 + 8)
+    if info.get("panel_groups"):  # column-panel layout: its stage stream replaces the SELL arrays
+        compulsory = int(info["panel_bytes"]) + n * (8 + 8 + 8 + 8 + 8)
     peak, peak_kind = peak_hbm()
     achieved = alg / (kernel_ms / 1e3) / 1e9
     r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -290,8 +294,12 @@ def run_b200(args):
 
     g, T, k = build_config(args.config)
     unit = g.unit_weights() and not args.weighted
-    dev = DeviceGraph(g, keep_weights=args.weighted, reorder="auto")  # as fast_spectral_cluster
+    # as fast_spectral_cluster: locality pre-order "auto", column panels for T >= 64 (declined
+    # by the library when the graph does not qualify)
+    dev = DeviceGraph(g, keep_weights=args.weighted, reorder="auto",
+                      panels=not args.sell and T >= 64)
     info = dev.info()
+    layout = "panels" if info["panel_groups"] else "sell"
     dev_reorder = dev.reorder or "none"
     dev.sample_irwin_hall(0)
     times, clocks = time_power(dev, T, args.steps, args.warmup, clocks=True)
@@ -299,7 +307,8 @@ def run_b200(args):
     value = g.nnz * T * args.steps / (tot_ms / 1e3) / 1e9
     kernel_ms = tot_ms / (args.steps * T)
     roofline = roofline_for(g, info, kernel_ms, reads_val=not unit)
-    roofline["traffic"] = traffic_from_profiles(args.config, unit)
+    roofline["traffic"] = traffic_from_profiles(args.config, unit, layout)
+    roofline["layout"] = layout
     dev.close()
     # the same graph through the weighted kernel (weights streamed even though all 1.0):
     # the north-star byte formula nnz*(idx+val) applies to this one
@@ -312,7 +321,7 @@ def run_b200(args):
             wk = sum(wt) / (len(wt) * T)
             weighted = {"value": g.nnz * T / (sum(wt) / len(wt) / 1e3) / 1e9, "unit": UNIT,
                         "kernel_ms": wk, "roofline": roofline_for(g, iw, wk, reads_val=True)}
-            weighted["roofline"]["traffic"] = traffic_from_profiles(args.config, False)
+            weighted["roofline"]["traffic"] = traffic_from_profiles(args.config, False, "sell")
     # ---- end to end through the public API, pinned host buffers
     gp = Graph(n=g.n, row_offsets=pinned_copy(g.row_offsets), col_indices=pinned_copy(g.col_indices),
                weights=None if g.weights is None else pinned_copy(g.weights),
@@ -354,7 +363,7 @@ def run_b200(args):
         "config": {"workload": f"config{args.config}",
                    "graph": GRAPH_DESC.get(args.config, "synthetic"),
                    "n": n, "nnz": g.nnz, "T": T, "k": k, "unit_weight_kernel": unit,
-                   "layout_preorder": dev_reorder,
+                   "layout_preorder": dev_reorder, "spmv_layout": layout,
                    "l2": "inputs larger than L2 (CSR streamed per iteration >= 0.2 GB)",
                    "parallelism": "single GPU"},
         "roofline": roofline,
@@ -367,7 +376,7 @@ def run_b200(args):
         "gpu_launches": args.steps * (T + 1),
         "clocks": clocks,
         "graph_info": {k_: info[k_] for k_ in ("ntiles", "long_rows", "stored_entries",
-                                               "device_bytes")},
+                                               "device_bytes", "panel_groups", "panel_bytes")},
     }
     if weighted:
         line["weighted_kernel"] = weighted

@@ -35,6 +35,7 @@ constexpr int kPanGMax = 48;       // groups per CTA
 constexpr int kPanCMax = 128;      // entries per segment (exclusive bound)
 constexpr int kPanThresh = 1024;   // entries of a CTA in a panel that make it dense
 constexpr double kPanMinCover = 0.5;  // fraction of entries in dense panels the layout needs
+constexpr double kPanMinSegment = 2.5;  // mean entries per dense segment it needs
 constexpr int kPanSMax = 16384;    // panels (n <= 134M)
 constexpr int kPanTPB = 1024;
 constexpr int kPanZBytes = 2 * (kPanZ + 16) * 8;
@@ -284,7 +285,8 @@ struct PanPlanQ {
 
 // Per CTA: panel histogram -> groups -> segment histogram per (group, count) -> stage sizes.
 // flag[0] |= 1 (too many groups), 2 (segment longer than kPanCMax - 1), 4 (stage > slot cap);
-// flag[1] = max stage bytes; cover[0] / cover[1] += entries in dense panels / all entries.
+// flag[1] = max stage bytes; cover[0] / cover[1] / cover[2] += entries in dense panels / all
+// entries / dense segments.
 __global__ void __launch_bounds__(kPanTPB) k_pan_plan(const int64_t *slice_ptr, const uint32_t *col,
                                                       int64_t n, int S, int rpc, uint32_t slot_cap,
                                                       int32_t *cta_ng, PanPlan *plan, PanPlanQ *planq,
@@ -385,6 +387,7 @@ __global__ void __launch_bounds__(kPanTPB) k_pan_plan(const int64_t *slice_ptr, 
             pos += h;
         }
         const uint32_t nq = (pos + 31) / 32;
+        if (gt[g].dense) atomicAdd(&cover[2], (unsigned long long)pos);
         const uint32_t esz = gt[g].dense ? 2 : 4;
         const uint32_t roff = (4 * nq + 15) & ~15u;
         const uint32_t eoff = roff + ((64 * nq + 15) & ~15u);
@@ -565,28 +568,30 @@ static int32_t build_panels_rpc(sc_graph *g, bool prof, int rpc, int32_t *declin
     e = cudaFuncSetAttribute(k_pan_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_plan);
     if (!e) e = cudaFuncSetAttribute(k_pan_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_plan);
     if (!e) e = cudaMallocAsync((void **)&cta_ng, (size_t)(ncta + 1) * 4, s);
-    if (!e) e = cudaMallocAsync((void **)&flag, 32, s);
+    if (!e) e = cudaMallocAsync((void **)&flag, 64, s);
     if (!e) e = cudaMallocAsync((void **)&plan, (size_t)ncta * kPanGMax * sizeof(PanPlan), s);
     if (!e) e = cudaMallocAsync((void **)&planq, (size_t)ncta * kPanGMax * sizeof(PanPlanQ), s);
-    if (!e) e = cudaMemsetAsync(flag, 0, 32, s);
+    if (!e) e = cudaMemsetAsync(flag, 0, 64, s);
     if (!e) e = cudaMemsetAsync(cta_ng + ncta, 0, 4, s);
     if (!e) {
         k_pan_plan<<<ncta, kPanTPB, smem_plan, s>>>(g->d_slice_ptr, g->d_col, n, S, rpc, slot_cap, cta_ng,
-                                                    plan, planq, flag, (unsigned long long *)(flag + 4));
+                                                    plan, planq, flag, (unsigned long long *)(flag + 8));
         e = cudaGetLastError();
     }
-    int32_t hflag[8] = {0};
-    if (!e) e = cudaMemcpyAsync(hflag, flag, 32, cudaMemcpyDeviceToHost, s);
+    int32_t hflag[16] = {0};
+    if (!e) e = cudaMemcpyAsync(hflag, flag, 64, cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
     if (e) {
         cleanup();
         return fail(SC_E_CUDA, "panel plan: %s", cudaGetErrorString(e));
     }
     // the layout pays off only when most entries fall into dense panels (graphs whose ids
-    // carry no locality stay on SELL)
-    unsigned long long cover[2];
-    memcpy(cover, hflag + 4, 16);
+    // carry no locality stay on SELL) and dense segments are long enough to amortise the
+    // partial-sum round trip through shared memory (config 5: 1.3 entries -> SELL is faster)
+    unsigned long long cover[3];
+    memcpy(cover, hflag + 8, 24);
     if (!hflag[0] && cover[0] < kPanMinCover * cover[1]) hflag[0] = 16;
+    if (!hflag[0] && cover[0] < kPanMinSegment * cover[2]) hflag[0] = 32;
     if (hflag[0]) {
         *declined = hflag[0];
         if (prof)

@@ -55,6 +55,8 @@ class SpectralParams:
     tol: float = 1e-6
     kmeans: str = "exact"        # "exact" (bit-exact replica) or "sorted" (fast, one_vector)
     reorder: str | None = "auto"  # device-layout pre-order: "auto", "bfs" or None (exact)
+    layout: str = "auto"         # SpMV layout: "auto" (column panels for T >= 64 when the
+                                 # graph qualifies), "panels" or "sell"; results identical
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -73,6 +75,8 @@ class SpectralParams:
             raise InputError(f"walk_sign must be +1 or -1, got {self.walk_sign}")
         if self.kmeans not in ("exact", "sorted"):
             raise InputError(f"kmeans must be 'exact' or 'sorted', got {self.kmeans!r}")
+        if self.layout not in ("auto", "panels", "sell"):
+            raise InputError(f"layout must be 'auto', 'panels' or 'sell', got {self.layout!r}")
 
     def num_columns(self, n: int) -> int:
         if self.mode == "one_vector":
@@ -118,6 +122,9 @@ def _kmeans_seed(seed: int) -> int:
     return int(np.random.SeedSequence([seed, _TAG_KMEANS]).generate_state(1)[0])
 
 
+PANEL_MIN_STEPS = 64
+
+
 def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGraph | None = None,
                           keep_x: bool = False) -> PipelineResult:
     """Cluster the graph's vertices into k parts (pipeline.py:127-178 contract).
@@ -135,8 +142,12 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
     if params.mode == "pm_log_k":
         return _pm_log_k(graph, params, steps, device_graph)
     t_start = time.perf_counter()
+    # the panel layout costs about a dozen SELL steps to build (device, ~1.7 ms at config 2)
+    # and saves ~13 % per step where it applies
+    panels = params.layout == "panels" or (params.layout == "auto" and steps >= PANEL_MIN_STEPS)
     dev = device_graph if device_graph is not None else DeviceGraph(graph, params.device,
-                                                                    reorder=params.reorder)
+                                                                    reorder=params.reorder,
+                                                                    panels=panels)
     try:
         t0 = time.perf_counter()
         if params.x0 is not None:
