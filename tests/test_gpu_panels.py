@@ -110,3 +110,18 @@ def test_declined_layouts_still_exact():
     _compare(gh, 5, expect_panels=False)
     gs = _blocked(3000, 1000, 10, 1, seed=7)   # fewer rows than one panel row block
     _compare(gs, 5, expect_panels=False)
+
+
+def test_pipeline_layouts_identical():
+    """fast_spectral_cluster: layout 'panels' (also the 'auto' choice at T >= 64) and 'sell'
+    give bit-identical embeddings and labels"""
+    from paper_2310_10939_b200 import SpectralParams, fast_spectral_cluster
+    g = _blocked(120_000, 40_000, 20, 2, seed=3)
+    out = {}
+    for layout in ("panels", "sell", "auto"):
+        res = fast_spectral_cluster(g, SpectralParams(k=3, t=70, mode="one_vector", seed=1,
+                                                      layout=layout))
+        out[layout] = res
+    for layout in ("sell", "auto"):
+        assert np.array_equal(out[layout].embedding.data, out["panels"].embedding.data)
+        assert np.array_equal(out[layout].partition.labels, out["panels"].partition.labels)
