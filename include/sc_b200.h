@@ -124,6 +124,12 @@ void sc_graph_destroy(sc_graph *g);
  * `device` (all devices if < 0) and returns the bytes released. */
 int64_t sc_release_cached_memory(int32_t device);
 int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *out);
+/* Builds the column-panel layout (SC_CREATE_PANELS) on an existing handle -- whole graphs or
+ * shards; declined silently when the graph does not qualify (panel_groups stays 0).  Steps
+ * over a shard's full row range then use it: the caller's z buffers must be 16-byte aligned
+ * and hold ncols + 16 doubles with z[ncols..] == 0 (the padding target; the handle's own
+ * buffers already do). */
+int32_t sc_graph_build_panels(sc_graph *g);
 /* The device layout renumbers rows (SELL-32-sigma: length-sorted inside 4096-row windows,
  * rows longer than 256 last).  sc_sell_order returns that permutation for a row_ptr
  * (perm[p] = original row of renumbered row p) so a multi-GPU driver can rename columns

@@ -1560,6 +1560,13 @@ void sc_graph_destroy(sc_graph *g) {
     delete g;
 }
 
+int32_t sc_graph_build_panels(sc_graph *g) {
+    SC_REQUIRE(g, SC_E_INVALID, "null graph");
+    if (g->pan_ctas) return SC_OK;
+    SC_CUDA(cudaSetDevice(g->device));
+    return sc::build_panels(g, getenv("SC_GRAPH_PROFILE") != nullptr);
+}
+
 int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *o) {
     SC_REQUIRE(g && o, SC_E_INVALID, "null argument");
     o->n = g->n;

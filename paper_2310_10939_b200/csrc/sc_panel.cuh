@@ -25,7 +25,8 @@
 //   Segments are sorted by decreasing count, so the 32 segments of an iteration have (nearly)
 //   the same count and the warp runs without divergence; one thread streams the stages into
 //   a shared-memory ring with bulk copies (cp.async.bulk + mbarrier).  Sparse padding entries
-//   index z[n], a zero slot kept past the vector (sc_graph::zstride > ncols).
+//   index z[ncols], a zero slot kept past the vector (sc_graph::zstride > ncols for whole
+//   graphs; shard callers pass z buffers with the same padding, see sc_graph_build_panels).
 // This header is included inside namespace sc.
 
 constexpr int kPanZ = 8192;        // panel width in doubles (64 KB)
@@ -84,7 +85,8 @@ struct PanArgs {
     const int32_t *blk;      // per CTA + 1: group range
     const PanGroup *grp;
     const uint8_t *stream;   // stages
-    int64_t n;               // rows (= columns: whole graphs only)
+    int64_t n;               // rows
+    int64_t ncols;           // z space length; z[ncols] is a zero slot (padding target)
     int slot;                // ring slot bytes
     int rpc;                 // rows per CTA (<= kPanR, multiple of 32)
     int exp;                 // diagnostics (SC_PANEL_EXP): 1 = no epilogue loads, 2 = no stores
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(kPanTPB, 1) k_rw_panel(StepArgs a, PanArgs p) 
     const int64_t r0 = (int64_t)b * p.rpc;
     const int rows_here = (int)((p.n - r0) < p.rpc ? (p.n - r0) : p.rpc);
     auto panel_bytes = [&](int pan) {
-        const int64_t left = p.n - (int64_t)pan * kPanZ;
+        const int64_t left = p.ncols - (int64_t)pan * kPanZ;
         return (uint32_t)(((left < kPanZ ? left : kPanZ) * 8 + 15) & ~15);
     };
     if (threadIdx.x == 0) {
@@ -284,7 +286,8 @@ struct PanPlanQ {
 };
 
 // Per CTA: panel histogram -> groups -> segment histogram per (group, count) -> stage sizes.
-// flag[0] |= 1 (too many groups), 2 (segment longer than kPanCMax - 1), 4 (stage > slot cap);
+// flag[0] |= 1 (too many groups), 2 (segment longer than kPanCMax - 1), 4 (stage > slot cap),
+// 8 (a row's stored order goes back to an earlier group);
 // flag[1] = max stage bytes; cover[0] / cover[1] / cover[2] += entries in dense panels / all
 // entries / dense segments.
 __global__ void __launch_bounds__(kPanTPB) k_pan_plan(const int64_t *slice_ptr, const uint32_t *col,
@@ -361,6 +364,10 @@ __global__ void __launch_bounds__(kPanTPB) k_pan_plan(const int64_t *slice_ptr, 
             pan_row_walk(slice_ptr, col, r0 + i, [&](uint32_t c) {
                 const int g = (int)hist[c / kPanZ];
                 if (g != cur) {
+                    // a row must visit its groups in increasing order (its stored column order
+                    // must not go back to an earlier panel): renamed shard columns, BFS
+                    // pre-orders or unsorted input rows can break that -> decline
+                    if (g < cur) atomicOr(&bad_s, 8);
                     if (cnt) {
                         if (cnt >= kPanCMax) atomicOr(&bad_s, 2);
                         else atomicAdd(&h2[cur * kPanCMax + cnt], 1u);
@@ -416,7 +423,8 @@ __global__ void k_pan_sizes(const int32_t *blk, const PanPlan *plan, int ncta, u
 // Per CTA: writes the group descriptors, headers, padding and then scatters every segment
 // (row id and entries) into its slot of the count-sorted order.
 __global__ void __launch_bounds__(kPanTPB) k_pan_fill(const int64_t *slice_ptr, const uint32_t *col,
-                                                      int64_t n, int S, int rpc, const int32_t *blk,
+                                                      int64_t n, int64_t ncols, int S, int rpc,
+                                                      const int32_t *blk,
                                                       const PanPlan *plan, const PanPlanQ *planq,
                                                       const uint64_t *offs, PanGroup *grp,
                                                       uint8_t *stream) {
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(kPanTPB) k_pan_fill(const int64_t *slice_ptr, 
             for (uint32_t i = threadIdx.x; i < pq.ent; i += kPanTPB) e[i] = (uint16_t)kPanZ;
         } else {
             uint32_t *e = (uint32_t *)(st + pq.eoff);
-            for (uint32_t i = threadIdx.x; i < pq.ent; i += kPanTPB) e[i] = (uint32_t)n;  // z[n] = 0
+            for (uint32_t i = threadIdx.x; i < pq.ent; i += kPanTPB) e[i] = (uint32_t)ncols;  // z[ncols] = 0
         }
     }
     __syncthreads();
@@ -536,8 +544,8 @@ static int32_t build_panels_rpc(sc_graph *g, bool prof, int rpc, int32_t *declin
 static int32_t build_panels(sc_graph *g, bool prof) {
     g->pan_ctas = 0;
     const int64_t n = g->n;
-    if (!g->unit || g->n_wide || g->ncols != n || g->col_offset != 0 || n < kPanR) return SC_OK;
-    if ((n + kPanZ - 1) / kPanZ > kPanSMax) return SC_OK;
+    if (!g->unit || g->n_wide || n < kPanR) return SC_OK;
+    if ((g->ncols + kPanZ - 1) / kPanZ > kPanSMax) return SC_OK;
     for (int rpc = kPanR; rpc >= 256; rpc = (rpc / 2) & ~31) {
         int32_t declined = 0;
         const int32_t st = build_panels_rpc(g, prof, rpc, &declined);
@@ -549,7 +557,7 @@ static int32_t build_panels(sc_graph *g, bool prof) {
 
 static int32_t build_panels_rpc(sc_graph *g, bool prof, int rpc, int32_t *declined) {
     const int64_t n = g->n;
-    const int S = (int)((n + kPanZ - 1) / kPanZ);
+    const int S = (int)((g->ncols + kPanZ - 1) / kPanZ);
     cudaStream_t s = g->stream;
     const int ncta = (int)((n + rpc - 1) / rpc);
     const uint32_t slot_cap = (uint32_t)(((kPanSmemMax - kPanFixedSmem) / kPanNS) & ~127);
@@ -637,14 +645,16 @@ static int32_t build_panels_rpc(sc_graph *g, bool prof, int rpc, int32_t *declin
         cleanup();
         return st;
     }
-    k_pan_fill<<<ncta, kPanTPB, smem_plan, s>>>(g->d_slice_ptr, g->d_col, n, S, rpc, g->d_pan_blk, plan, planq,
+    k_pan_fill<<<ncta, kPanTPB, smem_plan, s>>>(g->d_slice_ptr, g->d_col, n, g->ncols, S, rpc, g->d_pan_blk, plan, planq,
                                                 offs, g->d_pan_grp, g->d_pan_stream);
     e = cudaGetLastError();
     if (!e) e = cudaStreamSynchronize(s);
     cleanup();
     if (e) return fail(SC_E_CUDA, "panel fill: %s", cudaGetErrorString(e));
     g->pan_slot = (hflag[1] + 127) & ~127;
-    const int smem = kPanFixedSmem + kPanNS * g->pan_slot;
+    // the attribute is per function, shared by all handles: allow the largest ring any handle
+    // can have (a handle's launch asks for its own, smaller or equal, amount)
+    const int smem = kPanFixedSmem + kPanNS * (int)slot_cap;
     SC_CUDA(cudaFuncSetAttribute(k_rw_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     SC_CUDA(cudaFuncSetAttribute(k_rw_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     g->pan_ctas = ncta;
@@ -663,6 +673,7 @@ static cudaError_t launch_panel_step(const sc_graph *g, const StepArgs &a, bool 
     p.grp = g->d_pan_grp;
     p.stream = g->d_pan_stream;
     p.n = g->n;
+    p.ncols = g->ncols;
     p.slot = g->pan_slot;
     p.rpc = g->pan_rpc;
     static const int exp = getenv("SC_PANEL_EXP") ? atoi(getenv("SC_PANEL_EXP")) : 0;

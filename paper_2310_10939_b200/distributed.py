@@ -84,7 +84,10 @@ def piece_bounds(n: int, n_sell: int, pieces: int) -> np.ndarray:
 class ShardPlan:
     """Row blocks, every rank's renumbering, the pieces and the global z space."""
 
-    def __init__(self, starts, perms, n_sells=None, pieces: int = 1):
+    def __init__(self, starts, perms, n_sells=None, pieces: int = 1, align: int = 1):
+        """``align``: round every rank's z block up to a multiple of this many slots (8192
+        keeps the 4096-row renumbering windows inside 8192-column panels, so the column-panel
+        layout sees every row's columns in panel order)."""
         self.starts = np.asarray(starts, dtype=np.int64)
         self.world = self.starts.size - 1
         self.sizes = np.diff(self.starts)
@@ -97,6 +100,7 @@ class ShardPlan:
         self.bounds = [piece_bounds(int(self.sizes[r]), self.n_sells[r], self.pieces)
                        for r in range(self.world)]
         self.pmax = max(1, int(max(np.diff(b).max() for b in self.bounds)))
+        self.pmax = -(-self.pmax // int(align)) * int(align)
         self.n_max = int(self.sizes.max())
         # z slot of every global (original) vertex id
         slot = np.empty(self.n_global, dtype=np.int64)
@@ -131,7 +135,7 @@ class ShardPlan:
 
 
 def exchange_plan(local_row_ptr: np.ndarray, starts: np.ndarray, rank: int, world: int,
-                  group=None, pieces: int = 1) -> ShardPlan:
+                  group=None, pieces: int = 1, align: int = 1) -> ShardPlan:
     """Every rank computes its renumbering and all-gathers it (padded to n_max)."""
     import torch
     import torch.distributed as dist
@@ -146,7 +150,7 @@ def exchange_plan(local_row_ptr: np.ndarray, starts: np.ndarray, rank: int, worl
     dist.all_gather(out, buf.to(dev), group=group)
     perms = [out[r][: int(starts[r + 1] - starts[r])].cpu().numpy() for r in range(world)]
     n_sells = [int(out[r][n_max].item()) for r in range(world)]
-    return ShardPlan(starts, perms, n_sells, pieces)
+    return ShardPlan(starts, perms, n_sells, pieces, align)
 
 
 class HaloPlan:
@@ -317,6 +321,19 @@ class CudaShard:
 
     def zeros(self, m):
         return self.torch.zeros(m, dtype=self.torch.float64, device=self.tdev)
+
+    def zspace(self, m):
+        """a z-space buffer of m doubles followed by 16 zeros that are never written: the
+        padding target of the column-panel layout (sc_graph_build_panels contract); the
+        returned view covers the first m"""
+        return self.zeros(m + 16)[:m]
+
+    def build_panels(self) -> bool:
+        """column-panel layout for full-shard steps (pieces = 1); False if declined"""
+        _lib.check(_lib.load().sc_graph_build_panels(self.h))
+        gi = _lib.GraphInfo()
+        _lib.check(_lib.load().sc_graph_info_get(self.h, ctypes.byref(gi)))
+        return gi.panel_groups > 0
 
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.tdev).cuda_stream)
@@ -552,15 +569,16 @@ class ShardedPower:
         self.shard, self.plan, self.rank = shard, plan, rank
         self.sign, self.sym = sign, sym
         n = int(plan.sizes[rank])
+        zspace = getattr(shard, "zspace", shard.zeros)
         if comm is None:
             self.comm = PieceComm(plan, rank, group)
-            self.z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
+            self.z = [zspace(plan.ncols), zspace(plan.ncols)]
         elif hasattr(comm, "z0"):  # fused peer exchange: z lives in the mirrored allocation
             self.comm = comm
             self.z = [comm.z0, comm.z1]
         else:  # halo exchange
             self.comm = comm
-            self.z = [shard.zeros(plan.ncols), shard.zeros(plan.ncols)]
+            self.z = [zspace(plan.ncols), zspace(plan.ncols)]
         self.x = [shard.zeros(n), shard.zeros(n)]
         self.x0 = shard.zeros(n)
         self.graph = None
@@ -666,8 +684,16 @@ def bench_main(args, metric: str, unit: str):
     if halo:
         plan = exchange_halo_plan(rp, col, starts, rank, world)
     else:
-        plan = exchange_plan(rp, starts, rank, world, pieces=pieces)
+        plan = exchange_plan(rp, starts, rank, world, pieces=pieces,
+                             align=8192 if pieces == 1 else 1)
     shard = CudaShard(rp, plan.rename(col), None, deg, plan, rank, local)
+    # column panels for whole-shard steps (as the single-GPU pipeline at T >= 64); the peer
+    # exchange and multi-piece steps stay on SELL
+    panels = False
+    if not p2p and pieces == 1 and not getattr(args, "sell", False):
+        ok_t = torch.tensor([1 if shard.build_panels() else 0], device="cuda", dtype=torch.int32)
+        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+        panels = bool(ok_t.item())
     nnz_t = torch.tensor([int(rp[-1])], device="cuda", dtype=torch.int64)
     dist.all_reduce(nnz_t)
     nnz_total = int(nnz_t.item())
@@ -737,6 +763,7 @@ def bench_main(args, metric: str, unit: str):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config2 block per GPU (SBM n={params.n}, k={params.k})",
                        "n_per_gpu": n_loc, "nnz_total": nnz_total, "T": T, "pieces": plan.pieces,
+                       "spmv_layout": "panels" if panels else "sell",
                        "cuda_graph": use_graph,
                        "comm": "p2p" if p2p else "halo" if halo else "nccl",
                        "parallelism": (f"row-block shards x{world}, z stored into the peers' "

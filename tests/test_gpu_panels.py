@@ -71,6 +71,23 @@ def test_odd_n_partial_blocks():
     _compare(g, 9)
 
 
+def test_bfs_preorder_declined():
+    """a BFS pre-order renames columns out of stored order: rows would revisit panels, so the
+    layout is declined (the check in k_pan_plan) and results stay exact"""
+    g = _blocked(120_000, 40_000, 20, 2, seed=3)
+    rng = np.random.default_rng(12)
+    p = rng.permutation(g.n)  # scatter the ids so the BFS pre-order is worth applying
+    rp, col = g.row_offsets, g.col_indices
+    u = np.repeat(np.arange(g.n), np.diff(rp))
+    gs = _simple(g.n, p[u], p[col])
+    with DeviceGraph(gs, reorder="bfs", panels=True) as dg:
+        assert dg.info()["panel_groups"] == 0
+        x0 = dg.sample_irwin_hall(0, return_host=True)
+        xT, f = dg.power_iterate(6)
+    xo, fo = O.power_iterate(gs.row_offsets, gs.col_indices, None, gs.degrees, x0, 6)
+    assert np.array_equal(xT, xo) and np.array_equal(f, fo)
+
+
 def test_no_locality_declined():
     """ids without locality: few entries fall into dense panels -> SELL only"""
     rng = np.random.default_rng(5)
@@ -125,3 +142,61 @@ def test_pipeline_layouts_identical():
     for layout in ("sell", "auto"):
         assert np.array_equal(out[layout].embedding.data, out["panels"].embedding.data)
         assert np.array_equal(out[layout].partition.labels, out["panels"].partition.labels)
+
+
+@pytest.mark.parametrize("world,aligned", [(2, True), (3, True), (2, False)])
+def test_shard_panels_on_one_gpu_bit_exact(world, aligned):
+    """row-block shards with the panel layout (sc_graph_build_panels) over the global z space,
+    the all-gather emulated by device copies: bit-exact against the single-graph oracle"""
+    import torch
+
+    from paper_2310_10939_b200 import distributed as D
+
+    g = _blocked(150_000, 50_000, 20, 2, seed=11)
+    rp, col, deg = g.row_offsets, g.col_indices.astype(np.int32), g.degrees
+    starts = D.partition_rows(rp, world)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(world)]
+    # z blocks aligned to 8192 slots keep the renumbering windows inside panels; without the
+    # alignment rows revisit panels and the layout is declined (SELL, still exact)
+    plan = D.ShardPlan(starts, [D.sell_order(x) for x in lrps], [D.n_sell_rows(x) for x in lrps], 1,
+                       align=8192 if aligned else 1)
+    shards = []
+    for r in range(world):
+        lo, hi = int(starts[r]), int(starts[r + 1])
+        s = D.CudaShard(lrps[r], plan.rename(col[rp[lo]:rp[hi]]), None, deg[lo:hi], plan, r, 0)
+        built = s.build_panels()
+        assert built or not aligned
+        shards.append(s)
+    if not aligned:
+        assert not all(s_.build_panels() for s_ in shards)
+    T = 9
+    z = [[s.zspace(plan.ncols), s.zspace(plan.ncols)] for s in shards]
+    x = [[s.zeros(s.n), s.zeros(s.n)] for s in shards]
+    x0 = [s.zeros(s.n) for s in shards]
+
+    def gather(b):
+        torch.cuda.synchronize()
+        for r in range(world):
+            lo, hi = plan.own(0, r)
+            for q in range(world):
+                if q != r:
+                    z[q][b][lo:hi].copy_(z[r][b][lo:hi])
+
+    for r, s in enumerate(shards):
+        s.irwin_hall(2, x0[r])
+        s.scale_piece(0, x0[r], z[r][0])
+    gather(0)
+    for t in range(T):
+        a, b = t & 1, (t & 1) ^ 1
+        for r, s in enumerate(shards):
+            s.step_piece(0, z[r][a], x0[r] if t == 0 else x[r][a], x[r][b], z[r][b])
+        gather(b)
+    torch.cuda.synchronize()
+    xs = np.concatenate([s.to_original(x[r][T & 1]) for r, s in enumerate(shards)])
+    fs = np.concatenate([s.to_original(s.local_z(z[r][T & 1])) for r, s in enumerate(shards)])
+    x0_ref = O.irwin_hall(deg, 2)
+    xT, f = O.power_iterate(rp, col, None, deg, x0_ref, T)
+    assert np.array_equal(xs, xT)
+    assert np.array_equal(fs, f)
+    for s in shards:
+        s.close()
