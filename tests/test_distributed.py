@@ -227,6 +227,30 @@ def test_plan_renaming_is_a_bijection():
                 assert hi - lo == plan.pmax
 
 
+def test_plan_alignment_keeps_windows_inside_panels():
+    """ShardPlan(align=8192): every rank's z block starts on an 8192-slot boundary, so the
+    4096-row renumbering windows (the only reordering of a row's columns) never straddle a
+    column panel -- the condition the panel layout builder checks on the device"""
+    rng = np.random.default_rng(3)
+    rp = np.concatenate([[0], np.cumsum(rng.integers(1, 40, 30000))])
+    starts = D.partition_rows(rp, 3)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(3)]
+    perms = [D.sell_order(x) for x in lrps]
+    plan = D.ShardPlan(starts, perms, [D.n_sell_rows(x) for x in lrps], 1, align=8192)
+    base = D.ShardPlan(starts, perms, [D.n_sell_rows(x) for x in lrps], 1)
+    assert plan.pmax % 8192 == 0 and plan.pmax >= base.pmax
+    for r in range(3):
+        lo, _ = plan.own(0, r)
+        assert lo % 8192 == 0
+        ids = np.arange(int(starts[r]), int(starts[r + 1]))
+        slots = plan.slot_of[ids]
+        # original ids inside one 4096-row window of the rank stay inside one 8192 panel
+        win = (ids - starts[r]) // 4096
+        for w in np.unique(win):
+            assert np.unique(slots[win == w] // 8192).size == 1
+    assert np.unique(plan.slot_of).size == plan.slot_of.size
+
+
 def test_sbm_rows_concatenate_to_sample_sbm():
     p = SbmParams(n=4000, k=8, p=0.02, q=0.002, seed=4)
     g = sample_sbm(p).graph

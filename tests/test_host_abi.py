@@ -75,8 +75,9 @@ def test_params_semantics():
     assert p.num_steps(10**6) == int(np.ceil(10 * np.log(10**5)))
     assert SpectralParams(k=5, t=50, mode="one_vector").num_steps(1000) == 50
     assert "one_vector" in MODES
+    assert SpectralParams(k=5).layout == "auto"
     for bad in (dict(k=1), dict(k=3, mode="nope"), dict(k=3, t=-1), dict(k=3, seed=-2),
-                dict(k=3, epsilon=0.0), dict(k=3, walk_sign=2)):
+                dict(k=3, epsilon=0.0), dict(k=3, walk_sign=2), dict(k=3, layout="ell")):
         with pytest.raises(InputError):
             SpectralParams(**bad)
     assert _kmeans_seed(0) == 3141116543
