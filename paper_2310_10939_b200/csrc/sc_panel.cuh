@@ -89,7 +89,6 @@ struct PanArgs {
     int64_t ncols;           // z space length; z[ncols] is a zero slot (padding target)
     int slot;                // ring slot bytes
     int rpc;                 // rows per CTA (<= kPanR, multiple of 32)
-    int exp;                 // diagnostics (SC_PANEL_EXP): 1 = no epilogue loads, 2 = no stores
 };
 
 // Walks the entries of local row i of CTA b in the SELL layout (stored order).
@@ -222,7 +221,7 @@ __global__ void __launch_bounds__(kPanTPB, 1) k_rw_panel(StepArgs a, PanArgs p) 
                     pan_bulk(zs + (d & 1) * kStride, z + (int64_t)pan * kPanZ, panel_bytes(pan),
                              &zfull[d & 1]);
                     ++next_dense;
-                } else if (s_epi < 0 && !(rows_here & 1) && !(p.exp & 1)) {
+                } else if (s_epi < 0 && !(rows_here & 1)) {
                     // no dense panel left: this buffer is free for the rest of the kernel, so the
                     // epilogue's x_in and scale rows are prefetched into it
                     s_epi = d & 1;
@@ -257,7 +256,7 @@ __global__ void __launch_bounds__(kPanTPB, 1) k_rw_panel(StepArgs a, PanArgs p) 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int i = threadIdx.x + j * kPanTPB;
-        const bool ld = i < rows_here && !(p.exp & 1);
+        const bool ld = i < rows_here;
         if (epi >= 0) {
             xr[j] = ld ? eb[i] : 0.0;
             sv[j] = ld ? eb[rows_here + i] : 1.0;
@@ -265,10 +264,6 @@ __global__ void __launch_bounds__(kPanTPB, 1) k_rw_panel(StepArgs a, PanArgs p) 
             xr[j] = ld ? __ldcs(a.x_in + r0 + i) : 0.0;
             sv[j] = ld ? __ldcs(a.scale + r0 + i) : 1.0;
         }
-    }
-    if (p.exp & 2) {
-        if (part[threadIdx.x] == 12345.0) a.x_out[0] = xr[0] + sv[3];  // keep the work alive
-        return;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -676,8 +671,6 @@ static cudaError_t launch_panel_step(const sc_graph *g, const StepArgs &a, bool 
     p.ncols = g->ncols;
     p.slot = g->pan_slot;
     p.rpc = g->pan_rpc;
-    static const int exp = getenv("SC_PANEL_EXP") ? atoi(getenv("SC_PANEL_EXP")) : 0;
-    p.exp = exp;
     const int smem = kPanFixedSmem + kPanNS * g->pan_slot;
     if (sym) k_rw_panel<true><<<g->pan_ctas, kPanTPB, smem, s>>>(a, p);
     else k_rw_panel<false><<<g->pan_ctas, kPanTPB, smem, s>>>(a, p);
