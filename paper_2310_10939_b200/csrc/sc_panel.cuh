@@ -527,6 +527,62 @@ __global__ void __launch_bounds__(kPanTPB) k_pan_fill(const int64_t *slice_ptr, 
     }
 }
 
+// Bank-aware lane assignment: the 32 segments of an iteration may sit in any lanes (a segment
+// moves with its entries, so every row keeps its order).  part[row] is a double, so rows r
+// and r' collide in a half-warp access when r == r' (mod 16); this places the segments so
+// that each half-warp sees distinct residues where possible (greedy; dummy rows share one
+// address and are free), cutting the replayed wavefronts of the part[] loads and stores.
+__global__ void __launch_bounds__(256) k_pan_balance(const PanGroup *__restrict__ grp,
+                                                     uint8_t *__restrict__ stream) {
+    const PanGroup m = grp[blockIdx.x];
+    uint8_t *st = stream + m.off;
+    const uint32_t *hdr = (const uint32_t *)st;
+    uint16_t *rows = (uint16_t *)(st + m.roff);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t q = threadIdx.x >> 5; q < m.nq; q += blockDim.x >> 5) {
+        const uint32_t h = hdr[q];
+        const int c = (int)(h >> 24);
+        const uint32_t base = h & 0xffffffu;
+        const uint16_t row = rows[q * 32 + lane];
+        const bool dummy = row >= kPanR;
+        const int bank = row & 15;
+        uint32_t used[2] = {0u, 0u};
+        int cnt[2] = {0, 0}, mine = lane;
+        for (int pass = 0; pass < 2; ++pass)  // real segments first, then the dummies
+            for (int i = 0; i < 32; ++i) {
+                const int bi = __shfl_sync(0xffffffffu, bank, i);
+                const bool di = __shfl_sync(0xffffffffu, dummy, i);
+                if (di != (pass == 1)) continue;
+                int half;
+                if (!di && cnt[0] < 16 && !((used[0] >> bi) & 1)) half = 0;
+                else if (!di && cnt[1] < 16 && !((used[1] >> bi) & 1)) half = 1;
+                else half = cnt[0] < 16 ? 0 : 1;
+                if (!di) used[half] |= 1u << bi;
+                if (i == lane) mine = half * 16 + cnt[half];
+                ++cnt[half];
+            }
+        __syncwarp();
+        rows[q * 32 + mine] = row;
+        if (m.panel >= 0) {
+            uint16_t *e = (uint16_t *)(st + m.eoff) + base;
+            for (int k = 0; k < c; ++k) {
+                const uint16_t v = e[32 * k + lane];
+                __syncwarp();
+                e[32 * k + mine] = v;
+                __syncwarp();
+            }
+        } else {
+            uint32_t *e = (uint32_t *)(st + m.eoff) + base;
+            for (int k = 0; k < c; ++k) {
+                const uint32_t v = e[32 * k + lane];
+                __syncwarp();
+                e[32 * k + mine] = v;
+                __syncwarp();
+            }
+        }
+    }
+}
+
 // Builds g's panel layout from its SELL arrays.  Returns SC_OK with g->pan_ctas == 0 when the
 // graph does not qualify (weighted, wide rows, shard, too many panels/groups, long segments,
 // a stage larger than the ring slot); CUDA errors are returned.
@@ -643,6 +699,10 @@ static int32_t build_panels_rpc(sc_graph *g, bool prof, int rpc, int32_t *declin
     k_pan_fill<<<ncta, kPanTPB, smem_plan, s>>>(g->d_slice_ptr, g->d_col, n, g->ncols, S, rpc, g->d_pan_blk, plan, planq,
                                                 offs, g->d_pan_grp, g->d_pan_stream);
     e = cudaGetLastError();
+    if (!e && ngroups) {
+        k_pan_balance<<<ngroups, 256, 0, s>>>(g->d_pan_grp, g->d_pan_stream);
+        e = cudaGetLastError();
+    }
     if (!e) e = cudaStreamSynchronize(s);
     cleanup();
     if (e) return fail(SC_E_CUDA, "panel fill: %s", cudaGetErrorString(e));
