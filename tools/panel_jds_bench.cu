@@ -816,6 +816,166 @@ static void runS(const std::vector<int64_t> &rp, const std::vector<int> &col, in
     cudaFree(bg), cudaFree(dm), cudaFree(st), cudaFree(by);
 }
 
+
+// ---- v13: NW warps per CTA, ZB panel buffers (several CTAs per SM hide each other's
+// barrier and panel-load waits) ----
+template <int Z, int NS, int NW, int ZB>
+__global__ void __launch_bounds__(NW * 32)
+    k_ps2(const int *__restrict__ blk_g, const GrpMeta *__restrict__ meta, const uint2 *__restrict__ stg,
+          const uint8_t *__restrict__ bytes, const double *__restrict__ z, int R, int slot_bytes, int64_t n,
+          double *__restrict__ out) {
+    extern __shared__ __align__(128) double zs[];  // ZB x (Z + 16) | partial[R + 16] | NS x slot
+    __shared__ uint64_t sfull[NS], zfull[ZB];
+    constexpr int kStride = Z + 16;
+    double *part = zs + ZB * kStride;
+    uint8_t *ring = (uint8_t *)(part + ((R + 16 + 15) & ~15));
+    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g0 = blk_g[b], g1 = blk_g[b + 1];
+    int next_dense = g0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&sfull[i], 1);
+        for (int i = 0; i < ZB; ++i) mbar_init(&zfull[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int g = g0; g < g1 && g < g0 + NS; ++g) {
+            const uint2 sd = stg[g];
+            bulk_issue(ring + (g - g0) * slot_bytes, bytes + (int64_t)sd.x * 16, sd.y, &sfull[g - g0]);
+        }
+        int d = 0;
+        for (; next_dense < g1 && d < ZB; ++next_dense)
+            if (meta[next_dense].panel >= 0) {
+                bulk_issue(zs + d * kStride, z + (int64_t)meta[next_dense].panel * Z, Z * 8, &zfull[d]);
+                ++d;
+            }
+    }
+    for (int i = threadIdx.x; i < R + 16; i += blockDim.x) part[i] = 0.0;
+    if (threadIdx.x < ZB) zs[threadIdx.x * kStride + Z] = 0.0;
+    __syncthreads();
+    int d = 0;
+    for (int g = g0; g < g1; ++g) {
+        const int k = g - g0, slot = k % NS;
+        const GrpMeta m = meta[g];
+        const bool dense = m.panel >= 0;
+        const double *zb = zs + (d % ZB) * kStride;
+        const uint8_t *st = ring + slot * slot_bytes;
+        mbar_wait(&sfull[slot], (k / NS) & 1);
+        if (dense) mbar_wait(&zfull[d % ZB], (d / ZB) & 1);
+        const uint32_t *hdr = (const uint32_t *)st;
+        const uint16_t *rows = (const uint16_t *)(st + m.roff);
+        if (dense) {
+            const uint16_t *ent = (const uint16_t *)(st + m.eoff);
+            for (uint32_t q = w; q < m.nq; q += NW) {
+                const uint32_t h = hdr[q];
+                const int c = h >> 24;
+                const uint16_t *e = ent + (h & 0xffffff) + lane;
+                const int row = rows[q * 32 + lane];
+                double acc = part[row];
+                int kk = 0;
+                for (; kk + 4 <= c; kk += 4) {
+                    const int i0 = e[32 * kk], i1 = e[32 * kk + 32], i2 = e[32 * kk + 64], i3 = e[32 * kk + 96];
+                    const double v0 = zb[i0], v1 = zb[i1], v2 = zb[i2], v3 = zb[i3];
+                    acc = __dadd_rn(acc, v0);
+                    acc = __dadd_rn(acc, v1);
+                    acc = __dadd_rn(acc, v2);
+                    acc = __dadd_rn(acc, v3);
+                }
+                for (; kk < c; ++kk) acc = __dadd_rn(acc, zb[e[32 * kk]]);
+                part[row] = acc;
+            }
+        } else {
+            const uint32_t *ent = (const uint32_t *)(st + m.eoff);
+            for (uint32_t q = w; q < m.nq; q += NW) {
+                const uint32_t h = hdr[q];
+                const int c = h >> 24;
+                const uint32_t *e = ent + (h & 0xffffff) + lane;
+                const int row = rows[q * 32 + lane];
+                double acc = part[row];
+                int kk = 0;
+                for (; kk + 4 <= c; kk += 4) {
+                    const uint32_t i0 = e[32 * kk], i1 = e[32 * kk + 32], i2 = e[32 * kk + 64], i3 = e[32 * kk + 96];
+                    const double v0 = __ldg(z + i0), v1 = __ldg(z + i1), v2 = __ldg(z + i2), v3 = __ldg(z + i3);
+                    acc = __dadd_rn(acc, v0);
+                    acc = __dadd_rn(acc, v1);
+                    acc = __dadd_rn(acc, v2);
+                    acc = __dadd_rn(acc, v3);
+                }
+                for (; kk < c; ++kk) acc = __dadd_rn(acc, __ldg(z + e[32 * kk]));
+                part[row] = acc;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (g + NS < g1) {
+                const uint2 sd = stg[g + NS];
+                bulk_issue(ring + slot * slot_bytes, bytes + (int64_t)sd.x * 16, sd.y, &sfull[slot]);
+            }
+            if (dense) {
+                while (next_dense < g1 && meta[next_dense].panel < 0) ++next_dense;
+                if (next_dense < g1) {
+                    bulk_issue(zs + (d % ZB) * kStride, z + (int64_t)meta[next_dense].panel * Z, Z * 8,
+                               &zfull[d % ZB]);
+                    ++next_dense;
+                }
+            }
+        }
+        if (dense) ++d;
+    }
+    const int64_t r0 = (int64_t)b * R;
+    for (int i = threadIdx.x; i < R; i += blockDim.x)
+        if (r0 + i < n) out[r0 + i] = part[i];
+}
+
+template <int Z, int NS, int NW, int ZB>
+static void runS2(const std::vector<int64_t> &rp, const std::vector<int> &col, int64_t n, int R, int thresh,
+                  int ctas_per_sm, const double *dz, const std::vector<double> &ref, double *dout) {
+    const size_t fixed = ZB * (size_t)(Z + 16) * 8 + (size_t)((R + 16 + 15) & ~15) * 8;
+    const size_t per_cta = (228 * 1024) / ctas_per_sm - 1024 - 256;
+    if (fixed + 4096 > per_cta) {
+        printf("S2: no room\\n");
+        return;
+    }
+    const size_t slot_cap = ((per_cta - fixed) / NS) & ~(size_t)127;
+    LayoutS L = buildS(rp, col, n, R, Z, thresh, slot_cap);
+    if (L.max_stage > slot_cap) {
+        printf("S2 Z %d R %d NS %d NW %d ZB %d: max stage %zu > slot %zu\\n", Z, R, NS, NW, ZB, L.max_stage, slot_cap);
+        return;
+    }
+    const int slot = (int)((L.max_stage + 127) & ~(size_t)127);
+    std::vector<GrpMeta> meta(L.grp_panel.size());
+    for (size_t g = 0; g < meta.size(); ++g) meta[g] = {L.grp_panel[g], L.nq[g], L.roff[g], L.eoff[g]};
+    int *bg = up(L.blk_g);
+    GrpMeta *dm = up(meta);
+    uint2 *st = up(L.stg);
+    uint8_t *by = up(L.bytes);
+    const size_t smem = fixed + (size_t)NS * slot;
+    CK(cudaFuncSetAttribute(k_ps2<Z, NS, NW, ZB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ps2<Z, NS, NW, ZB>, NW * 32, smem));
+    auto launch = [&] { k_ps2<Z, NS, NW, ZB><<<L.G, NW * 32, smem>>>(bg, dm, st, by, dz, R, slot, n, dout); };
+    CK(cudaMemset(dout, 0, n * 8));
+    launch();
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    std::vector<double> got(n);
+    CK(cudaMemcpy(got.data(), dout, n * 8, cudaMemcpyDeviceToHost));
+    int64_t bad = 0;
+    for (int64_t i = 0; i < n; ++i) bad += memcmp(&got[i], &ref[i], 8) != 0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int r = 0; r < 3; ++r) launch();
+    const int reps = 20;
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    printf("S2 Z %5d R %5d NS %d NW %2d ZB %d occ %d | CTAs %d groups %zu smem %zu | %7.1f us %6.1f GNNZ/s | bad %lld\\n",
+           Z, R, NS, NW, ZB, occ, L.G, L.grp_panel.size(), smem, ms * 1e3, col.size() / ms / 1e6, (long long)bad);
+    cudaFree(bg), cudaFree(dm), cudaFree(st), cudaFree(by);
+}
+
 int main(int argc, char **argv) {
     int64_t n = 1000000;
     const int64_t blk = 100000;
@@ -866,16 +1026,15 @@ int main(int argc, char **argv) {
     CK(cudaMalloc(&dout, n * 8));
     printf("nnz %zu\n", col.size());
     if (argc > 1) {
-        runS<8192, 2>(rp, col, n, 3392, 512, dz, ref, dout);
         runS<8192, 2>(rp, col, n, 3392, 1024, dz, ref, dout);
+        runS2<8192, 2, 32, 2>(rp, col, n, 3392, 1024, 1, dz, ref, dout);
+        runS2<8192, 2, 16, 1>(rp, col, n, 1696, 512, 2, dz, ref, dout);
+        runS2<8192, 2, 16, 1>(rp, col, n, 1696, 1024, 2, dz, ref, dout);
+        runS2<4096, 2, 16, 2>(rp, col, n, 1696, 512, 2, dz, ref, dout);
+        runS2<8192, 3, 16, 1>(rp, col, n, 1696, 512, 2, dz, ref, dout);
+        runS2<4096, 2, 8, 2>(rp, col, n, 1696, 512, 3, dz, ref, dout);
+        runS2<4096, 2, 10, 1>(rp, col, n, 1184, 256, 3, dz, ref, dout);
         return 0;
     }
-    runS<8192, 2>(rp, col, n, 3392, 512, dz, ref, dout);
-    runW<8192, 2>(rp, col, n, 3392, 512, dz, ref, dout);
-    runW<8192, 3>(rp, col, n, 3392, 512, dz, ref, dout);
-    runW<6144, 2>(rp, col, n, 3392, 512, dz, ref, dout);
-    runW<6144, 3>(rp, col, n, 3392, 512, dz, ref, dout);
-    runW<8192, 2>(rp, col, n, 2976, 512, dz, ref, dout);
-    runW<8192, 2>(rp, col, n, 4464, 512, dz, ref, dout);
     return 0;
 }
