@@ -151,6 +151,9 @@ int32_t sc_set_x0(sc_graph *g, const double *x0_host);
  * device for sc_kmeans_create_from_graph. */
 int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, double *xT_out,
                          double *f_out, sc_timing *t_out);
+/* f of the last sc_power_iterate (original order) into a host buffer: lets a caller fetch the
+ * embedding while a k-means context built from the handle runs on another thread. */
+int32_t sc_graph_download_f(sc_graph *g, double *f_out);
 
 /* Block power method for the reference's pm_log_k mode (pipeline.py:144-147): T steps of
  * the signless operator M = (I + D^-1/2 A D^-1/2) / 2 on an (n, L) block x0 (host,

@@ -56,7 +56,7 @@ EXPORTS = (
     "sc_shard_set_peers", "sc_shard_barrier", "sc_ipc_export", "sc_ipc_import", "sc_ipc_release",
     "sc_keyed_sums", "sc_contingency", "sc_cut_sums", "sc_power_iterate_block",
     "sc_kmeans_create_nd", "sc_kmeans_lloyd_sorted", "sc_release_cached_memory",
-    "sc_gather_f64", "sc_graph_build_panels",
+    "sc_gather_f64", "sc_graph_build_panels", "sc_graph_download_f",
 )
 
 _lib = None
@@ -84,6 +84,7 @@ def load() -> ctypes.CDLL:
         "sc_graph_destroy": ([P], None),
         "sc_graph_info_get": ([P, ctypes.POINTER(GraphInfo)], i32),
         "sc_graph_build_panels": ([P], i32),
+        "sc_graph_download_f": ([P, P], i32),
         "sc_sample_irwin_hall": ([P, u64, u64, P], i32),
         "sc_set_x0": ([P, P], i32),
         "sc_power_iterate": ([P, i32, f64, u32, P, P, ctypes.POINTER(Timing)], i32),

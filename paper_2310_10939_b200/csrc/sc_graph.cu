@@ -1560,6 +1560,13 @@ void sc_graph_destroy(sc_graph *g) {
     delete g;
 }
 
+int32_t sc_graph_download_f(sc_graph *g, double *f_out) {
+    SC_REQUIRE(g && f_out, SC_E_INVALID, "null argument");
+    SC_REQUIRE(g->result >= 0, SC_E_STATE, "no power iteration has run on this handle");
+    SC_CUDA(cudaSetDevice(g->device));
+    return sc::to_host_original(g, g->d_z[g->result], f_out);
+}
+
 int32_t sc_graph_build_panels(sc_graph *g) {
     SC_REQUIRE(g, SC_E_INVALID, "null graph");
     if (g->pan_ctas) return SC_OK;

@@ -19,6 +19,7 @@ d-dimensional k-means.  pm_k and the eigs_* modes raise InputError.
 
 from __future__ import annotations
 
+import concurrent.futures
 import math
 import time
 from dataclasses import dataclass
@@ -123,6 +124,7 @@ def _kmeans_seed(seed: int) -> int:
 
 
 PANEL_MIN_STEPS = 64
+_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=1, thread_name_prefix="sc-download")
 
 
 def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGraph | None = None,
@@ -154,14 +156,21 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
             dev.set_x0(params.x0)
         else:
             dev.sample_irwin_hall(params.seed)
-        x_t, f = dev.power_iterate(steps, sign=float(params.walk_sign), want_x=keep_x,
-                                   want_f=True)
+        x_t, _ = dev.power_iterate(steps, sign=float(params.walk_sign), want_x=keep_x,
+                                   want_f=False)
         t1 = time.perf_counter()
-        embedding = EmbeddingMatrix(data=f[:, None], scaled=True, seed=params.seed)
-        t2 = time.perf_counter()
+        # the k-means context copies f on the device; the host copy of f (and its validation,
+        # spectral.py:123) overlaps the Lloyd iterations on a helper thread (both C calls
+        # release the GIL; they use different handles and streams)
         with KMeans1D(graph=dev) as km:
-            part = km.lloyd(params.k, _kmeans_seed(params.seed), max_iters=params.max_iters,
-                            tol=params.tol, restarts=params.restarts, method=params.kmeans)
+            emb = _POOL.submit(lambda: EmbeddingMatrix(data=dev.download_f()[:, None], scaled=True,
+                                                       seed=params.seed))
+            t2 = time.perf_counter()
+            try:
+                part = km.lloyd(params.k, _kmeans_seed(params.seed), max_iters=params.max_iters,
+                                tol=params.tol, restarts=params.restarts, method=params.kmeans)
+            finally:
+                embedding = emb.result()
             km_info = dict(km.last)
         t3 = time.perf_counter()
     finally:

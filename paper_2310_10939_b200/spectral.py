@@ -232,6 +232,12 @@ class DeviceGraph:
                             "d2h_ms": tm.d2h_ms}
         return xT, f
 
+    def download_f(self) -> np.ndarray:
+        """f = D^-1 x_T of the last power_iterate, original vertex order (host copy)"""
+        f = np.empty(self.n)
+        _lib.check(_lib.load().sc_graph_download_f(self.handle, _lib.ptr(f)))
+        return f
+
     def power_iterate_block(self, x0: np.ndarray, t: int, *, want_raw: bool = True):
         """t steps of the signless operator on an (n, L) block (pm_log_k's embedding,
         pipeline.py:144-147); returns (raw = M^t x0, scaled = raw * d^-1/2)."""
