@@ -16,7 +16,7 @@ gp = Graph(n=g.n, row_offsets=bench.pinned_copy(g.row_offsets),
            degrees=bench.pinned_copy(g.degrees))
 for rep in range(5):
     t = [time.perf_counter()]
-    dg = DeviceGraph(gp); t.append(time.perf_counter())
+    dg = DeviceGraph(gp, panels=True); t.append(time.perf_counter())
     dg.sample_irwin_hall(0); t.append(time.perf_counter())
     _, f = dg.power_iterate(T, want_x=False); t.append(time.perf_counter())
     km = KMeans1D(graph=dg); t.append(time.perf_counter())
