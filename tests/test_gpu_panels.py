@@ -200,3 +200,23 @@ def test_shard_panels_on_one_gpu_bit_exact(world, aligned):
     assert np.array_equal(fs, f)
     for s in shards:
         s.close()
+
+
+@pytest.mark.parametrize("n", [3392, 3393, 6785])
+def test_row_block_boundaries(n):
+    """one full row block, a last block of a single (odd) row, and one of one row past two
+    blocks: the epilogue's prefetch path and its direct-load fallback"""
+    g = _blocked(n, n, 4, 0, seed=n)  # ~8 entries per row: stages fit at 1696 rows per CTA
+    _compare(g, 6)
+
+
+def test_long_segment_declined():
+    """a row with >= 128 entries inside one panel exceeds the segment count field: declined"""
+    rng = np.random.default_rng(13)
+    n = 20_000
+    u = rng.integers(0, n, 12 * n)
+    v = (u + rng.integers(1, 2000, u.size)) % n
+    hub_v = rng.choice(np.arange(1, 4000), 200, replace=False)  # 200 neighbours in panel 0
+    g = _simple(n, np.concatenate([u, np.zeros(200, np.int64)]), np.concatenate([v, hub_v]))
+    assert np.diff(g.row_offsets).max() <= 256
+    _compare(g, 5, expect_panels=False)
