@@ -530,8 +530,8 @@ __global__ void __launch_bounds__(kPanTPB) k_pan_fill(const int64_t *slice_ptr, 
 // Bank-aware lane assignment: the 32 segments of an iteration may sit in any lanes (a segment
 // moves with its entries, so every row keeps its order).  part[row] is a double, so rows r
 // and r' collide in a half-warp access when r == r' (mod 16); this places the segments so
-// that each half-warp sees distinct residues where possible (greedy; dummy rows share one
-// address and are free), cutting the replayed wavefronts of the part[] loads and stores.
+// that each half-warp sees each residue at most about half as often (one match_any + two
+// ballots per iteration), cutting the replayed wavefronts of the part[] loads and stores.
 __global__ void __launch_bounds__(256) k_pan_balance(const PanGroup *__restrict__ grp,
                                                      uint8_t *__restrict__ stream) {
     const PanGroup m = grp[blockIdx.x];
@@ -545,22 +545,18 @@ __global__ void __launch_bounds__(256) k_pan_balance(const PanGroup *__restrict_
         const uint32_t base = h & 0xffffffu;
         const uint16_t row = rows[q * 32 + lane];
         const bool dummy = row >= kPanR;
-        const int bank = row & 15;
-        uint32_t used[2] = {0u, 0u};
-        int cnt[2] = {0, 0}, mine = lane;
-        for (int pass = 0; pass < 2; ++pass)  // real segments first, then the dummies
-            for (int i = 0; i < 32; ++i) {
-                const int bi = __shfl_sync(0xffffffffu, bank, i);
-                const bool di = __shfl_sync(0xffffffffu, dummy, i);
-                if (di != (pass == 1)) continue;
-                int half;
-                if (!di && cnt[0] < 16 && !((used[0] >> bi) & 1)) half = 0;
-                else if (!di && cnt[1] < 16 && !((used[1] >> bi) & 1)) half = 1;
-                else half = cnt[0] < 16 ? 0 : 1;
-                if (!di) used[half] |= 1u << bi;
-                if (i == lane) mine = half * 16 + cnt[half];
-                ++cnt[half];
-            }
+        // the k-th segment (in lane order) of each residue goes to half k & 1; dummy rows share
+        // one address and are spread the same way; overflow of a half spills into the other
+        const int bank = dummy ? 16 : (row & 15);
+        const uint32_t lt = (1u << lane) - 1u;
+        const unsigned same = __match_any_sync(0xffffffffu, bank);
+        const int half = __popc(same & lt) & 1;
+        const unsigned inA = __ballot_sync(0xffffffffu, half == 0);
+        const int nA = __popc(inA);
+        const int pos = __popc((half == 0 ? inA : ~inA) & lt);
+        int mine;
+        if (half == 0) mine = pos < 16 ? pos : 16 + (32 - nA) + (pos - 16);
+        else mine = pos < 16 ? 16 + pos : nA + (pos - 16);
         __syncwarp();
         rows[q * 32 + mine] = row;
         if (m.panel >= 0) {
