@@ -275,6 +275,25 @@ def roofline_for(g, info, kernel_ms, reads_val: bool):
     return r
 
 
+def smem_ceiling(cfg: int, kernel_ms: float):
+    """The column-panel kernel gathers z from shared memory: its data-pipe bound is one
+    shared-memory wavefront per SM-cycle.  Wavefronts per launch come from the committed ncu
+    capture (bank conflicts included); the SM clock is the B200 boost clock."""
+    p = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        wf = json.load(fh).get(f"c{cfg}_unit_panels_smem_wavefronts")
+    if not wf:
+        return None
+    sms, ghz = 148, 1.965
+    t_us = wf / sms / (ghz * 1e3)
+    return {"wavefronts_per_launch": wf, "bound_us": t_us, "kernel_us": kernel_ms * 1e3,
+            "frac": t_us / (kernel_ms * 1e3),
+            "source": "profiles/r01_spmv_panel_ncu_full.txt (l1tex__data_pipe_lsu_wavefronts_mem_shared.sum), "
+                      "148 SMs x 1.965 GHz x 1 wavefront/cycle"}
+
+
 def gather_ceiling():
     p = os.path.join(ROOT, "profiles", "gather_ceiling.json")
     if not os.path.exists(p):
@@ -309,6 +328,8 @@ def run_b200(args):
     roofline = roofline_for(g, info, kernel_ms, reads_val=not unit)
     roofline["traffic"] = traffic_from_profiles(args.config, unit, layout)
     roofline["layout"] = layout
+    if layout == "panels":
+        roofline["smem_ceiling"] = smem_ceiling(args.config, kernel_ms)
     dev.close()
     # the same graph through the weighted kernel (weights streamed even though all 1.0):
     # the north-star byte formula nnz*(idx+val) applies to this one
