@@ -1,5 +1,5 @@
 """Column-panel layout vs SELL on one handle (bench configs): build time, per-step kernel time
-from the T-step CUDA graph, bit-identity.  Usage: python tools/panel_probe.py [cfg ...]"""
+from the T-step CUDA graph, bit-identity.  Usage: python tools/panel_probe.py [cfg ...] [--weighted]"""
 import os
 import sys
 import time
@@ -12,13 +12,14 @@ import numpy as np  # noqa: E402
 import bench  # noqa: E402
 from paper_2310_10939_b200 import DeviceGraph  # noqa: E402
 
-cfgs = [int(a) for a in sys.argv[1:]] or [2]
+weighted = "--weighted" in sys.argv
+cfgs = [int(a) for a in sys.argv[1:] if a.isdigit()] or [2]
 for cfg in cfgs:
     t = time.time()
     g, T, k = bench.build_config(cfg)
     print(f"cfg {cfg}: n={g.n} nnz={g.nnz} built in {time.time() - t:.1f}s", flush=True)
     t = time.time()
-    dg = DeviceGraph(g, panels=True)
+    dg = DeviceGraph(g, panels=True, keep_weights=weighted)
     t_create = time.time() - t
     info = dg.info()
     print(f"  handle {t_create * 1e3:.0f} ms; panel groups {info['panel_groups']} "
