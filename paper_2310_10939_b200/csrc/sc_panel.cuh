@@ -3,9 +3,9 @@
 //
 // Why: the SELL kernel gathers every z value from L2 and runs at the L1->L2 random-request
 // limit (one 8-byte gather per SM-cycle).  When a block of rows references a
-// few contiguous column ranges heavily (planted-partition graphs numbered by block, BFS
-// pre-ordered graphs), those ranges ("panels" of kPanZ doubles) can be staged in shared
-// memory by TMA and gathered there at many per cycle; the thin remainder is gathered from L2.
+// few contiguous column ranges heavily (planted-partition graphs numbered by block), those
+// ranges ("panels" of kPanZ doubles) can be staged in shared memory by TMA and gathered there
+// at many per cycle; the thin remainder is gathered from L2.
 //
 // Exactness: a lane adds its row's entries strictly in stored column order.  Rows are split
 // into "segments" (row, entries of the row inside one group of columns); groups of a CTA are
@@ -15,7 +15,8 @@
 // +0.0, an exact no-op (a running sum that starts at +0.0 is never -0.0).
 //
 // Layout (built on the device from the SELL arrays, so it works on renumbered ids):
-//   CTA b owns renumbered rows [b*kPanR, (b+1)*kPanR).  Its columns are cut into groups:
+//   CTA b owns renumbered rows [b*rpc, (b+1)*rpc), rpc = kPanR unless stages would overflow
+//   the ring (then halved until they fit).  Its columns are cut into groups:
 //   a panel (kPanZ columns) with >= kPanThresh of the CTA's entries is a dense group (z panel
 //   staged in shared memory, 16-bit panel-local indices); runs of the other panels form sparse
 //   groups (32-bit indices, z gathered from global memory).  One group's data is a "stage":
@@ -23,7 +24,8 @@
 //     u16 row[32 nq]   local row of each segment (kPanR = dummy)
 //     entries          iteration q, entry k of lane l at base + 32 k + l
 //   Segments are sorted by decreasing count, so the 32 segments of an iteration have (nearly)
-//   the same count and the warp runs without divergence; one thread streams the stages into
+//   the same count and the warp runs without divergence (k_pan_balance then places them in
+//   lanes bank-aware for part[]); one thread streams the stages into
 //   a shared-memory ring with bulk copies (cp.async.bulk + mbarrier).  Sparse padding entries
 //   index z[ncols], a zero slot kept past the vector (sc_graph::zstride > ncols for whole
 //   graphs; shard callers pass z buffers with the same padding, see sc_graph_build_panels).
@@ -51,7 +53,7 @@ struct PanGroup {
     uint32_t eoff;   // byte offset of the entries
     uint64_t off;    // byte offset of the stage in the stream
     uint32_t bytes;  // stage bytes (multiple of 16)
-    uint32_t pad_;
+    uint32_t unused;
 };
 
 __device__ __forceinline__ uint32_t pan_smem_u32(const void *p) {
@@ -579,15 +581,12 @@ __global__ void __launch_bounds__(256) k_pan_balance(const PanGroup *__restrict_
     }
 }
 
-// Builds g's panel layout from its SELL arrays.  Returns SC_OK with g->pan_ctas == 0 when the
-// graph does not qualify (weighted, wide rows, shard, too many panels/groups, long segments,
-// a stage larger than the ring slot); CUDA errors are returned.
 static int32_t build_panels_rpc(sc_graph *g, bool prof, int rpc, int32_t *declined);
 
 // Builds g's panel layout from its SELL arrays.  Returns SC_OK with g->pan_ctas == 0 when the
-// graph does not qualify (weighted, wide rows, shard, too many panels/groups, long segments);
-// a stage larger than the ring slot is retried with half the rows per CTA.  CUDA errors are
-// returned.
+// graph does not qualify (weighted, wide rows, too many panels/groups, long segments, rows
+// that revisit a panel, too little dense coverage or too short dense segments); a stage
+// larger than the ring slot is retried with half the rows per CTA.  CUDA errors are returned.
 static int32_t build_panels(sc_graph *g, bool prof) {
     g->pan_ctas = 0;
     const int64_t n = g->n;
