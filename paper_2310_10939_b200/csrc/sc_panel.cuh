@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kPanTPB) k_pan_plan(const int64_t *slice_ptr, 
         int ng = 0, last_sparse = 0;
         uint32_t run = 0;
         unsigned long long dense_e = 0, all_e = 0;
-        const uint32_t budget = slot_cap - slot_cap / 4;
+        const uint32_t budget = slot_cap - slot_cap / 10;
         for (int s0 = 0; s0 < S; s0 += 32) {
             const uint32_t c = s0 + lane < S ? hist[s0 + lane] : 0;
             uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kPanTPB) k_pan_plan(const int64_t *slice_ptr, 
                 nz &= nz - 1;
                 const uint32_t cs = __shfl_sync(0xffffffffu, c, l);
                 const int s = s0 + l;
-                const uint32_t est = cs * 7;  // >= stage bytes per entry (idx + row + hdr)
+                const uint32_t est = cs * 13 / 2;  // ~ stage bytes per entry (idx + row + hdr)
                 if (lane == 0) {
                     all_e += cs;
                     if (cs >= (uint32_t)kPanThresh) dense_e += cs;
