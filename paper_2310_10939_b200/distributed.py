@@ -154,12 +154,15 @@ def exchange_plan(local_row_ptr: np.ndarray, starts: np.ndarray, rank: int, worl
 
 
 class HaloPlan:
-    """z space of one rank for the halo exchange (SURVEY §8(e) option 2): the rank's own rows
-    in renumbered order (slots [0, n)), then the remote entries its rows reference, grouped by
-    owner rank and sorted by global id.  Per step every rank sends each peer only the own
-    entries that peer references (``send_idx``, local renumbered slots, in the peer's halo
-    order) -- at config 5 on 8 GPUs ~19 M entries per GPU instead of the 87.5 M an all-gather
-    delivers.  Columns are only renamed, never reordered, so results stay bit-identical.
+    """z space of one rank for the halo exchange (SURVEY §8(e) option 2): the remote entries
+    its rows reference, grouped by owner rank and sorted by global id, with the rank's own rows
+    (renumbered order) in between -- owners below the rank first, then the own rows starting on
+    an 8192-slot boundary (``base``), then owners above.  That keeps every row's renamed
+    columns in stored (global id) order across 8192-column panels, so the column-panel layout
+    applies to halo shards too.  Per step every rank sends each peer only the own entries that
+    peer references (``send_idx``: z-space slots of its own rows, in the peer's halo order) --
+    at config 5 on 8 GPUs ~19 M entries per GPU instead of the 87.5 M an all-gather delivers.
+    Columns are only renamed, never reordered, so results stay bit-identical.
 
     Exposes the ShardPlan attributes CudaShard uses (one piece)."""
 
@@ -178,9 +181,14 @@ class HaloPlan:
         self.pieces = 1
         self.bounds = [np.array([0, int(sz)], dtype=np.int64) for sz in self.sizes]
         self.halo_ids = [np.asarray(h, dtype=np.int64) for h in halo_ids]  # per owner
-        self.send_idx = [np.asarray(h, dtype=np.int32) for h in send_idx]  # per peer
         cnt = np.array([h.size for h in self.halo_ids], dtype=np.int64)
-        self.halo_off = n + np.concatenate([[0], np.cumsum(cnt)])  # owner q: [off[q], off[q+1])
+        self.n_low = int(cnt[:rank].sum())                      # halo entries of lower owners
+        self.base = -(-self.n_low // 8192) * 8192               # first own slot
+        off = np.concatenate([[0], np.cumsum(cnt)])
+        off[rank + 1:] += self.base + n - self.n_low            # higher owners after own rows
+        self.halo_off = off  # owner q: [off[q], off[q+1]) (empty for q == rank)
+        self.send_idx = [np.asarray(h, dtype=np.int64).astype(np.int32) + self.base
+                         for h in send_idx]  # per peer, z-space slots of own rows
         self.n_halo = int(cnt.sum())
         self.pmax = n
         self.n_max = int(self.sizes.max())
@@ -192,20 +200,21 @@ class HaloPlan:
 
     @property
     def ncols(self) -> int:
-        return self.n + self.n_halo
+        return self.base + self.n + self.n_halo - self.n_low
 
     def own(self, j: int, rank: int) -> tuple[int, int]:
-        return 0, self.n
+        return self.base, self.base + self.n
 
     def rename(self, col_global: np.ndarray) -> np.ndarray:
         c = np.asarray(col_global, dtype=np.int64)
         lo, hi = int(self.starts[self.rank]), int(self.starts[self.rank + 1])
         out = np.empty(c.size, dtype=np.int64)
         mine = (c >= lo) & (c < hi)
-        out[mine] = self._inv[c[mine] - lo]
+        out[mine] = self.base + self._inv[c[mine] - lo]
         # halo ids are sorted within each owner and owners are ordered by id range, so the
-        # concatenation is globally sorted
-        out[~mine] = self.n + np.searchsorted(self._halo_all, c[~mine])
+        # concatenation is globally sorted; lower owners' entries sit below the own rows
+        pos = np.searchsorted(self._halo_all, c[~mine])
+        out[~mine] = np.where(pos < self.n_low, pos, pos - self.n_low + self.base + self.n)
         return out.astype(np.int32)
 
 

@@ -161,11 +161,19 @@ def test_halo_plans_local_match_distributed_lists():
     for r, pl in enumerate(plans):
         ren = pl.rename(lcols[r])
         assert ren.min() >= 0 and ren.max() < pl.ncols
+        # own rows start on an 8192-slot boundary and the halo blocks keep global-id order, so
+        # along every row the renamed columns never go back to an earlier 4096-slot window (the
+        # column-panel layout's condition)
+        assert pl.base % 8192 == 0 and pl.own(0, r) == (pl.base, pl.base + pl.n)
+        lr = lrps[r]
+        for i in range(pl.n):
+            w = ren[lr[i]:lr[i + 1]] // 4096
+            assert np.all(np.diff(w) >= 0)
         for q in range(3):
             if q == r:
                 continue
             # the ids q sends to r, mapped back through q's renumbering, are r's halo ids from q
-            sent = plans[q].perms[q][plans[q].send_idx[r]] + starts[q]
+            sent = plans[q].perms[q][plans[q].send_idx[r] - plans[q].base] + starts[q]
             assert np.array_equal(sent, pl.halo_ids[q])
 
 

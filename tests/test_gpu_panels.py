@@ -220,3 +220,60 @@ def test_long_segment_declined():
     g = _simple(n, np.concatenate([u, np.zeros(200, np.int64)]), np.concatenate([v, hub_v]))
     assert np.diff(g.row_offsets).max() <= 256
     _compare(g, 5, expect_panels=False)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_shard_panels_on_one_gpu_bit_exact(world):
+    """halo z spaces (lower owners' entries | own rows on an 8192 boundary | higher owners')
+    keep stored column order, so every halo shard takes the panel layout; the exchange is
+    emulated by packs copied into the peers' halo slots"""
+    import torch
+
+    from paper_2310_10939_b200 import distributed as D
+
+    g = _blocked(150_000, 50_000, 20, 2, seed=17)
+    rp, col, deg = g.row_offsets, g.col_indices.astype(np.int32), g.degrees
+    starts = D.partition_rows(rp, world)
+    lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(world)]
+    lcols = [col[rp[starts[r]]:rp[starts[r + 1]]] for r in range(world)]
+    plans = D.halo_plans_local(lrps, lcols, starts)
+    shards = []
+    for r in range(world):
+        s = D.CudaShard(lrps[r], plans[r].rename(lcols[r]), None, deg[starts[r]:starts[r + 1]],
+                        plans[r], r, 0)
+        assert s.build_panels()
+        shards.append(s)
+    z = [[s.zspace(plans[r].ncols), s.zspace(plans[r].ncols)] for r, s in enumerate(shards)]
+    x = [[s.zeros(s.n), s.zeros(s.n)] for s in shards]
+    x0 = [s.zeros(s.n) for s in shards]
+    idx = [[torch.from_numpy(plans[q].send_idx[r]).cuda() for r in range(world)]
+           for q in range(world)]
+
+    def exchange(b):
+        for r in range(world):
+            for q in range(world):
+                if q == r or idx[q][r].numel() == 0:
+                    continue
+                buf = shards[q].zeros(idx[q][r].numel())
+                shards[q].pack(z[q][b], idx[q][r], buf)
+                a, e = int(plans[r].halo_off[q]), int(plans[r].halo_off[q + 1])
+                z[r][b][a:e].copy_(buf)
+        torch.cuda.synchronize()
+
+    T = 8
+    for r, s in enumerate(shards):
+        s.irwin_hall(3, x0[r])
+        s.scale_piece(0, x0[r], z[r][0])
+    exchange(0)
+    for t in range(T):
+        a, b = t & 1, (t & 1) ^ 1
+        for r, s in enumerate(shards):
+            s.step_piece(0, z[r][a], x0[r] if t == 0 else x[r][a], x[r][b], z[r][b])
+        exchange(b)
+    xs = np.concatenate([s.to_original(x[r][T & 1]) for r, s in enumerate(shards)])
+    fs = np.concatenate([s.to_original(s.local_z(z[r][T & 1])) for r, s in enumerate(shards)])
+    xT, f = O.power_iterate(rp, col, None, deg, O.irwin_hall(deg, 3), T)
+    assert np.array_equal(xs, xT)
+    assert np.array_equal(fs, f)
+    for s in shards:
+        s.close()
