@@ -93,7 +93,7 @@ def build_config(cfg: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region (NVML, else nvidia-smi)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -105,19 +105,49 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
+    def _nvml_open(self):
+        """NVML handle, opened before the timed region starts (init costs ~0.1 s, longer than
+        a short timed region).  None if NVML is absent: nvidia-smi is polled instead."""
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml = (N, h, N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM),
+                          (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                           N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap))
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+            self.source = "nvidia-smi"
+
+    def _sample(self):
+        try:
+            if self._nvml:
+                N, h, mx, bits = self._nvml
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(sm), str(mx), "", hex(r)] +
+                                 ["Active" if r & b else "Not Active" for b in bits])
+            else:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
                 if out:
                     self.rows.append([v.strip() for v in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        except Exception:
+            pass
+
+    def _run(self):
+        # NVML every ~2 ms (the timed region is ~0.1 s, too short for nvidia-smi's ~50 ms/query)
+        period = 0.002 if self._nvml else 0.2
+        while True:
+            self._sample()
+            if self._stop.wait(period):
+                return
 
     def __enter__(self):
+        self._nvml_open()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -125,6 +155,9 @@ class ClockSampler:
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=6)
+        if self._nvml:
+            self._sample()  # the region's last clocks, however short it was
+            self._nvml[0].nvmlShutdown()
 
     def summary(self):
         if not self.rows:
@@ -136,7 +169,7 @@ class ClockSampler:
                           if len(r) > 4 + i and r[4 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": getattr(self, "source", None)}
 
 
 def peak_hbm():

@@ -739,11 +739,15 @@ def bench_main(args, metric: str, unit: str):
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        one_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    from bench import ClockSampler  # repo-root bench.py, the caller of bench_main
+
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    with clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -786,6 +790,7 @@ def bench_main(args, metric: str, unit: str):
             "exchange": {"kind": "halo send/recv" if halo else "all-gather",
                          "ms_per_step": ag_ms, "recv_bytes_per_gpu": recv_bytes,
                          "gbs_per_gpu": recv_bytes / (ag_ms / 1e3) / 1e9 if world > 1 else 0.0},
+            "clocks": clk.summary(),
             "gpu_launches": args.steps * (1 + (T + 1) * plan.pieces
                                           + ((T + 1) if p2p and world > 1 else 0)
                                           + ((T + 1) * sum(1 for q in comm.peers
