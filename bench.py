@@ -22,9 +22,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -90,86 +88,6 @@ def build_config(cfg: int):
     else:
         raise SystemExit(f"unknown config {cfg}")
     return g, CONFIG_T[cfg], CONFIG_K[cfg]
-
-
-class ClockSampler:
-    """SM clocks / throttle reasons sampled during the timed region (NVML, else nvidia-smi)."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int = 0):
-        self.index = index
-        self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _nvml_open(self):
-        """NVML handle, opened before the timed region starts (init costs ~0.1 s, longer than
-        a short timed region).  None if NVML is absent: nvidia-smi is polled instead."""
-        try:
-            import pynvml as N
-
-            N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            self._nvml = (N, h, N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM),
-                          (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
-                           N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap))
-            self.source = "nvml"
-        except Exception:
-            self._nvml = None
-            self.source = "nvidia-smi"
-
-    def _sample(self):
-        try:
-            if self._nvml:
-                N, h, mx, bits = self._nvml
-                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append([str(sm), str(mx), "", hex(r)] +
-                                 ["Active" if r & b else "Not Active" for b in bits])
-            else:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([v.strip() for v in out.split(",")])
-        except Exception:
-            pass
-
-    def _run(self):
-        # NVML every ~2 ms (the timed region is ~0.1 s, too short for nvidia-smi's ~50 ms/query)
-        period = 0.002 if self._nvml else 0.2
-        while True:
-            self._sample()
-            if self._stop.wait(period):
-                return
-
-    def __enter__(self):
-        self._nvml_open()
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        return self
-
-    def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=6)
-        if self._nvml:
-            self._sample()  # the region's last clocks, however short it was
-            self._nvml[0].nvmlShutdown()
-
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows), "source": getattr(self, "source", None)}
 
 
 def peak_hbm():
@@ -265,7 +183,9 @@ def time_power(dev, T, steps, warmup, clocks=False):
     for _ in range(max(warmup, 3)):
         dev.power_iterate(T, want_x=False, want_f=False)
     times = []
-    clk = ClockSampler() if clocks else None
+    from paper_2310_10939_b200.clocks import ClockSampler
+
+    clk = ClockSampler(dev.device) if clocks else None
     if clk:
         clk.__enter__()
     try:

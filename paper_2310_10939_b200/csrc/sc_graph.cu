@@ -781,7 +781,8 @@ size_t cache_cap() {
     return cap;
 }
 
-void *cache_take(int device, size_t bytes) {
+// returns a cached buffer of at least `bytes` and stores its real size in *got
+void *cache_take(int device, size_t bytes, size_t *got) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     int best = -1;
     for (int i = 0; i < (int)g_cache.size(); ++i) {
@@ -792,6 +793,7 @@ void *cache_take(int device, size_t bytes) {
     }
     if (best < 0) return nullptr;
     void *p = g_cache[best].p;
+    *got = g_cache[best].bytes;
     g_cache_bytes -= g_cache[best].bytes;
     g_cache.erase(g_cache.begin() + best);
     return p;
@@ -850,9 +852,10 @@ static int32_t dmalloc(sc_graph *g, void **p, size_t bytes) {
         g->bytes += (int64_t)bytes;
         return SC_OK;
     }
-    if ((*p = cache_take(g->device, bytes))) {
-        g->allocs.push_back({*p, bytes});
-        g->bytes += (int64_t)bytes;
+    size_t got = 0;
+    if ((*p = cache_take(g->device, bytes, &got))) {
+        g->allocs.push_back({*p, got});  // the real size, so the cache files it correctly
+        g->bytes += (int64_t)got;
         return SC_OK;
     }
     cudaError_t e = cudaMalloc(p, bytes);

@@ -24,6 +24,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "sc_common.cuh"
@@ -51,6 +52,8 @@ struct sc_kmeans {
     int32_t *h_changed = nullptr;    // pinned [2][R]
     int32_t *h_act = nullptr;        // pinned [2][2R]: active flags + compacted list per parity
     int cap_host_r = 0;
+    unsigned char *h_block = nullptr;  // owned pinned block behind h_cost/h_changed/h_act
+    size_t h_block_bytes = 0;
     // workspaces (grown on demand)
     int cap_r = 0, cap_k = 0;
     double *d_best = nullptr;      // [R][n] k-means++ D^2 weights
@@ -93,6 +96,35 @@ struct sc_kmeans {
 };
 
 namespace sc {
+
+// Pool of page-locked blocks shared by all k-means contexts of the process.  A block is
+// owned by exactly one context between pinned_take and pinned_give.
+std::mutex g_pinned_mu;
+std::vector<std::pair<size_t, unsigned char *>> g_pinned_free;
+
+unsigned char *pinned_take(size_t need) {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        size_t best = g_pinned_free.size();
+        for (size_t i = 0; i < g_pinned_free.size(); ++i)
+            if (g_pinned_free[i].first >= need &&
+                (best == g_pinned_free.size() || g_pinned_free[i].first < g_pinned_free[best].first))
+                best = i;
+        if (best < g_pinned_free.size()) {
+            unsigned char *p = g_pinned_free[best].second;
+            g_pinned_free.erase(g_pinned_free.begin() + best);
+            return p;
+        }
+    }
+    unsigned char *p = nullptr;
+    if (cudaMallocHost((void **)&p, need) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void pinned_give(unsigned char *p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.emplace_back(bytes, p);
+}
 
 constexpr int kEinsumBuf = 8192;  // numpy nditer buffer size (elements)
 
@@ -1477,24 +1509,19 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_changed, (size_t)2 * R, km->stream))) return st;
     if ((st = grow(&km->d_active, (size_t)2 * R, km->stream))) return st;
     if (R > km->cap_host_r) {
-        // page-locked result/flag slots live in a per-thread arena that outlives the
-        // context (cudaMallocHost/cudaFreeHost per clustering would cost milliseconds)
-        thread_local struct Arena {
-            unsigned char *p = nullptr;
-            size_t bytes = 0;
-        } arena;
+        // page-locked result/flag slots: each context owns one block drawn from a
+        // process-wide pool (cudaMallocHost per clustering would cost milliseconds); a block
+        // goes back to the pool only when its context grows or is destroyed, so no other
+        // context ever holds a pointer into it
         const size_t need = (size_t)R * (16 + 8 + 16);
-        if (arena.bytes < need) {
-            if (arena.p) cudaFreeHost(arena.p);
-            arena.p = nullptr;
-            arena.bytes = 0;
-            if (cudaMallocHost((void **)&arena.p, need) != cudaSuccess)
-                return fail(SC_E_OOM, "pinned host buffers");
-            arena.bytes = need;
-        }
-        km->h_cost = reinterpret_cast<double *>(arena.p);
-        km->h_changed = reinterpret_cast<int32_t *>(arena.p + (size_t)R * 16);
-        km->h_act = reinterpret_cast<int32_t *>(arena.p + (size_t)R * 24);
+        unsigned char *blk = pinned_take(need);
+        if (!blk) return fail(SC_E_OOM, "pinned host buffers");
+        if (km->h_block) pinned_give(km->h_block, km->h_block_bytes);
+        km->h_block = blk;
+        km->h_block_bytes = need;
+        km->h_cost = reinterpret_cast<double *>(blk);
+        km->h_changed = reinterpret_cast<int32_t *>(blk + (size_t)R * 16);
+        km->h_act = reinterpret_cast<int32_t *>(blk + (size_t)R * 24);
         km->cap_host_r = R;
     }
     if ((st = grow(&km->d_empty, (size_t)R, km->stream))) return st;
@@ -1642,6 +1669,7 @@ void sc_kmeans_destroy(sc_kmeans *km) {
     if (km->stream2) cudaStreamDestroy(km->stream2);
     if (km->ev_main) cudaEventDestroy(km->ev_main);
     if (km->ev_cost) cudaEventDestroy(km->ev_cost);
+    if (km->h_block) pinned_give(km->h_block, km->h_block_bytes);
     delete km;
 }
 
@@ -1966,6 +1994,12 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             const bool fin = std::isfinite(prev[r]);
             const bool unchanged = hch[r] == 0 && fin;
             const double c = hc[r];
+            // kmeans.py:206: assert cost <= prev_cost * (1 + 1e-12) + 1e-12
+            if (!(c <= prev[r] * (1.0 + 1e-12) + 1e-12)) {
+                cudaStreamSynchronize(s);
+                return fail(SC_E_INTERNAL, "k-means cost increased (restart %d, iteration %d: "
+                            "%.17g > %.17g)", r, iters[r], c, prev[r]);
+            }
             const bool small_gain = fin && (prev[r] - c <= tol * std::max(prev[r], 1e-300));
             if (r == 0 && trace)
                 fprintf(stderr, "exact  r0 it %d cost %.17g changed %d\n", iters[r], c, hch[r]);

@@ -186,7 +186,9 @@ class HaloPlan:
         self.base = -(-self.n_low // 8192) * 8192               # first own slot
         off = np.concatenate([[0], np.cumsum(cnt)])
         off[rank + 1:] += self.base + n - self.n_low            # higher owners after own rows
-        self.halo_off = off  # owner q: [off[q], off[q+1]) (empty for q == rank)
+        # owner q != rank: halo slots [off[q], off[q+1]).  off[rank] .. off[rank+1] spans the
+        # alignment padding and the own rows, so it is NOT a halo range -- use halo_range(q).
+        self.halo_off = off
         self.send_idx = [np.asarray(h, dtype=np.int64).astype(np.int32) + self.base
                          for h in send_idx]  # per peer, z-space slots of own rows
         self.n_halo = int(cnt.sum())
@@ -201,6 +203,12 @@ class HaloPlan:
     @property
     def ncols(self) -> int:
         return self.base + self.n + self.n_halo - self.n_low
+
+    def halo_range(self, q: int) -> tuple[int, int]:
+        """z-space slots [a, b) that receive owner q's entries (q != rank)."""
+        if q == self.rank:
+            raise ValueError("a rank has no halo range of its own")
+        return int(self.halo_off[q]), int(self.halo_off[q + 1])
 
     def own(self, j: int, rank: int) -> tuple[int, int]:
         return self.base, self.base + self.n
@@ -550,7 +558,7 @@ class HaloComm:
             if self.sbuf[q].numel():
                 self.shard.pack(z_full, self.idx[q], self.sbuf[q])
                 ops.append(dist.P2POp(dist.isend, self.sbuf[q], q, self.group))
-            a, b = int(plan.halo_off[q]), int(plan.halo_off[q + 1])
+            a, b = plan.halo_range(q)
             if b > a:
                 ops.append(dist.P2POp(dist.irecv, z_full[a:b], q, self.group))
         if ops:
@@ -739,9 +747,9 @@ def bench_main(args, metric: str, unit: str):
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    from bench import ClockSampler  # repo-root bench.py, the caller of bench_main
+    from .clocks import ClockSampler
 
-    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk = ClockSampler(torch.cuda.current_device())
     with clk:
         e0.record(stream)
         for _ in range(args.steps):

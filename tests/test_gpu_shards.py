@@ -102,7 +102,7 @@ def test_halo_shards_on_one_gpu_bit_exact(world):
                     continue
                 buf = shards[q].zeros(idx[q][r].numel())
                 shards[q].pack(z[q][b], idx[q][r], buf)
-                a, e = int(plans[r].halo_off[q]), int(plans[r].halo_off[q + 1])
+                a, e = plans[r].halo_range(q)
                 z[r][b][a:e].copy_(buf)
         torch.cuda.synchronize()
 
