@@ -33,6 +33,12 @@ namespace cg = cooperative_groups;
 #include "sc_seqsum.cuh"
 
 namespace sc {
+struct FusedLloyd;  // sc_kmeans_fused.cu
+bool fused_lloyd_eligible(int l, int k, int R, int64_t n);
+int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s, const double *d_x,
+                    int64_t n, int k, int R, const int64_t *d_chosen, int max_iters, double tol,
+                    int64_t *labels_out, double *costs_out, int32_t *iters_out, int32_t *best_out);
+void fused_lloyd_free(FusedLloyd *f);
 const double *graph_f_device(sc_graph *g);
 int64_t graph_n(const sc_graph *g);
 int graph_device(const sc_graph *g);
@@ -52,6 +58,7 @@ struct sc_kmeans {
     int32_t *h_changed = nullptr;    // pinned [2][R]
     int32_t *h_act = nullptr;        // pinned [2][2R]: active flags + compacted list per parity
     int cap_host_r = 0;
+    sc::FusedLloyd *fused = nullptr;  // persistent exact Lloyd (1-D, one sign, k <= 32)
     unsigned char *h_block = nullptr;  // owned pinned block behind h_cost/h_changed/h_act
     size_t h_block_bytes = 0;
     // workspaces (grown on demand)
@@ -1670,6 +1677,7 @@ void sc_kmeans_destroy(sc_kmeans *km) {
     if (km->ev_main) cudaEventDestroy(km->ev_main);
     if (km->ev_cost) cudaEventDestroy(km->ev_cost);
     if (km->h_block) pinned_give(km->h_block, km->h_block_bytes);
+    fused_lloyd_free(km->fused);
     delete km;
 }
 
@@ -1769,6 +1777,19 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     const int64_t nbuf = (n * l + kEinsumBuf - 1) / kEinsumBuf;
     const int rk = R * k;
     SC_CUDA(cudaMemcpyAsync(km->d_chosen, chosen, (size_t)rk * 8, cudaMemcpyHostToDevice, s));
+    if (fused_lloyd_eligible(l, k, R, n)) {
+        // every iteration of every restart in one persistent kernel (sc_kmeans_fused.cu);
+        // 1 = not applicable (points of both signs): the general path below
+        st = fused_lloyd(&km->fused, km->device, km->sm_count, s, km->d_x, n, k, R, km->d_chosen,
+                         max_iters, tol, labels_out, costs_out, iters_out, best_restart_out);
+        if (st != 1) {
+            if (ms_out)
+                *ms_out = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+            return st;
+        }
+        st = SC_OK;
+    }
     k_gather_centers<<<(rk * l + 255) / 256, 256, 0, s>>>(km->d_x, km->d_chosen, rk, l, km->d_cen);
     // labels start at zero (kmeans.py:195)
     SC_CUDA(cudaMemsetAsync(km->d_lab[0], 0, (size_t)R * n * 4, s));
