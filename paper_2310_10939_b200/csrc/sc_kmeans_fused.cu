@@ -1,6 +1,6 @@
 // sc_kmeans_fused.cu -- the exact restarted Lloyd (specluster/kmeans.py:167-215) for 1-D
 // points of one sign and k <= 32, every iteration of every restart inside ONE persistent
-// cooperative kernel: no host round trip, no sort, no per-phase launches.
+// cooperative kernel: no host round trip, no sort, two grid barriers per iteration.
 //
 // The arithmetic contract is the one of sc_kmeans.cu, element by element:
 //   distances   _sq_dists_to (kmeans.py:106-113) = d2ref, argmin lowest index (:199)
@@ -12,29 +12,40 @@
 //               orc_einsum_sumsq) -- see "stop decisions" below
 //   stop rules  kmeans.py:202-210, the cost assertion of :206, best = first strictly smallest
 //
-// How the means stay exact without sorting.  Points are cut into chunks of 1024 consecutive
-// indices (32 per lane, lane-contiguous).  Per (restart r, cluster j):
-//   P1  one warp per (r, chunk): assignment, changed count, and per cluster present in the
-//       chunk its count and an approximate sum (any order);
-//   P2  one warp per (r, j): approximate prefix over the chunks -> the binade the exact
-//       running sum is expected to sit in across each chunk (sc_seqsum.cuh "ulp grid");
-//   P3  one warp per (r, chunk): for each cluster whose chunk has a predicted binade, the
-//       parity map of its elements (sc_seqsum.cuh PMap) on that grid, composed in index order;
-//   P4  one warp per (r, j): walks the chunks in order with the EXACT running sum: 32 chunk
-//       maps are composed and applied at once when they share the running sum's grid and the
-//       result stays inside the binade, otherwise chunk by chunk, and a chunk whose prediction
-//       fails (a binade crossing) is added element by element.  Every shortcut is verified
-//       against the exact value, so predictions only decide speed, never bits.  The points
-//       are of one sign (x < 0 inputs run on -x: d2ref, the means and the cost are odd/even
-//       functions under exact negation), so running sums are monotone and "start and end in
-//       one binade" proves that no intermediate sum left it.
+// Assignment.  Per restart the distinct centres are sorted; around each midpoint a band of
+// half-width 8 u M^2 / gap bounds where the rounding of d2ref can decide (CenTab below).  A
+// point outside every band takes its interval's centre with integer compares only; inside a
+// band the two neighbours are evaluated with d2ref.
+//
+// Exact means without sorting.  Points are cut into chunks of 1024 consecutive indices.
+// Inside one binade of the running sum every double is a multiple of its ulp u, so
+// fl(s + a) = s + u * rne(a / u): a point acts on S = s/u as a translation by q or q+1
+// (sc_seqsum.cuh "parity map"), except on an exact tie (a/u = q + 1/2), where the result is
+// the even neighbour.  Per iteration:
+//   P1   one warp per (restart, chunk): assignment, the cost terms of the previous
+//        iteration, per cluster the count and an approximate sum, and -- for every cluster
+//        whose running sum the previous iteration predicted to stay in one binade across the
+//        chunk -- the chunk's parity map on that grid: the plain sum of the translations, or
+//        an index-ordered composition if a tie occurs.  Lanes take points 32 apart, so every
+//        load is coalesced and the chunk is staged by cp.async.
+//   P24  one warp per (restart, cluster): an approximate prefix over the chunks gives the
+//        binade predictions for the next iteration, and the EXACT walk over the chunks runs
+//        alongside: maximal runs of chunks mapped on the running sum's grid advance with one
+//        composed map (verified: the result must stay below the binade's top, which for a
+//        monotone sum proves no intermediate left it); any other chunk holding the cluster
+//        is added element by element from a staged tile (lanes own runs of 32; a run whose
+//        predicted binade is the running one advances by its map, a run holding a crossing
+//        adds its points one by one).  The walk writes the cluster's mean.
+//   Predictions only choose between these paths; every bit comes from a verified step.  The
+//   points are of one sign (x < 0 inputs run on -x: d2ref, the sums and the cost commute
+//   with exact negation), so running sums are monotone.
 //
 // Stop decisions without the einsum chain.  The reference's cost is a sum of the terms
 // t_i = fl(fl(x_i - mu)^2) in numpy's einsum order: chains of <= 4096 dependent adds per
 // 8192-element buffer, then one add per buffer.  Each iteration computes instead C~, the same
 // terms summed in a fixed tree order, and the proven bound |C - C~| <= delta * C~ with
-// delta = 2 * (4097 + nbuf + depth(tree)) * 2^-53 (both are sums of the same nonnegative
-// terms; each term passes through at most that many roundings).  The stop rule
+// delta = 2 * (4097 + nbuf + depth(tree)) * 2^-53 (sums of the same nonnegative terms; each
+// term passes through at most that many roundings).  The stop rule
 // (fl(P - C) <= fl(tol * max(P, 1e-300))) and the assertion are evaluated on intervals; only
 // if an interval straddles the threshold are the exact einsum-order costs of that iteration
 // and of the previous one computed (same kernel, all warps).  Unchanged labels stop without a
@@ -43,7 +54,7 @@
 //
 // Speculation.  P1 of iteration it+1 also accumulates the cost terms of iteration it (the
 // same pass reads x, the labels of it and the means of it), so the stop decision for it is
-// taken in P2 of it+1; a restart that stops ignores the work it did for it+1.  Labels and
+// taken in P24 of it+1; a restart that stops ignores the work it did for it+1.  Labels and
 // centres are triple-buffered so the previous iteration's labels/means survive for an exact
 // cost recomputation.
 #include <cuda_runtime.h>
@@ -63,21 +74,27 @@ namespace cg = cooperative_groups;
 namespace sc {
 
 constexpr int kFlChunk = 1024;  // points per chunk
-constexpr int kFlLane = 32;     // points per lane (lane-contiguous)
+constexpr int kFlLane = 32;     // points per lane
 constexpr int kFlMaxK = 32;
 constexpr int kFlMaxR = 64;
-constexpr int kFlMaxRK = 1024;
+constexpr int kFlMaxRK = 512;
 constexpr int kFlThreads = 256;
 constexpr int kFlWarps = kFlThreads / 32;
 constexpr int kFlEinsumBuf = 8192;
 constexpr int kSkip = kNoGrid + 1;  // chunk holds no element of the cluster
-constexpr int kCrossTag = 1 << 20;   // pred = kCrossTag + grid: one binade crossing predicted
+constexpr int kFlStage = 256;       // exact-cost staging window per warp
+constexpr int kXsPitch = 33;        // padded tile: lane t's run of 32 at xs[t * 33 + q]
+constexpr int kXsWarp = 32 * kXsPitch;
+constexpr int kTileBytes = kXsWarp * 8 + kFlChunk;  // x tile + label tile, per warp (>= 12 * 32 * k)
+// per-warp dynamic shared memory: the staging tile, or P1's accumulators (12 B per cluster
+// and lane)
+__host__ __device__ constexpr int fl_warp_bytes(int k) {
+    return ((kTileBytes > 12 * 32 * k ? kTileBytes : 12 * 32 * k) + 15) / 16 * 16;
+}
+
+constexpr int kCrossTag = 1 << 20;  // pred = kCrossTag + grid: one binade crossing predicted
 __device__ __forceinline__ bool is_cross(int p) { return p >= kCrossTag / 2; }
 __device__ __forceinline__ bool is_grid(int p) { return p > kSkip && p < kCrossTag / 2; }
-constexpr int kFlStage = 256;       // exact-cost staging window per warp
-constexpr int kXsPitch = 33;        // doubles per lane row of a warp's chunk tile (2-way banks)
-constexpr int kXsWarp = 32 * kXsPitch;
-constexpr int kFlDynSmem = kFlWarps * kXsWarp * 8;
 
 // control block (int32 slots)
 enum : int {
@@ -87,27 +104,33 @@ enum : int {
     kCtlErrIt = 3,
     kCtlIters = 4,    // iterations executed by the kernel
     kCtlBest = 5,
-    kCtlSlots = 8
+    kCtlNCross = 6,   // diagnostics: chunks added element by element
+    kCtlNTie = 7,     // diagnostics: chunk maps composed in index order (ties)
+    kCtlNX = 8,       // queued crossing records of the current iteration
+    kCtlSlots = 12
 };
 
 struct FlArgs {
     const double *x;  // [n] points, all >= 0
     int64_t n;
-    int64_t ln;        // label row stride (n rounded up to a chunk: aligned vector access)
+    int64_t ln;       // label row stride (n rounded up to a chunk)
     int k, R, nch, max_iters;
     int64_t nbuf;
+    int wd;            // doubles of dynamic shared memory per warp
     double tol, delta;
     double xmax;       // max point value (rounding bands of the sorted-centre assignment)
-    uint8_t *lab;      // [3][R][n]
+    uint8_t *lab;      // [3][R][ln]
     double *cen;       // [3][R][k]
     double *A;         // [R][k][nch] approximate chunk sums
     int32_t *cnt;      // [R][k][nch]
-    int32_t *pred;     // [R][k][nch] grid scale of the chunk, kNoGrid, kSkip
-    int64_t *M;        // [R][k][nch][2] parity maps (before the crossing, if any)
-    int64_t *MC;       // [R][k][nch][4] crossing chunks: map after, crossing value, grid after
+    int32_t *pred;     // [R][k][nch] grid, kCrossTag + grid, kNoGrid, kSkip
     double *AS;        // [R][k][nch] approximate running sum at each chunk start
+    int64_t *M;        // [R][k][nch] packed parity maps (before the crossing, if any)
+    int64_t *MC;       // [R][k][nch][2] crossing records: packed map after, crossing value
+    uint32_t *xlist;   // [R*k*nch] queued crossing records (c << 11 | r << 5 | j)
+    int32_t *rng;      // [R][k][2] first and last chunk holding the cluster
     double *cpart;     // [R][nch] approximate cost partials
-    int32_t *tot;      // [R][k] cluster sizes
+    int32_t *tot;      // [2][R][k] cluster sizes of even / odd iterations (atomics)
     int32_t *changed;  // [2][R]
     int32_t *ctl;      // kCtlSlots
     int32_t *stop;     // [R] sticky: restart finished
@@ -115,7 +138,6 @@ struct FlArgs {
     int32_t *rep;      // [R]
     int32_t *final_it; // [R]
     double *capprox;   // [R] cost of the previous decided iteration (C~ or exact)
-    double *cfresh;    // [R] C~ of the iteration being decided
     double *bpart;     // [2][R][nbuf] exact cost buffer partials
     double *cexact;    // [R] exact final costs
     double *own;       // [n] repair scratch
@@ -127,10 +149,25 @@ struct FlArgs {
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ uint8_t *lab_buf(const FlArgs &a, int it, int r) {
-    return a.lab + ((size_t)(it % 3) * a.R + r) * a.ln;
+    return a.lab + ((size_t)(((it % 3) + 3) % 3) * a.R + r) * a.ln;
+}
+__device__ __forceinline__ int32_t *tot_buf(const FlArgs &a, int it) {
+    return a.tot + (size_t)(it & 1) * a.R * a.k;
 }
 __device__ __forceinline__ double *cen_buf(const FlArgs &a, int it, int r) {
     return a.cen + ((size_t)(it % 3) * a.R + r) * a.k;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // ordered (index-order) composition of the 32 lanes' maps; result valid in lane 0
@@ -146,7 +183,7 @@ __device__ __forceinline__ PMap warp_reduce_pmap(PMap m) {
     return m;
 }
 
-// fixed-order warp sum (deterministic); result in every lane
+// fixed-order warp sums (the xor butterfly gives every lane the same bits)
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -157,8 +194,14 @@ __device__ __forceinline__ int warp_isum(int v) {
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+__device__ __forceinline__ long long warp_lsum(long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
-// the labels of a lane's 32 points, packed 4 per word
+// the labels of a lane's 32 points, packed 4 per word (indices are compile-time in the
+// unrolled loops, so this lives in registers)
 struct Lab32 {
     uint32_t w[8];
     __device__ __forceinline__ int get(int t) const { return (w[t >> 2] >> (8 * (t & 3))) & 0xff; }
@@ -167,60 +210,30 @@ struct Lab32 {
     }
 };
 
-__device__ __forceinline__ void load_lab32(const uint8_t *p, int m, Lab32 &L) {
-    if (m == kFlLane) {
-        const uint4 a = __ldcg(reinterpret_cast<const uint4 *>(p));
-        const uint4 b = __ldcg(reinterpret_cast<const uint4 *>(p) + 1);
-        L.w[0] = a.x; L.w[1] = a.y; L.w[2] = a.z; L.w[3] = a.w;
-        L.w[4] = b.x; L.w[5] = b.y; L.w[6] = b.z; L.w[7] = b.w;
-    } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) L.w[q] = 0;
-#pragma unroll
-        for (int t = 0; t < kFlLane; ++t)
-            if (t < m) L.set(t, __ldcg(p + t));
-    }
+// The running sum s on its own grid k = grid_of(s).k: S = s / u is the significand (with the
+// implicit bit; for k = 1074 the subnormal range and the first normal binade share the ulp
+// 2^-1074, and S is the raw bit pattern).  Pure integer work on the walk's critical path.
+__device__ __forceinline__ int64_t run_units(double s, int k) {
+    return (int64_t)__double_as_longlong(s) - ((int64_t)(1074 - k) << 52);
+}
+__device__ __forceinline__ double run_from(int64_t S, int k) {  // S inside the grid's binade
+    return __longlong_as_double(((int64_t)(1074 - k) << 52) + S);
+}
+// a point on grid k (k in [-971, 1074]): x * 2^k by exact power-of-two multiplications
+__device__ __forceinline__ double elem_units(double x, int k) {
+    if (k <= 1000) return __dmul_rn(x, __longlong_as_double((int64_t)(1023 + k) << 52));
+    return __dmul_rn(__dmul_rn(x, __longlong_as_double((int64_t)(23 + k) << 52)),
+                     __longlong_as_double((int64_t)(1023 + 1000) << 52));
 }
 
-__device__ __forceinline__ void store_lab32(uint8_t *p, int m, const Lab32 &L) {
-    if (m == kFlLane) {
-        __stcg(reinterpret_cast<uint4 *>(p), make_uint4(L.w[0], L.w[1], L.w[2], L.w[3]));
-        __stcg(reinterpret_cast<uint4 *>(p) + 1, make_uint4(L.w[4], L.w[5], L.w[6], L.w[7]));
-    } else {
-#pragma unroll
-        for (int t = 0; t < kFlLane; ++t)
-            if (t < m) p[t] = (uint8_t)L.get(t);
-    }
+// A chunk map (i0, i1) has |i1 - i0| <= 1 (after the first tie both parities of the start
+// give an even value), so it packs into one word: i0 << 2 | (i1 - i0 + 1).
+__device__ __forceinline__ int64_t pack_map(PMap m) { return (m.i0 << 2) | (m.i1 - m.i0 + 1); }
+__device__ __forceinline__ PMap unpack_map(int64_t v) {
+    const int64_t i0 = v >> 2;
+    return PMap{i0, i0 + (v & 3) - 1};
 }
 
-// chunk c's points into the warp's tile: lane t's run of 32 at xs[t * kXsPitch + q]; zeros
-// past n.  Coalesced global loads (256 contiguous bytes per warp instruction), 8 in flight.
-__device__ __forceinline__ void stage_chunk(const FlArgs &a, int c, double *xs) {
-    const int lane = lane_id();
-    const int64_t base = (int64_t)c * kFlChunk;
-    __syncwarp();
-    if (base + kFlChunk <= a.n) {
-#pragma unroll
-        for (int g = 0; g < 32; g += 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldg(a.x + base + 32 * (g + u) + lane);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) xs[(g + u) * kXsPitch + lane] = v[u];
-        }
-    } else {
-        for (int u = 0; u < 32; ++u) {
-            const int64_t i = base + 32 * u + lane;
-            xs[u * kXsPitch + lane] = i < a.n ? __ldg(a.x + i) : 0.0;
-        }
-    }
-    __syncwarp();
-}
-
-// ---------------------------------------------------------------------------------------
-// P1 for one (r, chunk).  assign: new labels from the centres in shared memory.
-// resum: the labels of iteration it are read back (after a repair).  cost: C~ terms of
-// iteration it-1 (neither assign nor resum: the cost terms only, for the last iteration).
 // Per-restart centre tables built by every block at the top of an iteration: the distinct
 // centre values sorted ascending (each with its lowest centre id: equal values have equal
 // distances, and argmin keeps the lowest id), and around each midpoint m_i a band
@@ -234,9 +247,19 @@ struct CenTab {
     double *cen;               // [R*k] by id
     double *sv;                // [R*k] sorted distinct values (restart r at r*k)
     uint8_t *sid;              // their ids
+    uint8_t *spos;             // [R*k] sorted position of each centre id's value
     unsigned long long *bl, *bh;  // band bounds (bits), kd-1 per restart
     int *kd;                   // distinct count, or -1: brute force
+    unsigned long long *flo, *fhi;  // [R*k] by centre id: the safe interior of its interval
+    uint8_t *flab;             // [R*k] by centre id: the label of that interval
 };
+
+// labels of points still inside the safe interior of their previous label's interval, or -1
+__device__ __forceinline__ int assign_fast(const CenTab &T, int r, int k, double xv, int prev) {
+    const unsigned long long xb = (unsigned long long)__double_as_longlong(xv);
+    const int o = r * k + prev;
+    return (xb > T.flo[o] && xb < T.fhi[o]) ? (int)T.flab[o] : -1;
+}
 
 __device__ __forceinline__ int assign_one(const CenTab &T, int r, int k, double xv) {
     const int kd = T.kd[r];
@@ -295,6 +318,8 @@ __device__ void build_tables(const CenTab &T, int R, int k, double xmax) {
         }
         T.sv[r * k + rank] = c;
         T.sid[r * k + rank] = (uint8_t)j;
+        for (int q = j; q < k; ++q)  // every id with this value
+            if (T.cen[r * k + q] == c) T.spos[r * k + q] = (uint8_t)rank;
         atomicAdd(T.kd + r, 1);
     }
     __syncthreads();
@@ -324,116 +349,179 @@ __device__ void build_tables(const CenTab &T, int R, int k, double xmax) {
     for (int t = threadIdx.x; t < R; t += blockDim.x)  // M^2 would overflow, or underflow so
         if (!(xmax <= 1e150 && xmax >= 1e-140)) T.kd[t] = -1;  // far that subnormal rounding counts
     __syncthreads();
+    for (int t = threadIdx.x; t < rk; t += blockDim.x) {
+        const int r = t / k;
+        const int kd = T.kd[r];
+        if (kd < 1) {
+            T.flo[t] = ~0ull;  // never hits
+            T.fhi[t] = 0ull;
+            T.flab[t] = 0;
+            continue;
+        }
+        const int pos = T.spos[t];
+        T.flo[t] = pos > 0 ? T.bh[r * k + pos - 1] : 0ull;
+        T.fhi[t] = pos < kd - 1 ? T.bl[r * k + pos] : ~0ull;
+        T.flab[t] = T.sid[r * k + pos];
+    }
+    __syncthreads();
 }
 
-__device__ void p1_chunk(const FlArgs &a, int it, int r, int c, bool assign, bool resum, bool cost,
-                         const CenTab &T, double *swarp, double *xs) {
-    const double *scen = T.cen;
-    const bool summ = assign || resum;
-    const int lane = lane_id();
-    const int k = a.k;
-    const int64_t i0 = (int64_t)c * kFlChunk + (int64_t)lane * kFlLane;
-    const int m = (int)max((int64_t)0, min((int64_t)kFlLane, a.n - i0));
-    const double *cr = scen + r * k;
-    stage_chunk(a, c, xs);
-    const double *xr = xs + lane * kXsPitch;
-    Lab32 prev, cur;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) prev.w[q] = cur.w[q] = 0;
-    if (m > 0) load_lab32(lab_buf(a, it + 2, r) + i0, m, prev);
-    if (resum && m > 0) load_lab32(lab_buf(a, it, r) + i0, m, cur);
+// ---------------------------------------------------------------------------------------
+// P1 for one (restart r, chunk c).  assign: new labels of iteration it.  resum: the labels of
+// it are read back (after a repair).  cost: the C~ terms of iteration it-1.  Lanes take points
+// 32 apart (coalesced loads, streamed 8 deep); per-cluster counts and approximate sums
+// accumulate per lane in shared memory (acc[j][lane]) and are reduced per present cluster.
+struct P1Mode {
+    bool assign, resum, cost;
+};
+
+__device__ void p1_task(const FlArgs &a, int it, int r, int c, P1Mode md, const CenTab &T,
+                        double *tile) {
+    const int lane = lane_id(), k = a.k;
+    const int64_t base = (int64_t)c * kFlChunk;
+    const bool summ = md.assign || md.resum;
+    double *accS = tile;
+    int *accC = reinterpret_cast<int *>(tile + k * 32);
+    if (summ)
+        for (int j = 0; j < k; ++j) {
+            accS[j * 32 + lane] = 0.0;
+            accC[j * 32 + lane] = 0;
+        }
+    __syncwarp();
+    const double *cr = T.cen + r * k;
+    const uint8_t *lp = lab_buf(a, it + 2, r) + base;
+    uint8_t *lc = lab_buf(a, it, r) + base;
     double csum = 0.0;
     int nchg = 0;
-    uint32_t mask = 0;
+    uint32_t mask = 0, miss = 0;
+    // points and labels of 8 steps in registers, the next 8 loading while these are processed
+    double xn[8];
+    int pn[8], cn8[8];
+    auto load8 = [&](int g) {
 #pragma unroll
-    for (int t = 0; t < kFlLane; ++t) {
-        if (t < m) {
-            const double xv = xr[t];
-            const int pl = prev.get(t);
-            if (cost) {
-                const double d = __dsub_rn(xv, cr[pl]);
-                csum = __dadd_rn(csum, __dmul_rn(d, d));
-            }
-            if (summ) {
-                int lb;
-                if (assign) {
-                    lb = assign_one(T, r, k, xv);
-                    cur.set(t, lb);
-                } else {
-                    lb = cur.get(t);
+        for (int u = 0; u < 8; ++u) {
+            const int e = 32 * (8 * g + u) + lane;
+            const bool v = base + e < a.n;
+            xn[u] = v ? __ldg(a.x + base + e) : 0.0;
+            pn[u] = v ? (int)__ldcg(lp + e) : 0;
+            cn8[u] = v && md.resum ? (int)__ldcg(lc + e) : 0;
+        }
+    };
+    load8(0);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        double xc[8];
+        int pc[8], cc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xc[u] = xn[u];
+            pc[u] = pn[u];
+            cc[u] = cn8[u];
+        }
+        if (g < 3) load8(g + 1);
+        int fast[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) fast[u] = md.assign ? assign_fast(T, r, k, xc[u], pc[u]) : cc[u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = 8 * g + u;
+            const int e = 32 * q + lane;
+            if (base + e < a.n) {
+                const double xv = xc[u];
+                const int pl = pc[u];
+                if (md.cost) {
+                    const double d = __dsub_rn(xv, cr[pl]);
+                    csum = __dadd_rn(csum, __dmul_rn(d, d));
                 }
-                nchg += lb != pl;
-                mask |= 1u << lb;
+                if (summ) {
+                    const int lb = fast[u];
+                    if (lb < 0) {  // searched after the loop, so lanes do not diverge here
+                        miss |= 1u << q;
+                        continue;
+                    }
+                    if (md.assign) lc[e] = (uint8_t)lb;
+                    nchg += lb != pl;
+                    mask |= 1u << lb;
+                    accS[lb * 32 + lane] += xv;
+                    accC[lb * 32 + lane] += 1;
+                }
             }
         }
     }
-    if (assign && m > 0) store_lab32(lab_buf(a, it, r) + i0, m, cur);
-    if (cost) {
+    while (miss) {  // the points that left the safe interior of their previous label's interval
+        const int q = __ffs(miss) - 1;
+        miss &= miss - 1;
+        const int e = 32 * q + lane;
+        const double xv = __ldg(a.x + base + e);
+        const int pl = __ldcg(lp + e);
+        const int lb = assign_one(T, r, k, xv);
+        lc[e] = (uint8_t)lb;
+        nchg += lb != pl;
+        mask |= 1u << lb;
+        accS[lb * 32 + lane] += xv;
+        accC[lb * 32 + lane] += 1;
+    }
+    if (md.cost) {
         csum = warp_sum(csum);
         if (lane == 0) __stcg(a.cpart + (size_t)r * a.nch + c, csum);
     }
     if (!summ) return;
-    // per-cluster counts and approximate sums, clusters present in the chunk only
-    double *sA = swarp;                                    // [k]
-    int *sC = reinterpret_cast<int *>(swarp + kFlMaxK);    // [k]
-    if (lane < k) {
-        sA[lane] = 0.0;
-        sC[lane] = 0;
-    }
     __syncwarp();
     uint32_t wm = mask;
 #pragma unroll
     for (int o = 16; o; o >>= 1) wm |= __shfl_xor_sync(0xffffffffu, wm, o);
-    while (wm) {
-        const int j = __ffs(wm) - 1;
-        wm &= wm - 1;
-        double sj = 0.0;
-        int q = 0;
-        if (mask & (1u << j)) {
-            uint32_t bits = 0;
-#pragma unroll
-            for (int t = 0; t < kFlLane; ++t)
-                if (t < m && cur.get(t) == j) bits |= 1u << t;
-            q = __popc(bits);
-            for (; bits; bits &= bits - 1) sj += xr[__ffs(bits) - 1];
-        }
-        sj = warp_sum(sj);
-        q = warp_isum(q);
-        if (lane == 0) {
-            sA[j] = sj;
-            sC[j] = q;
-        }
+    const size_t ob = (size_t)r * k * a.nch + c;  // + j * nch
+    if (lane < k && !((wm >> lane) & 1u)) {
+        __stcg(a.A + ob + (size_t)lane * a.nch, 0.0);
+        __stcg(a.cnt + ob + (size_t)lane * a.nch, 0);
     }
-    __syncwarp();
-    if (lane < k) {
-        const size_t o = ((size_t)r * k + lane) * a.nch + c;
-        __stcg(a.A + o, sA[lane]);
-        __stcg(a.cnt + o, sC[lane]);
+    for (uint32_t b = wm; b; b &= b - 1) {
+        const int j = __ffs(b) - 1;
+        const double sj = warp_sum(accS[j * 32 + lane]);
+        const int cj = warp_isum(accC[j * 32 + lane]);
+        if (lane == 0) {
+            __stcg(a.A + ob + (size_t)j * a.nch, sj);
+            __stcg(a.cnt + ob + (size_t)j * a.nch, cj);
+            atomicAdd(tot_buf(a, it) + (size_t)r * k + j, cj);
+        }
     }
     nchg = warp_isum(nchg);
-    if (lane == 0 && nchg) atomicAdd(a.changed + (it & 1) * a.R + r, nchg);
+    if (lane == 0 && nchg) atomicAdd(a.changed + (it % 3) * a.R + r, nchg);
     __syncwarp();
 }
 
 // ---------------------------------------------------------------------------------------
-// P2 for one (r, j): approximate prefix -> per chunk the binade the exact running sum is
-// expected in (or one predicted crossing into the next binade); cluster size.
-__device__ void p2_scan(const FlArgs &a, int r, int j) {
+// P2 for one (r, j): approximate prefix over the chunks -> per chunk the binade the exact
+// running sum is expected in (pred), or one predicted crossing into the next binade (pred =
+// kCrossTag + grid; the pair is queued for a crossing record); the approximate start of each
+// chunk (AS).
+__device__ void p2_task(const FlArgs &a, int r, int j) {
     const int lane = lane_id();
     const size_t base = ((size_t)r * a.k + j) * a.nch;
     const double lo_f = 1.0 - 1.0 / 1048576.0, hi_f = 1.0 + 1.0 / 1048576.0;
     double carry = 0.0;
-    int total = 0;
-    constexpr int kU = 4;  // batches in flight
+    int first = a.nch, last = -1;
+    constexpr int kU = 4;  // batches per group; the next group loads during this one
+    double avn[kU];
+    int cnn[kU];
+    auto fetch = [&](int c00) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int c = c00 + 32 * u + lane;
+            avn[u] = c < a.nch ? __ldcg(a.A + base + c) : 0.0;
+            cnn[u] = c < a.nch ? __ldcg(a.cnt + base + c) : 0;
+        }
+    };
+    fetch(0);
     for (int c00 = 0; c00 < a.nch; c00 += 32 * kU) {
         double av[kU];
         int cn[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const int c = c00 + 32 * u + lane;
-            av[u] = c < a.nch ? __ldcg(a.A + base + c) : 0.0;
-            cn[u] = c < a.nch ? __ldcg(a.cnt + base + c) : 0;
+            av[u] = avn[u];
+            cn[u] = cnn[u];
         }
+        fetch(c00 + 32 * kU);
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int c = c00 + 32 * u + lane;
@@ -459,151 +547,291 @@ __device__ void p2_scan(const FlArgs &a, int r, int j) {
                 }
                 __stcg(a.pred + base + c, kp);
                 __stcg(a.AS + base + c, st);
+                if (is_cross(kp)) {
+                    const int slot = atomicAdd(a.ctl + kCtlNX, 1);
+                    a.xlist[slot] = ((uint32_t)c << 11) | ((uint32_t)r << 5) | (uint32_t)j;
+                }
             }
             carry += __shfl_sync(0xffffffffu, incl, 31);
-            total += warp_isum(cn[u]);
+            const unsigned have = __ballot_sync(0xffffffffu, c < a.nch && cn[u] != 0);
+            if (have) {
+                first = min(first, c00 + 32 * u + __ffs(have) - 1);
+                last = c00 + 32 * u + 31 - __clz(have);
+            }
         }
     }
     if (lane == 0) {
-        __stcg(a.tot + (size_t)r * a.k + j, total);
-        if (total == 0) {
-            a.rep[r] = 1;
-            atomicExch(a.ctl + kCtlRepair, 1);
-        }
+        a.rng[2 * ((size_t)r * a.k + j)] = first;
+        a.rng[2 * ((size_t)r * a.k + j) + 1] = last;
     }
 }
 
 // ---------------------------------------------------------------------------------------
-// P3 for one (r, chunk): per cluster with a prediction, the parity map of its points on the
-// predicted grid; for a predicted crossing, the point whose add crosses into the next binade
-// (found on an approximate running sum with a relative margin of 2^-24, else the chunk is
-// left to the walk), the map of the points before it and the map of the points after it.
-__device__ void p3_chunk(const FlArgs &a, int it, int r, int c, int *spred, double *sas, double *xs) {
-    const int lane = lane_id();
-    const int k = a.k;
-    const int64_t i0 = (int64_t)c * kFlChunk + (int64_t)lane * kFlLane;
-    const int m = (int)max((int64_t)0, min((int64_t)kFlLane, a.n - i0));
-    if (lane < k) {
-        const size_t o = ((size_t)r * k + lane) * a.nch + c;
-        const int p = __ldcg(a.pred + o);
-        spred[lane] = p;
-        sas[lane] = is_cross(p) ? __ldcg(a.AS + o) : 0.0;
+// P3a for one (r, chunk): parity maps of the clusters predicted to stay in one binade across
+// the chunk: each point's translation q or q+1 on the predicted grid, summed per lane and
+// cluster in shared memory and reduced; a tie (a/u = q + 1/2) makes the parity matter, and
+// then the cluster's map is composed in index order (q-major, lane-minor).
+__device__ void p3a_task(const FlArgs &a, int it, int r, int c, int *spred, double *tile) {
+    const int lane = lane_id(), k = a.k;
+    const int64_t base = (int64_t)c * kFlChunk;
+    const size_t ob = (size_t)r * k * a.nch + c;
+    int pj = kSkip;
+    if (lane < k && __ldcg(a.cnt + ob + (size_t)lane * a.nch)) pj = __ldcg(a.pred + ob + (size_t)lane * a.nch);
+    const uint32_t want = __ballot_sync(0xffffffffu, lane < k && is_grid(pj));
+    if (!want) return;
+    if (lane < k) spred[lane] = pj;
+    long long *accQ = reinterpret_cast<long long *>(tile);
+    for (uint32_t b = want; b; b &= b - 1) accQ[(__ffs(b) - 1) * 32 + lane] = 0;
+    __syncwarp();
+    const uint8_t *lc = lab_buf(a, it, r) + base;
+    uint32_t tmask = 0, hmask = 0;  // clusters with a tie / with a point beyond the grid
+    uint32_t oddq = 0, tieq = 0;    // per step q: translation parity, tie
+    Lab32 L;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) L.w[q] = 0xffffffffu;  // 255: no point
+    double xn[8];
+    int ln8[8];
+    auto load8 = [&](int g) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = 32 * (8 * g + u) + lane;
+            const bool v = base + e < a.n;
+            xn[u] = v ? __ldg(a.x + base + e) : 0.0;
+            ln8[u] = v ? (int)__ldcg(lc + e) : 255;
+        }
+    };
+    load8(0);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        double xc[8];
+        int lcu[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xc[u] = xn[u];
+            lcu[u] = ln8[u];
+        }
+        if (g < 3) load8(g + 1);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = 8 * g + u;
+            const int lb = lcu[u];
+            if (lb == 255) continue;
+            L.set(q, lb);
+            if ((want >> lb) & 1u) {
+                // translation on the grid: q or q+1; on a tie d = q and the parity decides
+                const double v = elem_units(xc[u], spred[lb]);
+                int64_t d = 0;
+                int tie = 0;
+                if (!(v <= 4.5e15)) {
+                    hmask |= 1u << lb;
+                } else {
+                    const double fl = floor(v);
+                    const double f = v - fl;
+                    d = (int64_t)fl + (f > 0.5);
+                    tie = f == 0.5;
+                }
+                tmask |= (uint32_t)tie << lb;
+                oddq |= (uint32_t)(d & 1) << q;
+                tieq |= (uint32_t)tie << q;
+                accQ[lb * 32 + lane] += d;
+            }
+        }
     }
     __syncwarp();
-    uint32_t want = 0;
-    for (int j = 0; j < k; ++j) {
-        const int p = spred[j];
-        if (is_grid(p) || is_cross(p)) want |= 1u << j;
+    uint32_t wt = tmask, wh = hmask;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wt |= __shfl_xor_sync(0xffffffffu, wt, o);
+        wh |= __shfl_xor_sync(0xffffffffu, wh, o);
     }
-    if (!want) return;
-    stage_chunk(a, c, xs);
-    const double *xr = xs + lane * kXsPitch;
-    Lab32 cur;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) cur.w[q] = 0;
-    if (m > 0) load_lab32(lab_buf(a, it, r) + i0, m, cur);
-    const double mlo = 1.0 - 1.0 / 16777216.0, mhi = 1.0 + 1.0 / 16777216.0;
-    while (want) {
-        const int j = __ffs(want) - 1;
-        want &= want - 1;
-        const int p = spred[j];
-        uint32_t bits = 0;
-#pragma unroll
-        for (int t = 0; t < kFlLane; ++t)
-            if (t < m && cur.get(t) == j) bits |= 1u << t;
-        const size_t o = ((size_t)r * k + j) * a.nch + c;
-        if (is_grid(p)) {
-            PMap lm = pmap_id();
-            for (uint32_t b = bits; b; b &= b - 1) lm = pmap_then(lm, pmap_elem(to_units(xr[__ffs(b) - 1], p)));
-            lm = warp_reduce_pmap(lm);
-            if (lane == 0) {
-                __stcg(a.M + 2 * o, lm.i0);
-                __stcg(a.M + 2 * o + 1, lm.i1);
-            }
+    for (uint32_t b = want; b; b &= b - 1) {
+        const int j = __ffs(b) - 1;
+        const size_t oj = ob + (size_t)j * a.nch;
+        if ((wh >> j) & 1u) {  // a point beyond the predicted binade: the walk adds the chunk
+            if (lane == 0) __stcg(a.pred + oj, kNoGrid);
             continue;
         }
-        const int g1 = p - kCrossTag, g2 = g1 - 1;
-        const double B = scalbn(1.0, 53 - g1);  // bottom of the next binade
-        double as = 0.0;
-        for (uint32_t b = bits; b; b &= b - 1) as += xr[__ffs(b) - 1];
-        double incl = as;
+        const long long D = warp_lsum(accQ[j * 32 + lane]);
+        long long C0 = 0, C1 = 0;
+        if ((wt >> j) & 1u) {
+            // A tie maps S to the even one of S + q, S + q + 1, so it adds (S + q) & 1 and leaves
+            // an even value.  Track the running parity from an even (0) and an odd (1) start in
+            // index order (step-major, lane-minor) with ballots; only parities matter.
+            if (lane == 0 && a.tprof) atomicAdd(a.ctl + kCtlNTie, 1);
+            int cur0 = 0, cur1 = 1;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double ov = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += ov;
-        }
-        const double st = sas[j] + (incl - as), en = sas[j] + incl;
-        PMap m1 = pmap_id(), m2 = pmap_id();
-        double ac = 0.0;
-        int role;  // 0 before, 2 after, 1 holds the crossing, 3 undecidable
-        if (!bits || en < B * mlo) role = 0;
-        else if (st >= B * mhi) role = 2;
-        else if (st < B * mlo) role = 1;
-        else role = 3;
-        if (role == 0) {
-            for (uint32_t b = bits; b; b &= b - 1) m1 = pmap_then(m1, pmap_elem(to_units(xr[__ffs(b) - 1], g1)));
-        } else if (role == 2) {
-            for (uint32_t b = bits; b; b &= b - 1) m2 = pmap_then(m2, pmap_elem(to_units(xr[__ffs(b) - 1], g2)));
-        } else if (role == 1) {
-            double rr = st;
-            int phase = 0;
-            for (uint32_t b = bits; b; b &= b - 1) {
-                const double xv = xr[__ffs(b) - 1];
-                const double nr = rr + xv;
-                if (phase == 0 && nr >= B * mlo) {
-                    if (nr < B * mhi) role = 3;
-                    ac = xv;
-                    phase = 1;
-                } else if (phase == 0) {
-                    m1 = pmap_then(m1, pmap_elem(to_units(xv, g1)));
-                } else {
-                    m2 = pmap_then(m2, pmap_elem(to_units(xv, g2)));
+            for (int q = 0; q < kFlLane; ++q) {
+                const bool in = L.get(q) == j;
+                const unsigned tb = __ballot_sync(0xffffffffu, in && ((tieq >> q) & 1u));
+                const unsigned ob2 = __ballot_sync(0xffffffffu, in && ((oddq >> q) & 1u) && !((tieq >> q) & 1u));
+                if (!tb) {
+                    const int pp = __popc(ob2) & 1;
+                    cur0 ^= pp;
+                    cur1 ^= pp;
+                    continue;
                 }
-                rr = nr;
+                const unsigned tq = __ballot_sync(0xffffffffu, in && ((tieq >> q) & 1u) && ((oddq >> q) & 1u));
+                unsigned done = 0;
+                for (unsigned t = tb; t; t &= t - 1) {
+                    const int ln = __ffs(t) - 1;
+                    const unsigned below = ((1u << ln) - 1u) & ~done;
+                    const int pp = __popc(ob2 & below) & 1;
+                    cur0 ^= pp;
+                    cur1 ^= pp;
+                    const int qp = (tq >> ln) & 1;
+                    C0 += (cur0 + qp) & 1;
+                    C1 += (cur1 + qp) & 1;
+                    cur0 = cur1 = 0;  // the result of a tie is even
+                    done = (ln == 31) ? 0xffffffffu : ((2u << ln) - 1u);
+                }
+                const int pp = __popc(ob2 & ~done) & 1;
+                cur0 ^= pp;
+                cur1 ^= pp;
             }
-            if (!phase) role = 3;
         }
-        const unsigned holders = __ballot_sync(0xffffffffu, role == 1);
-        const bool ok = !__any_sync(0xffffffffu, role == 3) && __popc(holders) == 1;
-        m1 = warp_reduce_pmap(m1);
-        m2 = warp_reduce_pmap(m2);
-        const double acv = __shfl_sync(0xffffffffu, ac, holders ? __ffs(holders) - 1 : 0);
         if (lane == 0) {
-            if (ok) {
-                __stcg(a.M + 2 * o, m1.i0);
-                __stcg(a.M + 2 * o + 1, m1.i1);
-                __stcg(a.MC + 4 * o, m2.i0);
-                __stcg(a.MC + 4 * o + 1, m2.i1);
-                __stcg(reinterpret_cast<double *>(a.MC) + 4 * o + 2, acv);
-                __stcg(a.MC + 4 * o + 3, (int64_t)g2);
-            } else {
-                __stcg(a.pred + o, kNoGrid);  // the walk adds this chunk element by element
-            }
+            if (D + 2 >= (int64_t(1) << 53)) __stcg(a.pred + oj, kNoGrid);  // cannot stay in a binade
+            else __stcg(a.M + oj, pack_map(PMap{D + C0, D + C1}));
         }
     }
     __syncwarp();
 }
 
-// Exact addition of cluster j's points of chunk c to the running sum s where the chunk-level
-// prediction failed (binade crossings).  Each lane predicts the binade of its own run of 32
-// from s plus an approximate prefix and builds its run's parity map; the warp then advances
-// over maximal runs of lanes that share the running sum's binade with one composed map, and
-// adds a lane's run element by element only where a crossing falls inside it.
-__device__ double cross_chunk(const FlArgs &a, int it, int r, int j, int c, double s, double *xs) {
+// stage chunk c with lanes owning runs of 32 consecutive points: xs[t * 33 + q] and the run's
+// label bytes at lb[32 t + q] (cp.async, zeros / no labels past n)
+__device__ __forceinline__ void stage_runs(const FlArgs &a, int it, int r, int c, double *tile) {
     const int lane = lane_id();
+    double *xs = tile;
+    uint8_t *lb = reinterpret_cast<uint8_t *>(tile + kXsWarp);
+    const int64_t base = (int64_t)c * kFlChunk;
+    __syncwarp();
+    if (base + kFlChunk <= a.n) {
+#pragma unroll 8
+        for (int u = 0; u < 32; ++u) cp_async8(xs + u * kXsPitch + lane, a.x + base + 32 * u + lane);
+    } else {
+        for (int u = 0; u < 32; ++u) {
+            const int64_t i = base + 32 * u + lane;
+            xs[u * kXsPitch + lane] = i < a.n ? __ldg(a.x + i) : 0.0;
+        }
+    }
+    const uint8_t *src = lab_buf(a, it, r) + base;
+#pragma unroll
+    for (int i = lane; i < kFlChunk / 16; i += 32) cp_async16(lb + 16 * i, src + 16 * i);
+    cp_async_wait();
+    __syncwarp();
+}
+
+// P3b for one queued (r, j, chunk) with a predicted crossing: the point whose add crosses into
+// the next binade (found on an approximate running sum with a relative margin of 2^-24, else
+// the chunk is left to the walk), the map of the points before it and the map after it.
+__device__ void p3b_task(const FlArgs &a, int it, uint32_t item, double *tile) {
+    const int lane = lane_id();
+    const int j = item & 31, r = (item >> 5) & 63, c = (int)(item >> 11);
+    if (__ldcg(a.stop + r)) return;
+    const int k = a.k;
+    const size_t o = ((size_t)r * k + j) * a.nch + c;
+    const int p = __ldcg(a.pred + o);
+    const double as0 = __ldcg(a.AS + o);
+    stage_runs(a, it, r, c, tile);
     const int64_t i0 = (int64_t)c * kFlChunk + (int64_t)lane * kFlLane;
     const int m = (int)max((int64_t)0, min((int64_t)kFlLane, a.n - i0));
-    stage_chunk(a, c, xs);
-    const double *xr = xs + lane * kXsPitch;
-    Lab32 cur;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) cur.w[q] = 0;
-    if (m > 0) load_lab32(lab_buf(a, it, r) + i0, m, cur);
+    const double *xr = tile + lane * kXsPitch;
+    const uint8_t *lr = reinterpret_cast<const uint8_t *>(tile + kXsWarp) + lane * kFlLane;
     uint32_t bits = 0;
     double as = 0.0;
 #pragma unroll
     for (int t = 0; t < kFlLane; ++t)
-        if (t < m && cur.get(t) == j) {
+        if (t < m && lr[t] == j) {
+            bits |= 1u << t;
+            as += xr[t];
+        }
+    double incl = as;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double ov = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += ov;
+    }
+    const int g1 = p - kCrossTag, g2 = g1 - 1;
+    const double B = scalbn(1.0, 53 - g1);  // bottom of the next binade
+    const double mlo = 1.0 - 1.0 / 16777216.0, mhi = 1.0 + 1.0 / 16777216.0;
+    const double st = as0 + (incl - as), en = as0 + incl;
+    PMap m1 = pmap_id(), m2 = pmap_id();
+    double ac = 0.0;
+    int role;  // 0 before, 2 after, 1 holds the crossing, 3 undecidable
+    if (!bits || en < B * mlo) role = 0;
+    else if (st >= B * mhi) role = 2;
+    else if (st < B * mlo) role = 1;
+    else role = 3;
+    if (role == 0) {
+        for (uint32_t b = bits; b; b &= b - 1) m1 = pmap_then(m1, pmap_elem(elem_units(xr[__ffs(b) - 1], g1)));
+    } else if (role == 2) {
+        for (uint32_t b = bits; b; b &= b - 1) m2 = pmap_then(m2, pmap_elem(elem_units(xr[__ffs(b) - 1], g2)));
+    } else if (role == 1) {
+        double rr = st;
+        int phase = 0;
+        for (uint32_t b = bits; b; b &= b - 1) {
+            const double xv = xr[__ffs(b) - 1];
+            const double nr = rr + xv;
+            if (phase == 0 && nr >= B * mlo) {
+                if (nr < B * mhi) role = 3;
+                ac = xv;
+                phase = 1;
+            } else if (phase == 0) {
+                m1 = pmap_then(m1, pmap_elem(elem_units(xv, g1)));
+            } else {
+                m2 = pmap_then(m2, pmap_elem(elem_units(xv, g2)));
+            }
+            rr = nr;
+        }
+        if (!phase) role = 3;
+    }
+    const unsigned holders = __ballot_sync(0xffffffffu, role == 1);
+    m1 = warp_reduce_pmap(m1);
+    m2 = warp_reduce_pmap(m2);
+    const int64_t lim53 = int64_t(1) << 53;
+    const bool ok = !__any_sync(0xffffffffu, role == 3) && __popc(holders) == 1 &&
+                    __shfl_sync(0xffffffffu, (int)(m1.i0 >= 0 && m1.i0 < lim53 && m1.i1 >= 0 &&
+                                                   m1.i1 < lim53 && m2.i0 >= 0 && m2.i0 < lim53 &&
+                                                   m2.i1 >= 0 && m2.i1 < lim53), 0);
+    const double acv = __shfl_sync(0xffffffffu, ac, holders ? __ffs(holders) - 1 : 0);
+    if (lane == 0) {
+        if (ok) {
+            __stcg(a.M + o, pack_map(m1));
+            __stcg(a.MC + 2 * o, pack_map(m2));
+            __stcg(reinterpret_cast<double *>(a.MC) + 2 * o + 1, acv);
+        } else {
+            __stcg(a.pred + o, kNoGrid);  // the walk adds this chunk element by element
+        }
+    }
+    __syncwarp();
+}
+
+// Exact addition of cluster j's points of chunk c to the running sum s (no usable record):
+// lanes own runs of 32 consecutive points; each lane predicts the binade of its run from s plus
+// an approximate prefix and builds its run's map; the warp then advances over maximal runs of
+// lanes on the running sum's grid with one composed map, and adds a lane's run element by
+// element where a crossing falls inside it.
+__device__ __forceinline__ unsigned long long gtimer();
+__device__ double cross_chunk_impl(const FlArgs &a, int it, int r, int j, int c, double s, double *tile);
+__device__ double cross_chunk(const FlArgs &a, int it, int r, int j, int c, double s, double *tile) {
+    const unsigned long long t0 = a.tprof ? gtimer() : 0;
+    const double v = cross_chunk_impl(a, it, r, j, c, s, tile);
+    if (a.tprof && lane_id() == 0) atomicAdd(a.tprof + 256 * 8 + 3, gtimer() - t0);
+    return v;
+}
+__device__ double cross_chunk_impl(const FlArgs &a, int it, int r, int j, int c, double s, double *tile) {
+    const int lane = lane_id();
+    if (lane == 0 && a.tprof) atomicAdd(a.ctl + kCtlNCross, 1);
+    stage_runs(a, it, r, c, tile);
+    const int64_t i0 = (int64_t)c * kFlChunk + (int64_t)lane * kFlLane;
+    const int m = (int)max((int64_t)0, min((int64_t)kFlLane, a.n - i0));
+    const double *xr = tile + lane * kXsPitch;
+    const uint8_t *lr = reinterpret_cast<const uint8_t *>(tile + kXsWarp) + lane * kFlLane;
+    uint32_t bits = 0;
+    double as = 0.0;
+#pragma unroll
+    for (int t = 0; t < kFlLane; ++t)
+        if (t < m && lr[t] == j) {
             bits |= 1u << t;
             as += xr[t];
         }
@@ -623,11 +851,8 @@ __device__ double cross_chunk(const FlArgs &a, int it, int r, int j, int c, doub
             const Grid ga = grid_of(plo), gb = grid_of(phi);
             if (ga.k == gb.k) g = ga.k;
         }
-        if (g != kNoGrid) {
-#pragma unroll
-            for (int t = 0; t < kFlLane; ++t)
-                if ((bits >> t) & 1u) lm = pmap_then(lm, pmap_elem(to_units(xr[t], g)));
-        }
+        if (g != kNoGrid)
+            for (uint32_t b = bits; b; b &= b - 1) lm = pmap_then(lm, pmap_elem(elem_units(xr[__ffs(b) - 1], g)));
     }
     int L = 0;
     while (L < 32) {
@@ -639,112 +864,168 @@ __device__ double cross_chunk(const FlArgs &a, int it, int r, int j, int c, doub
             PMap pm = (lane >= L && lane < L2 && g != kSkip) ? lm : pmap_id();
             pm = warp_reduce_pmap(pm);
             const PMap bm{__shfl_sync(0xffffffffu, pm.i0, 0), __shfl_sync(0xffffffffu, pm.i1, 0)};
-            const int64_t S1 = pmap_apply(bm, (int64_t)to_units(s, gs.k));
+            const int64_t S1 = pmap_apply(bm, run_units(s, gs.k));
             if (S1 < gs.top) {
-                s = from_units(S1, gs.k);
+                s = run_from(S1, gs.k);
                 L = L2;
                 continue;
             }
         }
-        double v = s;  // lane L element by element
+        double v = s;  // lane L element by element (loads first, then the dependent adds)
         if (lane == L) {
+            double xv[kFlLane];
+#pragma unroll
+            for (int t = 0; t < kFlLane; ++t) xv[t] = xr[t];
 #pragma unroll
             for (int t = 0; t < kFlLane; ++t)
-                if ((bits >> t) & 1u) v = __dadd_rn(v, xr[t]);
+                if ((bits >> t) & 1u) v = __dadd_rn(v, xv[t]);
         }
         s = __shfl_sync(0xffffffffu, v, L);
         L += 1;
     }
+    __syncwarp();
     return s;
 }
 
-// P4 for one (r, j): the exact walk over the chunks, 32 at a time: maximal runs of chunks on
-// the running sum's grid advance with one composed map, a predicted crossing with its two
-// maps and one real add of the crossing point, anything else element by element.  Every
-// step is verified against the exact running value.  Writes the mean for iteration it+1.
-__device__ void p4_walk(const FlArgs &a, int it, int r, int j, double *xs) {
+// P4 for one (r, j): the exact walk over the chunks, 32 at a time with 4 batches of records in
+// flight: maximal runs of chunks on the running sum's grid advance with one composed map, a
+// predicted crossing with its two maps and one real add of the crossing point, anything else
+// element by element (cross_chunk).  Every step is verified against the exact running value.
+// Writes the cluster's mean for iteration it+1.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ void p4_task(const FlArgs &a, int it, int r, int j, double *tile) {
     const int lane = lane_id();
+    const unsigned long long t_start = a.tprof ? gtimer() : 0;
     const size_t base = ((size_t)r * a.k + j) * a.nch;
     double s = 0.0;
-    int pn = kSkip;
-    PMap mn = pmap_id(), m2n = pmap_id();
-    double acn = 0.0;
-    int g2n = 0;
-    auto fetch = [&](int c) {
-        pn = kSkip;
+    constexpr int kU = 2;  // batches per group; the next group's records load during this one
+    struct Rec {
+        int p;
+        int64_t m, m2;
+        double ac;
+    };
+    auto fetch = [&](int c, Rec &q) {
+        q.p = kSkip;
+        q.m = q.m2 = 1;  // identity
+        q.ac = 0.0;
         if (c < a.nch) {
-            pn = __ldcg(a.pred + base + c);
-            if (is_grid(pn) || is_cross(pn)) {
-                mn.i0 = __ldcg(a.M + 2 * (base + c));
-                mn.i1 = __ldcg(a.M + 2 * (base + c) + 1);
-            }
-            if (is_cross(pn)) {
-                m2n.i0 = __ldcg(a.MC + 4 * (base + c));
-                m2n.i1 = __ldcg(a.MC + 4 * (base + c) + 1);
-                acn = __ldcg(reinterpret_cast<const double *>(a.MC) + 4 * (base + c) + 2);
-                g2n = (int)__ldcg(a.MC + 4 * (base + c) + 3);
-            }
+            q.p = __ldcg(a.pred + base + c);
+            q.m = __ldcg(a.M + base + c);
+            q.m2 = __ldcg(a.MC + 2 * (base + c));
+            q.ac = __ldcg(reinterpret_cast<const double *>(a.MC) + 2 * (base + c) + 1);
         }
     };
-    fetch(lane);
-    for (int c0 = 0; c0 < a.nch; c0 += 32) {
-        const int p = pn, g2 = g2n;
-        const PMap mm = mn, m2 = m2n;
-        const double ac = acn;
-        fetch(c0 + 32 + lane);  // independent of the running value
-        const int lim = min(32, a.nch - c0);
-        if (__all_sync(0xffffffffu, p == kSkip)) continue;
-        int L = 0;
-        while (L < lim) {
-            const Grid gs = grid_of(s);
-            const bool ok = p == kSkip || p == gs.k;
-            const unsigned badm = __ballot_sync(0xffffffffu, !ok && lane >= L && lane < lim);
-            const int L2 = badm ? __ffs(badm) - 1 : lim;
-            if (L2 > L) {
-                const bool any = __any_sync(0xffffffffu, lane >= L && lane < L2 && p != kSkip);
-                if (any) {
-                    PMap pm = (lane >= L && lane < L2 && p != kSkip) ? mm : pmap_id();
-                    pm = warp_reduce_pmap(pm);
-                    const PMap bm{__shfl_sync(0xffffffffu, pm.i0, 0), __shfl_sync(0xffffffffu, pm.i1, 0)};
-                    const int64_t S1 = pmap_apply(bm, (int64_t)to_units(s, gs.k));
-                    if (S1 >= gs.top) {  // left the binade inside the run: first chunk by hand
-                        s = cross_chunk(a, it, r, j, c0 + L, s, xs);
-                        L += 1;
+    const int cfirst = __ldcg(a.rng + 2 * ((size_t)r * a.k + j));
+    const int clast = __ldcg(a.rng + 2 * ((size_t)r * a.k + j) + 1);
+    const int cbeg = cfirst / 32 * 32, cend = clast + 1;  // batches start on multiples of 32
+    Rec nx[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) fetch(cbeg + 32 * u + lane, nx[u]);
+    for (int c00 = cbeg; c00 < cend; c00 += 32 * kU) {
+        Rec cu[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) cu[u] = nx[u];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) fetch(c00 + 32 * (kU + u) + lane, nx[u]);
+        // off the critical path: per batch, the common grid of its chunks (if every chunk
+        // holding the cluster is mapped on one grid) and their composition
+        int gu[kU];
+        PMap bmu[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int p = cu[u].p;
+            const unsigned have = __ballot_sync(0xffffffffu, p != kSkip);
+            const int g0 = __shfl_sync(0xffffffffu, p, have ? __ffs(have) - 1 : 0);
+            const bool uni = __all_sync(0xffffffffu, p == kSkip || (is_grid(p) && p == g0));
+            gu[u] = have && uni ? g0 : kNoGrid;
+            PMap pm = is_grid(p) ? unpack_map(cu[u].m) : pmap_id();
+            pm = warp_reduce_pmap(pm);
+            bmu[u] = PMap{__shfl_sync(0xffffffffu, pm.i0, 0), __shfl_sync(0xffffffffu, pm.i1, 0)};
+            if (!have) gu[u] = kSkip;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int c0 = c00 + 32 * u;
+            if (c0 >= cend || gu[u] == kSkip) continue;
+            const int lim = min(32, a.nch - c0);
+            const int p = cu[u].p;
+            {  // whole batch on the running grid: one step
+                const Grid gs = grid_of(s);
+                if (gu[u] == gs.k) {
+                    const int64_t S1 = pmap_apply(bmu[u], run_units(s, gs.k));
+                    if (S1 < gs.top) {
+                        s = run_from(S1, gs.k);
+                        if (a.tprof && lane == 0) atomicAdd(a.tprof + 256 * 8 + 4, 1ull);
                         continue;
                     }
-                    s = from_units(S1, gs.k);
                 }
-                L = L2;
-                continue;
+                if (a.tprof && lane == 0) atomicAdd(a.tprof + 256 * 8 + 5, 1ull);
             }
-            // chunk L is off the running grid
-            const int pL = __shfl_sync(0xffffffffu, p, L);
-            bool done = false;
-            if (is_cross(pL) && pL - kCrossTag == gs.k) {
-                const PMap a1{__shfl_sync(0xffffffffu, mm.i0, L), __shfl_sync(0xffffffffu, mm.i1, L)};
-                const PMap a2{__shfl_sync(0xffffffffu, m2.i0, L), __shfl_sync(0xffffffffu, m2.i1, L)};
-                const double acl = __shfl_sync(0xffffffffu, ac, L);
-                const int g2l = __shfl_sync(0xffffffffu, g2, L);
-                const int64_t S1 = pmap_apply(a1, (int64_t)to_units(s, gs.k));
-                if (S1 < gs.top) {
-                    const double s2 = __dadd_rn(from_units(S1, gs.k), acl);
-                    const Grid g2s = grid_of(s2);
-                    if (g2s.k == g2l) {
-                        const int64_t S2 = pmap_apply(a2, (int64_t)to_units(s2, g2l));
-                        if (S2 < g2s.top) {
-                            s = from_units(S2, g2l);
-                            done = true;
+            const PMap mine = is_grid(p) || is_cross(p) ? unpack_map(cu[u].m) : pmap_id();
+            int L = 0;
+            while (L < lim) {
+                if (a.tprof && lane == 0) atomicAdd(a.tprof + 256 * 8 + 6, 1ull);
+                const Grid gs = grid_of(s);
+                const bool ok = p == kSkip || p == gs.k;
+                const unsigned badm = __ballot_sync(0xffffffffu, !ok && lane >= L && lane < lim);
+                const int L2 = badm ? __ffs(badm) - 1 : lim;
+                if (L2 > L) {
+                    const bool in = lane >= L && lane < L2 && p != kSkip;
+                    if (__any_sync(0xffffffffu, in)) {
+                        PMap pm = in ? mine : pmap_id();
+                        pm = warp_reduce_pmap(pm);
+                        const PMap bm{__shfl_sync(0xffffffffu, pm.i0, 0), __shfl_sync(0xffffffffu, pm.i1, 0)};
+                        const int64_t S1 = pmap_apply(bm, run_units(s, gs.k));
+                        if (S1 >= gs.top) {  // left the binade inside the run: first chunk by hand
+                            s = cross_chunk(a, it, r, j, c0 + L, s, tile);
+                            L += 1;
+                            continue;
+                        }
+                        s = run_from(S1, gs.k);
+                    }
+                    L = L2;
+                    continue;
+                }
+                // chunk L is off the running grid
+                const int pL = __shfl_sync(0xffffffffu, p, L);
+                bool done = false;
+                if (is_cross(pL) && pL - kCrossTag == gs.k) {
+                    const int64_t w1 = __shfl_sync(0xffffffffu, cu[u].m, L);
+                    const int64_t w2 = __shfl_sync(0xffffffffu, cu[u].m2, L);
+                    const double acl = __shfl_sync(0xffffffffu, cu[u].ac, L);
+                    const int g2l = gs.k - 1;
+                    const int64_t S1 = pmap_apply(unpack_map(w1), run_units(s, gs.k));
+                    if (S1 < gs.top) {
+                        const double s2 = __dadd_rn(run_from(S1, gs.k), acl);
+                        const Grid g2s = grid_of(s2);
+                        if (g2s.k == g2l) {
+                            const int64_t S2 = pmap_apply(unpack_map(w2), run_units(s2, g2l));
+                            if (S2 < g2s.top) {
+                                s = run_from(S2, g2l);
+                                done = true;
+                            }
                         }
                     }
                 }
+                if (!done) s = cross_chunk(a, it, r, j, c0 + L, s, tile);
+                L += 1;
             }
-            if (!done) s = cross_chunk(a, it, r, j, c0 + L, s, xs);
-            L += 1;
         }
     }
     if (lane == 0) {
-        const int t = __ldcg(a.tot + (size_t)r * a.k + j);
+        const int t = __ldcg(tot_buf(a, it) + (size_t)r * a.k + j);
         __stcg(cen_buf(a, it + 1, r) + j, t > 0 ? __ddiv_rn(s, (double)t) : 0.0);
+        if (a.tprof) {  // diagnostics: longest walk, latest walk end
+            const unsigned long long t_end = gtimer();
+            atomicMax(a.tprof + 256 * 8 + 0, t_end - t_start);
+            atomicMax(a.tprof + 256 * 8 + 1, t_end - a.tprof[(size_t)min(it, 255) * 8 + 4]);
+            atomicAdd(a.tprof + 256 * 8 + 2, t_end - t_start);
+        }
     }
 }
 
@@ -856,24 +1137,22 @@ __device__ int decide_exact(double P, double C, double tol, int *bad) {
 
 // ---------------------------------------------------------------------------------------
 // Repair of one restart's empty clusters after the assignment of iteration it
-// (kmeans.py:151-164), then its chunk summaries and scans are redone.  Grid-uniform.
-__device__ void repair_restart(const FlArgs &a, cg::grid_group &grid, int it, int r,
-                               const CenTab &T, double *swarp, double *xs, int gw, int nw) {
-    const double *scen = T.cen;
+// (kmeans.py:151-164).  Grid-uniform; the caller redoes the restart's chunk summaries.
+__device__ void repair_restart(const FlArgs &a, cg::grid_group &grid, int it, int r, const CenTab &T) {
     const int k = a.k;
     uint8_t *lab = lab_buf(a, it, r);
-    const double *cr = scen + r * k;
+    const double *cr = T.cen + r * k;
     // the empties, listed once (np.flatnonzero(counts == 0) before the loop)
     uint32_t empties = 0;
     for (int j = 0; j < k; ++j)
-        if (__ldcg(a.tot + (size_t)r * k + j) == 0) empties |= 1u << j;
+        if (__ldcg(tot_buf(a, it) + (size_t)r * k + j) == 0) empties |= 1u << j;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = tid; i < a.n; i += nth) {
         const double xv = __ldg(a.x + i);
-        const int l = __ldcg(lab + i);
+        const double cl = cr[__ldcg(lab + i)];
         const double xx = __dmul_rn(xv, xv), tx = __dmul_rn(2.0, xv);
-        double v = __dadd_rn(__dsub_rn(xx, __dmul_rn(tx, cr[l])), __dmul_rn(cr[l], cr[l]));
+        const double v = __dadd_rn(__dsub_rn(xx, __dmul_rn(tx, cl)), __dmul_rn(cl, cl));
         a.own[i] = v < 0.0 ? 0.0 : v;
     }
     grid.sync();
@@ -932,11 +1211,9 @@ __device__ void repair_restart(const FlArgs &a, cg::grid_group &grid, int it, in
         }
         grid.sync();
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.changed[(it & 1) * a.R + r] = 0;
-    grid.sync();
-    for (int c = gw; c < a.nch; c += nw) p1_chunk(a, it, r, c, false, true, false, T, swarp + (threadIdx.x >> 5) * 2 * kFlMaxK, xs);
-    grid.sync();
-    for (int j = gw; j < k; j += nw) p2_scan(a, r, j);
+    // fresh counters for the redone summaries
+    if (blockIdx.x == 0 && threadIdx.x < k) tot_buf(a, it)[(size_t)r * k + threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.changed[(it % 3) * a.R + r] = 0;
     grid.sync();
 }
 
@@ -952,21 +1229,21 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double scen[kFlMaxRK], ssv[kFlMaxRK];
     __shared__ unsigned long long sbl[kFlMaxRK], sbh[kFlMaxRK];
-    __shared__ uint8_t ssid[kFlMaxRK];
+    __shared__ uint8_t ssid[kFlMaxRK], sspos[kFlMaxRK], sflab[kFlMaxRK];
+    __shared__ unsigned long long sflo[kFlMaxRK], sfhi[kFlMaxRK];
     __shared__ int skd[kFlMaxR];
-    __shared__ double sas_all[kFlWarps][kFlMaxK];
-    CenTab T{scen, ssv, ssid, sbl, sbh, skd};
-    __shared__ double swarp[kFlWarps * 2 * kFlMaxK];
-    extern __shared__ double fl_dyn[];  // kFlWarps chunk tiles (also the exact-cost stage)
+    __shared__ int spred_all[kFlWarps][kFlMaxK];
     __shared__ int act[kFlMaxR];
-    __shared__ int nact_s;
+    __shared__ int nact_s, any_s;
+    extern __shared__ double fl_dyn[];  // per warp: a.wd doubles (tiles / accumulators)
+    CenTab T{scen, ssv, ssid, sspos, sbl, sbh, skd, sflo, sfhi, sflab};
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int gw = blockIdx.x * kFlWarps + warp, nw = gridDim.x * kFlWarps;
-    double *sw = swarp + warp * 2 * kFlMaxK;
-    double *xs = fl_dyn + warp * kXsWarp;
-    double *stage = xs;
+    double *tile = fl_dyn + (size_t)warp * a.wd;
+    int *spred = spred_all[warp];
     const int R = a.R, k = a.k, rk = R * k;
     auto load_active = [&]() {
+        __syncthreads();
         if (threadIdx.x == 0) {
             int q = 0;
             for (int r = 0; r < R; ++r)
@@ -980,24 +1257,62 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
     for (;; ++it) {
         tmark(a, it, 0);
         const bool assign = it < a.max_iters, cost = it > 0;
-        // centres of iteration it (= means of it-1) and their squares
-        for (int t = threadIdx.x; t < rk; t += blockDim.x) {
-            const double c = __ldcg(a.cen + (size_t)(it % 3) * rk + t);
-            scen[t] = c;
-        }
+        // centres of iteration it (= means of it-1)
+        for (int t = threadIdx.x; t < rk; t += blockDim.x) scen[t] = __ldcg(a.cen + (size_t)(it % 3) * rk + t);
         if (assign) build_tables(T, R, k, a.xmax);
         __syncthreads();
         const int nact = nact_s;
         // ---- P1: assignment of it, C~ terms of it-1
-        for (int t = gw; t < nact * a.nch; t += nw)
-            p1_chunk(a, it, act[t / a.nch], t % a.nch, assign, false, cost, T, sw, xs);
+        {
+            const P1Mode md{assign, false, cost};
+            const unsigned long long w0 = a.tprof ? gtimer() : 0;
+            int ntask = 0;
+            for (int t = gw; t < nact * a.nch; t += nw, ++ntask) {
+                const unsigned long long t0 = a.tprof ? gtimer() : 0;
+                p1_task(a, it, act[t / a.nch], t % a.nch, md, T, tile);
+                if (a.tprof && lane == 0) {
+                    const unsigned long long dt = gtimer() - t0;
+                    atomicAdd(a.tprof + 256 * 8 + 7, dt);
+                    atomicMax(a.tprof + 256 * 8 + 8, dt);
+                }
+            }
+            if (a.tprof && lane == 0) {
+                atomicMax(a.tprof + 256 * 8 + 9, gtimer() - w0);
+                atomicMax(a.tprof + 256 * 8 + 10, (unsigned long long)ntask);
+                atomicMax(a.tprof + 256 * 8 + 11, gtimer() - a.tprof[(size_t)min(it, 255) * 8 + 0]);
+            }
+        }
         grid.sync();
         tmark(a, it, 1);
-        // ---- P2: grid predictions of it; decision for it-1 (task index j == k)
+        // ---- empty clusters (rare): repair, then the restart's summaries again
+        if (assign) {
+            if (threadIdx.x == 0) {
+                int any = 0;
+                for (int q = 0; q < nact; ++q)
+                    for (int j = 0; j < k; ++j) any |= __ldcg(tot_buf(a, it) + (size_t)act[q] * k + j) == 0;
+                any_s = any;  // every block computes the same value
+            }
+            __syncthreads();
+            if (any_s) {
+                for (int q = 0; q < nact; ++q) {
+                    const int r = act[q];
+                    int emp = 0;
+                    for (int j = 0; j < k; ++j) emp |= __ldcg(tot_buf(a, it) + (size_t)r * k + j) == 0;
+                    if (!emp) continue;  // uniform: tot of r only changes inside its own repair
+                    repair_restart(a, grid, it, r, T);
+                    const P1Mode md{false, true, false};
+                    for (int c = gw; c < a.nch; c += nw) p1_task(a, it, r, c, md, T, tile);
+                    grid.sync();
+                }
+            }
+        }
+        // ---- P2: binade predictions of it; decision for it-1 (task index j == k)
         for (int t = gw; t < nact * (k + 1); t += nw) {
             const int r = act[t / (k + 1)], j = t % (k + 1);
             if (j < k) {
-                if (assign) p2_scan(a, r, j);
+                if (assign) p2_task(a, r, j);
+                if (j == 0 && lane == 0) a.changed[((it + 1) % 3) * R + r] = 0;
+                if (lane == 0) tot_buf(a, it + 1)[(size_t)r * k + j] = 0;  // for P1 of it+1
                 continue;
             }
             if (!cost) continue;
@@ -1008,21 +1323,16 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
             const int d_it = it - 1;  // iteration being decided
             const double P = a.capprox[r];
             const bool fin = d_it > 0;
-            const bool unchanged = fin && __ldcg(a.changed + (d_it & 1) * R + r) == 0;
+            const bool unchanged = fin && __ldcg(a.changed + (d_it % 3) * R + r) == 0;
             int stop = 0, amb = 0;
             if (unchanged) {
                 stop = 1;
             } else if (fin) {
                 int bad = 0;
                 const int sg = certify(P, cs, a.tol, a.delta, &bad);
-                if (sg < 0 || bad < 0) amb = 1;
-                else if (bad > 0) {
-                    amb = 1;  // confirm with exact costs before raising
-                } else {
-                    stop = sg;
-                }
+                if (sg < 0 || bad != 0) amb = 1;  // (a sure failure is confirmed exactly)
+                else stop = sg;
             }
-            a.cfresh[r] = cs;
             if (amb) {
                 a.amb[r] = 1;
                 atomicExch(a.ctl + kCtlAmb, 1);
@@ -1038,8 +1348,8 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
         tmark(a, it, 2);
         if (__ldcg(a.ctl + kCtlAmb)) {
             // exact costs of it-1 (slot 0) and it-2 (slot 1) for the undecided restarts
-            exact_partials(a, a.amb, it - 1, 0, stage, gw, nw);
-            exact_partials(a, a.amb, it - 2, 1, stage, gw, nw);
+            exact_partials(a, a.amb, it - 1, 0, tile, gw, nw);
+            exact_partials(a, a.amb, it - 2, 1, tile, gw, nw);
             grid.sync();
             if (blockIdx.x == 0 && threadIdx.x < R) {
                 const int r = threadIdx.x;
@@ -1063,29 +1373,23 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
             if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl[kCtlAmb] = 0;
             if (__ldcg(a.ctl + kCtlErr)) break;  // uniform: read after the sync
         }
-        __syncthreads();
         load_active();
         if (!assign || nact_s == 0) break;
-        // ---- repair of empty clusters (rare)
-        if (__ldcg(a.ctl + kCtlRepair)) {
-            for (int q = 0; q < nact_s; ++q) {
-                const int r = act[q];
-                if (__ldcg(a.rep + r)) repair_restart(a, grid, it, r, T, swarp, xs, gw, nw);
-            }
-            if (blockIdx.x == 0 && threadIdx.x < R) a.rep[threadIdx.x] = 0;
-            if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl[kCtlRepair] = 0;
-            // (the flags are next read after two more grid syncs)
-        }
-        // ---- P3: parity maps
         tmark(a, it, 3);
-        const int na = nact_s;
-        for (int t = gw; t < na * a.nch; t += nw)
-            p3_chunk(a, it, act[t / a.nch], t % a.nch, reinterpret_cast<int *>(sw), sas_all[warp], xs);
+        // ---- P3: chunk maps (a) and crossing records (b)
+        {
+            const int na = nact_s, nsteady = na * a.nch;
+            const int nx = __ldcg(a.ctl + kCtlNX);
+            for (int t = gw; t < nsteady + nx; t += nw) {
+                if (t < nsteady) p3a_task(a, it, act[t / a.nch], t % a.nch, spred, tile);
+                else p3b_task(a, it, __ldcg(a.xlist + (t - nsteady)), tile);
+            }
+        }
         grid.sync();
         tmark(a, it, 4);
         // ---- P4: exact walks -> means of it
-        for (int t = gw; t < na * k; t += nw) p4_walk(a, it, act[t / k], t % k, xs);
-        if (blockIdx.x == 0 && threadIdx.x < R) a.changed[((it + 1) & 1) * R + threadIdx.x] = 0;
+        for (int t = gw; t < nact_s * k; t += nw) p4_task(a, it, act[t / k], t % k, tile);
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl[kCtlNX] = 0;
         grid.sync();
         tmark(a, it, 5);
     }
@@ -1093,28 +1397,26 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl[kCtlIters] = it;
     if (__ldcg(a.ctl + kCtlErr)) return;
     // ---- exact final costs of every restart, best = first strictly smallest
-    {
-        int32_t *all = a.amb;  // reuse as "all restarts" flags
-        if (blockIdx.x == 0 && threadIdx.x < R) all[threadIdx.x] = 1;
-        grid.sync();
-        exact_partials(a, all, -1, 0, stage, gw, nw);
-        grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x < R) a.cexact[threadIdx.x] = exact_combine(a, 0, threadIdx.x);
-        __syncthreads();
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            int best = -1;
-            double bc = INFINITY;
-            for (int r = 0; r < R; ++r) {
-                a.amb[r] = 0;
-                if (a.cexact[r] < bc) {
-                    bc = a.cexact[r];
-                    best = r;
-                }
+    int32_t *all = a.amb;  // reused as "every restart" flags
+    if (blockIdx.x == 0 && threadIdx.x < R) all[threadIdx.x] = 1;
+    grid.sync();
+    exact_partials(a, all, -1, 0, tile, gw, nw);
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x < R) a.cexact[threadIdx.x] = exact_combine(a, 0, threadIdx.x);
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int best = -1;
+        double bc = INFINITY;
+        for (int r = 0; r < R; ++r) {
+            a.amb[r] = 0;
+            if (a.cexact[r] < bc) {
+                bc = a.cexact[r];
+                best = r;
             }
-            a.ctl[kCtlBest] = best;
         }
-        tmark(a, 255, 1);
+        a.ctl[kCtlBest] = best;
     }
+    tmark(a, 255, 1);
 }
 
 __global__ void k_fl_init(FlArgs a, const double *xsrc, double sign, const int64_t *chosen) {
@@ -1131,8 +1433,10 @@ __global__ void k_fl_init(FlArgs a, const double *xsrc, double sign, const int64
         a.capprox[t] = INFINITY;
         a.changed[t] = 0;
         a.changed[a.R + t] = 0;
+        a.changed[2 * a.R + t] = 0;
     }
     for (int64_t t = tid; t < kCtlSlots; t += nth) a.ctl[t] = 0;
+    for (int64_t t = tid; t < 2 * rk; t += nth) a.tot[t] = 0;
 }
 
 __global__ void k_fl_sign(const double *x, int64_t n, int32_t *flags, unsigned long long *amax) {
@@ -1224,16 +1528,18 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
             SC_CUDA(cudaMalloc((void **)&f->xneg, (size_t)n * 8));
             k_fl_negate<<<sm_count * 4, 256, 0, s>>>(d_x, n, f->xneg);
         }
-        int per = 0;
-        SC_CUDA(cudaFuncSetAttribute(k_fused_lloyd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kFlDynSmem));
-        SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused_lloyd, kFlThreads,
-                                                              kFlDynSmem));
-        f->grid = std::max(1, std::min(per, 2)) * sm_count;
         *pctx = f;
     }
     FusedLloyd *f = *pctx;
     if (f->sign == 0) return 1;
+    const int dyn = kFlWarps * fl_warp_bytes(k);
+    {
+        int per = 0;
+        SC_CUDA(cudaFuncSetAttribute(k_fused_lloyd, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused_lloyd, kFlThreads, dyn));
+        SC_REQUIRE(per >= 1, SC_E_INTERNAL, "fused k-means kernel does not fit on an SM");
+        f->grid = std::min(per, 2) * sm_count;
+    }
     const int64_t nch = (n + kFlChunk - 1) / kFlChunk;
     const int64_t nbuf = (n + kFlEinsumBuf - 1) / kFlEinsumBuf;
     const size_t rk = (size_t)R * k;
@@ -1246,14 +1552,15 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     };
     const int64_t ln = nch * kFlChunk;
     const size_t o_lab = carve((size_t)3 * R * ln), o_cen = carve(3 * rk * 8),
-                 o_A = carve(rk * nch * 8), o_cnt = carve(rk * nch * 4), o_pred = carve(rk * nch * 4),
-                 o_M = carve(rk * nch * 16), o_MC = carve(rk * nch * 32), o_AS = carve(rk * nch * 8),
-                 o_cpart = carve((size_t)R * nch * 8),
-                 o_tot = carve(rk * 4), o_chg = carve((size_t)2 * R * 4), o_ctl = carve(kCtlSlots * 4),
+                 o_A = carve(rk * nch * 8), o_cnt = carve(rk * nch * 4), o_p = carve(rk * nch * 4),
+                 o_AS = carve(rk * nch * 8), o_M = carve(rk * nch * 8), o_MC = carve(rk * nch * 16),
+                 o_xl = carve(rk * nch * 4), o_rng = carve(rk * 8),
+                 o_cpart = carve((size_t)R * nch * 8), o_tot = carve(2 * rk * 4),
+                 o_chg = carve((size_t)3 * R * 4), o_ctl = carve(kCtlSlots * 4),
                  o_stop = carve(R * 4), o_amb = carve(R * 4), o_rep = carve(R * 4),
-                 o_fin = carve(R * 4), o_cap = carve(R * 8), o_cfr = carve(R * 8),
-                 o_bp = carve((size_t)2 * R * nbuf * 8), o_cex = carve(R * 8), o_own = carve((size_t)n * 8),
-                 o_gv = carve((size_t)f->grid * 8), o_gi = carve((size_t)f->grid * 8);
+                 o_fin = carve(R * 4), o_cap = carve(R * 8), o_bp = carve((size_t)2 * R * nbuf * 8),
+                 o_cex = carve(R * 8), o_own = carve((size_t)n * 8), o_gv = carve((size_t)f->grid * 8),
+                 o_gi = carve((size_t)f->grid * 8);
     if (off > f->buf_bytes) {
         if (f->buf) cudaFreeAsync(f->buf, s);
         f->buf = nullptr;
@@ -1271,17 +1578,19 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     a.nch = (int)nch;
     a.max_iters = max_iters;
     a.nbuf = nbuf;
+    a.wd = fl_warp_bytes(k) / 8;
     a.tol = tol;
     a.delta = 2.0 * (double)(4097 + nbuf + 64 + nch / 32) * 1.1102230246251565e-16;
     a.lab = B + o_lab;
     a.cen = reinterpret_cast<double *>(B + o_cen);
     a.A = reinterpret_cast<double *>(B + o_A);
     a.cnt = reinterpret_cast<int32_t *>(B + o_cnt);
-    a.pred = reinterpret_cast<int32_t *>(B + o_pred);
-    a.M = reinterpret_cast<int64_t *>(B + o_M);
-    a.MC = reinterpret_cast<int64_t *>(B + o_MC);
+    a.pred = reinterpret_cast<int32_t *>(B + o_p);
     a.AS = reinterpret_cast<double *>(B + o_AS);
-    a.xmax = f->xmax;
+    a.MC = reinterpret_cast<int64_t *>(B + o_MC);
+    a.xlist = reinterpret_cast<uint32_t *>(B + o_xl);
+    a.rng = reinterpret_cast<int32_t *>(B + o_rng);
+    a.M = reinterpret_cast<int64_t *>(B + o_M);
     a.cpart = reinterpret_cast<double *>(B + o_cpart);
     a.tot = reinterpret_cast<int32_t *>(B + o_tot);
     a.changed = reinterpret_cast<int32_t *>(B + o_chg);
@@ -1291,23 +1600,23 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     a.rep = reinterpret_cast<int32_t *>(B + o_rep);
     a.final_it = reinterpret_cast<int32_t *>(B + o_fin);
     a.capprox = reinterpret_cast<double *>(B + o_cap);
-    a.cfresh = reinterpret_cast<double *>(B + o_cfr);
     a.bpart = reinterpret_cast<double *>(B + o_bp);
     a.cexact = reinterpret_cast<double *>(B + o_cex);
     a.own = reinterpret_cast<double *>(B + o_own);
     a.gval = reinterpret_cast<double *>(B + o_gv);
+    a.xmax = f->xmax;
     a.gidx = reinterpret_cast<int64_t *>(B + o_gi);
     const bool prof = getenv("SC_KMEANS_PROFILE") != nullptr;
     a.tprof = nullptr;
     if (prof) {
-        SC_CUDA(cudaMallocAsync((void **)&a.tprof, 256 * 8 * 8, s));
-        SC_CUDA(cudaMemsetAsync(a.tprof, 0, 256 * 8 * 8, s));
+        SC_CUDA(cudaMallocAsync((void **)&a.tprof, 258 * 8 * 8, s));
+        SC_CUDA(cudaMemsetAsync(a.tprof, 0, 258 * 8 * 8, s));
     }
     k_fl_init<<<f->grid, 256, 0, s>>>(a, d_x, f->sign < 0 ? -1.0 : 1.0, d_chosen);
     SC_CUDA(cudaGetLastError());
     void *args[] = {&a};
     SC_CUDA(cudaLaunchCooperativeKernel((const void *)k_fused_lloyd, f->grid, kFlThreads, args,
-                                        kFlDynSmem, s));
+                                        dyn, s));
     // results: control block, per-restart final iterations and exact costs, best labels
     SC_CUDA(cudaMemcpyAsync(f->h_ctl, a.ctl, kCtlSlots * 4, cudaMemcpyDeviceToHost, s));
     std::vector<int32_t> fin(R);
@@ -1316,7 +1625,7 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     SC_CUDA(cudaMemcpyAsync(cex.data(), a.cexact, R * 8, cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
     if (prof) {
-        std::vector<unsigned long long> tp(256 * 8);
+        std::vector<unsigned long long> tp(258 * 8);
         SC_CUDA(cudaMemcpy(tp.data(), a.tprof, tp.size() * 8, cudaMemcpyDeviceToHost));
         SC_CUDA(cudaFree(a.tprof));
         double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -1325,9 +1634,19 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
             for (int q = 1; q < 6; ++q)
                 if (tp[i * 8 + q] && tp[i * 8 + q - 1]) acc[q] += (tp[i * 8 + q] - tp[i * 8 + q - 1]) * 1e-3;
         fprintf(stderr, "[fused_lloyd] n=%lld k=%d R=%d grid=%d iterations %d: P1 %.1f us, P2 %.1f, "
-                "exact/decide %.1f, P3 %.1f, P4 %.1f; final costs %.1f us; total %.1f us\n",
+                "exact decisions %.1f, P3 %.1f, P4 %.1f; final costs %.1f us; total %.1f us; "
+                "element-wise chunks %d, ordered maps %d\n",
                 (long long)n, k, R, f->grid, its, acc[1], acc[2], acc[3], acc[4], acc[5],
-                (tp[255 * 8 + 1] - tp[255 * 8]) * 1e-3, (tp[255 * 8 + 1] - tp[0]) * 1e-3);
+                (tp[255 * 8 + 1] - tp[255 * 8]) * 1e-3, (tp[255 * 8 + 1] - tp[0]) * 1e-3,
+                f->h_ctl[kCtlNCross], f->h_ctl[kCtlNTie]);
+        fprintf(stderr, "[fused_lloyd] walks: longest %.1f us, latest end after P3 %.1f us, total %.1f us, "
+                "in element-wise chunks %.1f us; batches in one step %llu, stepped %llu, steps %llu\n",
+                tp[256 * 8] * 1e-3, tp[256 * 8 + 1] * 1e-3, tp[256 * 8 + 2] * 1e-3, tp[256 * 8 + 3] * 1e-3,
+                tp[256 * 8 + 4], tp[256 * 8 + 5], tp[256 * 8 + 6]);
+        fprintf(stderr, "[fused_lloyd] P1 tasks: mean %.2f us, max %.2f us; max per-warp P1 time %.2f us, "
+                "max tasks per warp %llu, max P1 end since iteration start %.2f us\n",
+                tp[256 * 8 + 7] * 1e-3 / (41.0 * 9770), tp[256 * 8 + 8] * 1e-3, tp[256 * 8 + 9] * 1e-3,
+                tp[256 * 8 + 10], tp[256 * 8 + 11] * 1e-3);
     }
     if (f->h_ctl[kCtlErr])
         return fail(SC_E_INTERNAL, "k-means cost increased (restart %d, iteration %d)",
