@@ -71,6 +71,9 @@ def load() -> ctypes.CDLL:
         raise DeviceError(
             f"native library {LIB_PATH} is missing; build it with "
             "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    # the library carries its own (static) CUDA runtime; load every kernel when it initialises
+    # instead of at each kernel's first launch (which put ~10 ms into the first clustering)
+    os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
     L = ctypes.CDLL(LIB_PATH)
     P, i32, i64, u32, u64, f64 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
                                   ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double)

@@ -123,12 +123,18 @@ struct FlArgs {
     double *cen;       // [3][R][k]
     double *A;         // [R][k][nch] approximate chunk sums
     int32_t *cnt;      // [R][k][nch]
-    int32_t *pred;     // [R][k][nch] grid, kCrossTag + grid, kNoGrid, kSkip
+    int32_t *pred2;    // [2][R][k][nch] per iteration parity: grid, kCrossTag + grid, kNoGrid, kSkip
+    int32_t *chg;      // [R][nch] labels changed in the chunk by the assignment of it
+    double *sfirst;    // [R][k] exact running sum after the cluster's first chunk
     double *AS;        // [R][k][nch] approximate running sum at each chunk start
     int64_t *M;        // [R][k][nch] packed parity maps (before the crossing, if any)
     int64_t *MC;       // [R][k][nch][2] crossing records: packed map after, crossing value
     uint32_t *xlist;   // [R*k*nch] queued crossing records (c << 11 | r << 5 | j)
     int32_t *rng;      // [R][k][2] first and last chunk holding the cluster
+    int nbat;          // batches of 32 chunks
+    int64_t *PP, *SS;  // [R][k][nch] packed prefix / suffix compositions inside the batch
+    int32_t *BG;       // [R][k][nbat] batch grid (kSkip / kNoGrid if not uniform)
+    int64_t *BM;       // [R][k][nbat] packed composition of the batch
     double *cpart;     // [R][nch] approximate cost partials
     int32_t *tot;      // [2][R][k] cluster sizes of even / odd iterations (atomics)
     int32_t *changed;  // [2][R]
@@ -150,6 +156,9 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ uint8_t *lab_buf(const FlArgs &a, int it, int r) {
     return a.lab + ((size_t)(((it % 3) + 3) % 3) * a.R + r) * a.ln;
+}
+__device__ __forceinline__ int32_t *pred_buf(const FlArgs &a, int it) {
+    return a.pred2 + (size_t)(it & 1) * a.R * a.k * a.nch;
 }
 __device__ __forceinline__ int32_t *tot_buf(const FlArgs &a, int it) {
     return a.tot + (size_t)(it & 1) * a.R * a.k;
@@ -486,7 +495,10 @@ __device__ void p1_task(const FlArgs &a, int it, int r, int c, P1Mode md, const 
         }
     }
     nchg = warp_isum(nchg);
-    if (lane == 0 && nchg) atomicAdd(a.changed + (it % 3) * a.R + r, nchg);
+    if (lane == 0) {
+        if (nchg) atomicAdd(a.changed + (it % 3) * a.R + r, nchg);
+        __stcg(a.chg + (size_t)r * a.nch + c, nchg);
+    }
     __syncwarp();
 }
 
@@ -495,8 +507,9 @@ __device__ void p1_task(const FlArgs &a, int it, int r, int c, P1Mode md, const 
 // running sum is expected in (pred), or one predicted crossing into the next binade (pred =
 // kCrossTag + grid; the pair is queued for a crossing record); the approximate start of each
 // chunk (AS).
-__device__ void p2_task(const FlArgs &a, int r, int j) {
+__device__ void p2_task(const FlArgs &a, int it, int r, int j) {
     const int lane = lane_id();
+    int32_t *pred = pred_buf(a, it);
     const size_t base = ((size_t)r * a.k + j) * a.nch;
     const double lo_f = 1.0 - 1.0 / 1048576.0, hi_f = 1.0 + 1.0 / 1048576.0;
     double carry = 0.0;
@@ -525,6 +538,13 @@ __device__ void p2_task(const FlArgs &a, int r, int j) {
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int c = c00 + 32 * u + lane;
+            if (!__any_sync(0xffffffffu, cn[u] != 0)) {  // no point of the cluster in the batch
+                if (c < a.nch) {
+                    __stcg(pred + base + c, kSkip);
+                    __stcg(a.AS + base + c, carry);
+                }
+                continue;
+            }
             double incl = av[u];
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -545,7 +565,7 @@ __device__ void p2_task(const FlArgs &a, int r, int j) {
                         kp = grid_of(0.0).k;  // zeros only: identity maps on the subnormal grid
                     }
                 }
-                __stcg(a.pred + base + c, kp);
+                __stcg(pred + base + c, kp);
                 __stcg(a.AS + base + c, st);
                 if (is_cross(kp)) {
                     const int slot = atomicAdd(a.ctl + kCtlNX, 1);
@@ -575,9 +595,15 @@ __device__ void p3a_task(const FlArgs &a, int it, int r, int c, int *spred, doub
     const int lane = lane_id(), k = a.k;
     const int64_t base = (int64_t)c * kFlChunk;
     const size_t ob = (size_t)r * k * a.nch + c;
+    int32_t *pred = pred_buf(a, it);
     int pj = kSkip;
-    if (lane < k && __ldcg(a.cnt + ob + (size_t)lane * a.nch)) pj = __ldcg(a.pred + ob + (size_t)lane * a.nch);
-    const uint32_t want = __ballot_sync(0xffffffffu, lane < k && is_grid(pj));
+    bool keep = false;  // same points and same grid as the last iteration: the map stands
+    if (lane < k && __ldcg(a.cnt + ob + (size_t)lane * a.nch)) {
+        pj = __ldcg(pred + ob + (size_t)lane * a.nch);
+        keep = it > 0 && __ldcg(a.chg + (size_t)r * a.nch + c) == 0 &&
+               __ldcg(pred_buf(a, it - 1) + ob + (size_t)lane * a.nch) == pj;
+    }
+    const uint32_t want = __ballot_sync(0xffffffffu, lane < k && is_grid(pj) && !keep);
     if (!want) return;
     if (lane < k) spred[lane] = pj;
     long long *accQ = reinterpret_cast<long long *>(tile);
@@ -648,7 +674,7 @@ __device__ void p3a_task(const FlArgs &a, int it, int r, int c, int *spred, doub
         const int j = __ffs(b) - 1;
         const size_t oj = ob + (size_t)j * a.nch;
         if ((wh >> j) & 1u) {  // a point beyond the predicted binade: the walk adds the chunk
-            if (lane == 0) __stcg(a.pred + oj, kNoGrid);
+            if (lane == 0) __stcg(pred + oj, kNoGrid);
             continue;
         }
         const long long D = warp_lsum(accQ[j * 32 + lane]);
@@ -690,7 +716,7 @@ __device__ void p3a_task(const FlArgs &a, int it, int r, int c, int *spred, doub
             }
         }
         if (lane == 0) {
-            if (D + 2 >= (int64_t(1) << 53)) __stcg(a.pred + oj, kNoGrid);  // cannot stay in a binade
+            if (D + 2 >= (int64_t(1) << 53)) __stcg(pred + oj, kNoGrid);  // cannot stay in a binade
             else __stcg(a.M + oj, pack_map(PMap{D + C0, D + C1}));
         }
     }
@@ -702,22 +728,29 @@ __device__ void p3a_task(const FlArgs &a, int it, int r, int c, int *spred, doub
 __device__ __forceinline__ void stage_runs(const FlArgs &a, int it, int r, int c, double *tile) {
     const int lane = lane_id();
     double *xs = tile;
-    uint8_t *lb = reinterpret_cast<uint8_t *>(tile + kXsWarp);
+    uint32_t *lb = reinterpret_cast<uint32_t *>(tile + kXsWarp);
     const int64_t base = (int64_t)c * kFlChunk;
-    __syncwarp();
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(lab_buf(a, it, r) + base);
+    // coalesced loads, all 32 + 8 in flight, then the padded stores
+    double v[32];
+    uint32_t w[8];
     if (base + kFlChunk <= a.n) {
-#pragma unroll 8
-        for (int u = 0; u < 32; ++u) cp_async8(xs + u * kXsPitch + lane, a.x + base + 32 * u + lane);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = __ldg(a.x + base + 32 * u + lane);
     } else {
+#pragma unroll
         for (int u = 0; u < 32; ++u) {
             const int64_t i = base + 32 * u + lane;
-            xs[u * kXsPitch + lane] = i < a.n ? __ldg(a.x + i) : 0.0;
+            v[u] = i < a.n ? __ldg(a.x + i) : 0.0;
         }
     }
-    const uint8_t *src = lab_buf(a, it, r) + base;
 #pragma unroll
-    for (int i = lane; i < kFlChunk / 16; i += 32) cp_async16(lb + 16 * i, src + 16 * i);
-    cp_async_wait();
+    for (int u = 0; u < 8; ++u) w[u] = __ldcg(src + 32 * u + lane);
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 32; ++u) xs[u * kXsPitch + lane] = v[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) lb[32 * u + lane] = w[u];
     __syncwarp();
 }
 
@@ -730,7 +763,8 @@ __device__ void p3b_task(const FlArgs &a, int it, uint32_t item, double *tile) {
     if (__ldcg(a.stop + r)) return;
     const int k = a.k;
     const size_t o = ((size_t)r * k + j) * a.nch + c;
-    const int p = __ldcg(a.pred + o);
+    int32_t *pred = pred_buf(a, it);
+    const int p = __ldcg(pred + o);
     const double as0 = __ldcg(a.AS + o);
     stage_runs(a, it, r, c, tile);
     const int64_t i0 = (int64_t)c * kFlChunk + (int64_t)lane * kFlLane;
@@ -800,7 +834,7 @@ __device__ void p3b_task(const FlArgs &a, int it, uint32_t item, double *tile) {
             __stcg(a.MC + 2 * o, pack_map(m2));
             __stcg(reinterpret_cast<double *>(a.MC) + 2 * o + 1, acv);
         } else {
-            __stcg(a.pred + o, kNoGrid);  // the walk adds this chunk element by element
+            __stcg(pred + o, kNoGrid);  // the walk adds this chunk element by element
         }
     }
     __syncwarp();
@@ -887,6 +921,15 @@ __device__ double cross_chunk_impl(const FlArgs &a, int it, int r, int j, int c,
     return s;
 }
 
+// P3c for one (r, j): the cluster's first chunk, from the exact running value 0 (binade
+// crossings at every doubling of the sum fall here), added off the walk's critical path
+__device__ void p3c_task(const FlArgs &a, int it, int r, int j, double *tile) {
+    const int c = __ldcg(a.rng + 2 * ((size_t)r * a.k + j));
+    double s = 0.0;
+    if (c < a.nch) s = cross_chunk(a, it, r, j, c, 0.0, tile);
+    if (lane_id() == 0) __stcg(a.sfirst + (size_t)r * a.k + j, s);
+}
+
 // P4 for one (r, j): the exact walk over the chunks, 32 at a time with 4 batches of records in
 // flight: maximal runs of chunks on the running sum's grid advance with one composed map, a
 // predicted crossing with its two maps and one real add of the crossing point, anything else
@@ -898,88 +941,117 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// P3.5 for one (r, j, batch of 32 chunks): off the walk's critical path, the batch's common
+// grid (when every chunk holding the cluster is mapped on one grid) with the composition of
+// all its chunks, and per chunk the composition of the batch's chunks up to it (prefix) and
+// from it to the batch end (suffix) -- the walk's runs start at a batch start or end at a batch
+// end except between two crossings.
+__device__ void p35_task(const FlArgs &a, int it, int r, int j, int b) {
+    const int lane = lane_id();
+    const size_t base = ((size_t)r * a.k + j) * a.nch;
+    const int c = 32 * b + lane;
+    const int32_t *pred = pred_buf(a, it);
+    const int cfirst = __ldcg(a.rng + 2 * ((size_t)r * a.k + j));
+    int p = kSkip;
+    PMap m = pmap_id();
+    if (c < a.nch && c > cfirst) {
+        p = __ldcg(pred + base + c);
+        if (is_grid(p)) m = unpack_map(__ldcg(a.M + base + c));
+    }
+    const unsigned have = __ballot_sync(0xffffffffu, p != kSkip);
+    const int g0 = __shfl_sync(0xffffffffu, p, have ? __ffs(have) - 1 : 0);
+    const bool uni = __all_sync(0xffffffffu, p == kSkip || (is_grid(p) && p == g0));
+    // inclusive prefix (lane order) and suffix compositions
+    PMap pre = m, suf = m;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        PMap o;
+        o.i0 = __shfl_up_sync(0xffffffffu, pre.i0, d);
+        o.i1 = __shfl_up_sync(0xffffffffu, pre.i1, d);
+        if (lane >= d) pre = pmap_then(o, pre);
+        PMap w;
+        w.i0 = __shfl_down_sync(0xffffffffu, suf.i0, d);
+        w.i1 = __shfl_down_sync(0xffffffffu, suf.i1, d);
+        if (lane + d < 32) suf = pmap_then(suf, w);
+    }
+    if (c < a.nch) {
+        __stcg(a.PP + base + c, pack_map(pre));
+        __stcg(a.SS + base + c, pack_map(suf));
+    }
+    if (lane == 31) {
+        const size_t ob = ((size_t)r * a.k + j) * a.nbat + b;
+        __stcg(a.BG + ob, !have ? kSkip : (uni ? g0 : kNoGrid));
+        __stcg(a.BM + ob, pack_map(pre));
+    }
+}
+
+// P4 for one (r, j): the exact walk over the chunks.  Per batch of 32: on the running sum's grid
+// in one step (P3.5's composition), else runs of mapped chunks with one prefix / suffix
+// composition each, a predicted crossing with its two maps and one real add of the crossing
+// point, anything else element by element (cross_chunk).  Every step is verified against the
+// exact running value.  Writes the cluster's mean for iteration it+1.
 __device__ void p4_task(const FlArgs &a, int it, int r, int j, double *tile) {
     const int lane = lane_id();
     const unsigned long long t_start = a.tprof ? gtimer() : 0;
     const size_t base = ((size_t)r * a.k + j) * a.nch;
-    double s = 0.0;
-    constexpr int kU = 2;  // batches per group; the next group's records load during this one
-    struct Rec {
-        int p;
-        int64_t m, m2;
-        double ac;
-    };
-    auto fetch = [&](int c, Rec &q) {
-        q.p = kSkip;
-        q.m = q.m2 = 1;  // identity
-        q.ac = 0.0;
-        if (c < a.nch) {
-            q.p = __ldcg(a.pred + base + c);
-            q.m = __ldcg(a.M + base + c);
-            q.m2 = __ldcg(a.MC + 2 * (base + c));
-            q.ac = __ldcg(reinterpret_cast<const double *>(a.MC) + 2 * (base + c) + 1);
-        }
-    };
+    const size_t bb = ((size_t)r * a.k + j) * a.nbat;
+    const int32_t *pred = pred_buf(a, it);
     const int cfirst = __ldcg(a.rng + 2 * ((size_t)r * a.k + j));
     const int clast = __ldcg(a.rng + 2 * ((size_t)r * a.k + j) + 1);
-    const int cbeg = cfirst / 32 * 32, cend = clast + 1;  // batches start on multiples of 32
-    Rec nx[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) fetch(cbeg + 32 * u + lane, nx[u]);
-    for (int c00 = cbeg; c00 < cend; c00 += 32 * kU) {
-        Rec cu[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) cu[u] = nx[u];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) fetch(c00 + 32 * (kU + u) + lane, nx[u]);
-        // off the critical path: per batch, the common grid of its chunks (if every chunk
-        // holding the cluster is mapped on one grid) and their composition
-        int gu[kU];
-        PMap bmu[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int p = cu[u].p;
-            const unsigned have = __ballot_sync(0xffffffffu, p != kSkip);
-            const int g0 = __shfl_sync(0xffffffffu, p, have ? __ffs(have) - 1 : 0);
-            const bool uni = __all_sync(0xffffffffu, p == kSkip || (is_grid(p) && p == g0));
-            gu[u] = have && uni ? g0 : kNoGrid;
-            PMap pm = is_grid(p) ? unpack_map(cu[u].m) : pmap_id();
-            pm = warp_reduce_pmap(pm);
-            bmu[u] = PMap{__shfl_sync(0xffffffffu, pm.i0, 0), __shfl_sync(0xffffffffu, pm.i1, 0)};
-            if (!have) gu[u] = kSkip;
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int c0 = c00 + 32 * u;
-            if (c0 >= cend || gu[u] == kSkip) continue;
-            const int lim = min(32, a.nch - c0);
-            const int p = cu[u].p;
-            {  // whole batch on the running grid: one step
+    double s = __ldcg(a.sfirst + (size_t)r * a.k + j);  // the first chunk was added in P3
+    const int b_beg = (cfirst + 1) / 32, b_end = clast / 32 + 1;
+    for (int b0 = b_beg; b0 < b_end; b0 += 32) {
+        // batch summaries of up to 32 batches, one per lane
+        const int bl = b0 + lane;
+        const int bg_l = bl < b_end ? __ldcg(a.BG + bb + bl) : kSkip;
+        const int64_t bm_l = bl < b_end ? __ldcg(a.BM + bb + bl) : 1;
+        const int nb = min(32, b_end - b0);
+        for (int q = 0; q < nb; ++q) {
+            const int bg = __shfl_sync(0xffffffffu, bg_l, q);
+            if (bg == kSkip) continue;
+            {
                 const Grid gs = grid_of(s);
-                if (gu[u] == gs.k) {
-                    const int64_t S1 = pmap_apply(bmu[u], run_units(s, gs.k));
+                if (bg == gs.k) {
+                    const int64_t S1 = pmap_apply(unpack_map(__shfl_sync(0xffffffffu, bm_l, q)), run_units(s, gs.k));
                     if (S1 < gs.top) {
                         s = run_from(S1, gs.k);
-                        if (a.tprof && lane == 0) atomicAdd(a.tprof + 256 * 8 + 4, 1ull);
                         continue;
                     }
                 }
-                if (a.tprof && lane == 0) atomicAdd(a.tprof + 256 * 8 + 5, 1ull);
             }
-            const PMap mine = is_grid(p) || is_cross(p) ? unpack_map(cu[u].m) : pmap_id();
+            // chunk by chunk inside batch b
+            const int b = b0 + q;
+            const int c0 = 32 * b, c = c0 + lane;
+            const int lim = min(32, a.nch - c0);
+            int p = kSkip;
+            int64_t mw = 1, pp = 1, ss = 1, m2w = 1;
+            double ac = 0.0;
+            if (c < a.nch && c > cfirst) {
+                p = __ldcg(pred + base + c);
+                mw = __ldcg(a.M + base + c);
+                pp = __ldcg(a.PP + base + c);
+                ss = __ldcg(a.SS + base + c);
+                m2w = __ldcg(a.MC + 2 * (base + c));
+                ac = __ldcg(reinterpret_cast<const double *>(a.MC) + 2 * (base + c) + 1);
+            }
             int L = 0;
             while (L < lim) {
-                if (a.tprof && lane == 0) atomicAdd(a.tprof + 256 * 8 + 6, 1ull);
                 const Grid gs = grid_of(s);
                 const bool ok = p == kSkip || p == gs.k;
                 const unsigned badm = __ballot_sync(0xffffffffu, !ok && lane >= L && lane < lim);
                 const int L2 = badm ? __ffs(badm) - 1 : lim;
                 if (L2 > L) {
-                    const bool in = lane >= L && lane < L2 && p != kSkip;
-                    if (__any_sync(0xffffffffu, in)) {
-                        PMap pm = in ? mine : pmap_id();
-                        pm = warp_reduce_pmap(pm);
-                        const PMap bm{__shfl_sync(0xffffffffu, pm.i0, 0), __shfl_sync(0xffffffffu, pm.i1, 0)};
+                    if (__any_sync(0xffffffffu, lane >= L && lane < L2 && p != kSkip)) {
+                        PMap bm;
+                        if (L == 0) {
+                            bm = unpack_map(__shfl_sync(0xffffffffu, pp, L2 - 1));
+                        } else if (L2 == lim) {
+                            bm = unpack_map(__shfl_sync(0xffffffffu, ss, L));
+                        } else {
+                            PMap pm = (lane >= L && lane < L2 && p != kSkip) ? unpack_map(mw) : pmap_id();
+                            pm = warp_reduce_pmap(pm);
+                            bm = PMap{__shfl_sync(0xffffffffu, pm.i0, 0), __shfl_sync(0xffffffffu, pm.i1, 0)};
+                        }
                         const int64_t S1 = pmap_apply(bm, run_units(s, gs.k));
                         if (S1 >= gs.top) {  // left the binade inside the run: first chunk by hand
                             s = cross_chunk(a, it, r, j, c0 + L, s, tile);
@@ -995,9 +1067,9 @@ __device__ void p4_task(const FlArgs &a, int it, int r, int j, double *tile) {
                 const int pL = __shfl_sync(0xffffffffu, p, L);
                 bool done = false;
                 if (is_cross(pL) && pL - kCrossTag == gs.k) {
-                    const int64_t w1 = __shfl_sync(0xffffffffu, cu[u].m, L);
-                    const int64_t w2 = __shfl_sync(0xffffffffu, cu[u].m2, L);
-                    const double acl = __shfl_sync(0xffffffffu, cu[u].ac, L);
+                    const int64_t w1 = __shfl_sync(0xffffffffu, mw, L);
+                    const int64_t w2 = __shfl_sync(0xffffffffu, m2w, L);
+                    const double acl = __shfl_sync(0xffffffffu, ac, L);
                     const int g2l = gs.k - 1;
                     const int64_t S1 = pmap_apply(unpack_map(w1), run_units(s, gs.k));
                     if (S1 < gs.top) {
@@ -1310,7 +1382,7 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
         for (int t = gw; t < nact * (k + 1); t += nw) {
             const int r = act[t / (k + 1)], j = t % (k + 1);
             if (j < k) {
-                if (assign) p2_task(a, r, j);
+                if (assign) p2_task(a, it, r, j);
                 if (j == 0 && lane == 0) a.changed[((it + 1) % 3) * R + r] = 0;
                 if (lane == 0) tot_buf(a, it + 1)[(size_t)r * k + j] = 0;  // for P1 of it+1
                 continue;
@@ -1378,12 +1450,37 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
         tmark(a, it, 3);
         // ---- P3: chunk maps (a) and crossing records (b)
         {
-            const int na = nact_s, nsteady = na * a.nch;
+            // the long first-chunk tasks first, then the crossing records, then the maps
+            const int na = nact_s, nfirst = na * k, nsteady = na * a.nch;
             const int nx = __ldcg(a.ctl + kCtlNX);
-            for (int t = gw; t < nsteady + nx; t += nw) {
-                if (t < nsteady) p3a_task(a, it, act[t / a.nch], t % a.nch, spred, tile);
-                else p3b_task(a, it, __ldcg(a.xlist + (t - nsteady)), tile);
+            const unsigned long long w0 = a.tprof ? gtimer() : 0;
+            for (int t = gw; t < nfirst + nx + nsteady; t += nw) {
+                const unsigned long long t0 = a.tprof ? gtimer() : 0;
+                int kind;
+                if (t < nfirst) {
+                    p3c_task(a, it, act[t / k], t % k, tile);
+                    kind = 0;
+                } else if (t < nfirst + nx) {
+                    p3b_task(a, it, __ldcg(a.xlist + (t - nfirst)), tile);
+                    kind = 1;
+                } else {
+                    p3a_task(a, it, act[(t - nfirst - nx) / a.nch], (t - nfirst - nx) % a.nch, spred, tile);
+                    kind = 2;
+                }
+                if (a.tprof && lane == 0) {
+                    const unsigned long long dt = gtimer() - t0;
+                    atomicAdd(a.tprof + 258 * 8 + kind, dt);
+                    atomicMax(a.tprof + 258 * 8 + 3 + kind, dt);
+                    atomicAdd(a.tprof + 259 * 8 + kind, 1ull);
+                }
             }
+            if (a.tprof && lane == 0) atomicMax(a.tprof + 259 * 8 + 3, gtimer() - w0);
+        }
+        grid.sync();
+        // ---- P3.5: batch compositions
+        for (int t = gw; t < nact_s * k * a.nbat; t += nw) {
+            const int rj = t / a.nbat;
+            p35_task(a, it, act[rj / k], rj % k, t % a.nbat);
         }
         grid.sync();
         tmark(a, it, 4);
@@ -1542,6 +1639,7 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     }
     const int64_t nch = (n + kFlChunk - 1) / kFlChunk;
     const int64_t nbuf = (n + kFlEinsumBuf - 1) / kFlEinsumBuf;
+    const int64_t nbat = (nch + 31) / 32;
     const size_t rk = (size_t)R * k;
     // one allocation, carved
     size_t off = 0;
@@ -1552,9 +1650,10 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     };
     const int64_t ln = nch * kFlChunk;
     const size_t o_lab = carve((size_t)3 * R * ln), o_cen = carve(3 * rk * 8),
-                 o_A = carve(rk * nch * 8), o_cnt = carve(rk * nch * 4), o_p = carve(rk * nch * 4),
+                 o_A = carve(rk * nch * 8), o_cnt = carve(rk * nch * 4), o_p = carve(2 * rk * nch * 4), o_chg2 = carve((size_t)R * nch * 4), o_sf = carve(rk * 8),
                  o_AS = carve(rk * nch * 8), o_M = carve(rk * nch * 8), o_MC = carve(rk * nch * 16),
-                 o_xl = carve(rk * nch * 4), o_rng = carve(rk * 8),
+                 o_xl = carve(rk * nch * 4), o_rng = carve(rk * 8), o_PP = carve(rk * nch * 8), o_SS = carve(rk * nch * 8),
+                 o_BG = carve(rk * nbat * 4), o_BM = carve(rk * nbat * 8),
                  o_cpart = carve((size_t)R * nch * 8), o_tot = carve(2 * rk * 4),
                  o_chg = carve((size_t)3 * R * 4), o_ctl = carve(kCtlSlots * 4),
                  o_stop = carve(R * 4), o_amb = carve(R * 4), o_rep = carve(R * 4),
@@ -1585,11 +1684,18 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     a.cen = reinterpret_cast<double *>(B + o_cen);
     a.A = reinterpret_cast<double *>(B + o_A);
     a.cnt = reinterpret_cast<int32_t *>(B + o_cnt);
-    a.pred = reinterpret_cast<int32_t *>(B + o_p);
+    a.pred2 = reinterpret_cast<int32_t *>(B + o_p);
+    a.chg = reinterpret_cast<int32_t *>(B + o_chg2);
+    a.sfirst = reinterpret_cast<double *>(B + o_sf);
     a.AS = reinterpret_cast<double *>(B + o_AS);
     a.MC = reinterpret_cast<int64_t *>(B + o_MC);
     a.xlist = reinterpret_cast<uint32_t *>(B + o_xl);
     a.rng = reinterpret_cast<int32_t *>(B + o_rng);
+    a.nbat = (int)nbat;
+    a.PP = reinterpret_cast<int64_t *>(B + o_PP);
+    a.SS = reinterpret_cast<int64_t *>(B + o_SS);
+    a.BG = reinterpret_cast<int32_t *>(B + o_BG);
+    a.BM = reinterpret_cast<int64_t *>(B + o_BM);
     a.M = reinterpret_cast<int64_t *>(B + o_M);
     a.cpart = reinterpret_cast<double *>(B + o_cpart);
     a.tot = reinterpret_cast<int32_t *>(B + o_tot);
@@ -1609,8 +1715,8 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     const bool prof = getenv("SC_KMEANS_PROFILE") != nullptr;
     a.tprof = nullptr;
     if (prof) {
-        SC_CUDA(cudaMallocAsync((void **)&a.tprof, 258 * 8 * 8, s));
-        SC_CUDA(cudaMemsetAsync(a.tprof, 0, 258 * 8 * 8, s));
+        SC_CUDA(cudaMallocAsync((void **)&a.tprof, 260 * 8 * 8, s));
+        SC_CUDA(cudaMemsetAsync(a.tprof, 0, 260 * 8 * 8, s));
     }
     k_fl_init<<<f->grid, 256, 0, s>>>(a, d_x, f->sign < 0 ? -1.0 : 1.0, d_chosen);
     SC_CUDA(cudaGetLastError());
@@ -1625,7 +1731,7 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     SC_CUDA(cudaMemcpyAsync(cex.data(), a.cexact, R * 8, cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
     if (prof) {
-        std::vector<unsigned long long> tp(258 * 8);
+        std::vector<unsigned long long> tp(260 * 8);
         SC_CUDA(cudaMemcpy(tp.data(), a.tprof, tp.size() * 8, cudaMemcpyDeviceToHost));
         SC_CUDA(cudaFree(a.tprof));
         double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -1643,6 +1749,12 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
                 "in element-wise chunks %.1f us; batches in one step %llu, stepped %llu, steps %llu\n",
                 tp[256 * 8] * 1e-3, tp[256 * 8 + 1] * 1e-3, tp[256 * 8 + 2] * 1e-3, tp[256 * 8 + 3] * 1e-3,
                 tp[256 * 8 + 4], tp[256 * 8 + 5], tp[256 * 8 + 6]);
+        for (int kind = 0; kind < 3; ++kind)
+            fprintf(stderr, "[fused_lloyd] P3 %s: %llu tasks, mean %.2f us, max %.2f us\n",
+                    kind == 0 ? "first chunks" : kind == 1 ? "crossing records" : "chunk maps",
+                    tp[259 * 8 + kind], tp[258 * 8 + kind] * 1e-3 / std::max(1ull, tp[259 * 8 + kind]),
+                    tp[258 * 8 + 3 + kind] * 1e-3);
+        fprintf(stderr, "[fused_lloyd] P3 max per-warp time %.2f us\n", tp[259 * 8 + 3] * 1e-3);
         fprintf(stderr, "[fused_lloyd] P1 tasks: mean %.2f us, max %.2f us; max per-warp P1 time %.2f us, "
                 "max tasks per warp %llu, max P1 end since iteration start %.2f us\n",
                 tp[256 * 8 + 7] * 1e-3 / (41.0 * 9770), tp[256 * 8 + 8] * 1e-3, tp[256 * 8 + 9] * 1e-3,
