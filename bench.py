@@ -64,15 +64,14 @@ def parse():
 GRAPH_DESC = {
     1: "SBM, reference sample_sbm semantics (seed 0)",
     2: "SBM, reference sample_sbm semantics (seed 0)",
-    3: "DC-SBM, Dirichlet blocks, power-law degrees 5..5000, weights U(0.5,1.5) (seed 0)",
-    4: "weighted 3-D RGG, 16-NN union, exp(-d^2/0.01) weights (seed 0)",
+    3: "DC-SBM, Dirichlet blocks, power-law degrees 5..5000, weights U(0.5,1.5), device generator (seed 0)",
+    4: "weighted 3-D RGG, 16-NN union, exp(-d^2/0.01) weights, device generator (seed 0)",
     5: "SBM config-5 law (blocks of 1e5, degree 16 in / 2 out), device generator (seed 0)",
 }
 
 
 def build_config(cfg: int):
-    from paper_2310_10939_b200.generate import (CONFIG_K, CONFIG_T, config_sbm, sample_dcsbm,
-                                                sample_sbm, sample_weighted_rgg)
+    from paper_2310_10939_b200.generate import CONFIG_K, CONFIG_T, config_sbm, config_device_csr, sample_sbm
 
     if cfg in (1, 2):
         g = sample_sbm(config_sbm(cfg)).graph
@@ -81,10 +80,10 @@ def build_config(cfg: int):
         from paper_2310_10939_b200.generate import sample_sbm_device
 
         g = sample_sbm_device(config_sbm(5), pinned=True).graph
-    elif cfg == 3:
-        g = sample_dcsbm(4_000_000, 50, seed=0).graph
-    elif cfg == 4:
-        g = sample_weighted_rgg(10_000_000, 100, seed=0).graph
+    elif cfg in (3, 4):
+        # device generators (sc_generate_wt.cu), page-locked download for the end-to-end leg
+        with config_device_csr(cfg) as d:
+            g = d.download(pinned=True).graph
     else:
         raise SystemExit(f"unknown config {cfg}")
     return g, CONFIG_T[cfg], CONFIG_K[cfg]

@@ -224,6 +224,23 @@ int32_t sc_csr_info(const sc_csr *h, int64_t *n, int64_t *nnz, int64_t *n_genera
 int32_t sc_csr_download(const sc_csr *h, int64_t *row_ptr, int32_t *col, double *deg,
                         int32_t *orig_ids);
 void sc_csr_destroy(sc_csr *h);
+/* weights of a weighted device CSR (nnz doubles; SC_E_STATE for unit-weight CSRs) */
+int32_t sc_csr_download_weights(const sc_csr *h, double *val);
+/* config 4 (weighted random geometric cluster graph): k Gaussian-like
+ * centres in [0,1]^3, n points, each joined to its knn (= 16) nearest by exact rounded d2,
+ * union symmetrised, weight exp(-d2 / scale) (sc_generate_wt.cu states the law; replaces the
+ * reference's brute-force unit-weight kNN builder, generate.py:176-220, which refuses
+ * n > 50,000) */
+int32_t sc_generate_knn3d(int64_t n, int32_t k, double sigma, int32_t knn, double scale,
+                          uint64_t key0, uint64_t key1, int32_t device, sc_csr **out);
+/* config 3 (degree-corrected SBM): block_offsets[nblocks + 1] from the
+ * host (Dirichlet sizes), integer power-law expected degrees (A = dmin^a, B = dmax^a,
+ * inv_a = 1/a, a = 1 - gamma), Chung-Lu stubs inside the block with probability 1 - mix,
+ * weights Uniform(wlo, whi); isolated vertices dropped */
+int32_t sc_generate_dcsbm(int64_t n, const int64_t *block_offsets, int32_t nblocks, double A,
+                          double B, double inv_a, int32_t dmin, int32_t dmax, double mix,
+                          double wlo, double whi, uint64_t key0, uint64_t key1, int32_t device,
+                          sc_csr **out);
 /* graph handle straight from a device-resident CSR (the column array is not copied to the
  * host; the handle does not keep a reference to h) */
 int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_graph **out);

@@ -377,3 +377,155 @@ def device_sbm(n: int, k: int, p: float, q: float, seed: int):
     rp = np.zeros(int(keep.sum()) + 1, dtype=np.int64)
     np.cumsum(deg[keep], out=rp[1:])
     return rp, newid[c].astype(np.int32), deg[keep].astype(np.float64), np.flatnonzero(keep)
+
+
+# ---------------------------------------------------------------------------
+# the weighted device generators' laws (sc_generate_wt.cu, configs 3 and 4), restated op for op
+# in numpy; small n only.  Ours, not reference algorithms (the reference has no generator for
+# either graph), so they are pinned by this restatement.
+
+KNN_TAG_CENTRES, KNN_TAG_POINTS = 0x43454E54, 0x504F494E
+DC_TAG_DEGREES, DC_TAG_STUBS = 0x44454752, 0x53545542
+DBL_MIN = 2.2250738585072014e-308
+
+
+def np_sc_exp(y: np.ndarray) -> np.ndarray:
+    """sc_genmath.cuh sc_exp: Cody-Waite reduction, degree-14 Taylor, exact 2^q scaling."""
+    y = np.asarray(y, dtype=np.float64)
+    q = np.rint(y * 1.4426950408889634)
+    r = (y - q * 0.6931471803691238) - q * 1.9082149292705877e-10
+    fact = [87178291200.0, 6227020800.0, 479001600.0, 39916800.0, 3628800.0, 362880.0, 40320.0,
+            5040.0, 720.0, 120.0, 24.0, 6.0]
+    p = np.full_like(r, 1.0 / fact[0])
+    for f in fact[1:]:
+        p = p * r + 1.0 / f
+    p = p * r + 0.5
+    p = p * r + 1.0
+    p = p * r + 1.0
+    qi = np.clip(q, -1000, 1000).astype(np.int64)
+    scale = ((qi + 1023).astype(np.uint64) << np.uint64(52)).view(np.float64)
+    out = p * scale
+    out = np.where(y > -700.0, out, 0.0)
+    return np.where(y > 700.0, np.inf, out)
+
+
+def _u53(raw: np.ndarray) -> np.ndarray:
+    return (raw >> np.uint64(11)).astype(np.float64) * 1.1102230246251565e-16
+
+
+def _words(key, ident: int, tag: int, count: int) -> np.ndarray:
+    return np.random.Philox(key=key, counter=[0, ident, tag, 0]).random_raw(count)
+
+
+def _seq_row_sums(rp: np.ndarray, val: np.ndarray) -> np.ndarray:
+    """Each row's weights summed left to right (one rounded add per entry, column order)."""
+    n = rp.size - 1
+    lens = np.diff(rp)
+    deg = np.zeros(n)
+    for t in range(int(lens.max()) if n else 0):
+        rows = np.flatnonzero(lens > t)
+        deg[rows] = deg[rows] + val[rp[rows] + t]
+    return deg
+
+
+def _csr_from_pairs(n: int, r: np.ndarray, c: np.ndarray, w: np.ndarray):
+    """Unique symmetric (r, c, w) -> (row_ptr, col, val, deg, orig) with empty rows dropped."""
+    order = np.lexsort((c, r))
+    r, c, w = r[order], c[order], w[order]
+    lens = np.bincount(r, minlength=n)
+    keep = lens > 0
+    newid = np.cumsum(keep) - 1
+    rp = np.zeros(int(keep.sum()) + 1, dtype=np.int64)
+    np.cumsum(lens[keep], out=rp[1:])
+    val = w.astype(np.float64)
+    return rp, newid[c].astype(np.int32), val, _seq_row_sums(rp, val), np.flatnonzero(keep)
+
+
+def device_knn3d_points(n: int, k: int, sigma: float, seed: int):
+    key = np.array(np.random.SeedSequence([seed, 10]).generate_state(2, np.uint64))
+    cen = np.array([_u53(_words(key, j, KNN_TAG_CENTRES, 3)) for j in range(k)])
+    pts = np.empty((n, 3))
+    lab = np.empty(n, dtype=np.int64)
+    for i in range(n):
+        u = _u53(_words(key, i, KNN_TAG_POINTS, 37))
+        lb = min(int(np.floor(u[0] * float(k))), k - 1)
+        lab[i] = lb
+        for c in range(3):
+            acc = 0.0
+            for t in range(12):
+                acc = acc + float(u[1 + 12 * c + t])
+            pts[i, c] = float(cen[lb, c]) + sigma * (acc - 6.0)
+    return pts, lab
+
+
+def device_knn3d(n: int, k: int, sigma: float, knn: int, scale: float, seed: int):
+    """sc_generate_knn3d restated: (row_ptr, col, val, deg, orig, points, labels)."""
+    pts, lab = device_knn3d_points(n, k, sigma, seed)
+    rs, cs, ws = [], [], []
+    idx = np.arange(n)
+    for i0 in range(0, n, 256):
+        blk = pts[i0:i0 + 256]
+        dx = blk[:, 0:1] - pts[None, :, 0]
+        dy = blk[:, 1:2] - pts[None, :, 1]
+        dz = blk[:, 2:3] - pts[None, :, 2]
+        d2 = (dx * dx + dy * dy) + dz * dz
+        for t in range(blk.shape[0]):
+            i = i0 + t
+            row = d2[t].copy()
+            row[i] = np.inf
+            order = np.lexsort((idx, row))[:knn]
+            rs.append(np.full(knn, i))
+            cs.append(order)
+            ws.append(np.maximum(np_sc_exp(-(row[order] / scale)), DBL_MIN))
+    r = np.concatenate(rs)
+    c = np.concatenate(cs)
+    w = np.concatenate(ws)
+    key = np.concatenate([r * n + c, c * n + r])
+    ww = np.concatenate([w, w])
+    key, first = np.unique(key, return_index=True)
+    rp, col, val, deg, orig = _csr_from_pairs(n, key // n, key % n, ww[first])
+    return rp, col, val, deg, orig, pts, lab
+
+
+def device_dcsbm(n: int, offsets, A: float, B: float, inv_a: float, dmin: int, dmax: int,
+                 mix: float, wlo: float, whi: float, seed: int):
+    """sc_generate_dcsbm restated: (row_ptr, col, val, deg, orig)."""
+    key = np.array(np.random.SeedSequence([seed, 11]).generate_state(2, np.uint64))
+    offsets = np.asarray(offsets, dtype=np.int64)
+    d = np.empty(n, dtype=np.int64)
+    m = np.empty(n, dtype=np.int64)
+    for i in range(n):
+        u = _u53(_words(key, i, DC_TAG_DEGREES, 2))
+        x = np_sc_exp(np_sc_log(np.array([A + u[0] * (B - A)])) * inv_a)[0]
+        fl = min(max(float(np.floor(x)), float(dmin)), float(dmax))
+        d[i] = int(fl)
+        m[i] = d[i] // 2 + (1 if (d[i] & 1) and u[1] < 0.5 else 0)
+    cum = np.cumsum(d)
+    W = int(cum[-1])
+    blk = np.searchsorted(offsets, np.arange(n), side="right") - 1
+    keys, ws = [], []
+    for i in range(n):
+        if m[i] == 0:
+            continue
+        u = _u53(_words(key, i, DC_TAG_STUBS, 3 * int(m[i]))).reshape(-1, 3)
+        b0, b1 = int(offsets[blk[i]]), int(offsets[blk[i] + 1])
+        before = int(cum[b0 - 1]) if b0 > 0 else 0
+        Wb = int(cum[b1 - 1]) - before
+        for ua, ub, uc in u:
+            if ua >= mix:
+                t = before + int(np.floor(ub * float(Wb)))
+                p = b0 + int(np.searchsorted(cum[b0:b1], t, side="right"))
+            else:
+                t = int(np.floor(ub * float(W)))
+                p = int(np.searchsorted(cum, t, side="right"))
+            w = wlo + (whi - wlo) * uc
+            if p == i:
+                continue
+            keys.append(min(i, p) * n + max(i, p))
+            ws.append(w)
+    keys = np.array(keys, dtype=np.int64)
+    ws = np.array(ws)
+    uk, first = np.unique(keys, return_index=True)  # first occurrence = first stub
+    a, b = uk // n, uk % n
+    w = ws[first]
+    return _csr_from_pairs(n, np.concatenate([a, b]), np.concatenate([b, a]), np.concatenate([w, w]))

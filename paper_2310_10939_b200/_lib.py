@@ -52,7 +52,8 @@ EXPORTS = (
     "sc_kmeans_create", "sc_kmeans_create_from_graph", "sc_kmeans_destroy", "sc_kmeans_pp",
     "sc_kmeans_lloyd", "sc_seqsum", "sc_sell_order", "sc_graph_order", "sc_graph_create_ex",
     "sc_shard_step_range", "sc_shard_scale_range", "sc_generate_sbm", "sc_csr_info",
-    "sc_csr_download", "sc_csr_destroy", "sc_graph_create_from_csr", "sc_shard_buffers",
+    "sc_csr_download", "sc_csr_destroy", "sc_graph_create_from_csr", "sc_csr_download_weights",
+    "sc_generate_knn3d", "sc_generate_dcsbm", "sc_shard_buffers",
     "sc_shard_set_peers", "sc_shard_barrier", "sc_ipc_export", "sc_ipc_import", "sc_ipc_release",
     "sc_keyed_sums", "sc_contingency", "sc_cut_sums", "sc_power_iterate_block",
     "sc_kmeans_create_nd", "sc_kmeans_lloyd_sorted", "sc_release_cached_memory",
@@ -109,6 +110,10 @@ def load() -> ctypes.CDLL:
         "sc_csr_info": ([P, P, P, P], i32),
         "sc_csr_download": ([P, P, P, P, P], i32),
         "sc_csr_destroy": ([P], None),
+        "sc_csr_download_weights": ([P, P], i32),
+        "sc_generate_knn3d": ([i64, i32, f64, i32, f64, u64, u64, i32, PP], i32),
+        "sc_generate_dcsbm": ([i64, P, i32, f64, f64, f64, i32, i32, f64, f64, f64, u64, u64, i32, PP],
+                              i32),
         "sc_graph_create_from_csr": ([P, u32, PP], i32),
         "sc_shard_buffers": ([P, PP, PP], i32),
         "sc_shard_set_peers": ([P, P, P, i32, i32], i32),

@@ -28,53 +28,12 @@
 
 #include "sc_common.cuh"
 
-struct sc_csr {
-    int device = 0;
-    int64_t n = 0;          // vertices kept
-    int64_t n_gen = 0;      // vertices generated
-    int64_t nnz = 0;
-    int64_t *d_rp = nullptr;
-    int32_t *d_col = nullptr;
-    double *d_deg = nullptr;
-    int32_t *d_orig = nullptr;  // original (generated) id of every kept vertex
-};
+#include "sc_csr.cuh"
+#include "sc_genmath.cuh"
 
 namespace sc {
 
 constexpr uint64_t kGenTag = 0x5bd1e995u;
-
-// natural log of x in (0, 2^1024) from correctly rounded +,-,*,/ only (no FMA: the library
-// is built with -fmad=false), so host and device agree bit for bit.
-// x = 2^e * m, m in [sqrt(1/2), sqrt(2)); log m = 2 atanh(t), t = (m - 1) / (m + 1),
-// |t| <= 0.1716: 12 odd terms leave a truncation error below 1e-19 relative.
-__host__ __device__ inline double sc_log(double x) {
-    uint64_t b;
-    memcpy(&b, &x, 8);
-    int e = (int)((b >> 52) & 0x7ff) - 1023;
-    b = (b & 0x000fffffffffffffull) | 0x3ff0000000000000ull;  // m in [1, 2)
-    double m;
-    memcpy(&m, &b, 8);
-    if (m > 1.4142135623730951) {
-        m = m * 0.5;
-        e += 1;
-    }
-    const double t = (m - 1.0) / (m + 1.0);
-    const double t2 = t * t;
-    double p = 1.0 / 25.0;
-    p = p * t2 + 1.0 / 23.0;
-    p = p * t2 + 1.0 / 21.0;
-    p = p * t2 + 1.0 / 19.0;
-    p = p * t2 + 1.0 / 17.0;
-    p = p * t2 + 1.0 / 15.0;
-    p = p * t2 + 1.0 / 13.0;
-    p = p * t2 + 1.0 / 11.0;
-    p = p * t2 + 1.0 / 9.0;
-    p = p * t2 + 1.0 / 7.0;
-    p = p * t2 + 1.0 / 5.0;
-    p = p * t2 + 1.0 / 3.0;
-    p = p * t2 + 1.0;
-    return (double)e * 0.6931471805599453 + 2.0 * t * p;
-}
 
 struct RowStream {
     uint64_t u, k0, k1;
@@ -335,6 +294,14 @@ int32_t sc_csr_info(const sc_csr *h, int64_t *n, int64_t *nnz, int64_t *n_genera
     return SC_OK;
 }
 
+int32_t sc_csr_download_weights(const sc_csr *h, double *val) {
+    SC_REQUIRE(h && val, SC_E_INVALID, "null argument");
+    SC_REQUIRE(h->d_val, SC_E_STATE, "the CSR has unit weights");
+    SC_CUDA(cudaSetDevice(h->device));
+    if (h->nnz) SC_CUDA(cudaMemcpy(val, h->d_val, (size_t)h->nnz * 8, cudaMemcpyDeviceToHost));
+    return SC_OK;
+}
+
 int32_t sc_csr_download(const sc_csr *h, int64_t *row_ptr, int32_t *col, double *deg,
                         int32_t *orig_ids) {
     SC_REQUIRE(h, SC_E_INVALID, "null csr");
@@ -353,6 +320,7 @@ void sc_csr_destroy(sc_csr *h) {
     cudaFree(h->d_col);
     cudaFree(h->d_deg);
     cudaFree(h->d_orig);
+    if (h->d_val) cudaFree(h->d_val);
     delete h;
 }
 
@@ -361,8 +329,9 @@ void sc_csr_destroy(sc_csr *h) {
 namespace sc {
 // device-side view for sc_graph_create_from_csr (sc_graph.cu)
 int32_t csr_device_arrays(const sc_csr *h, const int64_t **rp, const int32_t **col,
-                          const double **deg, int32_t *device) {
+                          const double **deg, const double **val, int32_t *device) {
     SC_REQUIRE(h, SC_E_INVALID, "null csr");
+    *val = h->d_val;
     *rp = h->d_rp;
     *col = h->d_col;
     *deg = h->d_deg;

@@ -1006,7 +1006,8 @@ static cudaError_t reorder_bfs(sc_graph *g, cudaStream_t s, const int64_t *rp, c
 static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const double *val,
                           const double *deg, int64_t n, int64_t nnz, int64_t ncols,
                           int64_t col_offset, int64_t global_row0, int rename, uint32_t cflags, int32_t device,
-                          sc_graph **out, const int32_t *dcol = nullptr) {
+                          sc_graph **out, const int32_t *dcol = nullptr,
+                          const double *dval = nullptr) {
     SC_REQUIRE(out, SC_E_INVALID, "out is null");
     *out = nullptr;
     const bool prof = getenv("SC_GRAPH_PROFILE") != nullptr;
@@ -1058,8 +1059,8 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->col_offset = col_offset;
     g->global_row0 = global_row0;
     cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
-    bool unit = (val == nullptr);
-    if (!unit) {
+    bool unit = (val == nullptr && dval == nullptr);
+    if (val) {
         unit = true;
         for (int64_t j = 0; j < nnz && unit; ++j) unit = (val[j] == 1.0);
         if (cflags & SC_CREATE_KEEP_WEIGHTS) unit = false;
@@ -1102,9 +1103,10 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     auto free_tmp = [&]() {
         for (void *p_ : {(void *)t_rp, (void *)t_sizes, (void *)t_stats, (void *)t_wlen,
                          (void *)t_flag, (void *)t_keys, (void *)t_keys2, (void *)t_iota,
-                         (void *)t_val, (void *)t_deg, t_cub})
+                         (void *)t_deg, t_cub})
             if (p_) cudaFreeAsync(p_, s);
         if (t_col && !dcol) cudaFreeAsync(t_col, s);
+        if (t_val && !dval) cudaFreeAsync(t_val, s);
     };
     auto need_cub = [&](size_t bytes) -> cudaError_t {
         if (bytes <= cub_cap) return cudaSuccess;
@@ -1122,7 +1124,8 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     cudaError_t e = cudaSuccess;
     if (dcol) t_col = const_cast<int32_t *>(dcol);
     else e = cudaMallocAsync((void **)&t_col, (size_t)std::max<int64_t>(nnz, 1) * 4, s);
-    if (!e && !unit) e = cudaMallocAsync((void **)&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8, s);
+    if (dval) t_val = const_cast<double *>(dval);
+    else if (!e && !unit) e = cudaMallocAsync((void **)&t_val, (size_t)std::max<int64_t>(nnz, 1) * 8, s);
     if (!e) e = cudaMallocAsync((void **)&t_rp, (size_t)(n + 1) * 8, s);
     if (!e) e = cudaMallocAsync((void **)&t_deg, (size_t)n * 8, s);
     if (!e) e = cudaMallocAsync((void **)&t_flag, 64, s);
@@ -1133,7 +1136,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if (!e) e = cudaEventRecord(g->ev_fork, s);  // allocations done -> side stream may copy
     if (!e) e = cudaStreamWaitEvent(s2, g->ev_fork, 0);
     if (!e && nnz && !dcol) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s2);
-    if (!e && t_val) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s2);
+    if (!e && t_val && !dval) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s2);
     if (!e) e = cudaMemsetAsync(t_flag, 0, 64, s);
     if (!e && nnz) {
         // flag[0]: any column index out of range (side stream, right after the copy)
@@ -1451,7 +1454,7 @@ static int32_t to_host_original(sc_graph *g, const double *dev, double *host) {
 }
 
 int32_t csr_device_arrays(const sc_csr *h, const int64_t **rp, const int32_t **col,
-                          const double **deg, int32_t *device);  // sc_generate.cu
+                          const double **deg, const double **val, int32_t *device);  // sc_generate.cu
 
 }  // namespace sc
 
@@ -1509,9 +1512,9 @@ int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_grap
     if (st) return st;
     const int64_t *d_rp;
     const int32_t *d_col;
-    const double *d_deg;
+    const double *d_deg, *d_val;
     int32_t device;
-    if ((st = sc::csr_device_arrays(h, &d_rp, &d_col, &d_deg, &device))) return st;
+    if ((st = sc::csr_device_arrays(h, &d_rp, &d_col, &d_deg, &d_val, &device))) return st;
     SC_CUDA(cudaSetDevice(device));
     // the renumbering is computed on the host from the row offsets (n + 1 words); the
     // column array stays on the device
@@ -1520,7 +1523,7 @@ int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_grap
     SC_CUDA(cudaMemcpy(rp.data(), d_rp, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost));
     SC_CUDA(cudaMemcpy(deg.data(), d_deg, (size_t)n * 8, cudaMemcpyDeviceToHost));
     return graph_init(rp.data(), nullptr, nullptr, deg.data(), n, nnz, n, 0, 0, 1, create_flags,
-                      device, out, d_col);
+                      device, out, d_col, d_val);
 }
 
 int64_t sc_release_cached_memory(int32_t device) {

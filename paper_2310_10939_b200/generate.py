@@ -260,6 +260,35 @@ def sample_weighted_rgg(n: int, k: int, seed: int, *, sigma: float = 0.05, knn: 
 # host cannot build (config 5: n = 1e8, ~1.8e9 stored entries)
 
 
+TAG_DEVICE_KNN = 10
+TAG_DEVICE_DCSBM = 11
+
+
+def device_key(seed: int, tag: int) -> tuple[int, int]:
+    """Philox key SeedSequence([seed, tag]) of a device generator."""
+    if seed < 0:
+        raise InputError(f"seed must be a nonnegative integer, got {seed}")
+    k = np.random.SeedSequence([seed, tag]).generate_state(2, np.uint64)
+    return int(k[0]), int(k[1])
+
+
+def dcsbm_block_offsets(n: int, k: int, seed: int, alpha: float = 2.0) -> np.ndarray:
+    """Block offsets of the device DC-SBM: Dirichlet(alpha) sizes (host numpy, stream
+    rng_for(seed, 11)), rounded, the last block taking the remainder."""
+    rng = rng_for(seed, TAG_DEVICE_DCSBM)
+    sizes = np.maximum(1, np.round(rng.dirichlet(np.full(k, alpha)) * n).astype(np.int64))
+    sizes[-1] += n - sizes.sum()
+    if sizes[-1] < 1:
+        raise InputError("dirichlet block sizes degenerate; choose another seed")
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
+def dcsbm_power_law(gamma: float = 2.5, dmin: int = 5, dmax: int = 5000):
+    """(dmin^a, dmax^a, 1/a), a = 1 - gamma: the inverse-CDF constants of the degree law."""
+    a = 1.0 - gamma
+    return float(dmin) ** a, float(dmax) ** a, 1.0 / a
+
+
 def device_sbm_key(seed: int) -> tuple[int, int]:
     """Philox key of the device generator: SeedSequence([seed, 9]) (tag 9 unused by the
     reference, spectral.py:26-29)."""
@@ -281,22 +310,66 @@ def inv_log1m(prob: float) -> float:
 
 
 class DeviceCSR:
-    """A CSR generated and kept on one GPU (``sc_csr`` handle)."""
+    """A CSR generated and kept on one GPU (``sc_csr`` handle): the SBM law (configs 1, 2, 5;
+    ``DeviceCSR(params)``), the degree-corrected SBM of config 3 (``DeviceCSR.dcsbm``) or the
+    weighted 3-D kNN cluster graph of config 4 (``DeviceCSR.knn3d``)."""
 
-    def __init__(self, params: SbmParams, device: int = 0):
+    def __init__(self, params: SbmParams | None, device: int = 0, *, _handle=None,
+                 weighted: bool = False, planted_of=None):
         import ctypes
 
         from . import _lib
 
         L = _lib.require_device()
-        k0, k1 = device_sbm_key(params.seed)
-        h = ctypes.c_void_p()
-        _lib.check(L.sc_generate_sbm(params.n, params.k, params.p, params.q, inv_log1m(params.p),
-                                     inv_log1m(params.q), k0, k1, device, ctypes.byref(h)))
+        if _handle is None:
+            k0, k1 = device_sbm_key(params.seed)
+            h = ctypes.c_void_p()
+            _lib.check(L.sc_generate_sbm(params.n, params.k, params.p, params.q,
+                                         inv_log1m(params.p), inv_log1m(params.q), k0, k1, device,
+                                         ctypes.byref(h)))
+            planted_of = lambda orig: (orig // params.block_size).astype(np.int64)  # noqa: E731
+        else:
+            h = _handle
         self._h, self.params, self.device = h, params, device
+        self.weighted = weighted
+        self._planted_of = planted_of
         n, nnz, ng = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _lib.check(L.sc_csr_info(h, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(ng)))
         self.n, self.nnz, self.n_generated = n.value, nnz.value, ng.value
+
+    @classmethod
+    def knn3d(cls, n: int, k: int, seed: int, *, sigma: float = 0.05, knn: int = 16,
+              scale: float = 0.01, device: int = 0) -> "DeviceCSR":
+        """Config 4's law on the device (sc_generate_knn3d; oracle.device_knn3d restates it)."""
+        import ctypes
+
+        from . import _lib
+
+        L = _lib.require_device()
+        k0, k1 = device_key(seed, TAG_DEVICE_KNN)
+        h = ctypes.c_void_p()
+        _lib.check(L.sc_generate_knn3d(n, k, float(sigma), knn, float(scale), k0, k1, device,
+                                       ctypes.byref(h)))
+        return cls(None, device, _handle=h, weighted=True)
+
+    @classmethod
+    def dcsbm(cls, n: int, k: int, seed: int, *, alpha: float = 2.0, gamma: float = 2.5,
+              dmin: int = 5, dmax: int = 5000, mix: float = 0.1, wlo: float = 0.5,
+              whi: float = 1.5, device: int = 0) -> "DeviceCSR":
+        """Config 3's law on the device (sc_generate_dcsbm; oracle.device_dcsbm restates it)."""
+        import ctypes
+
+        from . import _lib
+
+        L = _lib.require_device()
+        offs = dcsbm_block_offsets(n, k, seed, alpha)
+        A, B, inv_a = dcsbm_power_law(gamma, dmin, dmax)
+        k0, k1 = device_key(seed, TAG_DEVICE_DCSBM)
+        h = ctypes.c_void_p()
+        _lib.check(L.sc_generate_dcsbm(n, _lib.ptr(offs), k, A, B, inv_a, dmin, dmax, float(mix),
+                                       float(wlo), float(whi), k0, k1, device, ctypes.byref(h)))
+        planted_of = lambda orig: (np.searchsorted(offs, orig, side="right") - 1).astype(np.int64)  # noqa: E731
+        return cls(None, device, _handle=h, weighted=True, planted_of=planted_of)
 
     @property
     def handle(self):
@@ -321,8 +394,12 @@ class DeviceCSR:
         deg, orig = empty(self.n, np.float64), np.empty(self.n, dtype=np.int32)
         _lib.check(_lib.load().sc_csr_download(self.handle, _lib.ptr(rp), _lib.ptr(col),
                                                _lib.ptr(deg), _lib.ptr(orig)))
-        g = Graph(n=self.n, row_offsets=rp, col_indices=col, weights=None, degrees=deg)
-        planted = (orig // self.params.block_size).astype(np.int64)
+        val = None
+        if self.weighted:
+            val = empty(self.nnz, np.float64)
+            _lib.check(_lib.load().sc_csr_download_weights(self.handle, _lib.ptr(val)))
+        g = Graph(n=self.n, row_offsets=rp, col_indices=col, weights=val, degrees=deg)
+        planted = self._planted_of(orig) if self._planted_of else None
         kept = np.zeros(self.n_generated, dtype=bool)
         kept[orig] = True
         return SbmSample(graph=g, planted=planted, dropped=list(np.flatnonzero(~kept)),
@@ -346,6 +423,17 @@ class DeviceCSR:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def config_device_csr(cfg: int, seed: int = 0, device: int = 0) -> DeviceCSR:
+    """BASELINE.json configs 3, 4 and 5 generated on the device."""
+    if cfg == 3:
+        return DeviceCSR.dcsbm(4_000_000, 50, seed, device=device)
+    if cfg == 4:
+        return DeviceCSR.knn3d(10_000_000, 100, seed, device=device)
+    if cfg == 5:
+        return DeviceCSR(config_sbm(5, seed), device)
+    raise InputError(f"config {cfg} has no device generator (configs 1 and 2 use sample_sbm)")
 
 
 def sample_sbm_device(params: SbmParams, device: int = 0, pinned: bool = False) -> SbmSample:

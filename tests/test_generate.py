@@ -94,3 +94,34 @@ def test_device_sbm_law_restatement_statistics():
     assert abs(e_out - q * t_out) < 5 * np.sqrt(q * t_out)
     assert np.array_equal(np.sort(row * n + col), np.sort(col.astype(np.int64) * n + row))
     assert np.array_equal(deg, np.diff(rp))
+
+
+def test_restated_weighted_generator_laws_are_symmetric_graphs():
+    """oracle.device_knn3d / device_dcsbm (the laws of sc_generate_wt.cu): symmetric, sorted
+    rows without self loops, every kNN row holds at least 16 neighbours, degrees are the
+    rows' left-to-right weight sums, and sc_exp tracks exp to a few ulps."""
+    import functools
+    import operator
+
+    from oracle import oracle as O
+    from paper_2310_10939_b200.generate import dcsbm_block_offsets, dcsbm_power_law
+
+    y = np.linspace(-50.0, 8.0, 2001)
+    assert np.max(np.abs(O.np_sc_exp(y) / np.exp(y) - 1.0)) < 4e-16
+    rp, col, val, deg, orig, pts, lab = O.device_knn3d(400, 4, 0.05, 16, 0.01, 1)
+    offs = dcsbm_block_offsets(500, 5, 3)
+    A, B, inv_a = dcsbm_power_law()
+    graphs = [(rp, col, val, deg), O.device_dcsbm(500, offs, A, B, inv_a, 5, 5000, 0.1, 0.5, 1.5, 3)[:4]]
+    assert np.all(np.diff(rp) >= 16)
+    for rp_, col_, val_, deg_ in graphs:
+        n = rp_.size - 1
+        row = np.repeat(np.arange(n), np.diff(rp_))
+        assert np.all(col_ != row)
+        assert np.all((np.diff(col_) > 0) | (np.diff(row) != 0))
+        key, tkey = row * n + col_, col_.astype(np.int64) * n + row
+        o1, o2 = np.argsort(key), np.argsort(tkey)
+        assert np.array_equal(key[o1], tkey[o2]) and np.array_equal(val_[o1], val_[o2])
+        # (functools.reduce: Python's sum() compensates float rounding since 3.12)
+        ref = np.array([functools.reduce(operator.add, val_[rp_[i]:rp_[i + 1]].tolist(), 0.0)
+                        for i in range(n)])
+        assert np.array_equal(deg_, ref)

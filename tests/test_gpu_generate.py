@@ -59,3 +59,50 @@ def test_config5_law_at_scale():
     key = row * g.n + col
     tkey = col * g.n + row
     assert np.array_equal(np.sort(key), np.sort(tkey))
+
+
+# ---- weighted device generators (sc_generate_wt.cu): configs 3 and 4
+
+
+@pytest.mark.parametrize("n,k,sigma,seed", [(3000, 7, 0.05, 3),   # clustered
+                                             (1500, 1, 0.3, 4),    # one diffuse cluster
+                                             (600, 5, 0.0, 5)])    # exact duplicates: d2 ties
+def test_device_knn3d_matches_restated_law(n, k, sigma, seed):
+    with DeviceCSR.knn3d(n, k, seed, sigma=sigma) as d:
+        s = d.download()
+    rp, col, val, deg, orig, _, _ = O.device_knn3d(n, k, sigma, 16, 0.01, seed)
+    g = s.graph
+    assert np.array_equal(g.row_offsets, rp)
+    assert np.array_equal(g.col_indices, col)
+    assert np.array_equal(g.weights, val)
+    assert np.array_equal(g.degrees, deg)
+
+
+@pytest.mark.parametrize("n,k,seed", [(3000, 6, 2), (2500, 1, 7), (4000, 40, 9)])
+def test_device_dcsbm_matches_restated_law(n, k, seed):
+    from paper_2310_10939_b200.generate import dcsbm_block_offsets, dcsbm_power_law
+
+    with DeviceCSR.dcsbm(n, k, seed) as d:
+        s = d.download()
+    offs = dcsbm_block_offsets(n, k, seed)
+    A, B, inv_a = dcsbm_power_law()
+    rp, col, val, deg, orig = O.device_dcsbm(n, offs, A, B, inv_a, 5, 5000, 0.1, 0.5, 1.5, seed)
+    g = s.graph
+    assert np.array_equal(g.row_offsets, rp)
+    assert np.array_equal(g.col_indices, col)
+    assert np.array_equal(g.weights, val)
+    assert np.array_equal(g.degrees, deg)
+    assert np.array_equal(s.planted, np.searchsorted(offs, orig, side="right") - 1)
+    assert len(s.dropped) == n - orig.size
+
+
+def test_weighted_device_csr_graph_equals_host_upload():
+    """sc_graph_create_from_csr with device weights == the same graph uploaded from the host."""
+    with DeviceCSR.dcsbm(300_000, 12, 1) as d:
+        host = d.download()
+        with DeviceGraph.from_device_csr(d) as dg1, DeviceGraph(host.graph) as dg2:
+            dg1.sample_irwin_hall(2)
+            dg2.sample_irwin_hall(2)
+            a, fa = dg1.power_iterate(30)
+            b, fb = dg2.power_iterate(30)
+    assert np.array_equal(a, b) and np.array_equal(fa, fb)
