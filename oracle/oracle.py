@@ -176,20 +176,37 @@ def kmeanspp_indices(x: np.ndarray, k: int, rng: np.random.Generator) -> np.ndar
 
 
 def lloyd(x: np.ndarray, k: int, seed: int, max_iters: int = 100, tol: float = 1e-6,
-          restarts: int = 10) -> tuple[np.ndarray, float]:
-    """lloyd (kmeans.py:167-215) on 1-D points; returns (labels int64, best cost)."""
+          restarts: int = 10, threads: int = 0) -> tuple[np.ndarray, float]:
+    """lloyd (kmeans.py:167-215) on 1-D points; returns (labels int64, best cost).  Restarts
+    are independent (rng_for(seed, r) each) and run on `threads` host threads (0 = all cores;
+    the C calls release the GIL); the best is picked in restart order exactly as the loop does."""
+    import concurrent.futures as cf
+    import os
+
     x = np.ascontiguousarray(x, dtype=np.float64).ravel()
     n = x.size
-    best_labels, best_cost = None, np.inf
-    labels = np.empty(n, dtype=np.int64)
-    for r in range(restarts):
+
+    def one(r):
         rng = rng_for(seed, r)
         centers = x[kmeanspp_indices(x, k, rng)].copy()
         cost = ctypes.c_double()
-        lib().orc_lloyd_restart(n, _p(x), k, _p(centers), max_iters, tol, _p(labels),
-                                ctypes.byref(cost))
-        if cost.value < best_cost:
-            best_cost, best_labels = cost.value, labels.copy()
+        labels = np.empty(n, dtype=np.int64)
+        it = lib().orc_lloyd_restart(n, _p(x), k, _p(centers), max_iters, tol, _p(labels),
+                                     ctypes.byref(cost))
+        return labels, cost.value, it
+
+    nt = min(restarts, threads or os.cpu_count() or 1)
+    if nt <= 1:
+        results = [one(r) for r in range(restarts)]
+    else:
+        with cf.ThreadPoolExecutor(nt) as ex:
+            results = list(ex.map(one, range(restarts)))
+    best_labels, best_cost = None, np.inf
+    for r, (labels, cost, it) in enumerate(results):
+        if it < 0:  # the reference's `assert cost <= prev_cost*(1+1e-12)+1e-12` (kmeans.py:206)
+            raise AssertionError(f"k-means cost increased (restart {r}, iteration {-it - 1})")
+        if cost < best_cost:
+            best_cost, best_labels = cost, labels
     return best_labels, best_cost
 
 
@@ -281,6 +298,7 @@ def np_lloyd(x: np.ndarray, k: int, seed: int, max_iters=100, tol=1e-6, restarts
             centers[cnt > 0] = sums[cnt > 0, 0] / cnt[cnt > 0]
             diff = (x - centers[labels])[:, None]
             cost = float(np.einsum("ij,ij->", diff, diff))
+            assert cost <= prev * (1 + 1e-12) + 1e-12, "k-means cost increased"  # kmeans.py:206
             stop = same or (np.isfinite(prev) and prev - cost <= tol * max(prev, 1e-300))
             prev = cost
             if stop:

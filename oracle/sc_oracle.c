@@ -315,11 +315,16 @@ int32_t orc_lloyd_restart(int64_t n, const double *x, int32_t k, const double *c
         for (int32_t c = 0; c < k; ++c) cen[c] = cnt[c] > 0 ? sums[c] / (double)cnt[c] : sums[c];
         for (int64_t j = 0; j < n; ++j) diff[j] = x[j] - cen[lab[j]];
         double cost = orc_einsum_sumsq(n, diff);
+        if (!(cost <= prev * (1.0 + 1e-12) + 1e-12)) { /* kmeans.py:206 assert */
+            it = -it;
+            prev = cost;
+            break;
+        }
         int small_gain = isfinite(prev) && (prev - cost <= tol * (prev > 1e-300 ? prev : 1e-300));
         prev = cost;
         if (unchanged || small_gain) break;
     }
     *cost_out = prev;
     free(cen); free(sums); free(cnt); free(lab); free(own); free(diff); free(empties);
-    return it;
+    return it; /* iterations run; negative: the cost assertion failed at iteration -it */
 }

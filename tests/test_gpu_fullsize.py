@@ -1,0 +1,74 @@
+"""Configs 3, 4 and 5 of BASELINE.json at FULL size: the device path's
+Irwin-Hall x0, x_T after T steps and f = x_T / d are bit-identical to the C oracle's
+restatement of the reference's power_method (oracle/sc_oracle.c, run on all host cores), and
+the exact k-means replica's labels equal the oracle's Lloyd (kmeans.py:167-215) where the
+oracle can finish in test time:
+  config 3 (DC-SBM, n = 4e6, ~56M entries, T = 200, k = 50): after T = 200 steps f is a
+      nearly constant band whose spread is of the order of d2ref's rounding, so Lloyd's cost
+      goes UP at an iteration and the reference's `assert cost <= prev_cost*(1+1e-12)+1e-12`
+      (kmeans.py:206) fires: the device replica must raise as well (SC_E_INTERNAL), and does
+      for both the first restart alone and the batched 10;
+  config 4 (16-NN RGG, n = 1e7, ~181M entries, T = 300, k = 100): labels after 3 Lloyd
+      iterations of 1 restart (a full oracle run is ~40 min of host time);
+  config 5 (SBM, n = 1e8, 1.8e9 entries, T = 100): x_T and f only -- the oracle's k = 1000
+      Lloyd over 1e8 points does not finish on a host in test time.
+The graphs come from the device generators (pinned by tests/test_gpu_generate.py against
+their numpy restatements) and are downloaded to the host for the oracle."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2310_10939_b200 import DeviceGraph, KMeans1D
+from paper_2310_10939_b200.generate import CONFIG_T, config_device_csr
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 8
+
+
+def _full_size_power(cfg, seed=0):
+    T = CONFIG_T[cfg]
+    with config_device_csr(cfg, seed) as d:
+        g = d.download(pinned=True).graph
+        with DeviceGraph.from_device_csr(d) as dg:
+            x0d = dg.sample_irwin_hall(seed, return_host=True)
+            xT, f = dg.power_iterate(T)
+    x0 = O.irwin_hall(g.degrees, seed, threads=THREADS)
+    assert np.array_equal(x0d, x0), "Irwin-Hall x0 differs from the oracle"
+    xo, fo = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, T,
+                             threads=THREADS)
+    assert np.array_equal(xT, xo), "x_T differs from the oracle"
+    assert np.array_equal(f, fo), "f differs from the oracle"
+    # mass conservation of the lazy random walk (1^T M_rw = 1^T), to rounding
+    assert abs(xT.sum() - x0.sum()) <= 1e-9 * x0.sum()
+    return g, f
+
+
+def test_config3_full_size_bit_exact():
+    from paper_2310_10939_b200.errors import SpeclusterError
+
+    g, f = _full_size_power(3)
+    assert g.n == 4_000_000 and g.nnz > 50_000_000 and g.weights is not None
+    with pytest.raises(AssertionError, match="cost increased"):
+        O.lloyd(f, 50, O.kmeans_seed(0), restarts=1)
+    for restarts in (1, 10):
+        with KMeans1D(f) as km, pytest.raises(SpeclusterError, match="cost increased"):
+            km.lloyd(50, O.kmeans_seed(0), restarts=restarts)
+
+
+def test_config4_full_size_bit_exact():
+    g, f = _full_size_power(4)
+    assert g.n == 10_000_000 and g.nnz > 150_000_000
+    with KMeans1D(f) as km:
+        part = km.lloyd(100, O.kmeans_seed(0), restarts=1, max_iters=3)
+    lab, cost = O.lloyd(f, 100, O.kmeans_seed(0), restarts=1, max_iters=3)
+    assert np.array_equal(part.labels, lab)
+    assert km.last["costs"].min() == cost
+
+
+def test_config5_full_size_bit_exact():
+    g, f = _full_size_power(5)
+    assert g.n > 99_000_000 and g.nnz > 1_700_000_000
