@@ -73,6 +73,9 @@ typedef struct sc_graph_info {
     int64_t stored_entries; /* SELL-32 entries incl. padding (+ wide-row entries excluded) */
     int64_t panel_groups;   /* column-panel layout: stages (0 = no panel layout) */
     int64_t panel_bytes;    /* column-panel layout: bytes streamed per step */
+    int64_t zstride;        /* doubles between the handle's two z buffers (sc_shard_buffers) */
+    int32_t n_gpus;         /* shards of a multi-GPU handle (sc_graph_create_multi), else 1 */
+    int32_t reserved;
 } sc_graph_info;
 
 typedef struct sc_timing {
@@ -118,6 +121,23 @@ int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double
                         const double *deg, int64_t n, int64_t nnz, int64_t ncols,
                         int64_t col_offset, int64_t global_row0, int32_t device,
                         sc_graph **out);
+/* Multi-GPU handle in ONE process (SURVEY.md §8(b)'s n_gpus; replaces the single-GPU graph
+ * behind fast_spectral_cluster, ref: pipeline.py:127 -- the call stays one call).  Rows are
+ * cut into n_gpus blocks balanced by stored entries, one shard per entry of `devices`
+ * (nullable = 0..n_gpus-1; a device may repeat: several shards share it).  Every device holds
+ * the whole gathered vector; each step's epilogue stores its z values into all peers' copies
+ * over peer memory (NVLink P2P) and the shards' streams are ordered by events.  The handle
+ * works with sc_sample_irwin_hall, sc_set_x0, sc_power_iterate, sc_graph_download_f,
+ * sc_graph_info_get and sc_kmeans_create_from_graph (f gathered to the first device); x_T
+ * and f are bit-identical to the single-GPU handle's.  create_flags: SC_CREATE_PANELS,
+ * SC_CREATE_KEEP_WEIGHTS, SC_CREATE_FP32_VALUES (no BFS pre-order). */
+int32_t sc_graph_create_multi(const int64_t *row_ptr, const int32_t *col, const double *val,
+                              const double *deg, int64_t n, int64_t nnz, int32_t n_gpus,
+                              const int32_t *devices, uint32_t create_flags, sc_graph **out);
+/* where shard `shard` of a multi-GPU handle lives: its global rows [row0, row0 + rows), its
+ * z-space block [zoff, zoff + rows) and its device (all outputs nullable) */
+int32_t sc_graph_shard_layout(const sc_graph *g, int32_t shard, int64_t *row0, int64_t *rows,
+                              int64_t *zoff, int32_t *device);
 void sc_graph_destroy(sc_graph *g);
 /* Destroyed handles return their device buffers to a process-wide cache (reused by the next
  * handle; capped by SC_BUFFER_CACHE_MB, default 16384).  This frees the cached buffers of
@@ -180,7 +200,8 @@ int32_t sc_shard_scale_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const 
 int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t flags,
                        void *stream);
 /* ---- fused z exchange over peer memory (NVLink P2P), instead of an all-gather ------- */
-/* sc_shard_buffers: the handle's own z allocation (2*ncols doubles: z0 then z1, zeroed) and
+/* sc_shard_buffers: the handle's own z allocation (z0 then z1 = z0 + zstride, zeroed; zstride
+ * from sc_graph_info, >= ncols + 1 so z[ncols] stays a zero slot) and
  * its 64-word flag array.  Ranks export both with sc_ipc_export, import the peers' with
  * sc_ipc_import, and hand all world bases to sc_shard_set_peers (entries for `rank` ignored).
  * From then on every z value a step / scale writes into the handle's z allocation is also
@@ -270,6 +291,14 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t restarts, const int32_t *
 int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t restarts, const int64_t *chosen,
                         int32_t max_iters, double tol, int64_t *labels_out, double *costs_out,
                         int32_t *iters_out, int32_t *best_restart_out, double *ms_out);
+
+/* Context options.  SC_KM_NO_COST_ASSERT: do not raise SC_E_INTERNAL when a restart's cost
+ * goes up between iterations -- the reference's check is a Python `assert`
+ * (kmeans.py:206) that `python -O` skips; with it skipped the increase simply stops that
+ * restart (kmeans.py:207: prev - cost <= tol * prev holds for a negative gain).  The host
+ * mirror sets the flag when Python runs without __debug__. */
+#define SC_KM_NO_COST_ASSERT 0x1u
+int32_t sc_kmeans_set_flags(sc_kmeans *km, uint32_t flags);
 
 /* Fast mode (north star step 3): the same seeds, then Lloyd on the sorted values -- every
  * cluster is an interval of the sorted points, so an iteration is k binary searches plus

@@ -176,10 +176,13 @@ def kmeanspp_indices(x: np.ndarray, k: int, rng: np.random.Generator) -> np.ndar
 
 
 def lloyd(x: np.ndarray, k: int, seed: int, max_iters: int = 100, tol: float = 1e-6,
-          restarts: int = 10, threads: int = 0) -> tuple[np.ndarray, float]:
+          restarts: int = 10, threads: int = 0,
+          assert_cost: bool = True) -> tuple[np.ndarray, float]:
     """lloyd (kmeans.py:167-215) on 1-D points; returns (labels int64, best cost).  Restarts
     are independent (rng_for(seed, r) each) and run on `threads` host threads (0 = all cores;
-    the C calls release the GIL); the best is picked in restart order exactly as the loop does."""
+    the C calls release the GIL); the best is picked in restart order exactly as the loop does.
+    assert_cost=False is the reference under `python -O` (kmeans.py:206's assert skipped: a
+    cost increase ends the restart through the small-gain test, with that cost and labels)."""
     import concurrent.futures as cf
     import os
 
@@ -203,7 +206,7 @@ def lloyd(x: np.ndarray, k: int, seed: int, max_iters: int = 100, tol: float = 1
             results = list(ex.map(one, range(restarts)))
     best_labels, best_cost = None, np.inf
     for r, (labels, cost, it) in enumerate(results):
-        if it < 0:  # the reference's `assert cost <= prev_cost*(1+1e-12)+1e-12` (kmeans.py:206)
+        if it < 0 and assert_cost:  # `assert cost <= prev_cost*(1+1e-12)+1e-12` (kmeans.py:206)
             raise AssertionError(f"k-means cost increased (restart {r}, iteration {-it - 1})")
         if cost < best_cost:
             best_cost, best_labels = cost, labels

@@ -37,6 +37,7 @@ class GraphInfo(ctypes.Structure):
         ("device", ctypes.c_int32), ("sm_count", ctypes.c_int32),
         ("stored_entries", ctypes.c_int64),
         ("panel_groups", ctypes.c_int64), ("panel_bytes", ctypes.c_int64),
+        ("zstride", ctypes.c_int64), ("n_gpus", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 
@@ -57,7 +58,8 @@ EXPORTS = (
     "sc_shard_set_peers", "sc_shard_barrier", "sc_ipc_export", "sc_ipc_import", "sc_ipc_release",
     "sc_keyed_sums", "sc_contingency", "sc_cut_sums", "sc_power_iterate_block",
     "sc_kmeans_create_nd", "sc_kmeans_lloyd_sorted", "sc_release_cached_memory",
-    "sc_gather_f64", "sc_graph_build_panels", "sc_graph_download_f",
+    "sc_gather_f64", "sc_graph_build_panels", "sc_graph_download_f", "sc_kmeans_set_flags",
+    "sc_graph_create_multi", "sc_graph_shard_layout",
 )
 
 _lib = None
@@ -100,6 +102,9 @@ def load() -> ctypes.CDLL:
         "sc_kmeans_destroy": ([P], None),
         "sc_kmeans_pp": ([P, i32, i32, P, P, P, P], i32),
         "sc_kmeans_lloyd": ([P, i32, i32, P, i32, f64, P, P, P, P, P], i32),
+        "sc_kmeans_set_flags": ([P, u32], i32),
+        "sc_graph_create_multi": ([P, P, P, P, i64, i64, i32, P, u32, PP], i32),
+        "sc_graph_shard_layout": ([P, i32, P, P, P, P], i32),
         "sc_seqsum": ([P, i32, P, i32, P, P], i32),
         "sc_sell_order": ([P, i64, P], i32),
         "sc_graph_create_ex": ([P, P, P, P, i64, i64, i32, u32, PP], i32),

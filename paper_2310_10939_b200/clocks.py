@@ -45,14 +45,16 @@ class ClockSampler:
             N.nvmlInit()
             if self.bus_id is None:
                 raise RuntimeError("no PCI bus id for the CUDA device")
-            h = N.nvmlDeviceGetHandleByPciBusId_v2(self.bus_id.encode())
+            get = getattr(N, "nvmlDeviceGetHandleByPciBusId_v2", None) or N.nvmlDeviceGetHandleByPciBusId
+            h = get(self.bus_id.encode())
             self._nvml = (N, h, N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM),
                           (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
                            N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap))
             self.source = "nvml"
-        except Exception:
+        except Exception as e:  # noqa: BLE001 -- any NVML failure falls back to nvidia-smi
             self._nvml = None
             self.source = "nvidia-smi"
+            self.nvml_error = f"{type(e).__name__}: {e}"
 
     def _sample(self):
         try:
@@ -104,4 +106,6 @@ class ClockSampler:
                           if len(r) > 4 + i and r[4 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows), "source": getattr(self, "source", None)}
+                "samples": len(self.rows), "source": getattr(self, "source", None),
+                **({"nvml_error": self.nvml_error} if getattr(self, "nvml_error", None) else {}),
+                "bus_id": self.bus_id}

@@ -705,6 +705,10 @@ namespace sc {
 struct PanGroup;
 }
 
+namespace sc {
+struct Multi;  // sc_multi.cuh: one handle over several GPUs
+}
+
 struct sc_graph {
     int device = 0;
     int sm_count = 0;
@@ -752,8 +756,26 @@ struct sc_graph {
     int32_t *d_pan_blk = nullptr;
     sc::PanGroup *d_pan_grp = nullptr;
     uint8_t *d_pan_stream = nullptr;
-    int64_t zstride = 0;  // d_z[1] - d_z[0] (ncols, rounded up to 32 for whole graphs)
+    int64_t zstride = 0;  // d_z[1] - d_z[0] (ncols + a zero slot, rounded up to 32)
+    // peers synchronised by stream events (sc_multi.cuh) instead of sc_shard_barrier: the
+    // panel kernel may then mirror z into peers too (it has no system fence of its own)
+    bool peer_events = false;
+    sc::Multi *multi = nullptr;  // multi-GPU handle: the shards live there, this one is a shell
 };
+
+namespace sc {  // sc_multi.cuh (included at the end of this file)
+static void multi_free(sc_graph *mg);
+static int32_t multi_sample(sc_graph *mg, uint64_t key0, uint64_t key1, double *x0_out);
+static int32_t multi_set_x0(sc_graph *mg, const double *x0);
+static int32_t multi_power(sc_graph *mg, int32_t T, double sign, uint32_t flags, double *xT_out,
+                           double *f_out, sc_timing *t_out);
+static int32_t multi_download_f(sc_graph *mg, double *f_out);
+static const double *multi_f_device(sc_graph *mg);
+static int32_t multi_info(const sc_graph *mg, sc_graph_info *o);
+}  // namespace sc
+// whole-handle entry points that a multi-GPU shell forwards; shard-level ones refuse it
+#define SC_NOT_MULTI(g) \
+    SC_REQUIRE(!(g)->multi, SC_E_STATE, "not available on a multi-GPU handle")
 
 namespace sc {
 
@@ -1205,10 +1227,10 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     }
     // both z buffers in one allocation so one L2 access-policy window covers them
     double *zz = nullptr;
-    // whole graphs: z[1] 256-byte aligned (bulk copies of panels need 16-byte alignment), a
-    // zero slot z[ncols] in both buffers (padding target of the panel layout), and 64 bytes of
-    // slack after z[1] (the last panel copy is rounded up to 16 bytes)
-    g->zstride = rename ? (ncols + 32) & ~(int64_t)31 : ncols;
+    // z[1] 256-byte aligned (bulk copies of panels need 16-byte alignment), a zero slot
+    // z[ncols] in both buffers (padding target of the panel layout; never written, also not
+    // by peers), and 64 bytes of slack after z[1] (the last panel copy is rounded up to 16)
+    g->zstride = (ncols + 32) & ~(int64_t)31;
     if ((st = dmalloc(g, (void **)&zz, (size_t)g->zstride * 16 + 64))) {
         cudaStreamSynchronize(s2);
         free_tmp();
@@ -1324,7 +1346,7 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     if (row_hi < 0) row_hi = g->n;
     // whole-graph steps use the column-panel layout when the handle has one
     const bool panel = g->pan_ctas && !(flags & SC_FORCE_SELL) && row_lo == 0 && row_hi == g->n &&
-                       g->npeer == 0;
+                       (g->npeer == 0 || g->peer_events);
     StepArgs a;
     a.slice_lo = std::min(row_lo, g->n_sell) / kSlice;
     a.slice_hi = (std::min(row_hi, g->n_sell) + kSlice - 1) / kSlice;
@@ -1354,7 +1376,7 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.peer_off = 0;
     if (g->npeer) {
         // the exchange mirrors the handle's own z allocation only
-        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + 2 * g->ncols, SC_E_STATE,
+        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + g->zstride + g->ncols, SC_E_STATE,
                    "peer exchange needs z_out inside the handle's z buffers (sc_shard_buffers)");
         a.npeer = g->npeer;
         a.peer_off = z_out - g->d_z[0];
@@ -1541,6 +1563,11 @@ int32_t sc_sell_order(const int64_t *row_ptr, int64_t n, int32_t *perm_out) {
 
 void sc_graph_destroy(sc_graph *g) {
     if (!g) return;
+    if (g->multi) {
+        sc::multi_free(g);
+        delete g;
+        return;
+    }
     cudaSetDevice(g->device);
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->side) cudaStreamSynchronize(g->side);
@@ -1568,6 +1595,7 @@ void sc_graph_destroy(sc_graph *g) {
 
 int32_t sc_graph_download_f(sc_graph *g, double *f_out) {
     SC_REQUIRE(g && f_out, SC_E_INVALID, "null argument");
+    if (g->multi) return sc::multi_download_f(g, f_out);
     SC_REQUIRE(g->result >= 0, SC_E_STATE, "no power iteration has run on this handle");
     SC_CUDA(cudaSetDevice(g->device));
     return sc::to_host_original(g, g->d_z[g->result], f_out);
@@ -1575,6 +1603,7 @@ int32_t sc_graph_download_f(sc_graph *g, double *f_out) {
 
 int32_t sc_graph_build_panels(sc_graph *g) {
     SC_REQUIRE(g, SC_E_INVALID, "null graph");
+    SC_NOT_MULTI(g);  // (multi-GPU handles take SC_CREATE_PANELS at creation)
     if (g->pan_ctas) return SC_OK;
     SC_CUDA(cudaSetDevice(g->device));
     return sc::build_panels(g, getenv("SC_GRAPH_PROFILE") != nullptr);
@@ -1582,6 +1611,7 @@ int32_t sc_graph_build_panels(sc_graph *g) {
 
 int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *o) {
     SC_REQUIRE(g && o, SC_E_INVALID, "null argument");
+    if (g->multi) return sc::multi_info(g, o);
     o->n = g->n;
     o->nnz = g->nnz;
     o->ncols = g->ncols;
@@ -1596,11 +1626,14 @@ int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *o) {
     o->panel_groups = g->pan_ctas ? g->pan_groups : 0;
     o->panel_bytes = g->pan_ctas ? g->pan_bytes : 0;
     o->stored_entries = g->sell_entries;
+    o->zstride = g->zstride;
+    o->n_gpus = 1;
     return SC_OK;
 }
 
 int32_t sc_graph_order(const sc_graph *g, int32_t *perm_out) {
     SC_REQUIRE(g && perm_out, SC_E_INVALID, "null argument");
+    SC_NOT_MULTI(g);
     SC_CUDA(cudaSetDevice(g->device));
     SC_CUDA(cudaMemcpy(perm_out, g->d_perm, (size_t)g->n * 4, cudaMemcpyDeviceToHost));
     return SC_OK;
@@ -1608,6 +1641,7 @@ int32_t sc_graph_order(const sc_graph *g, int32_t *perm_out) {
 
 int32_t sc_sample_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x0_out) {
     SC_REQUIRE(g, SC_E_INVALID, "null graph");
+    if (g->multi) return sc::multi_sample(g, key0, key1, x0_out);
     SC_CUDA(cudaSetDevice(g->device));
     k_irwin_hall<<<grid_for(g, g->n, 128), 128, 0, g->stream>>>(g->d_deg, g->d_perm, g->d_x0,
                                                                 g->n, g->global_row0, key0, key1);
@@ -1624,6 +1658,7 @@ int32_t sc_sample_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *
 
 int32_t sc_set_x0(sc_graph *g, const double *x0_host) {
     SC_REQUIRE(g && x0_host, SC_E_INVALID, "null argument");
+    if (g->multi) return sc::multi_set_x0(g, x0_host);
     SC_CUDA(cudaSetDevice(g->device));
     SC_CUDA(cudaMemcpyAsync(g->d_tmp, x0_host, (size_t)g->n * 8, cudaMemcpyHostToDevice,
                             g->stream));
@@ -1641,6 +1676,7 @@ int32_t sc_power_iterate(sc_graph *g, int32_t T, double sign, uint32_t flags, do
     SC_REQUIRE(g, SC_E_INVALID, "null graph");
     SC_REQUIRE(T >= 0, SC_E_INVALID, "power method step count must be >= 0, got %d", T);
     SC_REQUIRE(sign == 1.0 || sign == -1.0, SC_E_INVALID, "sign must be +1 or -1");
+    if (g->multi) return sc::multi_power(g, T, sign, flags, xT_out, f_out, t_out);
     SC_REQUIRE(g->have_x0, SC_E_STATE, "no start vector: call sc_sample_irwin_hall or sc_set_x0");
     SC_REQUIRE(g->ncols == g->n, SC_E_STATE,
                "sc_power_iterate needs a whole graph; shards use sc_shard_step");
@@ -1749,6 +1785,7 @@ int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *
     SC_REQUIRE(T >= 0, SC_E_INVALID, "power method step count must be >= 0, got %d", T);
     SC_REQUIRE(L >= 1 && L <= kMaxBlockCols, SC_E_INVALID, "block width %d outside [1, %d]", L,
                kMaxBlockCols);
+    SC_NOT_MULTI(g);
     SC_REQUIRE(g->ncols == g->n, SC_E_STATE, "block power method needs a whole graph");
     SC_REQUIRE(!g->f32, SC_E_STATE, "block power method needs fp64 weights (no SC_CREATE_FP32_VALUES)");
     SC_CUDA(cudaSetDevice(g->device));
@@ -1821,6 +1858,7 @@ int32_t sc_power_iterate_block(sc_graph *g, int32_t T, int32_t L, const double *
 int32_t sc_shard_step(sc_graph *g, const double *z_in, const double *x_in, double *x_out,
                       double *z_out, double sign, uint32_t flags, void *stream) {
     SC_REQUIRE(g && z_in && x_in && x_out && z_out, SC_E_INVALID, "null argument");
+    SC_NOT_MULTI(g);
     SC_CUDA(cudaSetDevice(g->device));
     cudaStream_t s = (cudaStream_t)stream;  // the caller's stream, 0 = legacy default stream
     int32_t st;
@@ -1833,6 +1871,7 @@ int32_t sc_shard_step_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const d
                             const double *x_in, double *x_out, double *z_out, double sign,
                             uint32_t flags, void *stream) {
     SC_REQUIRE(g && z_in && x_in && x_out && z_out, SC_E_INVALID, "null argument");
+    SC_NOT_MULTI(g);
     SC_REQUIRE(0 <= row_lo && row_lo <= row_hi && row_hi <= g->n, SC_E_RANGE,
                "row range [%lld, %lld) outside [0, %lld)", (long long)row_lo, (long long)row_hi,
                (long long)g->n);
@@ -1860,7 +1899,7 @@ int32_t sc_shard_scale_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const 
         if ((st = ensure_isd(g, s))) return st;
     int64_t poff = 0;
     if (g->npeer) {
-        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + 2 * g->ncols, SC_E_STATE,
+        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + g->zstride + g->ncols, SC_E_STATE,
                    "peer exchange needs z_out inside the handle's z buffers (sc_shard_buffers)");
         poff = z_out - g->d_z[0];
     }
@@ -1874,6 +1913,7 @@ int32_t sc_shard_scale_range(sc_graph *g, int64_t row_lo, int64_t row_hi, const 
 
 int32_t sc_shard_buffers(sc_graph *g, double **z_base, uint32_t **flags) {
     SC_REQUIRE(g && z_base && flags, SC_E_INVALID, "null argument");
+    SC_NOT_MULTI(g);
     SC_CUDA(cudaSetDevice(g->device));
     if (!g->d_flags) {
         int32_t st = dmalloc(g, (void **)&g->d_flags, 64 * 4);
@@ -1888,6 +1928,7 @@ int32_t sc_shard_buffers(sc_graph *g, double **z_base, uint32_t **flags) {
 int32_t sc_shard_set_peers(sc_graph *g, void *const *z_bases, void *const *flag_bases,
                            int32_t world, int32_t rank) {
     SC_REQUIRE(g && z_bases && flag_bases, SC_E_INVALID, "null argument");
+    SC_NOT_MULTI(g);
     SC_REQUIRE(world >= 1 && world <= kMaxWorld && rank >= 0 && rank < world, SC_E_INVALID,
                "bad world/rank (%d/%d; at most %d ranks)", world, rank, kMaxWorld);
     SC_CUDA(cudaSetDevice(g->device));
@@ -1973,7 +2014,7 @@ int32_t sc_shard_scale(sc_graph *g, const double *x, double *z_out, uint32_t fla
         if ((st = ensure_isd(g, s))) return st;
     int64_t poff = 0;
     if (g->npeer) {
-        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + 2 * g->ncols, SC_E_STATE,
+        SC_REQUIRE(z_out >= g->d_z[0] && z_out < g->d_z[0] + g->zstride + g->ncols, SC_E_STATE,
                    "peer exchange needs z_out inside the handle's z buffers (sc_shard_buffers)");
         poff = z_out - g->d_z[0];
     }
@@ -2001,6 +2042,7 @@ int32_t sc_shard_irwin_hall(sc_graph *g, uint64_t key0, uint64_t key1, double *x
 namespace sc {
 // f (= z_T) in ORIGINAL vertex order, materialised on the device on demand
 const double *graph_f_device(sc_graph *g) {
+    if (g->multi) return multi_f_device(g);
     if (g->result < 0) return nullptr;
     if (!g->d_f_orig && dmalloc(g, (void **)&g->d_f_orig, (size_t)g->n * 8)) return nullptr;
     k_gather_perm<<<grid_for(g, g->n, 256), 256, 0, g->stream>>>(g->d_z[g->result], g->d_iperm,
@@ -2011,3 +2053,5 @@ const double *graph_f_device(sc_graph *g) {
 int64_t graph_n(const sc_graph *g) { return g->n; }
 int graph_device(const sc_graph *g) { return g->device; }
 }  // namespace sc
+
+#include "sc_multi.cuh"

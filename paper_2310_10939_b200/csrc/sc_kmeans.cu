@@ -37,7 +37,8 @@ struct FusedLloyd;  // sc_kmeans_fused.cu
 bool fused_lloyd_eligible(int l, int k, int R, int64_t n);
 int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s, const double *d_x,
                     int64_t n, int k, int R, const int64_t *d_chosen, int max_iters, double tol,
-                    int64_t *labels_out, double *costs_out, int32_t *iters_out, int32_t *best_out);
+                    bool assert_cost, int64_t *labels_out, double *costs_out, int32_t *iters_out,
+                    int32_t *best_out);
 void fused_lloyd_free(FusedLloyd *f);
 const double *graph_f_device(sc_graph *g);
 int64_t graph_n(const sc_graph *g);
@@ -58,6 +59,7 @@ struct sc_kmeans {
     int32_t *h_changed = nullptr;    // pinned [2][R]
     int32_t *h_act = nullptr;        // pinned [2][2R]: active flags + compacted list per parity
     int cap_host_r = 0;
+    bool assert_cost = true;         // kmeans.py:206's assert (off: SC_KM_NO_COST_ASSERT)
     sc::FusedLloyd *fused = nullptr;  // persistent exact Lloyd (1-D, one sign, k <= 32)
     unsigned char *h_block = nullptr;  // owned pinned block behind h_cost/h_changed/h_act
     size_t h_block_bytes = 0;
@@ -1652,6 +1654,14 @@ int32_t sc_kmeans_create_from_graph(sc_graph *g, sc_kmeans **out) {
     return SC_OK;
 }
 
+int32_t sc_kmeans_set_flags(sc_kmeans *km, uint32_t flags) {
+    SC_REQUIRE(km != nullptr, SC_E_INVALID, "null k-means context");
+    SC_REQUIRE((flags & ~SC_KM_NO_COST_ASSERT) == 0, SC_E_INVALID, "unknown k-means flags 0x%x",
+               flags);
+    km->assert_cost = !(flags & SC_KM_NO_COST_ASSERT);
+    return SC_OK;
+}
+
 void sc_kmeans_destroy(sc_kmeans *km) {
     if (!km) return;
     cudaSetDevice(km->device);
@@ -1781,7 +1791,8 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         // every iteration of every restart in one persistent kernel (sc_kmeans_fused.cu);
         // 1 = not applicable (points of both signs): the general path below
         st = fused_lloyd(&km->fused, km->device, km->sm_count, s, km->d_x, n, k, R, km->d_chosen,
-                         max_iters, tol, labels_out, costs_out, iters_out, best_restart_out);
+                         max_iters, tol, km->assert_cost, labels_out, costs_out, iters_out,
+                         best_restart_out);
         if (st != 1) {
             if (ms_out)
                 *ms_out = std::chrono::duration<double, std::milli>(
@@ -2016,7 +2027,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             const bool unchanged = hch[r] == 0 && fin;
             const double c = hc[r];
             // kmeans.py:206: assert cost <= prev_cost * (1 + 1e-12) + 1e-12
-            if (!(c <= prev[r] * (1.0 + 1e-12) + 1e-12)) {
+            if (km->assert_cost && !(c <= prev[r] * (1.0 + 1e-12) + 1e-12)) {
                 cudaStreamSynchronize(s);
                 return fail(SC_E_INTERNAL, "k-means cost increased (restart %d, iteration %d: "
                             "%.17g > %.17g)", r, iters[r], c, prev[r]);

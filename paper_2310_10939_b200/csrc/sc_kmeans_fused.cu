@@ -118,6 +118,7 @@ struct FlArgs {
     int64_t nbuf;
     int wd;            // doubles of dynamic shared memory per warp
     double tol, delta;
+    int assert_cost;   // kmeans.py:206's assert (0: SC_KM_NO_COST_ASSERT, python -O)
     double xmax;       // max point value (rounding bands of the sorted-centre assignment)
     uint8_t *lab;      // [3][R][ln]
     double *cen;       // [3][R][k]
@@ -1402,7 +1403,9 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
             } else if (fin) {
                 int bad = 0;
                 const int sg = certify(P, cs, a.tol, a.delta, &bad);
-                if (sg < 0 || bad != 0) amb = 1;  // (a sure failure is confirmed exactly)
+                // (a sure failure is confirmed exactly; without the assert only the stop
+                // decision matters: a cost increase stops, kmeans.py:207)
+                if (sg < 0 || (a.assert_cost && bad != 0)) amb = 1;
                 else stop = sg;
             }
             if (amb) {
@@ -1429,7 +1432,7 @@ __global__ void __launch_bounds__(kFlThreads, 2) k_fused_lloyd(FlArgs a) {
                     const double C = exact_combine(a, 0, r), P = exact_combine(a, 1, r);
                     int bad = 0;
                     const int stop = decide_exact(P, C, a.tol, &bad);
-                    if (bad) {
+                    if (bad && a.assert_cost) {
                         atomicCAS(a.ctl + kCtlErr, 0, r + 1);
                         a.ctl[kCtlErrIt] = it - 1;
                     }
@@ -1604,7 +1607,8 @@ bool fused_lloyd_eligible(int l, int k, int R, int64_t n) {
 // general path
 int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s, const double *d_x,
                     int64_t n, int k, int R, const int64_t *d_chosen, int max_iters, double tol,
-                    int64_t *labels_out, double *costs_out, int32_t *iters_out, int32_t *best_out) {
+                    bool assert_cost, int64_t *labels_out, double *costs_out, int32_t *iters_out,
+                    int32_t *best_out) {
     if (!*pctx) {
         FusedLloyd *f = new FusedLloyd();
         f->device = device;
@@ -1679,6 +1683,7 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     a.nbuf = nbuf;
     a.wd = fl_warp_bytes(k) / 8;
     a.tol = tol;
+    a.assert_cost = assert_cost ? 1 : 0;
     a.delta = 2.0 * (double)(4097 + nbuf + 64 + nch / 32) * 1.1102230246251565e-16;
     a.lab = B + o_lab;
     a.cen = reinterpret_cast<double *>(B + o_cen);

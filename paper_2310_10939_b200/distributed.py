@@ -402,8 +402,10 @@ class CudaShard:
         zb, fl = ctypes.c_void_p(), ctypes.c_void_p()
         _lib.check(_lib.load().sc_shard_buffers(self.h, ctypes.byref(zb), ctypes.byref(fl)))
         nc = self.plan.ncols
+        gi = _lib.GraphInfo()
+        _lib.check(_lib.load().sc_graph_info_get(self.h, ctypes.byref(gi)))
         z0 = _device_view(zb.value, nc, self.device)
-        z1 = _device_view(zb.value + 8 * nc, nc, self.device)
+        z1 = _device_view(zb.value + 8 * gi.zstride, nc, self.device)
         return z0, z1, zb.value, fl.value
 
     def to_original(self, v_local):

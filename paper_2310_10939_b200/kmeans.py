@@ -157,9 +157,15 @@ class KMeans1D:
         return chosen
 
     def lloyd(self, k: int, seed: int, max_iters: int = 100, tol: float = 1e-6,
-              restarts: int = 10, method: str = "exact") -> Partition:
+              restarts: int = 10, method: str = "exact",
+              assert_cost: bool | None = None) -> Partition:
         """method "exact": the bit-exact replica; "sorted": the same seeds, then Lloyd on the
-        sorted values with prefix-sum means (1-D only, k <= 2048; not bit-exact)."""
+        sorted values with prefix-sum means (1-D only, k <= 2048; not bit-exact, see
+        DESIGN.md §8 -- an approximation, not a parity path).
+
+        ``assert_cost``: raise (SpeclusterError) when a restart's cost goes up, as the
+        reference's ``assert`` at kmeans.py:206 does; None follows the interpreter like that
+        ``assert`` (skipped under ``python -O``, where the increase stops the restart)."""
         if method not in ("exact", "sorted"):
             raise InputError(f"method must be 'exact' or 'sorted', got {method!r}")
         if not 1 <= k <= self.n:
@@ -168,6 +174,9 @@ class KMeans1D:
             raise InputError(f"restarts must be >= 1, got {restarts}")
         if max_iters < 1:
             raise InputError(f"max_iters must be >= 1, got {max_iters}")
+        if assert_cost is None:
+            assert_cost = __debug__
+        _lib.check(_lib.load().sc_kmeans_set_flags(self._h, 0 if assert_cost else 1))
         chosen = self.seed_centers(k, seed, restarts)
         labels = np.empty(self.n, dtype=np.int64)
         costs = np.empty(restarts)

@@ -54,10 +54,14 @@ class SpectralParams:
     restarts: int = 10
     max_iters: int = 100
     tol: float = 1e-6
-    kmeans: str = "exact"        # "exact" (bit-exact replica) or "sorted" (fast, one_vector)
+    kmeans: str = "exact"        # "exact" (bit-exact replica) or "sorted" (approximate:
+                                 # labels may differ from the reference's)
+    cost_assert: bool | None = None  # kmeans.py:206's assert; None: on unless python -O
     reorder: str | None = "auto"  # device-layout pre-order: "auto", "bfs" or None (exact)
     layout: str = "auto"         # SpMV layout: "auto" (column panels for T >= 64 when the
                                  # graph qualifies), "panels" or "sell"; results identical
+    gpus: int = 1                # row-block shards over this many GPUs of this process
+    devices: tuple | None = None  # explicit shard devices (overrides gpus; may repeat)
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -76,6 +80,8 @@ class SpectralParams:
             raise InputError(f"walk_sign must be +1 or -1, got {self.walk_sign}")
         if self.kmeans not in ("exact", "sorted"):
             raise InputError(f"kmeans must be 'exact' or 'sorted', got {self.kmeans!r}")
+        if self.gpus < 1 or (self.devices is not None and len(self.devices) < 1):
+            raise InputError(f"gpus must be >= 1, got {self.gpus}")
         if self.layout not in ("auto", "panels", "sell"):
             raise InputError(f"layout must be 'auto', 'panels' or 'sell', got {self.layout!r}")
 
@@ -147,9 +153,9 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
     # the panel layout costs about a dozen SELL steps to build (device, ~1.7 ms at config 2)
     # and saves ~13 % per step where it applies
     panels = params.layout == "panels" or (params.layout == "auto" and steps >= PANEL_MIN_STEPS)
-    dev = device_graph if device_graph is not None else DeviceGraph(graph, params.device,
-                                                                    reorder=params.reorder,
-                                                                    panels=panels)
+    dev = device_graph if device_graph is not None else DeviceGraph(
+        graph, params.device, reorder=params.reorder, panels=panels, gpus=params.gpus,
+        devices=params.devices)
     try:
         t0 = time.perf_counter()
         if params.x0 is not None:
@@ -168,7 +174,8 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
             t2 = time.perf_counter()
             try:
                 part = km.lloyd(params.k, _kmeans_seed(params.seed), max_iters=params.max_iters,
-                                tol=params.tol, restarts=params.restarts, method=params.kmeans)
+                                tol=params.tol, restarts=params.restarts, method=params.kmeans,
+                                assert_cost=params.cost_assert)
             finally:
                 embedding = emb.result()
             km_info = dict(km.last)

@@ -108,21 +108,41 @@ class DeviceGraph:
     layout; degrees copied verbatim, never recomputed)."""
 
     def __init__(self, graph, device: int = 0, keep_weights: bool = False,
-                 fp32_values: bool = False, reorder: str | None = None, panels: bool = False):
+                 fp32_values: bool = False, reorder: str | None = None, panels: bool = False,
+                 gpus: int = 1, devices=None):
         """``panels``: also build the column-panel layout (sc_panel.cuh; unit weights and rows
         of <= 256 entries only, declined silently otherwise -- see ``info()['panel_groups']``);
         whole-graph steps then stage heavily referenced column ranges in shared memory.
         ``fp32_values``: store the weights as fp32 (the optional fp32-value variant:
         half the weight bytes, results within 1e-5 relative of fp64; unit-weight graphs are
         unaffected).  ``reorder="bfs"``: renumber the vertices by a multi-source BFS before the
-        SELL layout (locality for graphs whose ids carry none; results unchanged)."""
+        SELL layout (locality for graphs whose ids carry none; results unchanged).
+        ``gpus`` / ``devices``: one handle over several GPUs in this process
+        (sc_graph_create_multi): row blocks balanced by entries, one shard per GPU (``devices``
+        lists them, default ``device .. device + gpus - 1``; a device may repeat), z exchanged
+        by peer stores from the SpMV epilogue; results bit-identical to one GPU.  Multi-GPU
+        handles keep the shards' own order (no BFS pre-order)."""
         if reorder not in (None, "bfs", "auto"):
             raise InputError(f"reorder must be None, 'bfs' or 'auto', got {reorder!r}")
         g = as_graph(graph)
         _check_shapes(g)  # content (ranges, monotonicity, degrees) is validated by the C-ABI
+        if devices is not None:
+            devices = [int(d) for d in devices]
+            gpus = len(devices)
+        elif gpus > 1:
+            devices = list(range(device, device + gpus))
+        if gpus < 1:
+            raise InputError(f"gpus must be >= 1, got {gpus}")
+        multi = gpus > 1
+        if multi:
+            if reorder == "bfs":
+                raise InputError("the BFS pre-order applies to single-GPU handles")
+            reorder = None
         if reorder == "auto":
             reorder = "bfs" if id_locality(g) > LOCALITY_THRESHOLD else None
         self.reorder = reorder
+        self.gpus = gpus
+        self.devices = devices if multi else [device]
         L = _lib.require_device()
         self.graph = g
         self.n = g.n
@@ -138,15 +158,21 @@ class DeviceGraph:
             w = None if (g.weights is None or g.unit_weights()) else np.ascontiguousarray(
                 g.weights, dtype=np.float64)
         h = ctypes.c_void_p()
-        _lib.check(L.sc_graph_create_ex(_lib.ptr(self._rp), _lib.ptr(self._col), _lib.ptr(w),
-                                        _lib.ptr(self._deg), g.n, g.nnz, device,
-                                        (_lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0)
-                                        | (_lib.SC_CREATE_FP32_VALUES if fp32_values else 0)
-                                        | (_lib.SC_CREATE_REORDER_BFS if reorder == "bfs" else 0)
-                                        | (_lib.SC_CREATE_PANELS if panels else 0),
-                                        ctypes.byref(h)))
+        cflags = ((_lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0)
+                  | (_lib.SC_CREATE_FP32_VALUES if fp32_values else 0)
+                  | (_lib.SC_CREATE_REORDER_BFS if reorder == "bfs" else 0)
+                  | (_lib.SC_CREATE_PANELS if panels else 0))
+        if multi:
+            dv = np.ascontiguousarray(devices, dtype=np.int32)
+            _lib.check(L.sc_graph_create_multi(_lib.ptr(self._rp), _lib.ptr(self._col),
+                                               _lib.ptr(w), _lib.ptr(self._deg), g.n, g.nnz,
+                                               gpus, _lib.ptr(dv), cflags, ctypes.byref(h)))
+        else:
+            _lib.check(L.sc_graph_create_ex(_lib.ptr(self._rp), _lib.ptr(self._col), _lib.ptr(w),
+                                            _lib.ptr(self._deg), g.n, g.nnz, device, cflags,
+                                            ctypes.byref(h)))
         self._h = h
-        self.device = device
+        self.device = self.devices[0]
         self.last_timing = None
 
     @classmethod
@@ -163,6 +189,7 @@ class DeviceGraph:
         self._h = h
         self.graph = None
         self.reorder = None
+        self.gpus, self.devices = 1, [csr.device]
         self.n, self.nnz = csr.n, csr.nnz
         self.device = csr.device
         self.last_timing = None
@@ -195,7 +222,18 @@ class DeviceGraph:
     def info(self) -> dict:
         gi = _lib.GraphInfo()
         _lib.check(_lib.load().sc_graph_info_get(self.handle, ctypes.byref(gi)))
-        return {f: getattr(gi, f) for f, _ in gi._fields_}
+        return {f: getattr(gi, f) for f, _ in gi._fields_ if f != "reserved"}
+
+    def shard_layout(self) -> list:
+        """multi-GPU handles: per shard (row0, rows, z offset, device)"""
+        out = []
+        for w in range(self.gpus if self.gpus > 1 else 0):
+            r0, nr, zo, dv = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+            _lib.check(_lib.load().sc_graph_shard_layout(self.handle, w, ctypes.byref(r0),
+                                                         ctypes.byref(nr), ctypes.byref(zo),
+                                                         ctypes.byref(dv)))
+            out.append((r0.value, nr.value, zo.value, dv.value))
+        return out
 
     # -- start vector
     def sample_irwin_hall(self, seed: int, return_host: bool = False):

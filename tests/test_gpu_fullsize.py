@@ -7,7 +7,8 @@ oracle can finish in test time:
       nearly constant band whose spread is of the order of d2ref's rounding, so Lloyd's cost
       goes UP at an iteration and the reference's `assert cost <= prev_cost*(1+1e-12)+1e-12`
       (kmeans.py:206) fires: the device replica must raise as well (SC_E_INTERNAL), and does
-      for both the first restart alone and the batched 10;
+      for both the first restart alone and the batched 10; with the assert skipped (the
+      reference under `python -O`) all 10 restarts' labels equal the oracle's;
   config 4 (16-NN RGG, n = 1e7, ~181M entries, T = 300, k = 100): labels after 3 Lloyd
       iterations of 1 restart (a full oracle run is ~40 min of host time);
   config 5 (SBM, n = 1e8, 1.8e9 entries, T = 100): x_T and f only -- the oracle's k = 1000
@@ -56,7 +57,14 @@ def test_config3_full_size_bit_exact():
         O.lloyd(f, 50, O.kmeans_seed(0), restarts=1)
     for restarts in (1, 10):
         with KMeans1D(f) as km, pytest.raises(SpeclusterError, match="cost increased"):
-            km.lloyd(50, O.kmeans_seed(0), restarts=restarts)
+            km.lloyd(50, O.kmeans_seed(0), restarts=restarts, assert_cost=True)
+    # the reference under `python -O` (the assert skipped, the increase ends the restart via
+    # the small-gain test): all 10 restarts, labels and best cost identical
+    lab, cost = O.lloyd(f, 50, O.kmeans_seed(0), restarts=10, threads=THREADS, assert_cost=False)
+    with KMeans1D(f) as km:
+        part = km.lloyd(50, O.kmeans_seed(0), restarts=10, assert_cost=False)
+        assert km.last["costs"].min() == cost
+    assert np.array_equal(part.labels, lab)
 
 
 def test_config4_full_size_bit_exact():
