@@ -114,14 +114,48 @@ __device__ __forceinline__ void peer_fence(const StepArgs &a) {
     if (a.npeer) __threadfence_system();
 }
 
-// Wide rows (> kExtreme entries): one warp per row.  The warp gathers 128 products per
-// step into its double-buffered shared-memory slot and lane 0 adds them strictly in order
-// (the scipy order) while the next 128 gathers are already in flight.
+// Wide rows (> kExtreme entries): one warp per row.  The in-order fold of a row is a chain
+// of dependent adds, so the row's time is bounded below by (entries x add latency); every
+// memory latency is kept off that chain: the warp gathers 128 products per step into its
+// double-buffered shared-memory slot while lane 0 adds the previous 128 strictly in order
+// (the scipy order), and the column indices are fetched one step earlier still, so a
+// gather never waits for its index load.
 constexpr int kWideBatch = 128;
+constexpr int kWidePL = kWideBatch / 32;
+
+// s + v[0] + v[1] + ... + v[m-1], left to right (v 16-byte aligned): shared-memory loads of
+// the next 8 values are issued before the adds of the current 8
+__device__ __forceinline__ double wide_fold(double s, const double *v, int m) {
+    const double2 *v2 = reinterpret_cast<const double2 *>(v);
+    const int mf = m & ~7;
+    double2 cur[4], nxt[4];
+    if (mf) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[u] = v2[u];
+    }
+    for (int t = 0; t < mf; t += 8) {
+        const bool more = t + 8 < mf;
+        if (more) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) nxt[u] = v2[(t + 8) / 2 + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            s = __dadd_rn(s, cur[u].x);
+            s = __dadd_rn(s, cur[u].y);
+        }
+        if (more) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+        }
+    }
+    for (int t = mf; t < m; ++t) s = __dadd_rn(s, v[t]);
+    return s;
+}
 
 template <bool UNIT, bool SYM, bool F32 = false>
-__global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
-    __shared__ double wbuf[kStepTPB / 32][2][kWideBatch];
+__global__ void __launch_bounds__(kStepTPB, 2) k_rw_wide(StepArgs a) {
+    __shared__ __align__(16) double wbuf[kStepTPB / 32][2][kWideBatch];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t w = a.wide_lo + (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
@@ -130,35 +164,55 @@ __global__ void __launch_bounds__(kStepTPB) k_rw_wide(StepArgs a) {
     const double xr = __ldcs(a.x_in + r), sc = __ldcs(a.scale + r);
     const int64_t lo = a.wide_ptr[w], hi = a.wide_ptr[w + 1];
     double *buf0 = wbuf[warp][0], *buf1 = wbuf[warp][1];
-    auto gather = [&](int64_t base, double (&p)[kWideBatch / 32]) {
+    auto load_cols = [&](int64_t base, uint32_t (&c)[kWidePL]) {
 #pragma unroll
-        for (int q = 0; q < kWideBatch / 32; ++q) {
+        for (int q = 0; q < kWidePL; ++q) {
             const int64_t j = base + 32 * q + lane;
-            p[q] = 0.0;
+            c[q] = j < hi ? __ldcs(a.wcol + j) : 0u;
+        }
+    };
+    // loads only: the products are formed after the fold, so the fold never waits on them
+    auto issue = [&](int64_t base, const uint32_t (&c)[kWidePL], double (&zr)[kWidePL],
+                     double (&wr)[kWidePL]) {
+#pragma unroll
+        for (int q = 0; q < kWidePL; ++q) {
+            const int64_t j = base + 32 * q + lane;
+            zr[q] = 0.0;
+            wr[q] = 1.0;
             if (j < hi) {
-                const double zv = __ldg(a.z_in + __ldcs(a.wcol + j));
-                const double wv = UNIT ? 1.0 : F32 ? (double)__ldcs(a.wval32 + j) : __ldcs(a.wval + j);
-                p[q] = UNIT ? zv : __dmul_rn(wv, zv);
+                zr[q] = __ldg(a.z_in + c[q]);
+                if (!UNIT) wr[q] = F32 ? (double)__ldcs(a.wval32 + j) : __ldcs(a.wval + j);
             }
         }
     };
-    double p[kWideBatch / 32];
-    gather(lo, p);
+    auto store = [&](double *buf, const double (&zr)[kWidePL], const double (&wr)[kWidePL]) {
 #pragma unroll
-    for (int q = 0; q < kWideBatch / 32; ++q) buf0[32 * q + lane] = p[q];
+        for (int q = 0; q < kWidePL; ++q) buf[32 * q + lane] = UNIT ? zr[q] : __dmul_rn(wr[q], zr[q]);
+    };
+    uint32_t cn[kWidePL];
+    double zr[kWidePL], wr[kWidePL];
+    load_cols(lo, cn);
+    issue(lo, cn, zr, wr);
+    if (lo + kWideBatch < hi) load_cols(lo + kWideBatch, cn);  // indices of step 1
+    store(buf0, zr, wr);
     double s = 0.0;
     for (int64_t base = lo; base < hi; base += kWideBatch) {
         __syncwarp();
         const bool more = base + kWideBatch < hi;
-        if (more) gather(base + kWideBatch, p);  // in flight during the fold below
+        uint32_t cnn[kWidePL];
+        if (more) {
+            issue(base + kWideBatch, cn, zr, wr);  // in flight during the fold below
+            if (base + 2 * kWideBatch < hi) load_cols(base + 2 * kWideBatch, cnn);
+        }
         if (lane == 0) {
             const int m = (int)(hi - base < kWideBatch ? hi - base : kWideBatch);
-            for (int t = 0; t < m; ++t) s = __dadd_rn(s, buf0[t]);
+            s = wide_fold(s, buf0, m);
         }
         __syncwarp();
         if (more) {
+            store(buf1, zr, wr);
 #pragma unroll
-            for (int q = 0; q < kWideBatch / 32; ++q) buf1[32 * q + lane] = p[q];
+            for (int q = 0; q < kWidePL; ++q) cn[q] = cnn[q];
         }
         double *tb = buf0;
         buf0 = buf1;

@@ -35,6 +35,14 @@ namespace cg = cooperative_groups;
 namespace sc {
 struct FusedLloyd;  // sc_kmeans_fused.cu
 bool fused_lloyd_eligible(int l, int k, int R, int64_t n);
+// sc_kmeans_small.cu: one CTA per restart for n <= 4096
+bool small_kmeans_eligible(int l, int k, int64_t n);
+int32_t small_kpp(int device, cudaStream_t s, const double *d_x, int64_t n, int k, int R,
+                  const int32_t *d_start, const double *d_u, int64_t *d_chosen, int32_t *d_degen);
+int32_t small_lloyd(cudaStream_t s, const double *d_x, int64_t n, int k, int R,
+                    const int64_t *d_chosen, int max_iters, double tol, bool assert_cost,
+                    int32_t *d_lab, double *d_cost, int32_t *d_iters, int32_t *d_err,
+                    int64_t *labels_out, double *costs_out, int32_t *iters_out, int32_t *best_out);
 int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s, const double *d_x,
                     int64_t n, int k, int R, const int64_t *d_chosen, int max_iters, double tol,
                     bool assert_cost, int64_t *labels_out, double *costs_out, int32_t *iters_out,
@@ -102,6 +110,9 @@ struct sc_kmeans {
     int64_t *d_sq0 = nullptr, *d_sq1 = nullptr;  // super-chunk maps
     double *d_svmax = nullptr;
     int32_t *d_skp = nullptr;
+    int32_t *d_kmap = nullptr;     // [chunks] grid the chunk map in d_q0/d_q1 was built on
+    double *d_sstart = nullptr;    // [supers] k-means++: exact running sum at super starts
+    int32_t *d_sflag = nullptr;
 };
 
 namespace sc {
@@ -184,9 +195,19 @@ struct SeqWork {
     int64_t *sq0, *sq1;
     double *svmax;
     int32_t *skp;     // common predicted grid, or kNoGrid (walk the chunks one by one)
+    // k-means++ search by super-chunk (compose mode 2): exact running sum at every super
+    // start, and whether the super was advanced whole (1: its chunk starts follow from the
+    // chunk maps) or chunk by chunk (0: cstart holds them)
+    double *sstart = nullptr;
+    int32_t *sflag = nullptr;
 };
 
 constexpr int kSuper = 32;
+// stride of a restart's k-means++ weights: n rounded up to whole super-chunks
+constexpr int64_t kppStrideAlign = (int64_t)kSuper * kSeqChunk;
+__host__ __device__ __forceinline__ int64_t kpp_stride(int64_t n) {
+    return (n + kppStrideAlign - 1) / kppStrideAlign * kppStrideAlign;
+}
 
 __device__ __forceinline__ int seg_of_chunk(const SegView &v, int64_t c) {
     int lo = 0, hi = v.S;  // cofs[lo] <= c < cofs[hi]
@@ -475,7 +496,11 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
             const unsigned valm = __ballot_sync(0xffffffffu, valid);
             const int Lb = badm ? __ffs(badm) - 1 : 32;
             const int nadv = min(Lb, __popc(valm));
-            if (want_cstart && lane < nadv) {
+            if (want_cstart == 2 && lane < nadv) {
+                w.sstart[G] = sgn * from_units(Sl, g.k);
+                w.sflag[G] = 1;
+            }
+            if (want_cstart == 1 && lane < nadv) {
                 // exact start of every chunk of this super-chunk (for the k-means++ search);
                 // the chunk maps are fetched 8 at a time so a step pays 4 memory latencies
                 int64_t S = Sl;
@@ -541,6 +566,10 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         const int Le = __popc(valm);                  // valid lanes form a prefix
         const int nadv = min(Lb, Le);
         if (want_cstart && lane < nadv) w.cstart[cl] = sgn * from_units(Sl, g.k);
+        if (want_cstart == 2 && lane < nadv && (cl & (kSuper - 1)) == 0) {
+            w.sstart[cl / kSuper] = sgn * from_units(Sl, g.k);
+            w.sflag[cl / kSuper] = 0;
+        }
         if (nadv > 0) {
             const int64_t Send = __shfl_sync(0xffffffffu, pmap_apply(m, Sl), nadv - 1);
             run = from_units(Send, g.k);
@@ -549,6 +578,10 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         if (Lb < Le) {
             // step chunk c element by element
             if (want_cstart && lane == 0) w.cstart[c] = sgn * run;
+            if (want_cstart == 2 && lane == 0 && (c & (kSuper - 1)) == 0) {
+                w.sstart[c / kSuper] = sgn * run;
+                w.sflag[c / kSuper] = 0;
+            }
             double a[kSeqPerLane];
             int64_t first;
             const int mcount = load_chunk(v, s, c, a, first);
@@ -565,18 +598,24 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
 // best[r][j] = min over chosen[r][0..start_r-1] of d2(x_j, x[chosen])
 __global__ void k_kpp_init(const double *__restrict__ x, int64_t n, int l, int k,
                            const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
-                           const int32_t *__restrict__ on, double *__restrict__ best) {
+                           const int32_t *__restrict__ on, double *__restrict__ best,
+                           int32_t *__restrict__ kpred, int64_t cps) {
     const int r = blockIdx.y;
     if (!on[r]) return;
     const int s = start[r];
-    double *b = best + (int64_t)r * n;
+    const int64_t nb = kpp_stride(n);
+    double *b = best + (int64_t)r * nb;
     const int64_t *ch = chosen + (int64_t)r * k;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nb;
          j += (int64_t)gridDim.x * blockDim.x) {
-        const double *xj = x + j * l;
-        double v = d2nd(xj, x + ch[0] * l, l);
-        for (int i = 1; i < s; ++i) v = fmin(v, d2nd(xj, x + ch[i] * l, l));
+        double v = 0.0;  // padding past n stays 0 (adds nothing to any running sum)
+        if (j < n) {
+            const double *xj = x + j * l;
+            v = d2nd(xj, x + ch[0] * l, l);
+            for (int i = 1; i < s; ++i) v = fmin(v, d2nd(xj, x + ch[i] * l, l));
+        }
         b[j] = v;
+        if (j < cps) kpred[(int64_t)r * cps + j] = kNoGrid;  // no speculative grid yet
     }
 }
 
@@ -598,7 +637,7 @@ __global__ void k_kpp_update_sum(const double *__restrict__ x, int64_t n, int l,
         if (!round_on[r]) continue;
         const bool upd = on[r] && i - 1 >= start[r];
         const double *cn = upd ? x + chosen[(int64_t)r * k + i - 1] * l : nullptr;
-        double *b = best + (int64_t)r * n;
+        double *b = best + (int64_t)r * kpp_stride(n);
         const int64_t j0 = (c - (int64_t)r * cps) * kSeqChunk + lane * kSeqPerLane;
         double sum = 0.0, mx = 0.0;
         int bad = 0;
@@ -634,6 +673,167 @@ __global__ void k_kpp_update_sum(const double *__restrict__ x, int64_t n, int l,
 }
 
 // per-round segment flags: restart still seeding and round i belongs to this call
+// 1-D k-means++ round, one pass over the weights: one warp per chunk position, all restarts
+// (x of the chunk is read once).  Each restart's weights take the distance to its newest
+// centre (kmeans.py:137 np.minimum), the chunk's approximate sum / max are written for the
+// prediction, and -- speculatively, on the grid the previous round predicted for the chunk
+// (the weights only shrink, so most chunks keep their binade) -- the chunk's parity map.
+// kmap records the grid each map was built on; k_seq_chunkmap_fix rebuilds the chunks whose
+// new prediction differs, so no map is ever used on the wrong grid.
+__global__ void k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
+                                 const int64_t *__restrict__ chosen,
+                                 const int32_t *__restrict__ start, const int32_t *__restrict__ on,
+                                 const int32_t *__restrict__ round_on, double *__restrict__ best,
+                                 SeqWork w, int32_t *__restrict__ kmap, int64_t cps, int R) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nb = kpp_stride(n);
+    for (int64_t cc = wid; cc < cps; cc += nw) {
+        const int64_t j0 = cc * kSeqChunk + lane * kSeqPerLane;
+        double xv[kSeqPerLane];
+#pragma unroll
+        for (int t = 0; t < kSeqPerLane; ++t) xv[t] = j0 + t < n ? __ldg(x + j0 + t) : 0.0;
+        for (int r = 0; r < R; ++r) {
+            if (!round_on[r]) continue;
+            const int64_t c = (int64_t)r * cps + cc;
+            const bool upd = on[r] && i - 1 >= start[r];
+            const double cn = upd ? __ldg(x + chosen[(int64_t)r * k + i - 1]) : 0.0;
+            double *b = best + (int64_t)r * nb;
+            double a[kSeqPerLane];
+#pragma unroll
+            for (int t = 0; t < kSeqPerLane; ++t) a[t] = b[j0 + t];
+            double sum = 0.0, mx = 0.0;
+            int bad = 0;
+#pragma unroll
+            for (int t = 0; t < kSeqPerLane; ++t) {
+                if (upd && j0 + t < n) {
+                    const double d = d2ref(xv[t], cn);
+                    if (d < a[t]) {
+                        a[t] = d;
+                        b[j0 + t] = d;
+                    }
+                }
+                sum += a[t];
+                mx = fmax(mx, a[t]);
+                bad |= !(a[t] >= 0.0) || !isfinite(a[t]);
+            }
+            const int kp = w.kpred[c];
+            PMap lm = pmap_id();
+            if (kp != kNoGrid) {
+#pragma unroll
+                for (int t = 0; t < kSeqPerLane; ++t) lm = pmap_then(lm, pmap_elem(to_units(a[t], kp)));
+            }
+#pragma unroll
+            for (int d = 16; d; d >>= 1) {
+                sum += __shfl_xor_sync(0xffffffffu, sum, d);
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+                bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+            }
+            if (kp != kNoGrid) lm = warp_scan_pmap(lm);
+            if (lane == 31) {
+                w.A[c] = sum;
+                w.vmax[c] = mx;
+                if (bad) w.neg[r] = 4;
+                if (kp != kNoGrid) {
+                    w.q0[c] = lm.i0;
+                    w.q1[c] = lm.i1;
+                }
+                kmap[c] = kp;
+            }
+        }
+    }
+}
+
+// one warp per chunk: rebuild the parity map of every chunk whose predicted grid differs from
+// the one its map was built on (k_kpp_update_map's speculation missed)
+__global__ void k_seq_chunkmap_fix(SegView v, SeqWork w, int32_t *__restrict__ kmap,
+                                   const int64_t *__restrict__ pn) {
+    const int64_t nchunks = *pn;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = wid; c < nchunks; c += nw) {
+        const int kp = w.kpred[c];
+        if (kp == kNoGrid || kp == kmap[c]) continue;
+        const int s = seg_of_chunk(v, c);
+        if (!seg_on(v, s)) continue;
+        double a[kSeqPerLane];
+        int64_t first;
+        const int m = load_chunk(v, s, c, a, first);
+        PMap lm = pmap_id();
+#pragma unroll
+        for (int t = 0; t < kSeqPerLane; ++t)
+            if (lane * kSeqPerLane + t < m) lm = pmap_then(lm, pmap_elem(to_units(a[t], kp)));
+        const PMap tot = warp_scan_pmap(lm);
+        if (lane == 31) {
+            w.q0[c] = tot.i0;
+            w.q1[c] = tot.i1;
+            kmap[c] = kp;
+        }
+    }
+}
+
+// k-means++ draw (kmeans.py:116-118: searchsorted(cumsum(w), u * cumsum(w)[-1], 'right'),
+// clipped) from the super-chunk starts of compose mode 2: binary search for the super, its
+// chunk starts from the chunk maps (whole supers) or cstart (chunk-walked supers), then the
+// chunk element by element.  Segments are super-aligned (kpp_stride).
+__global__ void k_kpp_search2(SegView v, SeqWork w, int64_t n, int k, int i,
+                              const double *__restrict__ u, int64_t *__restrict__ chosen,
+                              int32_t *__restrict__ on, int32_t *__restrict__ degen) {
+    const int lane = threadIdx.x & 31;
+    const int r = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (r >= v.S || !seg_on(v, r)) return;
+    const double tot = w.total[r];
+    if (!(tot > 0.0)) {
+        if (lane == 0) {
+            degen[r] = i;
+            on[r] = 0;
+        }
+        return;
+    }
+    const double target = __dmul_rn(u[(int64_t)r * (k - 1) + (i - 1)], tot);
+    const int64_t c0 = v.cofs[r], c1 = v.cofs[r + 1];
+    const int64_t G0 = c0 / kSuper, G1 = c1 / kSuper;
+    // first super whose end exceeds target (ends are nondecreasing: the weights are >= 0)
+    int64_t lo = G0, hi = G1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const double end = mid + 1 < G1 ? w.sstart[mid + 1] : tot;
+        if (end > target) hi = mid;
+        else lo = mid + 1;
+    }
+    __shared__ double sbuf[8][kSeqChunk];  // launched with 256 threads
+    int64_t idx = n - 1;
+    if (lo < G1) {
+        const int64_t G = lo;
+        const double sst = w.sstart[G];
+        const double send = G + 1 < G1 ? w.sstart[G + 1] : tot;
+        const int64_t cb = G * kSuper;
+        double cst;  // exact start of this lane's chunk cb + lane
+        if (w.sflag[G]) {
+            const Grid g = grid_of(sst);
+            const int64_t S0 = (int64_t)to_units(sst, g.k);
+            const PMap m{w.q0[cb + lane], w.q1[cb + lane]};
+            cst = from_units(pmap_apply(warp_exclusive(warp_scan_pmap(m)), S0), g.k);
+        } else {
+            cst = w.cstart[cb + lane];
+        }
+        const double nxt = __shfl_down_sync(0xffffffffu, cst, 1);  // (every lane shuffles)
+        const double cend = lane + 1 < kSuper ? nxt : send;
+        const unsigned hit_m = __ballot_sync(0xffffffffu, cend > target);
+        const int cl = hit_m ? __ffs(hit_m) - 1 : kSuper - 1;
+        double run = __shfl_sync(0xffffffffu, cst, cl);
+        double a[kSeqPerLane];
+        int64_t first;
+        const int m = load_chunk(v, r, cb + cl, a, first);
+        const int hit = warp_step_seq(a, m, run, target, true, sbuf[(threadIdx.x >> 5) & 7]);
+        if (hit >= 0) idx = first - v.seg_off[r] + hit;
+        if (idx >= n) idx = n - 1;  // (padding never exceeds the target; clip like :118)
+    }
+    if (lane == 0) chosen[(int64_t)r * k + i] = idx;
+}
+
 __global__ void k_kpp_round_on(int R, int i, const int32_t *__restrict__ start,
                                const int32_t *__restrict__ on, int32_t *__restrict__ round_on,
                                int32_t *__restrict__ neg) {
@@ -1477,10 +1677,13 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     const int64_t n = km->n;
     const int64_t nbuf = (n * km->l + kEinsumBuf - 1) / kEinsumBuf;
     // chunks: kpp uses R * ceil(n/C); Lloyd's R*k segments need at most R*n/C + R*k
-    const int64_t nch = (int64_t)R * ((n + kSeqChunk - 1) / kSeqChunk) + (int64_t)R * k + 1;
+    // k-means++ lays restart r's D^2 weights out at best + r * nb, nb = n rounded up to a
+    // super-chunk, so every super-chunk lies inside one restart (zero padding)
+    const int64_t nb = kpp_stride(n);
+    const int64_t nch = (int64_t)R * (nb / kSeqChunk) + (int64_t)R * k + 1;
     const int64_t S = (int64_t)R * k + 1;
     int32_t st;
-    if ((st = grow(&km->d_best, (size_t)R * n, km->stream))) return st;
+    if ((st = grow(&km->d_best, (size_t)R * nb, km->stream))) return st;
     if ((st = grow(&km->d_lab[0], (size_t)R * n, km->stream))) return st;
     if ((st = grow(&km->d_lab[1], (size_t)R * n, km->stream))) return st;
     if ((st = grow(&km->d_keys, (size_t)R * n, km->stream))) return st;
@@ -1544,6 +1747,9 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     if ((st = grow(&km->d_sq1, (size_t)nch / kSuper + 1, km->stream))) return st;
     if ((st = grow(&km->d_svmax, (size_t)nch / kSuper + 1, km->stream))) return st;
     if ((st = grow(&km->d_skp, (size_t)nch / kSuper + 1, km->stream))) return st;
+    if ((st = grow(&km->d_kmap, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_sstart, (size_t)nch / kSuper + 1, km->stream))) return st;
+    if ((st = grow(&km->d_sflag, (size_t)nch / kSuper + 1, km->stream))) return st;
     if ((st = grow(&km->d_total, (size_t)S, km->stream))) return st;
     if ((st = grow(&km->d_neg, (size_t)S, km->stream))) return st;
     if ((st = grow(&km->d_cofs, (size_t)S + 1, km->stream))) return st;
@@ -1583,6 +1789,8 @@ static SeqWork seq_work(sc_kmeans *km) {
     w.sq1 = km->d_sq1;
     w.svmax = km->d_svmax;
     w.skp = km->d_skp;
+    w.sstart = km->d_sstart;
+    w.sflag = km->d_sflag;
     return w;
 }
 
@@ -1674,6 +1882,7 @@ void sc_kmeans_destroy(sc_kmeans *km) {
                     km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
                     km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
                     km->d_sq0, km->d_sq1, km->d_svmax, km->d_skp, km->d_idx, km->d_idx_alt,
+                    km->d_kmap, km->d_sstart, km->d_sflag,
                     km->d_elist, km->d_mlist, km->d_pval, km->d_pidx,
                     km->d_segkpp};
     if (km->stream2) cudaStreamSynchronize(km->stream2);
@@ -1723,11 +1932,23 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
         on[r] = start_round[r] < k;
     }
     SC_CUDA(cudaMemcpyAsync(km->d_on, on.data(), (size_t)R * 4, cudaMemcpyHostToDevice, s));
-    // segments r over the D^2 weights best[r][0..n)
-    const int64_t cps = (n + kSeqChunk - 1) / kSeqChunk;
+    if (k > 1 && small_kmeans_eligible(km->l, k, n)) {
+        // every round of every restart in one launch (one CTA per restart)
+        if ((st = small_kpp(km->device, s, km->d_x, n, k, R, km->d_start, km->d_u, km->d_chosen,
+                            km->d_degen)))
+            return st;
+        SC_CUDA(cudaMemcpyAsync(chosen, km->d_chosen, (size_t)R * k * 8, cudaMemcpyDeviceToHost, s));
+        SC_CUDA(cudaMemcpyAsync(degenerate_out, km->d_degen, (size_t)R * 4, cudaMemcpyDeviceToHost, s));
+        SC_CUDA(cudaStreamSynchronize(s));
+        return SC_OK;
+    }
+    // segments r over the D^2 weights best[r * nb + (0..nb)] (zero past n; nb a whole
+    // number of super-chunks, so supers never straddle restarts)
+    const int64_t nb = kpp_stride(n);
+    const int64_t cps = nb / kSeqChunk;
     std::vector<int64_t> segoff(R + 1), cofs(R + 1);
     for (int r = 0; r <= R; ++r) {
-        segoff[r] = (int64_t)r * n;
+        segoff[r] = (int64_t)r * nb;
         cofs[r] = (int64_t)r * cps;
     }
     const int64_t nch = (int64_t)R * cps;
@@ -1746,19 +1967,39 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     const int gw = grid_1d(km, nch * 32, 256);
     const int gs = (R * 32 + 255) / 256;
     k_kpp_init<<<g2, 256, 0, s>>>(km->d_x, n, km->l, k, km->d_chosen, km->d_start, km->d_on,
-                                  km->d_best);
+                                  km->d_best, km->d_kpred, cps);
     SC_CUDA(cudaGetLastError());
+    // no chunk map of this call yet (0x7f7f7f7f is no grid exponent and not kNoGrid)
+    SC_CUDA(cudaMemsetAsync(km->d_kmap, 0x7f, (size_t)nch * 4, s));
+    const bool fused1d = km->l == 1 && getenv("SC_KPP_CLASSIC") == nullptr;
+    const int gu = grid_1d(km, cps * 32, 256);
     for (int i = smin; i < k; ++i) {
         k_kpp_round_on<<<(R + 127) / 128, 128, 0, s>>>(R, i, km->d_start, km->d_on,
                                                        km->d_round_on, km->d_neg);
-        k_kpp_update_sum<<<gw, 256, 0, s>>>(km->d_x, n, km->l, k, i, km->d_chosen, km->d_start,
-                                            km->d_on, km->d_round_on, km->d_best, w, cps, R);
-        k_seq_predict<<<R, 32 * kPredictWarps, 0, s>>>(v, w);
-        k_seq_chunkmap<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
-        k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
-        k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem, s>>>(v, w, 1);
-        k_kpp_search<<<gs, 256, 0, s>>>(v, w, n, k, i, km->d_u, km->d_chosen, km->d_on,
-                                         km->d_degen);
+        if (fused1d) {
+            // one pass: weights, chunk summaries and (speculative) chunk maps; x read once
+            k_kpp_update_map<<<gu, 256, 0, s>>>(km->d_x, n, k, i, km->d_chosen, km->d_start,
+                                                km->d_on, km->d_round_on, km->d_best, w,
+                                                km->d_kmap, cps, R);
+            k_seq_predict<<<R, 32 * kPredictWarps, 0, s>>>(v, w);
+            k_seq_chunkmap_fix<<<gw, 256, 0, s>>>(v, w, km->d_kmap, km->d_nchunks);
+            k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
+            k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
+                            kComposeSmem, s>>>(v, w, 2);
+            k_kpp_search2<<<gs, 256, 0, s>>>(v, w, n, k, i, km->d_u, km->d_chosen, km->d_on,
+                                             km->d_degen);
+        } else {
+            k_kpp_update_sum<<<gw, 256, 0, s>>>(km->d_x, n, km->l, k, i, km->d_chosen,
+                                                km->d_start, km->d_on, km->d_round_on,
+                                                km->d_best, w, cps, R);
+            k_seq_predict<<<R, 32 * kPredictWarps, 0, s>>>(v, w);
+            k_seq_chunkmap<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
+            k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
+            k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
+                            kComposeSmem, s>>>(v, w, 1);
+            k_kpp_search<<<gs, 256, 0, s>>>(v, w, n, k, i, km->d_u, km->d_chosen, km->d_on,
+                                             km->d_degen);
+        }
     }
     SC_CUDA(cudaGetLastError());
     SC_CUDA(cudaMemcpyAsync(chosen, km->d_chosen, (size_t)R * k * 8, cudaMemcpyDeviceToHost, s));
@@ -1787,6 +2028,15 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     const int64_t nbuf = (n * l + kEinsumBuf - 1) / kEinsumBuf;
     const int rk = R * k;
     SC_CUDA(cudaMemcpyAsync(km->d_chosen, chosen, (size_t)rk * 8, cudaMemcpyHostToDevice, s));
+    if (small_kmeans_eligible(l, k, n)) {
+        st = small_lloyd(s, km->d_x, n, k, R, km->d_chosen, max_iters, tol, km->assert_cost,
+                         km->d_lab[0], km->d_cost, km->d_active, km->d_empty, labels_out,
+                         costs_out, iters_out, best_restart_out);
+        if (ms_out)
+            *ms_out = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                          .count();
+        return st;
+    }
     if (fused_lloyd_eligible(l, k, R, n)) {
         // every iteration of every restart in one persistent kernel (sc_kmeans_fused.cu);
         // 1 = not applicable (points of both signs): the general path below

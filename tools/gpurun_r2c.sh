@@ -1,0 +1,5 @@
+mkdir -p gpurun_out/r2c
+for c in 1 2 3 4 5; do timeout 600 python tools/km_split.py $c 2 >> gpurun_out/r2c/km_split.log 2>&1; done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_multi.py -q -x > gpurun_out/r2c/tests.log 2>&1; echo "exit $?" >> gpurun_out/r2c/tests.log
+timeout 600 python bench.py --config 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/r2c/bench_c3.json 2> gpurun_out/r2c/bench_c3.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2c/launches_c3.csv python tools/prof_spmv.py 3 --cfg 3 > gpurun_out/r2c/launches_c3.log 2>&1
