@@ -485,6 +485,8 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
                 m = PMap{w.sq0[G], w.sq1[G]};
                 vmu = to_units(w.svmax[G], g.k);
                 ok = true;
+            } else if (valid && w.svmax[G] == 0.0) {
+                ok = true;  // all zeros (elements are >= 0 here): fl(s + 0) = s, any grid
             }
             const PMap excl = warp_exclusive(warp_scan_pmap(m));
             const int64_t Sl = pmap_apply(excl, S0);
@@ -553,6 +555,9 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
             m = PMap{sq0[cl - blk], sq1[cl - blk]};
             vmu = to_units(svm[cl - blk], g.k);
             ok = true;
+        } else if (valid && svm[cl - blk] == 0.0) {
+            ok = true;  // all zeros: identity (a long zero prefix keeps the sum at 0, whose
+                        // subnormal grid no chunk map is built on)
         }
         const PMap excl = warp_exclusive(warp_scan_pmap(m));
         const int64_t Sl = pmap_apply(excl, S0);
@@ -680,67 +685,81 @@ __global__ void k_kpp_update_sum(const double *__restrict__ x, int64_t n, int l,
 // (the weights only shrink, so most chunks keep their binade) -- the chunk's parity map.
 // kmap records the grid each map was built on; k_seq_chunkmap_fix rebuilds the chunks whose
 // new prediction differs, so no map is ever used on the wrong grid.
-__global__ void k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
-                                 const int64_t *__restrict__ chosen,
-                                 const int32_t *__restrict__ start, const int32_t *__restrict__ on,
-                                 const int32_t *__restrict__ round_on, double *__restrict__ best,
-                                 SeqWork w, int32_t *__restrict__ kmap, int64_t cps, int R) {
+__global__ void __launch_bounds__(256, 4)
+k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
+                 const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
+                 const int32_t *__restrict__ on, const int32_t *__restrict__ round_on,
+                 double *__restrict__ best, SeqWork w, int32_t *__restrict__ kmap, int64_t cps,
+                 int R) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nb = kpp_stride(n);
-    for (int64_t cc = wid; cc < cps; cc += nw) {
+    // task t = (chunk position cc, restart r), r fastest: the R warps of one chunk position
+    // read the same x lines (one HBM read, the rest from L1/L2)
+    for (int64_t t = wid; t < cps * R; t += nw) {
+        const int64_t cc = t / R;
+        const int r = (int)(t - cc * R);
+        if (!round_on[r]) continue;
         const int64_t j0 = cc * kSeqChunk + lane * kSeqPerLane;
-        double xv[kSeqPerLane];
+        const int64_t c = (int64_t)r * cps + cc;
+        const bool upd = on[r] && i - 1 >= start[r];
+        const double cn = upd ? __ldg(x + chosen[(int64_t)r * k + i - 1]) : 0.0;
+        double *b = best + (int64_t)r * nb;
+        const int kp = w.kpred[c];
+        double a[kSeqPerLane], xv[kSeqPerLane];
 #pragma unroll
-        for (int t = 0; t < kSeqPerLane; ++t) xv[t] = j0 + t < n ? __ldg(x + j0 + t) : 0.0;
-        for (int r = 0; r < R; ++r) {
-            if (!round_on[r]) continue;
-            const int64_t c = (int64_t)r * cps + cc;
-            const bool upd = on[r] && i - 1 >= start[r];
-            const double cn = upd ? __ldg(x + chosen[(int64_t)r * k + i - 1]) : 0.0;
-            double *b = best + (int64_t)r * nb;
-            double a[kSeqPerLane];
+        for (int q = 0; q < kSeqPerLane; q += 2) {
+            const double2 bb = *reinterpret_cast<const double2 *>(b + j0 + q);
+            a[q] = bb.x;
+            a[q + 1] = bb.y;
+        }
+        if (upd) {
 #pragma unroll
-            for (int t = 0; t < kSeqPerLane; ++t) a[t] = b[j0 + t];
-            double sum = 0.0, mx = 0.0;
-            int bad = 0;
+            for (int q = 0; q < kSeqPerLane; ++q) xv[q] = j0 + q < n ? __ldg(x + j0 + q) : 0.0;
+        }
+        double sum = 0.0, mx = 0.0;
+        int bad = 0;
+        bool wr = false;
 #pragma unroll
-            for (int t = 0; t < kSeqPerLane; ++t) {
-                if (upd && j0 + t < n) {
-                    const double d = d2ref(xv[t], cn);
-                    if (d < a[t]) {
-                        a[t] = d;
-                        b[j0 + t] = d;
-                    }
+        for (int q = 0; q < kSeqPerLane; ++q) {
+            if (upd && j0 + q < n) {
+                const double d = d2ref(xv[q], cn);
+                if (d < a[q]) {
+                    a[q] = d;
+                    wr = true;
                 }
-                sum += a[t];
-                mx = fmax(mx, a[t]);
-                bad |= !(a[t] >= 0.0) || !isfinite(a[t]);
             }
-            const int kp = w.kpred[c];
-            PMap lm = pmap_id();
+            sum += a[q];
+            mx = fmax(mx, a[q]);
+            bad |= !(a[q] >= 0.0) || !isfinite(a[q]);
+        }
+        if (wr) {
+#pragma unroll
+            for (int q = 0; q < kSeqPerLane; q += 2)
+                *reinterpret_cast<double2 *>(b + j0 + q) = make_double2(a[q], a[q + 1]);
+        }
+        PMap lm = pmap_id();
+        if (kp != kNoGrid) {
+#pragma unroll
+            for (int q = 0; q < kSeqPerLane; ++q) lm = pmap_then(lm, pmap_elem(to_units(a[q], kp)));
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+        }
+        if (kp != kNoGrid) lm = warp_scan_pmap(lm);
+        if (lane == 31) {
+            w.A[c] = sum;
+            w.vmax[c] = mx;
+            if (bad) w.neg[r] = 4;
             if (kp != kNoGrid) {
-#pragma unroll
-                for (int t = 0; t < kSeqPerLane; ++t) lm = pmap_then(lm, pmap_elem(to_units(a[t], kp)));
+                w.q0[c] = lm.i0;
+                w.q1[c] = lm.i1;
             }
-#pragma unroll
-            for (int d = 16; d; d >>= 1) {
-                sum += __shfl_xor_sync(0xffffffffu, sum, d);
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-                bad |= __shfl_xor_sync(0xffffffffu, bad, d);
-            }
-            if (kp != kNoGrid) lm = warp_scan_pmap(lm);
-            if (lane == 31) {
-                w.A[c] = sum;
-                w.vmax[c] = mx;
-                if (bad) w.neg[r] = 4;
-                if (kp != kNoGrid) {
-                    w.q0[c] = lm.i0;
-                    w.q1[c] = lm.i1;
-                }
-                kmap[c] = kp;
-            }
+            kmap[c] = kp;
         }
     }
 }
@@ -748,7 +767,8 @@ __global__ void k_kpp_update_map(const double *__restrict__ x, int64_t n, int k,
 // one warp per chunk: rebuild the parity map of every chunk whose predicted grid differs from
 // the one its map was built on (k_kpp_update_map's speculation missed)
 __global__ void k_seq_chunkmap_fix(SegView v, SeqWork w, int32_t *__restrict__ kmap,
-                                   const int64_t *__restrict__ pn) {
+                                   const int64_t *__restrict__ pn,
+                                   unsigned long long *__restrict__ stats) {
     const int64_t nchunks = *pn;
     const int lane = threadIdx.x & 31;
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -770,6 +790,7 @@ __global__ void k_seq_chunkmap_fix(SegView v, SeqWork w, int32_t *__restrict__ k
             w.q0[c] = tot.i0;
             w.q1[c] = tot.i1;
             kmap[c] = kp;
+            if (stats) atomicAdd(stats, 1ull);
         }
     }
 }
@@ -1972,7 +1993,13 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     // no chunk map of this call yet (0x7f7f7f7f is no grid exponent and not kNoGrid)
     SC_CUDA(cudaMemsetAsync(km->d_kmap, 0x7f, (size_t)nch * 4, s));
     const bool fused1d = km->l == 1 && getenv("SC_KPP_CLASSIC") == nullptr;
-    const int gu = grid_1d(km, cps * 32, 256);
+    // SC_KPP_STATS: count the chunk maps the fix-up pass had to rebuild (diagnostics)
+    unsigned long long *d_stats = nullptr;
+    if (getenv("SC_KPP_STATS")) {
+        SC_CUDA(cudaMallocAsync((void **)&d_stats, 8, s));
+        SC_CUDA(cudaMemsetAsync(d_stats, 0, 8, s));
+    }
+    const int gu = grid_1d(km, cps * R * 32, 256);
     for (int i = smin; i < k; ++i) {
         k_kpp_round_on<<<(R + 127) / 128, 128, 0, s>>>(R, i, km->d_start, km->d_on,
                                                        km->d_round_on, km->d_neg);
@@ -1982,7 +2009,7 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
                                                 km->d_on, km->d_round_on, km->d_best, w,
                                                 km->d_kmap, cps, R);
             k_seq_predict<<<R, 32 * kPredictWarps, 0, s>>>(v, w);
-            k_seq_chunkmap_fix<<<gw, 256, 0, s>>>(v, w, km->d_kmap, km->d_nchunks);
+            k_seq_chunkmap_fix<<<gw, 256, 0, s>>>(v, w, km->d_kmap, km->d_nchunks, d_stats);
             k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
             k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
                             kComposeSmem, s>>>(v, w, 2);
@@ -2005,6 +2032,13 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     SC_CUDA(cudaMemcpyAsync(chosen, km->d_chosen, (size_t)R * k * 8, cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaMemcpyAsync(degenerate_out, km->d_degen, (size_t)R * 4, cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
+    if (d_stats) {
+        unsigned long long h = 0;
+        cudaMemcpy(&h, d_stats, 8, cudaMemcpyDeviceToHost);
+        cudaFree(d_stats);
+        fprintf(stderr, "[kpp] rounds %d..%d, R=%d, chunks %lld: chunk maps rebuilt %llu (%.2f per round per restart)\n",
+                smin, k - 1, R, (long long)cps, h, (double)h / std::max(1, k - smin) / R);
+    }
     return SC_OK;
 }
 

@@ -18,3 +18,14 @@ with KMeans1D(x) as km:
     t = time.perf_counter()
     km.seed_centers(k, 3, 10)
     print(f"n={n} k={k} scale={sc}: {1e3 * (time.perf_counter() - t):.1f} ms", flush=True)
+
+if len(sys.argv) > 4 and sys.argv[4] == "check":
+    # the oracle's own k-means++ (oracle/sc_oracle.c orc_kmeanspp + host draws) per restart
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    from paper_2310_10939_b200.generate import rng_for
+
+    with KMeans1D(x) as km:
+        ch = km.seed_centers(k, 3, 10)
+    ok = all(np.array_equal(ch[r], O.kmeanspp_indices(x, k, rng_for(3, r))) for r in range(10))
+    print(f"oracle check n={n} k={k} scale={sc}: identical={ok}", flush=True)
