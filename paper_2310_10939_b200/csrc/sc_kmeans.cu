@@ -203,6 +203,8 @@ struct SeqWork {
 };
 
 constexpr int kSuper = 32;
+constexpr int kNoMap = 0x7f7f7f7f;  // k-means++ kmap: no valid chunk map (no grid exponent)
+constexpr int kMaxKppR = 64;        // restarts of the one-pass k-means++ round
 // stride of a restart's k-means++ weights: n rounded up to whole super-chunks
 constexpr int64_t kppStrideAlign = (int64_t)kSuper * kSeqChunk;
 __host__ __device__ __forceinline__ int64_t kpp_stride(int64_t n) {
@@ -318,14 +320,15 @@ constexpr int kPredictWarps = 8;
 // one CTA per segment: each warp takes a contiguous share of the segment's chunks, the
 // warps' approximate totals are scanned in shared memory, then every warp walks its share
 // from its carry (approximate prefixes: they only steer the prediction, compose re-checks)
-__global__ void __launch_bounds__(32 * kPredictWarps) k_seq_predict(SegView v, SeqWork w) {
+template <int PW = kPredictWarps>
+__global__ void __launch_bounds__(32 * PW) k_seq_predict(SegView v, SeqWork w) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int s = blockIdx.x;
     if (s >= v.S || !seg_on(v, s)) return;
     const int64_t c0s = v.cofs[s], c1s = v.cofs[s + 1];
-    const int64_t per = ((c1s - c0s + kPredictWarps - 1) / kPredictWarps + 31) / 32 * 32;
+    const int64_t per = ((c1s - c0s + PW - 1) / PW + 31) / 32 * 32;
     const int64_t c0 = min(c1s, c0s + wid * per), c1 = min(c1s, c0 + per);
-    __shared__ double part[kPredictWarps];
+    __shared__ double part[PW];
     double tot = 0.0;
     for (int64_t c = c0 + lane; c < c1; c += 32) tot += w.A[c];
 #pragma unroll
@@ -471,6 +474,22 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
         return;
     }
     int64_t c = c0, blk = -1, blk_end = -1;
+    // super metadata of the next 32 supers, loaded one step ahead (a full super step then
+    // costs one memory latency less)
+    int64_t pfG = -1;
+    int pf_kp = kNoGrid;
+    int64_t pf_q0 = 0, pf_q1 = 0;
+    double pf_vm = 0.0;
+    auto super_meta = [&](int64_t G0) {
+        const int64_t Gl = G0 + lane;
+        if ((Gl + 1) * kSuper <= c1) {
+            pf_kp = w.skp[Gl];
+            pf_q0 = w.sq0[Gl];
+            pf_q1 = w.sq1[Gl];
+            pf_vm = w.svmax[Gl];
+        }
+        pfG = G0;
+    };
     while (c < c1) {
         if ((c & (kSuper - 1)) == 0 && c + kSuper <= c1) {
             // super step: up to 32 super-chunks (1024 chunks) on the current grid at once
@@ -478,14 +497,19 @@ __global__ void __launch_bounds__(32 * kComposeWarps) k_seq_compose(SegView v, S
             const int64_t S0 = (int64_t)to_units(run, g.k);
             const int64_t G = c / kSuper + lane;
             const bool valid = (G + 1) * kSuper <= c1;
+            if (pfG != c / kSuper) super_meta(c / kSuper);
+            const int m_kp = pf_kp;
+            const int64_t m_q0 = pf_q0, m_q1 = pf_q1;
+            const double m_vm = pf_vm;
+            super_meta(c / kSuper + 32);  // in flight during this step
             bool ok = false;
             PMap m = pmap_id();
             double vmu = 0.0;
-            if (valid && g.top == (int64_t(1) << 53) && w.skp[G] == g.k) {
-                m = PMap{w.sq0[G], w.sq1[G]};
-                vmu = to_units(w.svmax[G], g.k);
+            if (valid && g.top == (int64_t(1) << 53) && m_kp == g.k) {
+                m = PMap{m_q0, m_q1};
+                vmu = to_units(m_vm, g.k);
                 ok = true;
-            } else if (valid && w.svmax[G] == 0.0) {
+            } else if (valid && m_vm == 0.0) {
                 ok = true;  // all zeros (elements are >= 0 here): fl(s + 0) = s, any grid
             }
             const PMap excl = warp_exclusive(warp_scan_pmap(m));
@@ -695,16 +719,27 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nb = kpp_stride(n);
+    // per-restart state once per block (no dependent global loads in the task loop)
+    __shared__ int s_mode[kMaxKppR];  // 0 off, 1 on without a new centre, 2 update
+    __shared__ double s_cn[kMaxKppR];
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        const bool ro = round_on[r] != 0;
+        const bool upd = ro && on[r] && i - 1 >= start[r];
+        s_mode[r] = ro ? (upd ? 2 : 1) : 0;
+        s_cn[r] = upd ? __ldg(x + chosen[(int64_t)r * k + i - 1]) : 0.0;
+    }
+    __syncthreads();
     // task t = (chunk position cc, restart r), r fastest: the R warps of one chunk position
     // read the same x lines (one HBM read, the rest from L1/L2)
     for (int64_t t = wid; t < cps * R; t += nw) {
         const int64_t cc = t / R;
         const int r = (int)(t - cc * R);
-        if (!round_on[r]) continue;
+        const int mode = s_mode[r];
+        if (!mode) continue;
         const int64_t j0 = cc * kSeqChunk + lane * kSeqPerLane;
         const int64_t c = (int64_t)r * cps + cc;
-        const bool upd = on[r] && i - 1 >= start[r];
-        const double cn = upd ? __ldg(x + chosen[(int64_t)r * k + i - 1]) : 0.0;
+        const bool upd = mode == 2;
+        const double cn = s_cn[r];
         double *b = best + (int64_t)r * nb;
         const int kp = w.kpred[c];
         double a[kSeqPerLane], xv[kSeqPerLane];
@@ -715,8 +750,18 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
             a[q + 1] = bb.y;
         }
         if (upd) {
+            // (x holds n doubles: vector loads only for chunks wholly inside [0, n))
+            if (j0 + kSeqPerLane <= n) {
 #pragma unroll
-            for (int q = 0; q < kSeqPerLane; ++q) xv[q] = j0 + q < n ? __ldg(x + j0 + q) : 0.0;
+                for (int q = 0; q < kSeqPerLane; q += 2) {
+                    const double2 xx = __ldg(reinterpret_cast<const double2 *>(x + j0 + q));
+                    xv[q] = xx.x;
+                    xv[q + 1] = xx.y;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kSeqPerLane; ++q) xv[q] = j0 + q < n ? __ldg(x + j0 + q) : 0.0;
+            }
         }
         double sum = 0.0, mx = 0.0;
         int bad = 0;
@@ -739,8 +784,11 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
             for (int q = 0; q < kSeqPerLane; q += 2)
                 *reinterpret_cast<double2 *>(b + j0 + q) = make_double2(a[q], a[q + 1]);
         }
+        // a chunk none of whose weights changed keeps its map if it was built on kp already
+        const bool changed = __any_sync(0xffffffffu, wr);
+        const bool need_map = kp != kNoGrid && (changed || kmap[c] != kp);
         PMap lm = pmap_id();
-        if (kp != kNoGrid) {
+        if (need_map) {
 #pragma unroll
             for (int q = 0; q < kSeqPerLane; ++q) lm = pmap_then(lm, pmap_elem(to_units(a[q], kp)));
         }
@@ -750,16 +798,18 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
             bad |= __shfl_xor_sync(0xffffffffu, bad, d);
         }
-        if (kp != kNoGrid) lm = warp_scan_pmap(lm);
+        if (need_map) lm = warp_scan_pmap(lm);
         if (lane == 31) {
             w.A[c] = sum;
             w.vmax[c] = mx;
             if (bad) w.neg[r] = 4;
-            if (kp != kNoGrid) {
+            if (need_map) {
                 w.q0[c] = lm.i0;
                 w.q1[c] = lm.i1;
+                kmap[c] = kp;
+            } else if (changed) {
+                kmap[c] = kNoMap;  // the old map no longer describes the chunk
             }
-            kmap[c] = kp;
         }
     }
 }
@@ -773,24 +823,37 @@ __global__ void k_seq_chunkmap_fix(SegView v, SeqWork w, int32_t *__restrict__ k
     const int lane = threadIdx.x & 31;
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t c = wid; c < nchunks; c += nw) {
-        const int kp = w.kpred[c];
-        if (kp == kNoGrid || kp == kmap[c]) continue;
-        const int s = seg_of_chunk(v, c);
-        if (!seg_on(v, s)) continue;
-        double a[kSeqPerLane];
-        int64_t first;
-        const int m = load_chunk(v, s, c, a, first);
-        PMap lm = pmap_id();
+    // 32 chunks per warp step: each lane checks one, then the warp rebuilds the misses
+    for (int64_t c0 = wid * 32; c0 < nchunks; c0 += nw * 32) {
+        const int64_t cl = c0 + lane;
+        int kpl = kNoGrid;
+        bool miss = false;
+        if (cl < nchunks) {
+            kpl = w.kpred[cl];
+            miss = kpl != kNoGrid && kpl != kmap[cl];
+        }
+        unsigned mm = __ballot_sync(0xffffffffu, miss);
+        while (mm) {
+            const int b = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const int64_t c = c0 + b;
+            const int kp = __shfl_sync(0xffffffffu, kpl, b);
+            const int s = seg_of_chunk(v, c);
+            if (!seg_on(v, s)) continue;
+            double a[kSeqPerLane];
+            int64_t first;
+            const int m = load_chunk(v, s, c, a, first);
+            PMap lm = pmap_id();
 #pragma unroll
-        for (int t = 0; t < kSeqPerLane; ++t)
-            if (lane * kSeqPerLane + t < m) lm = pmap_then(lm, pmap_elem(to_units(a[t], kp)));
-        const PMap tot = warp_scan_pmap(lm);
-        if (lane == 31) {
-            w.q0[c] = tot.i0;
-            w.q1[c] = tot.i1;
-            kmap[c] = kp;
-            if (stats) atomicAdd(stats, 1ull);
+            for (int t = 0; t < kSeqPerLane; ++t)
+                if (lane * kSeqPerLane + t < m) lm = pmap_then(lm, pmap_elem(to_units(a[t], kp)));
+            const PMap tot = warp_scan_pmap(lm);
+            if (lane == 31) {
+                w.q0[c] = tot.i0;
+                w.q1[c] = tot.i1;
+                kmap[c] = kp;
+                if (stats) atomicAdd(stats, 1ull);
+            }
         }
     }
 }
@@ -1992,7 +2055,7 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     SC_CUDA(cudaGetLastError());
     // no chunk map of this call yet (0x7f7f7f7f is no grid exponent and not kNoGrid)
     SC_CUDA(cudaMemsetAsync(km->d_kmap, 0x7f, (size_t)nch * 4, s));
-    const bool fused1d = km->l == 1 && getenv("SC_KPP_CLASSIC") == nullptr;
+    const bool fused1d = km->l == 1 && R <= kMaxKppR && getenv("SC_KPP_CLASSIC") == nullptr;
     // SC_KPP_STATS: count the chunk maps the fix-up pass had to rebuild (diagnostics)
     unsigned long long *d_stats = nullptr;
     if (getenv("SC_KPP_STATS")) {
@@ -2008,8 +2071,9 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
             k_kpp_update_map<<<gu, 256, 0, s>>>(km->d_x, n, k, i, km->d_chosen, km->d_start,
                                                 km->d_on, km->d_round_on, km->d_best, w,
                                                 km->d_kmap, cps, R);
-            k_seq_predict<<<R, 32 * kPredictWarps, 0, s>>>(v, w);
-            k_seq_chunkmap_fix<<<gw, 256, 0, s>>>(v, w, km->d_kmap, km->d_nchunks, d_stats);
+            k_seq_predict<32><<<R, 32 * 32, 0, s>>>(v, w);
+            k_seq_chunkmap_fix<<<grid_1d(km, nch, 256), 256, 0, s>>>(v, w, km->d_kmap,
+                                                                    km->d_nchunks, d_stats);
             k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
             k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
                             kComposeSmem, s>>>(v, w, 2);
@@ -2019,7 +2083,7 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
             k_kpp_update_sum<<<gw, 256, 0, s>>>(km->d_x, n, km->l, k, i, km->d_chosen,
                                                 km->d_start, km->d_on, km->d_round_on,
                                                 km->d_best, w, cps, R);
-            k_seq_predict<<<R, 32 * kPredictWarps, 0, s>>>(v, w);
+            k_seq_predict<><<<R, 32 * kPredictWarps, 0, s>>>(v, w);
             k_seq_chunkmap<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
             k_seq_superize<<<gw, 256, 0, s>>>(v, w, km->d_nchunks);
             k_seq_compose<<<(R + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
@@ -2253,7 +2317,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
             SC_CUDA(cudaMemsetAsync(km->d_neg, 0, (size_t)nseg * 4, s));
             k_seq_summarize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
             k_seq_flip<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
-            k_seq_predict<<<nseg, 32 * kPredictWarps, 0, s>>>(vm, wm);
+            k_seq_predict<><<<nseg, 32 * kPredictWarps, 0, s>>>(vm, wm);
             k_seq_chunkmap<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
             k_seq_superize<<<gwm, 256, 0, s>>>(vm, wm, km->d_nchunks);
             k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps,
@@ -2725,7 +2789,7 @@ static int32_t seqsum_device(const double *d_vals, int32_t nseg, const int64_t *
         const int gs = (nseg * 32 + 255) / 256;
         k_seq_summarize<<<gw, 256>>>(v, w, d_nch);
         k_seq_flip<<<gw, 256>>>(v, w, d_nch);
-        k_seq_predict<<<nseg, 32 * kPredictWarps>>>(v, w);
+        k_seq_predict<><<<nseg, 32 * kPredictWarps>>>(v, w);
         k_seq_chunkmap<<<gw, 256>>>(v, w, d_nch);
         k_seq_superize<<<gw, 256>>>(v, w, d_nch);
         k_seq_compose<<<(nseg + kComposeWarps - 1) / kComposeWarps, 32 * kComposeWarps, kComposeSmem>>>(
