@@ -763,8 +763,11 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
                 for (int q = 0; q < kSeqPerLane; ++q) xv[q] = j0 + q < n ? __ldg(x + j0 + q) : 0.0;
             }
         }
-        double sum = 0.0, mx = 0.0;
-        int bad = 0;
+        // chunk summaries in fp32: the sum only steers the prediction, and the max is
+        // rounded UP, so it stays an upper bound (all the exact walk needs); a zero chunk
+        // keeps a zero max.  Half the shuffle traffic of fp64 reductions.
+        float sum = 0.f, mx = 0.f;
+        bool bad = false;
         bool wr = false;
 #pragma unroll
         for (int q = 0; q < kSeqPerLane; ++q) {
@@ -775,8 +778,8 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
                     wr = true;
                 }
             }
-            sum += a[q];
-            mx = fmax(mx, a[q]);
+            sum += __double2float_rn(a[q]);
+            mx = fmaxf(mx, __double2float_ru(a[q]));
             bad |= !(a[q] >= 0.0) || !isfinite(a[q]);
         }
         if (wr) {
@@ -795,14 +798,14 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
 #pragma unroll
         for (int d = 16; d; d >>= 1) {
             sum += __shfl_xor_sync(0xffffffffu, sum, d);
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-            bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
         }
+        const bool anybad = __any_sync(0xffffffffu, bad);
         if (need_map) lm = warp_scan_pmap(lm);
         if (lane == 31) {
-            w.A[c] = sum;
-            w.vmax[c] = mx;
-            if (bad) w.neg[r] = 4;
+            w.A[c] = (double)sum;
+            w.vmax[c] = (double)mx;
+            if (anybad) w.neg[r] = 4;
             if (need_map) {
                 w.q0[c] = lm.i0;
                 w.q1[c] = lm.i1;
