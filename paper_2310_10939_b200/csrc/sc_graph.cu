@@ -67,6 +67,7 @@ constexpr int kSlice = 32;         // rows per slice (one per lane)
 constexpr int kSigma = 4096;       // sorting window (rows)
 constexpr int kSellMax = 256;      // longer rows are laid out first, globally length-sorted
 constexpr int kExtreme = kSellMax;  // longer rows ("wide") get one warp each
+constexpr int64_t kWideKeyMax = int64_t(1) << 24;  // wide rows are ordered by min(length, this)
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry of a slice
 constexpr int kStepTPB = 256;      // 8 warps per CTA
 constexpr int kUnroll = 8;         // slice steps in flight per lane
@@ -565,14 +566,15 @@ __global__ void k_finish_stats(int64_t *stats, int64_t n) {
     stats[3] = n - stats[6];
 }
 
-// sort key of the SELL renumbering: (window, kSellMax - length); wide rows after every window
+// sort key of the SELL renumbering: (window, kSellMax - length); wide rows after every window,
+// by decreasing length (sell_order's order exactly)
 __global__ void k_sell_keys(const int64_t *__restrict__ rp, int64_t n, int64_t sigma, int64_t nwin,
                             uint32_t *__restrict__ keys, int32_t *__restrict__ iota) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
          r += (int64_t)gridDim.x * blockDim.x) {
         const int64_t len = rp[r + 1] - rp[r];
         keys[r] = len <= kSellMax ? (uint32_t)((r / sigma) * 512 + (kSellMax - len))
-                                  : (uint32_t)(nwin * 512);
+                                  : (uint32_t)(nwin * 512 + (kWideKeyMax - (len < kWideKeyMax ? len : kWideKeyMax)));
         iota[r] = (int32_t)r;
     }
 }
@@ -650,7 +652,7 @@ __global__ void k_sell_keys_ord(const int64_t *__restrict__ rp, const int32_t *_
         const int32_t r = ord[p];
         const int64_t len = rp[r + 1] - rp[r];
         keys[p] = len <= kSellMax ? (uint32_t)((p / sigma) * 512 + (kSellMax - len))
-                                  : (uint32_t)(nwin * 512);
+                                  : (uint32_t)(nwin * 512 + (kWideKeyMax - (len < kWideKeyMax ? len : kWideKeyMax)));
         payload[p] = r;
     }
 }
@@ -953,7 +955,9 @@ static int32_t dmalloc(sc_graph *g, void **p, size_t bytes) {
 //      sorting packs rows of similar length into a slice (little padding);
 //   2. every window of kSigma rows: rows of length <= kSellMax in decreasing length
 //      (counting sort, stable) -- keeps the columns' locality;
-//   3. extreme rows (len > kExtreme) in original order: one warp per row.
+//   3. extreme rows (len > kExtreme) by decreasing length (stable; lengths saturate at
+//      kWideKeyMax): one warp per row, so the longest in-order folds start first instead of
+//      forming the tail of the wide-row kernel.
 // Returns the number of rows laid out as SELL slices (groups 1 + 2).
 static int64_t sell_order(const int64_t *rp, int64_t n, std::vector<int32_t> &perm) {
     perm.resize((size_t)n);
@@ -1007,8 +1011,16 @@ static int64_t sell_order(const int64_t *rp, int64_t n, std::vector<int32_t> &pe
         pos += acc;
     }
     const int64_t n_sell = pos;
-    for (int64_t r = 0; r < n; ++r)
-        if (rp[r + 1] - rp[r] > kExtreme) perm[(size_t)pos++] = (int32_t)r;
+    std::vector<std::pair<int64_t, int32_t>> ext;
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t len = rp[r + 1] - rp[r];
+        if (len > kExtreme) ext.emplace_back(-std::min<int64_t>(len, kWideKeyMax), (int32_t)r);
+    }
+    std::stable_sort(ext.begin(), ext.end(),
+                     [](const std::pair<int64_t, int32_t> &a, const std::pair<int64_t, int32_t> &b) {
+                         return a.first < b.first;
+                     });
+    for (auto &pr : ext) perm[(size_t)pos++] = pr.second;
     return n_sell;
 }
 
@@ -1258,7 +1270,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->bfs_nwin = nwin;
 
     int end_bit = 1;
-    while ((int64_t(1) << end_bit) <= (nwin + 1) * 512) ++end_bit;
+    while ((int64_t(1) << end_bit) <= nwin * 512 + kWideKeyMax) ++end_bit;
     if (!e) e = cudaMallocAsync((void **)&t_keys, (size_t)n * 4, s);
     if (!e) e = cudaMallocAsync((void **)&t_keys2, (size_t)n * 4, s);
     if (!e) e = cudaMallocAsync((void **)&t_iota, (size_t)n * 4, s);
