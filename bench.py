@@ -160,6 +160,44 @@ def cpu_baseline(g, T, k, threads, cfg=2):
     return out
 
 
+def reference_python_sample(g, T, k, x0, f_dev):
+    """The reference's OWN numpy/scipy path (the unmodified package installed into
+    baseline/_ref with `pip install --no-deps --target baseline/_ref`), timed on this host:
+    power_method with the rw operator `0.5*x + 0.5*(A @ (x/d))` (spectral.py:87-102, scipy
+    csr_matvec, one core) for all T steps from the device's Irwin-Hall x0, then ONE restart of
+    its lloyd (kmeans.py:167-215) on the resulting embedding; the 10-restart time is that
+    restart x 10 (restarts are independent).  Also checks the device's f against the
+    reference's own f bit for bit.  None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "specluster")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from specluster.graph import Graph as RGraph
+    from specluster.kmeans import PointSet, lloyd
+    from specluster.pipeline import _kmeans_seed
+    from specluster.spectral import power_method
+
+    w = np.ones(g.nnz) if g.weights is None else g.weights
+    rg = RGraph(g.n, g.row_offsets, g.col_indices, w, g.degrees)
+    A, d = rg.adjacency_csr(), g.degrees
+    t0 = time.perf_counter()
+    xT = power_method(lambda x: 0.5 * x + 0.5 * (A @ (x / d)), x0, T)
+    t1 = time.perf_counter()
+    f = xT / d
+    part = lloyd(PointSet(f[:, None]), k, _kmeans_seed(0), restarts=1)
+    t2 = time.perf_counter()
+    power_s, km1_s = t1 - t0, t2 - t1
+    est = power_s + 10 * km1_s
+    return {"value": g.nnz * T / est / 1e9, "unit": UNIT, "cores": 1, "kind": "reference",
+            "power_s": power_s, "power_only_value": g.nnz * T / power_s / 1e9,
+            "kmeans_1restart_s": km1_s, "est_total_s": est,
+            "f_bit_identical_to_device": bool(np.array_equal(f, f_dev)),
+            "sample": f"specluster (reference package, baseline/_ref): power_method {T} rw steps "
+                      f"(scipy, 1 core) + lloyd with 1 of the 10 restarts; total = power + 10 x "
+                      f"that restart"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -388,6 +426,15 @@ def run_b200(args):
         line["weighted_kernel"] = weighted
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(g, T, k, os.cpu_count() or 1, args.config)
+        if args.config in (1, 2) and not devs:
+            try:
+                with DeviceGraph(g) as dx:
+                    x0 = dx.sample_irwin_hall(0, return_host=True)
+                rp = reference_python_sample(g, T, k, x0, res.embedding.data[:, 0])
+                if rp:
+                    line["cpu_baseline"]["reference_python"] = rp
+            except Exception as e:  # noqa: BLE001 -- the extra baseline never fails the bench
+                line["cpu_baseline"]["reference_python"] = {"error": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
 
 
