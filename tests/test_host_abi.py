@@ -134,3 +134,44 @@ def test_from_edges_semantics():
         from_edges(4, [0], [1])  # isolated vertices
     g2 = from_csr(3, [0, 1, 3, 4], [1, 0, 2, 1])
     assert g2.unit_weights() and g2.degrees.tolist() == [1.0, 2.0, 1.0]
+
+
+def test_multi_gpu_handle_rejects_bad_input_without_gpu():
+    """sc_graph_create_multi validates its arguments before touching a device."""
+    L = _lib.load()
+    rp = np.array([0, 1, 2, 3, 4], dtype=np.int64)
+    col = np.array([1, 0, 3, 2], dtype=np.int32)
+    deg = np.ones(4)
+    h = ctypes.c_void_p()
+    args = (_lib.ptr(rp), _lib.ptr(col), None, _lib.ptr(deg), 4, 4)
+    assert L.sc_graph_create_multi(*args, 0, None, 0, ctypes.byref(h)) == -1   # n_gpus < 1
+    assert L.sc_graph_create_multi(*args, 5, None, 0, ctypes.byref(h)) == -1   # n < n_gpus
+    assert L.sc_graph_create_multi(*args, 2, None, _lib.SC_CREATE_REORDER_BFS,
+                                   ctypes.byref(h)) == -1                       # BFS: 1 GPU only
+    rp_bad = np.array([0, 1, 2, 3, 5], dtype=np.int64)
+    assert L.sc_graph_create_multi(_lib.ptr(rp_bad), _lib.ptr(col), None, _lib.ptr(deg), 4, 4,
+                                   2, None, 0, ctypes.byref(h)) == -2
+    assert L.sc_kmeans_set_flags(None, 0) == -1
+    with pytest.raises(InputError):
+        SpectralParams(k=3, gpus=0)
+    assert SpectralParams(k=3).cost_assert is None and SpectralParams(k=3).gpus == 1
+
+
+def test_bench_helpers():
+    """bench.py: bounded CPU samples above config 2, ncu traffic keyed by layout + pre-order"""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+
+    class G:
+        nnz = 1_800_041_874
+
+    assert bench.cpu_sample_steps(G, 100, 5) == (66, False)
+    assert bench.cpu_sample_steps(G, 100, 2) == (100, True)
+    assert bench.traffic_from_profiles(4, False, "sell", "bfs") is not None
+    assert bench.traffic_from_profiles(5, True, "sell", "none") is not None
+    assert bench.traffic_from_profiles(2, True, "panels", "none") is not None
