@@ -265,6 +265,14 @@ int32_t sc_generate_dcsbm(int64_t n, const int64_t *block_offsets, int32_t nbloc
 /* graph handle straight from a device-resident CSR (the column array is not copied to the
  * host; the handle does not keep a reference to h) */
 int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_graph **out);
+/* Row-block shard [row_lo, row_hi) straight from a device-resident CSR of the WHOLE graph on
+ * this device (e.g. a device generator's output: every rank generates the graph and keeps its
+ * rows, so no column ever visits the host); columns are renamed on the device through
+ * d_slot_of (device, n int32: global vertex -> z slot of the shard plan).  ncols / col_offset
+ * as sc_shard_create.  The CSR may be destroyed after the call. */
+int32_t sc_shard_create_from_csr(const sc_csr *h, int64_t row_lo, int64_t row_hi,
+                                 const int32_t *d_slot_of, int64_t ncols, int64_t col_offset,
+                                 sc_graph **out);
 
 /* ---- 1-D k-means replica ------------------------------------------------ */
 /* points: host f (n doubles) or, with _from_graph, the f left on the device by the last

@@ -59,7 +59,7 @@ EXPORTS = (
     "sc_keyed_sums", "sc_contingency", "sc_cut_sums", "sc_power_iterate_block",
     "sc_kmeans_create_nd", "sc_kmeans_lloyd_sorted", "sc_release_cached_memory",
     "sc_gather_f64", "sc_graph_build_panels", "sc_graph_download_f", "sc_kmeans_set_flags",
-    "sc_graph_create_multi", "sc_graph_shard_layout",
+    "sc_graph_create_multi", "sc_graph_shard_layout", "sc_shard_create_from_csr",
 )
 
 _lib = None
@@ -105,6 +105,7 @@ def load() -> ctypes.CDLL:
         "sc_kmeans_set_flags": ([P, u32], i32),
         "sc_graph_create_multi": ([P, P, P, P, i64, i64, i32, P, u32, PP], i32),
         "sc_graph_shard_layout": ([P, i32, P, P, P, P], i32),
+        "sc_shard_create_from_csr": ([P, i64, i64, P, i64, i64, PP], i32),
         "sc_seqsum": ([P, i32, P, i32, P, P], i32),
         "sc_sell_order": ([P, i64, P], i32),
         "sc_graph_create_ex": ([P, P, P, P, i64, i64, i32, u32, PP], i32),

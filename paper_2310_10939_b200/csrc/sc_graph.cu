@@ -665,6 +665,23 @@ __global__ void k_wide_lens(const int64_t *__restrict__ rp, const int32_t *__res
         len[w] = w < n_wide ? rp[wperm[w] + 1] - rp[wperm[w]] : 0;
 }
 
+// out[i] = slot_of[col[i]] (global vertex -> z slot of a multi-GPU plan); *bad = 1 on an
+// out-of-range column
+__global__ void k_rename_cols(const int32_t *__restrict__ col, int64_t m,
+                              const int32_t *__restrict__ slot_of, int64_t n,
+                              int32_t *__restrict__ out, int32_t *__restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = col[i];
+        if ((uint32_t)c >= (uint64_t)n) {
+            *bad = 1;
+            out[i] = 0;
+        } else {
+            out[i] = __ldg(slot_of + c);
+        }
+    }
+}
+
 // flag[0] = 1 if any column index is outside [0, ncols)
 __global__ void k_col_range(const int32_t *__restrict__ col, int64_t nnz, int64_t ncols,
                             int32_t *__restrict__ flag) {
@@ -1612,6 +1629,59 @@ int32_t sc_graph_create_from_csr(const sc_csr *h, uint32_t create_flags, sc_grap
     SC_CUDA(cudaMemcpy(deg.data(), d_deg, (size_t)n * 8, cudaMemcpyDeviceToHost));
     return graph_init(rp.data(), nullptr, nullptr, deg.data(), n, nnz, n, 0, 0, 1, create_flags,
                       device, out, d_col, d_val);
+}
+
+int32_t sc_shard_create_from_csr(const sc_csr *h, int64_t row_lo, int64_t row_hi,
+                                 const int32_t *d_slot_of, int64_t ncols, int64_t col_offset,
+                                 sc_graph **out) {
+    SC_REQUIRE(h && d_slot_of && out, SC_E_INVALID, "null argument");
+    int64_t n = 0, nnz = 0;
+    int32_t st = sc_csr_info(h, &n, &nnz, nullptr);
+    if (st) return st;
+    SC_REQUIRE(0 <= row_lo && row_lo < row_hi && row_hi <= n, SC_E_RANGE,
+               "row range [%lld, %lld) outside [0, %lld)", (long long)row_lo, (long long)row_hi,
+               (long long)n);
+    const int64_t *d_rp;
+    const int32_t *d_col;
+    const double *d_deg, *d_val;
+    int32_t device;
+    if ((st = sc::csr_device_arrays(h, &d_rp, &d_col, &d_deg, &d_val, &device))) return st;
+    SC_CUDA(cudaSetDevice(device));
+    const int64_t nl = row_hi - row_lo;
+    std::vector<int64_t> rp((size_t)nl + 1);
+    std::vector<double> deg((size_t)nl);
+    SC_CUDA(cudaMemcpy(rp.data(), d_rp + row_lo, (size_t)(nl + 1) * 8, cudaMemcpyDeviceToHost));
+    SC_CUDA(cudaMemcpy(deg.data(), d_deg + row_lo, (size_t)nl * 8, cudaMemcpyDeviceToHost));
+    const int64_t e0 = rp[0];
+    for (auto &v : rp) v -= e0;
+    const int64_t nnzl = rp[(size_t)nl];
+    // the block's columns renamed into the z space on the device (range-checked there)
+    int32_t *d_ren = nullptr;
+    int32_t *d_bad = nullptr;
+    SC_CUDA(cudaMalloc((void **)&d_ren, (size_t)std::max<int64_t>(nnzl, 1) * 4));
+    cudaError_t e = cudaMalloc((void **)&d_bad, 4);
+    if (!e) e = cudaMemset(d_bad, 0, 4);
+    if (!e && nnzl) {
+        sc::k_rename_cols<<<(unsigned)std::min<int64_t>((nnzl + 255) / 256, 148 * 16), 256>>>(
+            d_col + e0, nnzl, d_slot_of, n, d_ren, d_bad);
+        e = cudaGetLastError();
+    }
+    int32_t bad = 0;
+    if (!e) e = cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost);
+    cudaFree(d_bad);
+    if (e) {
+        cudaFree(d_ren);
+        return fail(SC_E_CUDA, "shard column renaming: %s", cudaGetErrorString(e));
+    }
+    if (bad) {
+        cudaFree(d_ren);
+        return fail(SC_E_RANGE, "a column index is outside [0, %lld)", (long long)n);
+    }
+    st = graph_init(rp.data(), nullptr, nullptr, deg.data(), nl, nnzl, ncols, col_offset, row_lo, 0,
+                    0u, device, out, d_ren, d_val ? d_val + e0 : nullptr);
+    cudaDeviceSynchronize();
+    cudaFree(d_ren);
+    return st;
 }
 
 int64_t sc_release_cached_memory(int32_t device) {

@@ -331,6 +331,33 @@ class CudaShard:
         self.torch = torch
         self.tdev = torch.device("cuda", device)
 
+    @classmethod
+    def from_device_csr(cls, csr, plan: ShardPlan, rank: int, device: int):
+        """The rank's row block straight from a device-resident CSR of the whole graph on
+        `device` (sc_shard_create_from_csr): columns renamed on the device through the plan's
+        slot map, nothing but row offsets and degrees of the block visits the host."""
+        import torch
+
+        L = _lib.require_device()
+        self = cls.__new__(cls)
+        self.rank, self.plan, self.device = rank, plan, device
+        self.n = int(plan.sizes[rank])
+        self._keep = ()
+        slot = torch.from_numpy(plan.slot_of.astype(np.int32)).to(torch.device("cuda", device))
+        lo, hi = int(plan.starts[rank]), int(plan.starts[rank + 1])
+        h = ctypes.c_void_p()
+        _lib.check(L.sc_shard_create_from_csr(csr.handle, lo, hi, ctypes.c_void_p(slot.data_ptr()),
+                                              plan.ncols, 0, ctypes.byref(h)))
+        del slot
+        self.h = h
+        gi = _lib.GraphInfo()
+        _lib.check(L.sc_graph_info_get(h, ctypes.byref(gi)))
+        if self.n - gi.long_rows != plan.n_sells[rank]:
+            raise InputError("shard layout disagrees with the plan's SELL row count")
+        self.torch = torch
+        self.tdev = torch.device("cuda", device)
+        return self
+
     def close(self):
         if self.h:
             _lib.load().sc_graph_destroy(self.h)
@@ -672,40 +699,75 @@ def _init_dist():
     return rank, world, local
 
 
+def entry_balanced_starts(row_ptr: np.ndarray, world: int) -> np.ndarray:
+    """Row-block starts balancing stored entries (the multi-GPU handle's rule): block w starts
+    at the first row whose offset reaches w * nnz / world (each block keeps >= 1 row)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    n, nnz = rp.size - 1, int(rp[-1])
+    st = np.zeros(world + 1, dtype=np.int64)
+    st[world] = n
+    for w in range(1, world):
+        r = int(np.searchsorted(rp, nnz * w // world, side="left"))
+        st[w] = min(max(r, st[w - 1] + 1), n - (world - w))
+    return st
+
+
 def bench_main(args, metric: str, unit: str):
-    """Weak scaling: rank r owns one config-2 sized row block (1e6 rows, 10 SBM blocks) of an
-    SBM with n = N * 1e6, k = 10 N, expected in-block degree 40 and out-of-block degree 4;
-    T = 100 steps, each pipelined over P pieces with an NCCL all-gather per piece."""
+    """Default (the driver's scaling run): WEAK scaling -- rank r owns one config-2 sized row
+    block (1e6 rows, 10 SBM blocks) of an SBM with n = N * 1e6, k = 10 N, expected in-block
+    degree 40 and out-of-block degree 4; T = 100 steps, each pipelined over P pieces with an
+    NCCL all-gather per piece.  `--config 3|4|5`: STRONG scaling of that BASELINE config --
+    every rank generates the whole graph on its own GPU with the device generator, keeps its
+    entry-balanced row block (columns renamed on the device, sc_shard_create_from_csr) and
+    frees the rest; the total work is fixed as N grows."""
     import torch
     import torch.distributed as dist
 
     from .generate import SbmParams, sbm_rows
 
     rank, world, local = _init_dist()
+    strong = int(getattr(args, "config", 2)) in (3, 4, 5)
     n_loc = 10**6
     params = SbmParams(n=world * n_loc, k=10 * world, p=40 / (10**5 - 1),
                        q=4 / (world * n_loc - 10**5), seed=0)
     T = 100
     p2p = getattr(args, "comm", "nccl") == "p2p"
     halo = getattr(args, "comm", "nccl") == "halo"
+    if strong and halo:
+        raise InputError("the strong-scaling configs use the all-gather or the peer exchange")
     # Splitting a step into P pieces costs ~12 us per extra piece on one B200 (smaller grids,
     # one more collective) and hides up to (P-1)/P of the all-gather, which moves
     # (W-1) * 8 MB per GPU per step (~12 us at W = 2, ~80 us at W = 8 over NVLink): only
     # worth it for the widest runs.
     default_pieces = 2 if world >= 8 else 1
     pieces = 1 if (p2p or halo) else int(getattr(args, "pieces", 0) or default_pieces)
-    starts = np.arange(world + 1, dtype=np.int64) * n_loc
-    rp, col, deg, iso = sbm_rows(params, int(starts[rank]), int(starts[rank + 1]))
-    iso_t = torch.tensor([iso], device="cuda")
-    dist.all_reduce(iso_t)
-    if int(iso_t.item()):
-        raise InputError("isolated vertices in the scaling graph; choose another seed")
-    if halo:
-        plan = exchange_halo_plan(rp, col, starts, rank, world)
+    if strong:
+        from .generate import CONFIG_T, config_device_csr
+
+        cfg = int(args.config)
+        T = CONFIG_T[cfg]
+        with config_device_csr(cfg, 0, local) as dcsr:
+            rp_all = np.empty(dcsr.n + 1, dtype=np.int64)
+            _lib.check(_lib.load().sc_csr_download(dcsr.handle, _lib.ptr(rp_all), None, None, None))
+            starts = entry_balanced_starts(rp_all, world)
+            rp = rp_all[starts[rank]:starts[rank + 1] + 1] - rp_all[starts[rank]]
+            plan = exchange_plan(rp, starts, rank, world, pieces=pieces,
+                                 align=8192 if pieces == 1 else 1)
+            shard = CudaShard.from_device_csr(dcsr, plan, rank, local)
+        del rp_all
     else:
-        plan = exchange_plan(rp, starts, rank, world, pieces=pieces,
-                             align=8192 if pieces == 1 else 1)
-    shard = CudaShard(rp, plan.rename(col), None, deg, plan, rank, local)
+        starts = np.arange(world + 1, dtype=np.int64) * n_loc
+        rp, col, deg, iso = sbm_rows(params, int(starts[rank]), int(starts[rank + 1]))
+        iso_t = torch.tensor([iso], device="cuda")
+        dist.all_reduce(iso_t)
+        if int(iso_t.item()):
+            raise InputError("isolated vertices in the scaling graph; choose another seed")
+        if halo:
+            plan = exchange_halo_plan(rp, col, starts, rank, world)
+        else:
+            plan = exchange_plan(rp, starts, rank, world, pieces=pieces,
+                                 align=8192 if pieces == 1 else 1)
+        shard = CudaShard(rp, plan.rename(col), None, deg, plan, rank, local)
     # column panels for whole-shard steps (as the single-GPU pipeline at T >= 64); the peer
     # exchange and multi-piece steps stay on SELL
     panels = False
@@ -783,9 +845,13 @@ def bench_main(args, metric: str, unit: str):
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config2 block per GPU (SBM n={params.n}, k={params.k})",
-                       "n_per_gpu": n_loc, "nnz_total": nnz_total, "T": T, "pieces": plan.pieces,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": (f"config{args.config} (whole graph, row blocks balanced by "
+                                    "entries)" if strong else
+                                    f"config2 block per GPU (SBM n={params.n}, k={params.k})"),
+                       "n_per_gpu": int(plan.n_max) if strong else n_loc,
+                       "nnz_total": nnz_total, "T": T, "pieces": plan.pieces,
                        "spmv_layout": "panels" if panels else "sell",
                        "cuda_graph": use_graph,
                        "comm": "p2p" if p2p else "halo" if halo else "nccl",

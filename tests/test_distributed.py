@@ -270,3 +270,20 @@ def test_sbm_rows_concatenate_to_sample_sbm():
     assert np.array_equal(rp, g.row_offsets)
     assert np.array_equal(col, g.col_indices)
     assert np.array_equal(np.concatenate([pp[2] for pp in parts]), g.degrees)
+
+
+def test_entry_balanced_starts():
+    from paper_2310_10939_b200.distributed import entry_balanced_starts
+
+    rng = np.random.default_rng(0)
+    lens = rng.integers(0, 50, 1000)
+    lens[100:110] = 5000  # heavy rows
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    for world in (1, 2, 3, 8):
+        st = entry_balanced_starts(rp, world)
+        assert st[0] == 0 and st[-1] == 1000 and np.all(np.diff(st) >= 1)
+        loads = rp[st[1:]] - rp[st[:-1]]
+        assert loads.max() - loads.min() <= 2 * lens.max()
+    # every block keeps a row even when one row holds everything
+    rp = np.array([0, 10**6, 10**6, 10**6, 10**6], dtype=np.int64)
+    assert np.all(np.diff(entry_balanced_starts(rp, 4)) == 1)

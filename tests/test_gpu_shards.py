@@ -232,3 +232,51 @@ def test_peer_exchange_requires_own_buffers():
         shards[0].scale_piece(0, x, shards[0].zeros(plan.ncols))
     for s in shards:
         s.close()
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_shards_from_device_csr_bit_exact(world):
+    """The strong-scaling setup of bench_main: every rank keeps its entry-balanced row block of
+    a DEVICE-generated graph, columns renamed on the device (sc_shard_create_from_csr); a
+    weighted heavy-tailed DC-SBM with wide rows, exchange emulated by device copies."""
+    import torch
+
+    from paper_2310_10939_b200.generate import DeviceCSR
+
+    with DeviceCSR.dcsbm(120_000, 6, 3) as d:
+        g = d.download().graph
+        rp, col, val, deg = g.row_offsets, g.col_indices, g.weights, g.degrees
+        starts = D.entry_balanced_starts(rp, world)
+        lrps = [rp[starts[r]:starts[r + 1] + 1] - rp[starts[r]] for r in range(world)]
+        plan = D.ShardPlan(starts, [D.sell_order(x) for x in lrps],
+                           [D.n_sell_rows(x) for x in lrps], 1, 8192)
+        shards = [D.CudaShard.from_device_csr(d, plan, r, 0) for r in range(world)]
+    assert any(s.n > 0 for s in shards)
+    T = 9
+    z = [[s.zspace(plan.ncols), s.zspace(plan.ncols)] for s in shards]
+    x = [[s.zeros(s.n), s.zeros(s.n)] for s in shards]
+    x0 = [s.zeros(s.n) for s in shards]
+
+    def gather(b):
+        torch.cuda.synchronize()
+        for r in range(world):
+            lo, hi = plan.own(0, r)
+            for q in range(world):
+                if q != r:
+                    z[q][b][lo:hi].copy_(z[r][b][lo:hi])
+
+    for r, s in enumerate(shards):
+        s.irwin_hall(2, x0[r])
+        s.scale_piece(0, x0[r], z[r][0])
+    gather(0)
+    for t in range(T):
+        a, b = t & 1, (t & 1) ^ 1
+        for r, s in enumerate(shards):
+            s.step_piece(0, z[r][a], x0[r] if t == 0 else x[r][a], x[r][b], z[r][b])
+        gather(b)
+    torch.cuda.synchronize()
+    xs = np.concatenate([s.to_original(x[r][T & 1]) for r, s in enumerate(shards)])
+    xo, fo = O.power_iterate(rp, col, val, deg, O.irwin_hall(deg, 2), T)
+    assert np.array_equal(xs, xo)
+    for s in shards:
+        s.close()
