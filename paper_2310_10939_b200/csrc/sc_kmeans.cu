@@ -1476,6 +1476,7 @@ __device__ __forceinline__ int cs_key(const CsSlot &sl, int64_t t, int64_t n, in
     return (int)(s * k + lab[(int64_t)act[s] * n + j]);
 }
 
+template <int TILE = kCsTile>
 __global__ void __launch_bounds__(32 * kCsWarps) k_cs_hist(int64_t m, int64_t n, int k,
                                                            const int32_t *__restrict__ lab,
                                                            const int32_t *__restrict__ act,
@@ -1484,15 +1485,16 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs_hist(int64_t m, int64_t n,
     extern __shared__ int32_t cs_h[];
     for (int q = threadIdx.x; q < nseg; q += blockDim.x) cs_h[q] = 0;
     __syncthreads();
-    const int64_t t0 = (int64_t)blockIdx.x * kCsTile;
+    const int64_t t0 = (int64_t)blockIdx.x * TILE;
     const CsSlot sl(t0, n);
-    for (int64_t t = t0 + threadIdx.x; t < min(m, t0 + kCsTile); t += blockDim.x)
+    for (int64_t t = t0 + threadIdx.x; t < min(m, t0 + TILE); t += blockDim.x)
         atomicAdd(&cs_h[cs_key(sl, t, n, k, lab, act)], 1);
     __syncthreads();
     for (int q = threadIdx.x; q < nseg; q += blockDim.x)
         bh[(int64_t)q * ntiles + blockIdx.x] = cs_h[q];
 }
 
+template <int TILE = kCsTile>
 __global__ void __launch_bounds__(32 * kCsWarps) k_cs_scatter(
     int64_t m, int64_t n, int k, const int32_t *__restrict__ lab, const int32_t *__restrict__ act,
     int nseg, int ntiles, const int32_t *__restrict__ off, const double *__restrict__ x,
@@ -1502,8 +1504,8 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs_scatter(
     int32_t *run = cs_s + w * nseg;
     for (int q = threadIdx.x; q < kCsWarps * nseg; q += blockDim.x) cs_s[q] = 0;
     __syncthreads();
-    const int64_t t0 = (int64_t)blockIdx.x * kCsTile;
-    constexpr int SUB = kCsTile / kCsWarps;
+    const int64_t t0 = (int64_t)blockIdx.x * TILE;
+    constexpr int SUB = TILE / kCsWarps;
     const int64_t s0 = t0 + (int64_t)w * SUB, s1 = min(m, s0 + SUB);
     const CsSlot sl(t0, n);
     for (int64_t t = s0 + lane; t < s1; t += 32) atomicAdd(&run[cs_key(sl, t, n, k, lab, act)], 1);
@@ -2168,6 +2170,8 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         SC_CUDA(cudaFuncSetAttribute(k_assign1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_assign));
     }
+    const char *cst = getenv("SC_CS_TILE");  // counting-sort tile (A/B: 4096, 8192, 16384)
+    const int cs_tile = cst ? atoi(cst) : kCsTile;
     const char *smk = getenv("SC_KMEANS_SORTED_MIN_K");
     const int sorted_min_k = smk ? atoi(smk) : kSortedMinK;
     const bool sorted_assign = l == 1 && k >= sorted_min_k && k <= kSortedMaxK &&
@@ -2287,16 +2291,31 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
         const int64_t m = (int64_t)nact * n;
         size_t tb = km->cub_bytes;
         if (l == 1 && nseg <= kCsMaxKeys && getenv("SC_KMEANS_RADIX_SORT") == nullptr) {
-            const int ntiles = (int)((m + kCsTile - 1) / kCsTile);
+            // tile of the counting sort: larger tiles shrink the (key, tile) count matrix and its
+            // scan (nseg x m / tile ints), at ~4 elements per key per 4096-tile at k = 100
+            const int tile = cs_tile;
+            const int ntiles = (int)((m + tile - 1) / tile);
             int32_t *bh = km->d_keys, *boff = km->d_keys_alt;  // nseg * ntiles <= m ints each
-            k_cs_hist<<<ntiles, 32 * kCsWarps, (size_t)nseg * 4, s>>>(
-                m, n, k, km->d_lab[nxt], km->d_empty, nseg, ntiles, bh);
+            auto hist = [&](auto tl) {
+                constexpr int TL = decltype(tl)::value;
+                k_cs_hist<TL><<<ntiles, 32 * kCsWarps, (size_t)nseg * 4, s>>>(
+                    m, n, k, km->d_lab[nxt], km->d_empty, nseg, ntiles, bh);
+            };
+            auto scatter = [&](auto tl) {
+                constexpr int TL = decltype(tl)::value;
+                k_cs_scatter<TL><<<ntiles, 32 * kCsWarps, (size_t)nseg * kCsWarps * 4, s>>>(
+                    m, n, k, km->d_lab[nxt], km->d_empty, nseg, ntiles, boff, km->d_x,
+                    km->d_vals_alt);
+            };
+            if (tile == 16384) hist(std::integral_constant<int, 16384>{});
+            else if (tile == 8192) hist(std::integral_constant<int, 8192>{});
+            else hist(std::integral_constant<int, 4096>{});
             size_t sb = km->cub_bytes;
             SC_CUDA(cub::DeviceScan::ExclusiveSum(km->d_cub, sb, bh, boff, (int64_t)nseg * ntiles,
                                                   s));
-            k_cs_scatter<<<ntiles, 32 * kCsWarps, (size_t)nseg * kCsWarps * 4, s>>>(
-                m, n, k, km->d_lab[nxt], km->d_empty, nseg, ntiles, boff, km->d_x,
-                km->d_vals_alt);
+            if (tile == 16384) scatter(std::integral_constant<int, 16384>{});
+            else if (tile == 8192) scatter(std::integral_constant<int, 8192>{});
+            else scatter(std::integral_constant<int, 4096>{});
         } else if (l == 1) {
             k_make_keys<<<grid_1d(km, m, 256), 256, 0, s>>>(n, k, km->d_lab[nxt], km->d_empty,
                                                              nact, km->d_keys, km->d_vals, km->d_x);
