@@ -132,3 +132,13 @@ def test_bad_column_rejected_before_upload():
     g = from_csr(2, rp, col, None, np.array([1.0, 1.0]))
     with pytest.raises(InputError):
         DeviceGraph(g, devices=[0, 0])
+
+
+def test_fp32_values_shards_equal_single(heavy):
+    """the optional fp32-value variant on shards: the same fp32 weights and fp64 sums as the
+    single handle, so the results are identical to it (and within 1e-5 of the fp64 oracle)"""
+    _, xs, fs, _, _ = _run(heavy, 25, fp32_values=True)
+    _, xm, fm, _, _ = _run(heavy, 25, fp32_values=True, devices=[0, 0, 0])
+    assert np.array_equal(xs, xm) and np.array_equal(fs, fm)
+    _, x64, _, _, _ = _run(heavy, 25)
+    assert np.max(np.abs(xm - x64) / np.abs(x64)) < 1e-5
