@@ -70,7 +70,10 @@ constexpr int kExtreme = kSellMax;  // longer rows ("wide") get one warp each
 constexpr int64_t kWideKeyMax = int64_t(1) << 24;  // wide rows are ordered by min(length, this)
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry of a slice
 constexpr int kStepTPB = 256;      // 8 warps per CTA
-constexpr int kUnroll = 8;         // slice steps in flight per lane
+#ifndef SC_UNROLL
+#define SC_UNROLL 8
+#endif
+constexpr int kUnroll = SC_UNROLL;  // slice steps in flight per lane
 
 struct StepArgs {
     const int64_t *slice_ptr;  // nslices + 1 (entries, multiples of 32)
@@ -223,8 +226,14 @@ __global__ void __launch_bounds__(kStepTPB, 2) k_rw_wide(StepArgs a) {
     peer_fence(a);
 }
 
+#ifndef SC_MINB_U
+#define SC_MINB_U 1
+#endif
+#ifndef SC_MINB_W
+#define SC_MINB_W 1
+#endif
 template <bool UNIT, bool SYM, bool F32 = false>
-__global__ void __launch_bounds__(kStepTPB) k_rw_step(StepArgs a) {
+__global__ void __launch_bounds__(kStepTPB, (UNIT || F32) ? SC_MINB_U : SC_MINB_W) k_rw_step(StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     // ---- SELL slices: one warp per slice, one lane per row
