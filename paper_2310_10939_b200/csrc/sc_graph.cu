@@ -41,6 +41,10 @@
 #include "sc_common.cuh"
 
 namespace sc {
+#include "sc_hostcopy.cuh"
+}  // namespace sc
+
+namespace sc {
 
 thread_local std::string g_last_error;
 
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(kStepTPB, 2) k_rw_wide(StepArgs a) {
 #define SC_MINB_U 1
 #endif
 #ifndef SC_MINB_W
-#define SC_MINB_W 1
+#define SC_MINB_W 5  // weighted: 5 CTAs of 256 (C4 539 -> 497 us, C3 275 -> 270; 6 spills and thrashes C4)
 #endif
 template <bool UNIT, bool SYM, bool F32 = false>
 __global__ void __launch_bounds__(kStepTPB, (UNIT || F32) ? SC_MINB_U : SC_MINB_W) k_rw_step(StepArgs a) {
@@ -1184,7 +1188,19 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
 
     lap("unit check");
     int32_t st;
+    // (worker thread of the staged column upload below; joined before any exit)
+    struct Joiner {
+        std::thread t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } col_up;
+    cudaError_t col_up_err = cudaSuccess;
+    auto join_up = [&]() {
+        if (col_up.t.joinable()) col_up.t.join();
+    };
     auto cleanup = [&](int32_t code) {
+        join_up();
         sc_graph_destroy(g);
         return code;
     };
@@ -1214,7 +1230,11 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     double *t_val = nullptr, *t_deg = nullptr;
     void *t_cub = nullptr;
     size_t cub_cap = 0;
+    // pageable column / weight arrays are staged through pinned slots by host threads
+    // (sc_hostcopy.cuh); that upload is host-bound, so it runs on a worker thread beside the
+    // row validation and renumbering below, and is joined before the columns are used
     auto free_tmp = [&]() {
+        join_up();
         for (void *p_ : {(void *)t_rp, (void *)t_sizes, (void *)t_stats, (void *)t_wlen,
                          (void *)t_flag, (void *)t_keys, (void *)t_keys2, (void *)t_iota,
                          (void *)t_deg, t_cub})
@@ -1229,6 +1249,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         return cudaMallocAsync(&t_cub, bytes, s);
     };
     auto bail = [&](cudaError_t err, const char *what) {
+        join_up();
         cudaStreamSynchronize(s2);
         free_tmp();
         fail(err == cudaErrorMemoryAllocation ? SC_E_OOM : SC_E_CUDA, "%s: %s", what,
@@ -1245,19 +1266,29 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if (!e) e = cudaMallocAsync((void **)&t_flag, 64, s);
     if (!e) e = cudaMallocAsync((void **)&t_stats, 64, s);
     // row offsets and degrees first (they gate the renumbering), then the big arrays
-    if (!e) e = cudaMemcpyAsync(t_rp, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemcpyAsync(t_deg, deg, (size_t)n * 8, cudaMemcpyHostToDevice, s);
+    if (!e) e = h2d_upload(t_rp, row_ptr, (size_t)(n + 1) * 8, s);
+    if (!e) e = h2d_upload(t_deg, deg, (size_t)n * 8, s);
+    if (!e) e = cudaMemsetAsync(t_flag, 0, 64, s);
     if (!e) e = cudaEventRecord(g->ev_fork, s);  // allocations done -> side stream may copy
     if (!e) e = cudaStreamWaitEvent(s2, g->ev_fork, 0);
-    if (!e && nnz && !dcol) e = cudaMemcpyAsync(t_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s2);
-    if (!e && t_val && !dval) e = cudaMemcpyAsync(t_val, val, (size_t)nnz * 8, cudaMemcpyHostToDevice, s2);
-    if (!e) e = cudaMemsetAsync(t_flag, 0, 64, s);
-    if (!e && nnz) {
-        // flag[0]: any column index out of range (side stream, right after the copy)
-        k_col_range<<<grid_for(g, nnz, 256), 256, 0, s2>>>(t_col, nnz, ncols, t_flag);
-        e = cudaGetLastError();
+    auto upload_cols = [&, t_col, t_val]() -> cudaError_t {
+        cudaError_t r = cudaSetDevice(device);
+        if (!r && nnz && !dcol) r = h2d_upload(t_col, col, (size_t)nnz * 4, s2);
+        if (!r && t_val && !dval) r = h2d_upload(t_val, val, (size_t)nnz * 8, s2);
+        if (!r && nnz) {
+            // flag[0]: any column index out of range (side stream, right after the copy)
+            k_col_range<<<grid_for(g, nnz, 256), 256, 0, s2>>>(t_col, nnz, ncols, t_flag);
+            r = cudaGetLastError();
+        }
+        if (!r) r = cudaEventRecord(g->ev_join, s2);
+        return r;
+    };
+    if (!e) {
+        const bool host_bound = (nnz && !dcol && h2d_staged(col, (size_t)nnz * 4)) ||
+                                (t_val && !dval && h2d_staged(val, (size_t)nnz * 8));
+        if (host_bound) col_up.t = std::thread([&, upload_cols]() { col_up_err = upload_cols(); });
+        else e = upload_cols();
     }
-    if (!e) e = cudaEventRecord(g->ev_join, s2);
     if (!e) e = cudaMemsetAsync(t_stats, 0, 64, s);
     if (!e) {
         k_validate_rows<<<grid_for(g, n, 256), 256, 0, s>>>(t_rp, t_deg, n, t_flag, t_stats);
@@ -1335,7 +1366,9 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     // (a heavy-tailed graph is sorted by length globally, which would undo any pre-order)
     if (!e && (cflags & SC_CREATE_REORDER_BFS) && sigma < n) {
         // locality pre-order from a multi-source BFS (needs the columns on the device)
-        e = reorder_bfs(g, s, t_rp, t_col, n, t_keys, t_iota, prof);
+        join_up();
+        if (!e) e = col_up_err;
+        if (!e) e = reorder_bfs(g, s, t_rp, t_col, n, t_keys, t_iota, prof);
         lap("BFS pre-order");
     } else if (!e) {
         k_sell_keys<<<grid_for(g, n, 256), 256, 0, s>>>(t_rp, n, sigma, nwin, t_keys, t_iota);
@@ -1369,6 +1402,8 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     if (!e) e = cudaMemcpyAsync(&g->sell_entries, g->d_slice_ptr + g->nslices, 8,
                                 cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaMemcpyAsync(&wide_total, g->d_wide_ptr + g->n_wide, 8, cudaMemcpyDeviceToHost, s);
+    join_up();
+    if (!e) e = col_up_err;
     if (!e) e = cudaStreamWaitEvent(s, g->ev_join, 0);  // columns copied and range-checked
     int32_t col_bad = 0;
     if (!e) e = cudaMemcpyAsync(&col_bad, t_flag, 4, cudaMemcpyDeviceToHost, s);
