@@ -109,7 +109,8 @@ def traffic_from_profiles(cfg: int, unit: bool, layout: str = "sell", preorder: 
         return None
     with open(p) as fh:
         d = json.load(fh)
-    return d.get(f"c{cfg}_{'unit' if unit else 'weighted'}" + ("_panels" if layout == "panels" else "")
+    return d.get(f"c{cfg}_{'unit' if unit else 'weighted'}"
+                 + ("_panels" if layout == "panels" else "_windows" if layout == "windows" else "")
                  + (f"_{preorder}" if preorder not in (None, "none") else ""))
 
 
@@ -277,6 +278,8 @@ def roofline_for(g, info, kernel_ms, reads_val: bool):
     compulsory = stored * idx_val + n * (8 + 8 + 8 + 8 + 8)
     if info.get("panel_groups"):  # column-panel layout: its stage stream replaces the SELL arrays
         compulsory = int(info["panel_bytes"]) + n * (8 + 8 + 8 + 8 + 8)
+    if info.get("window_items"):  # row windows: 16-bit indices (+ the far column lists)
+        compulsory = stored * (idx_val - 2) + n * (8 + 8 + 8 + 8 + 8)
     peak, peak_kind = peak_hbm()
     achieved = alg / (kernel_ms / 1e3) / 1e9
     r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -338,9 +341,11 @@ def run_b200(args):
     # as fast_spectral_cluster: locality pre-order "auto", column panels for T >= 64 (declined
     # by the library when the graph does not qualify)
     dev = DeviceGraph(g, keep_weights=args.weighted, reorder="auto",
-                      panels=not args.sell and T >= 64, devices=devs)
+                      panels=not args.sell and T >= 64, devices=devs,
+                      windows=not args.sell and T >= 64)
     info = dev.info()
-    layout = "panels" if info["panel_groups"] else "sell"
+    layout = ("panels" if info["panel_groups"] else "windows" if info.get("window_items")
+              else "sell")
     dev_reorder = dev.reorder or "none"
     dev.sample_irwin_hall(0)
     times, clocks = time_power(dev, T, args.steps, args.warmup, clocks=True)

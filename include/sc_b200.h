@@ -75,7 +75,7 @@ typedef struct sc_graph_info {
     int64_t panel_bytes;    /* column-panel layout: bytes streamed per step */
     int64_t zstride;        /* doubles between the handle's two z buffers (sc_shard_buffers) */
     int32_t n_gpus;         /* shards of a multi-GPU handle (sc_graph_create_multi), else 1 */
-    int32_t reserved;
+    int32_t window_items;   /* row-window layout: CTA work items per step (0 = no window layout) */
 } sc_graph_info;
 
 typedef struct sc_timing {
@@ -111,6 +111,15 @@ int32_t sc_graph_create(const int64_t *row_ptr, const int32_t *col, const double
  * and gathered there, the rest from L2; bit-identical results.  Declined silently when the
  * graph does not qualify (sc_graph_info.panel_groups == 0). */
 #define SC_CREATE_PANELS 0x8u
+/* row-window layout in addition to SELL (any weights; whole-handle steps): for graphs whose
+ * renumbered rows reference mostly their own 4096-row neighbourhood (k-NN / geometric graphs,
+ * typically after SC_CREATE_REORDER_BFS) each CTA stages its panel's 4096 z values (one bulk
+ * copy) and the z values of its out-of-panel entries (gathered once, off the rows' add chains)
+ * in shared memory and streams 16-bit shared-memory indices instead of 32-bit columns;
+ * bit-identical results.  Declined silently when fewer than 60 % of the stored entries fall
+ * into the rows' own panels (sc_graph_info.window_items == 0) or when the handle already has
+ * a column-panel layout. */
+#define SC_CREATE_WINDOWS 0x10u
 int32_t sc_graph_create_ex(const int64_t *row_ptr, const int32_t *col, const double *val,
                            const double *deg, int64_t n, int64_t nnz, int32_t device,
                            uint32_t create_flags, sc_graph **out);
@@ -150,6 +159,10 @@ int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *out);
  * and hold ncols + 16 doubles with z[ncols..] == 0 (the padding target; the handle's own
  * buffers already do). */
 int32_t sc_graph_build_panels(sc_graph *g);
+/* Builds the row-window layout (SC_CREATE_WINDOWS) on an existing single-GPU handle or shard;
+ * declined silently when the graph does not qualify (window_items stays 0).  Whole-handle
+ * steps then use it when the z buffer is 16-byte aligned and holds z[ncols] == 0. */
+int32_t sc_graph_build_windows(sc_graph *g);
 /* The device layout renumbers rows (SELL-32-sigma: length-sorted inside 4096-row windows,
  * rows longer than 256 last).  sc_sell_order returns that permutation for a row_ptr
  * (perm[p] = original row of renumbered row p) so a multi-GPU driver can rename columns

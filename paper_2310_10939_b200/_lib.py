@@ -27,6 +27,7 @@ SC_CREATE_KEEP_WEIGHTS = 0x1
 SC_CREATE_FP32_VALUES = 0x2
 SC_CREATE_REORDER_BFS = 0x4
 SC_CREATE_PANELS = 0x8
+SC_CREATE_WINDOWS = 0x10
 
 
 class GraphInfo(ctypes.Structure):
@@ -37,7 +38,7 @@ class GraphInfo(ctypes.Structure):
         ("device", ctypes.c_int32), ("sm_count", ctypes.c_int32),
         ("stored_entries", ctypes.c_int64),
         ("panel_groups", ctypes.c_int64), ("panel_bytes", ctypes.c_int64),
-        ("zstride", ctypes.c_int64), ("n_gpus", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("zstride", ctypes.c_int64), ("n_gpus", ctypes.c_int32), ("window_items", ctypes.c_int32),
     ]
 
 
@@ -60,6 +61,7 @@ EXPORTS = (
     "sc_kmeans_create_nd", "sc_kmeans_lloyd_sorted", "sc_release_cached_memory",
     "sc_gather_f64", "sc_graph_build_panels", "sc_graph_download_f", "sc_kmeans_set_flags",
     "sc_graph_create_multi", "sc_graph_shard_layout", "sc_shard_create_from_csr",
+    "sc_graph_build_windows",
 )
 
 _lib = None
@@ -90,6 +92,7 @@ def load() -> ctypes.CDLL:
         "sc_graph_destroy": ([P], None),
         "sc_graph_info_get": ([P, ctypes.POINTER(GraphInfo)], i32),
         "sc_graph_build_panels": ([P], i32),
+        "sc_graph_build_windows": ([P], i32),
         "sc_graph_download_f": ([P, P], i32),
         "sc_sample_irwin_hall": ([P, u64, u64, P], i32),
         "sc_set_x0": ([P, P], i32),

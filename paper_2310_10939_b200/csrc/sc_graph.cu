@@ -789,6 +789,7 @@ using namespace sc;
 
 namespace sc {
 struct PanGroup;
+struct WinItem;
 }
 
 namespace sc {
@@ -843,6 +844,16 @@ struct sc_graph {
     sc::PanGroup *d_pan_grp = nullptr;
     uint8_t *d_pan_stream = nullptr;
     int64_t zstride = 0;  // d_z[1] - d_z[0] (ncols + a zero slot, rounded up to 32)
+    // row-window layout (sc_window.cuh; SC_CREATE_WINDOWS), used for whole-handle steps
+    int win_items = 0;
+    int64_t win_far = 0, win_pairs = 0;
+    double win_cover = 0.0;
+    sc::WinItem *d_win_items = nullptr;
+    int64_t *d_win_ptr = nullptr;
+    uint32_t *d_win_idx = nullptr;
+    double2 *d_win_val = nullptr;
+    float2 *d_win_val32 = nullptr;
+    uint32_t *d_win_far = nullptr;
     // peers synchronised by stream events (sc_multi.cuh) instead of sc_shard_barrier: the
     // panel kernel may then mirror z into peers too (it has no system fence of its own)
     bool peer_events = false;
@@ -1118,6 +1129,7 @@ static cudaError_t reorder_bfs(sc_graph *g, cudaStream_t s, const int64_t *rp, c
 }
 
 #include "sc_panel.cuh"  // (inside namespace sc)
+#include "sc_window.cuh"
 
 // col == nullptr with dcol != nullptr: the column array is already on `device` (borrowed,
 // e.g. from sc_generate_sbm) and is neither copied nor freed.
@@ -1452,6 +1464,10 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
         if ((st = build_panels(g, prof))) return cleanup(st);
         lap("panel layout");
     }
+    if ((cflags & SC_CREATE_WINDOWS) && !g->pan_ctas) {
+        if ((st = build_windows(g, prof))) return cleanup(st);
+        lap("window layout");
+    }
     *out = g;
     return SC_OK;
 }
@@ -1474,6 +1490,9 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     // whole-graph steps use the column-panel layout when the handle has one
     const bool panel = g->pan_ctas && !(flags & SC_FORCE_SELL) && row_lo == 0 && row_hi == g->n &&
                        (g->npeer == 0 || g->peer_events);
+    // ... or the row-window layout (z_in must allow 16-byte aligned bulk copies)
+    const bool window = !panel && g->win_items && !(flags & SC_FORCE_SELL) && row_lo == 0 &&
+                        row_hi == g->n && ((uintptr_t)z_in & 15) == 0;
     StepArgs a;
     a.slice_lo = std::min(row_lo, g->n_sell) / kSlice;
     a.slice_hi = (std::min(row_hi, g->n_sell) + kSlice - 1) / kSlice;
@@ -1532,7 +1551,9 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
             else k_rw_wide<false, false><<<wg, kStepTPB, 0, g->side>>>(a);
         }
     }
-    if (sblocks) {
+    if (sblocks && window) {
+        SC_CUDA(launch_window_step(g, a, sym, s));
+    } else if (sblocks) {
         const dim3 grid((unsigned)sblocks);
         if (g->unit) {
             if (sym) k_rw_step<true, true><<<grid, kStepTPB, 0, s>>>(a);
@@ -1789,6 +1810,14 @@ int32_t sc_graph_build_panels(sc_graph *g) {
     return sc::build_panels(g, getenv("SC_GRAPH_PROFILE") != nullptr);
 }
 
+int32_t sc_graph_build_windows(sc_graph *g) {
+    SC_REQUIRE(g, SC_E_INVALID, "null graph");
+    SC_NOT_MULTI(g);
+    if (g->win_items) return SC_OK;
+    SC_CUDA(cudaSetDevice(g->device));
+    return sc::build_windows(g, getenv("SC_GRAPH_PROFILE") != nullptr);
+}
+
 int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *o) {
     SC_REQUIRE(g && o, SC_E_INVALID, "null argument");
     if (g->multi) return sc::multi_info(g, o);
@@ -1808,6 +1837,7 @@ int32_t sc_graph_info_get(const sc_graph *g, sc_graph_info *o) {
     o->stored_entries = g->sell_entries;
     o->zstride = g->zstride;
     o->n_gpus = 1;
+    o->window_items = g->win_items;
     return SC_OK;
 }
 

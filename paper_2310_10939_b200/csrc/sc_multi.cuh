@@ -352,6 +352,7 @@ static int32_t multi_info(const sc_graph *mg, sc_graph_info *o) {
     o->device = mg->device;
     o->sm_count = mg->sm_count;
     o->n_gpus = (int32_t)m->sh.size();
+    o->window_items = 0;
     for (const auto &s : m->sh) {
         o->ntiles += s.g->nslices;
         o->long_rows += s.g->n_wide;

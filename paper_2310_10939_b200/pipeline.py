@@ -58,8 +58,9 @@ class SpectralParams:
                                  # labels may differ from the reference's)
     cost_assert: bool | None = None  # kmeans.py:206's assert; None: on unless python -O
     reorder: str | None = "auto"  # device-layout pre-order: "auto", "bfs" or None (exact)
-    layout: str = "auto"         # SpMV layout: "auto" (column panels for T >= 64 when the
-                                 # graph qualifies), "panels" or "sell"; results identical
+    layout: str = "auto"         # SpMV layout: "auto" (column panels, else row windows, for
+                                 # T >= 64 when the graph qualifies), "panels", "windows"
+                                 # or "sell"; results identical
     gpus: int = 1                # row-block shards over this many GPUs of this process
     devices: tuple | None = None  # explicit shard devices (overrides gpus; may repeat)
 
@@ -82,8 +83,9 @@ class SpectralParams:
             raise InputError(f"kmeans must be 'exact' or 'sorted', got {self.kmeans!r}")
         if self.gpus < 1 or (self.devices is not None and len(self.devices) < 1):
             raise InputError(f"gpus must be >= 1, got {self.gpus}")
-        if self.layout not in ("auto", "panels", "sell"):
-            raise InputError(f"layout must be 'auto', 'panels' or 'sell', got {self.layout!r}")
+        if self.layout not in ("auto", "panels", "windows", "sell"):
+            raise InputError(f"layout must be 'auto', 'panels', 'windows' or 'sell', "
+                             f"got {self.layout!r}")
 
     def num_columns(self, n: int) -> int:
         if self.mode == "one_vector":
@@ -153,9 +155,12 @@ def fast_spectral_cluster(g, params: SpectralParams, *, device_graph: DeviceGrap
     # the panel layout costs about a dozen SELL steps to build (device, ~1.7 ms at config 2)
     # and saves ~13 % per step where it applies
     panels = params.layout == "panels" or (params.layout == "auto" and steps >= PANEL_MIN_STEPS)
+    # the row-window layout (one pass over the columns to decide, ~2 SELL steps to build) is
+    # tried when the handle has no panel layout
+    windows = params.layout == "windows" or (params.layout == "auto" and steps >= PANEL_MIN_STEPS)
     dev = device_graph if device_graph is not None else DeviceGraph(
         graph, params.device, reorder=params.reorder, panels=panels, gpus=params.gpus,
-        devices=params.devices)
+        devices=params.devices, windows=windows)
     try:
         t0 = time.perf_counter()
         if params.x0 is not None:

@@ -109,10 +109,15 @@ class DeviceGraph:
 
     def __init__(self, graph, device: int = 0, keep_weights: bool = False,
                  fp32_values: bool = False, reorder: str | None = None, panels: bool = False,
-                 gpus: int = 1, devices=None):
+                 gpus: int = 1, devices=None, windows: bool = False):
         """``panels``: also build the column-panel layout (sc_panel.cuh; unit weights and rows
         of <= 256 entries only, declined silently otherwise -- see ``info()['panel_groups']``);
         whole-graph steps then stage heavily referenced column ranges in shared memory.
+        ``windows``: also try the row-window layout (sc_window.cuh; any weights): for graphs
+        whose renumbered rows reference mostly their own 4096-row neighbourhood (k-NN /
+        geometric graphs after the BFS pre-order) each CTA stages its z panel and its
+        out-of-panel z values in shared memory and streams 16-bit indices; declined silently
+        otherwise (``info()['window_items']``), single-GPU handles only.
         ``fp32_values``: store the weights as fp32 (the optional fp32-value variant:
         half the weight bytes, results within 1e-5 relative of fp64; unit-weight graphs are
         unaffected).  ``reorder="bfs"``: renumber the vertices by a multi-source BFS before the
@@ -161,7 +166,8 @@ class DeviceGraph:
         cflags = ((_lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0)
                   | (_lib.SC_CREATE_FP32_VALUES if fp32_values else 0)
                   | (_lib.SC_CREATE_REORDER_BFS if reorder == "bfs" else 0)
-                  | (_lib.SC_CREATE_PANELS if panels else 0))
+                  | (_lib.SC_CREATE_PANELS if panels else 0)
+                  | (_lib.SC_CREATE_WINDOWS if windows and not multi else 0))
         if multi:
             dv = np.ascontiguousarray(devices, dtype=np.int32)
             _lib.check(L.sc_graph_create_multi(_lib.ptr(self._rp), _lib.ptr(self._col),
@@ -176,7 +182,9 @@ class DeviceGraph:
         self.last_timing = None
 
     @classmethod
-    def from_device_csr(cls, csr, keep_weights: bool = False, panels: bool = False) -> "DeviceGraph":
+    def from_device_csr(cls, csr, keep_weights: bool = False, panels: bool = False,
+                        reorder: str | None = None, windows: bool = False,
+                        fp32_values: bool = False) -> "DeviceGraph":
         """Graph handle straight from a device-resident CSR (``generate.DeviceCSR``): the
         column array never visits the host (sc_graph_create_from_csr)."""
         L = _lib.require_device()
@@ -184,11 +192,14 @@ class DeviceGraph:
         h = ctypes.c_void_p()
         _lib.check(L.sc_graph_create_from_csr(csr.handle,
                                               (_lib.SC_CREATE_KEEP_WEIGHTS if keep_weights else 0)
-                                              | (_lib.SC_CREATE_PANELS if panels else 0),
+                                              | (_lib.SC_CREATE_PANELS if panels else 0)
+                                              | (_lib.SC_CREATE_REORDER_BFS if reorder == "bfs" else 0)
+                                              | (_lib.SC_CREATE_WINDOWS if windows else 0)
+                                              | (_lib.SC_CREATE_FP32_VALUES if fp32_values else 0),
                                               ctypes.byref(h)))
         self._h = h
         self.graph = None
-        self.reorder = None
+        self.reorder = reorder
         self.gpus, self.devices = 1, [csr.device]
         self.n, self.nnz = csr.n, csr.nnz
         self.device = csr.device
@@ -222,7 +233,7 @@ class DeviceGraph:
     def info(self) -> dict:
         gi = _lib.GraphInfo()
         _lib.check(_lib.load().sc_graph_info_get(self.handle, ctypes.byref(gi)))
-        return {f: getattr(gi, f) for f, _ in gi._fields_ if f != "reserved"}
+        return {f: getattr(gi, f) for f, _ in gi._fields_ }
 
     def shard_layout(self) -> list:
         """multi-GPU handles: per shard (row0, rows, z offset, device)"""

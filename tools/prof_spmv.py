@@ -1,5 +1,5 @@
 """Profiling driver: config-2 power iteration without CUDA graphs (so ncu sees each
-kernel launch), a few iterations.  Usage: python tools/prof_spmv.py [T] [--weighted] [--panels] [--cfg N] [--no-reorder]"""
+kernel launch), a few iterations.  Usage: python tools/prof_spmv.py [T] [--weighted] [--panels] [--windows] [--cfg N] [--no-reorder]"""
 import os
 import sys
 import time
@@ -22,7 +22,7 @@ import bench  # noqa: E402
 g, _, _ = bench.build_config(cfg)
 print(f"graph n={g.n} nnz={g.nnz} in {time.time()-t:.1f}s", flush=True)
 # same pre-order choice as the bench and fast_spectral_cluster ("auto": BFS for scattered ids)
-dg = DeviceGraph(g, keep_weights=weighted, panels=panels,
+dg = DeviceGraph(g, keep_weights=weighted, panels=panels, windows="--windows" in sys.argv,
                  reorder=None if "--no-reorder" in sys.argv else "auto")
 print("layout", {k: v for k, v in dg.info().items()}, "reorder", dg.reorder, flush=True)
 dg.sample_irwin_hall(0)
