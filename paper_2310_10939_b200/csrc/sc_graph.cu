@@ -1180,14 +1180,6 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     SC_REQUIRE(device >= 0 && device < ndev, SC_E_INVALID, "device %d not present (%d GPUs)",
                device, ndev);
     SC_CUDA(cudaSetDevice(device));
-    if (const char *fg = getenv("SC_L2_FETCH")) {  // probe: DRAM fetch granularity of an L2 miss
-        size_t before = 0, after = 0;
-        cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
-        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
-        cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
-        if (prof) fprintf(stderr, "[sc_graph_create] L2 fetch granularity %zu -> %zu\n", before, after);
-        cudaGetLastError();
-    }
 
     sc_graph *g = new sc_graph();
     g->device = device;

@@ -31,22 +31,14 @@
 //             far entries (a single slice always fits: 32 rows x 256 entries)
 
 constexpr int kWinZ = 4096;          // panel width = the SELL sorting window
-#ifndef SC_WIN_FAR
-#define SC_WIN_FAR 8192
-#endif
-#ifndef SC_WIN_MINB
-#define SC_WIN_MINB 2
-#endif
-constexpr int kWinFarMax = SC_WIN_FAR;  // far slots per item (64 KB)
-#ifndef SC_WIN_TPB
-#define SC_WIN_TPB 512
-#endif
-constexpr int kWinTPB = SC_WIN_TPB;  // 2 CTAs/SM: 64 registers per thread
+constexpr int kWinFarMax = 8192;     // far slots per item (64 KB)
+constexpr int kWinTPB = 512;         // 2 CTAs/SM: 64 registers per thread
 constexpr int kWinSlicesMax = 4 * (kWinTPB / 32);  // slices per item: four per warp
 constexpr int kWinFar0 = kWinZ + 1;  // first far slot; kWinZ is the zero slot
 constexpr double kWinMinCover = 0.6; // fraction of entries inside the own panel the layout needs
 static_assert(kWinZ == kSigma, "panels are the SELL sorting windows");
 
+static_assert(kWinFarMax >= kSlice * kSellMax, "one slice must fit an item");
 static_assert(kWinFar0 + kWinFarMax <= 65536, "16-bit indices");
 static_assert(kWinSlicesMax / (kWinTPB / 32) <= 32, "a lane per slice of the warp");
 
@@ -74,7 +66,7 @@ constexpr int kWinFarPT = (kWinFarMax + kWinTPB - 1) / kWinTPB;  // far slots pe
 constexpr uint32_t kWinPadPair = (uint32_t)kWinZ | ((uint32_t)kWinZ << 16);
 
 template <bool UNIT, bool SYM, bool F32>
-__global__ void __launch_bounds__(kWinTPB, SC_WIN_MINB) k_rw_win(StepArgs a, WinArgs w) {
+__global__ void __launch_bounds__(kWinTPB, 2) k_rw_win(StepArgs a, WinArgs w) {
     extern __shared__ __align__(128) double wz[];  // panel (kWinZ) | zero slot | far slots
     __shared__ uint64_t zfull;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
