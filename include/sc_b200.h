@@ -139,7 +139,7 @@ int32_t sc_shard_create(const int64_t *row_ptr, const int32_t *col, const double
  * works with sc_sample_irwin_hall, sc_set_x0, sc_power_iterate, sc_graph_download_f,
  * sc_graph_info_get and sc_kmeans_create_from_graph (f gathered to the first device); x_T
  * and f are bit-identical to the single-GPU handle's.  create_flags: SC_CREATE_PANELS,
- * SC_CREATE_KEEP_WEIGHTS, SC_CREATE_FP32_VALUES (no BFS pre-order). */
+ * SC_CREATE_WINDOWS, SC_CREATE_KEEP_WEIGHTS, SC_CREATE_FP32_VALUES (no BFS pre-order). */
 int32_t sc_graph_create_multi(const int64_t *row_ptr, const int32_t *col, const double *val,
                               const double *deg, int64_t n, int64_t nnz, int32_t n_gpus,
                               const int32_t *devices, uint32_t create_flags, sc_graph **out);

@@ -190,6 +190,8 @@ static int32_t multi_create(const int64_t *rp, const int32_t *col, const double 
         SC_REQUIRE(s.g->n_sell + s.g->n_wide == s.n, SC_E_INTERNAL, "shard layout mismatch");
         s.g->peer_events = true;
         if ((cflags & SC_CREATE_PANELS) && (st = build_panels(s.g, false))) return fail_out(st);
+        if ((cflags & SC_CREATE_WINDOWS) && !s.g->pan_ctas && (st = build_windows(s.g, false)))
+            return fail_out(st);
         SC_CUDA(cudaSetDevice(s.device));
         for (auto &e : s.ev) SC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
@@ -353,6 +355,7 @@ static int32_t multi_info(const sc_graph *mg, sc_graph_info *o) {
     o->sm_count = mg->sm_count;
     o->n_gpus = (int32_t)m->sh.size();
     o->window_items = 0;
+    for (const MultiShard &s : m->sh) o->window_items += s.g->win_items;
     for (const auto &s : m->sh) {
         o->ntiles += s.g->nslices;
         o->long_rows += s.g->n_wide;

@@ -117,7 +117,7 @@ class DeviceGraph:
         whose renumbered rows reference mostly their own 4096-row neighbourhood (k-NN /
         geometric graphs after the BFS pre-order) each CTA stages its z panel and its
         out-of-panel z values in shared memory and streams 16-bit indices; declined silently
-        otherwise (``info()['window_items']``), single-GPU handles only.
+        otherwise (``info()['window_items']``).
         ``fp32_values``: store the weights as fp32 (the optional fp32-value variant:
         half the weight bytes, results within 1e-5 relative of fp64; unit-weight graphs are
         unaffected).  ``reorder="bfs"``: renumber the vertices by a multi-source BFS before the
@@ -167,7 +167,7 @@ class DeviceGraph:
                   | (_lib.SC_CREATE_FP32_VALUES if fp32_values else 0)
                   | (_lib.SC_CREATE_REORDER_BFS if reorder == "bfs" else 0)
                   | (_lib.SC_CREATE_PANELS if panels else 0)
-                  | (_lib.SC_CREATE_WINDOWS if windows and not multi else 0))
+                  | (_lib.SC_CREATE_WINDOWS if windows else 0))
         if multi:
             dv = np.ascontiguousarray(devices, dtype=np.int32)
             _lib.check(L.sc_graph_create_multi(_lib.ptr(self._rp), _lib.ptr(self._col),

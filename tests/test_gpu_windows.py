@@ -168,3 +168,22 @@ def test_config4_shape_device_csr():
             xT, f = dg.power_iterate(30)
     xo, fo = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, 30)
     assert np.array_equal(xT, xo) and np.array_equal(f, fo)
+
+
+def test_multi_gpu_shards_with_windows():
+    """the in-process multi-GPU handle (three shards sharing the GPU): every shard builds its
+    own window layout over the shared z space; x_T and f equal the single handle's and the
+    oracle's"""
+    g = _banded(90_000, 10, 1, seed=11, weighted=True)
+    with DeviceGraph(g, windows=True) as dg:
+        x0 = dg.sample_irwin_hall(4, return_host=True)
+        single = dg.power_iterate(14)
+    with DeviceGraph(g, windows=True, devices=[0, 0, 0]) as mg:
+        info = mg.info()
+        assert info["n_gpus"] == 3 and info["window_items"] > 0, info
+        x0m = mg.sample_irwin_hall(4, return_host=True)
+        multi = mg.power_iterate(14)
+    assert np.array_equal(x0, x0m)
+    assert np.array_equal(single[0], multi[0]) and np.array_equal(single[1], multi[1])
+    xo, fo = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, 14)
+    assert np.array_equal(multi[0], xo) and np.array_equal(multi[1], fo)
