@@ -69,7 +69,11 @@ int32_t fail(int32_t code, const char *fmt, ...) {
 
 constexpr int kSlice = 32;         // rows per slice (one per lane)
 constexpr int kSigma = 4096;       // sorting window (rows)
-constexpr int kSellMax = 256;      // longer rows are laid out first, globally length-sorted
+#ifndef SC_SELL_MAX
+#define SC_SELL_MAX 256
+#endif
+constexpr int kSellMax = SC_SELL_MAX;  // longer rows are laid out first, globally length-sorted
+static_assert(kSellMax < 512, "the renumbering key packs kSellMax - length into 9 bits");
 constexpr int kExtreme = kSellMax;  // longer rows ("wide") get one warp each
 constexpr int64_t kWideKeyMax = int64_t(1) << 24;  // wide rows are ordered by min(length, this)
 constexpr uint32_t kPad = 0xffffffffu;  // padding entry of a slice
@@ -129,6 +133,12 @@ __device__ __forceinline__ void peer_fence(const StepArgs &a) {
 // (the scipy order), and the column indices are fetched one step earlier still, so a
 // gather never waits for its index load.
 constexpr int kWideBatch = 128;
+// Grid cap of the wide-row kernel (x SM count).  The kernel needs 114 registers per thread, so
+// two resident CTAs leave the concurrent slice kernel no room on an SM and the two ran back to
+// back (C3: 207 us slices + 74 us wide rows = 272 us per step).  One CTA per SM keeps 36 K
+// registers for the slices: 272 -> 261 us.  Graphs whose wide rows hold a quarter of the entries
+// or more keep two.
+constexpr int kWideCtasPerSM = 1;
 constexpr int kWidePL = kWideBatch / 32;
 
 // s + v[0] + v[1] + ... + v[m-1], left to right (v 16-byte aligned): shared-memory loads of
@@ -161,13 +171,19 @@ __device__ __forceinline__ double wide_fold(double s, const double *v, int m) {
     return s;
 }
 
+#ifndef SC_WIDE_MINB
+#define SC_WIDE_MINB 2  // 114 registers; 3 (80) and 4 (64) spill into the in-order fold: 278 / 333 us at C3
+#endif
 template <bool UNIT, bool SYM, bool F32 = false>
-__global__ void __launch_bounds__(kStepTPB, 2) k_rw_wide(StepArgs a) {
+__global__ void __launch_bounds__(kStepTPB, SC_WIDE_MINB) k_rw_wide(StepArgs a) {
     __shared__ __align__(16) double wbuf[kStepTPB / 32][2][kWideBatch];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int64_t w = a.wide_lo + (int64_t)blockIdx.x * (kStepTPB / 32) + warp;
-    if (w >= a.wide_hi) return;
+    // rows are dealt round-robin over the grid's warps (they come in decreasing length, so the
+    // longest in-order folds start first); the grid is capped at a few CTAs per SM so the
+    // concurrent slice kernel keeps most of every SM (launch_step)
+    for (int64_t w = a.wide_lo + (int64_t)blockIdx.x * (kStepTPB / 32) + warp; w < a.wide_hi;
+         w += (int64_t)gridDim.x * (kStepTPB / 32)) {
     const int64_t r = a.n_sell + w;
     const double xr = __ldcs(a.x_in + r), sc = __ldcs(a.scale + r);
     const int64_t lo = a.wide_ptr[w], hi = a.wide_ptr[w + 1];
@@ -227,6 +243,8 @@ __global__ void __launch_bounds__(kStepTPB, 2) k_rw_wide(StepArgs a) {
         buf1 = tb;
     }
     if (lane == 0) row_epilogue<SYM>(a, r, s, xr, sc);
+    __syncwarp();
+    }
     peer_fence(a);
 }
 
@@ -800,7 +818,7 @@ struct sc_graph {
     int device = 0;
     int sm_count = 0;
     int64_t n = 0, nnz = 0, ncols = 0, col_offset = 0, global_row0 = 0;
-    int64_t n_sell = 0, n_wide = 0, nslices = 0, sell_entries = 0;
+    int64_t n_sell = 0, n_wide = 0, nslices = 0, sell_entries = 0, wide_entries = 0;
     bool unit = false;
     int32_t *d_perm = nullptr;    // renumbered row -> original local row
     int32_t *d_iperm = nullptr;   // original local row -> renumbered row
@@ -1432,6 +1450,7 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
             }
         return cleanup(SC_E_RANGE);
     }
+    g->wide_entries = wide_total;
     if ((st = dmalloc(g, (void **)&g->d_col, (size_t)g->sell_entries * 4 + 16)) ||
         (!unit && !g->f32 &&
          (st = dmalloc(g, (void **)&g->d_val, (size_t)g->sell_entries * 8 + 16))) ||
@@ -1539,7 +1558,16 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     if (a.wide_blocks) {
         SC_CUDA(cudaEventRecord(g->ev_fork, s));
         SC_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
-        const dim3 wg((unsigned)a.wide_blocks);
+        // at most kWideCtasPerSM CTAs per SM (SC_WIDE_CAP overrides; 0 = one CTA per 8 rows)
+        static const int wide_env = [] {
+            const char *e = getenv("SC_WIDE_CAP");
+            return e ? atoi(e) : -1;
+        }();
+        const int wide_cap = wide_env >= 0 ? wide_env
+                             : g->wide_entries * 4 >= g->nnz ? 2 * kWideCtasPerSM : kWideCtasPerSM;
+        const int wide_grid = wide_cap > 0 ? std::min(a.wide_blocks, wide_cap * std::max(g->sm_count, 1))
+                                           : a.wide_blocks;
+        const dim3 wg((unsigned)wide_grid);
         if (g->unit) {
             if (sym) k_rw_wide<true, true><<<wg, kStepTPB, 0, g->side>>>(a);
             else k_rw_wide<true, false><<<wg, kStepTPB, 0, g->side>>>(a);

@@ -38,7 +38,6 @@ constexpr int kWinFar0 = kWinZ + 1;  // first far slot; kWinZ is the zero slot
 constexpr double kWinMinCover = 0.6; // fraction of entries inside the own panel the layout needs
 static_assert(kWinZ == kSigma, "panels are the SELL sorting windows");
 
-static_assert(kWinFarMax >= kSlice * kSellMax, "one slice must fit an item");
 static_assert(kWinFar0 + kWinFarMax <= 65536, "16-bit indices");
 static_assert(kWinSlicesMax / (kWinTPB / 32) <= 32, "a lane per slice of the warp");
 
@@ -178,7 +177,8 @@ __global__ void __launch_bounds__(kWinTPB, 2) k_rw_win(StepArgs a, WinArgs w) {
 // ---- layout construction (device) ----
 
 // per slice: far entries (stored, not padding, outside the slice's own panel); totals[0] +=
-// entries inside the own panel, totals[1] += stored entries (padding excluded)
+// entries inside the own panel, totals[1] += stored entries (padding excluded), totals[2] =
+// max far entries of one slice (an item holds at least one slice, so it must fit the far slots)
 __global__ void k_win_count(const int64_t *__restrict__ slice_ptr, const uint32_t *__restrict__ col,
                             int64_t nslices, int64_t col_offset, int32_t *__restrict__ far_cnt,
                             unsigned long long *__restrict__ totals) {
@@ -204,6 +204,7 @@ __global__ void k_win_count(const int64_t *__restrict__ slice_ptr, const uint32_
         far_cnt[sl] = nfar;
         atomicAdd(&totals[0], (unsigned long long)nin);
         atomicAdd(&totals[1], (unsigned long long)(nin + nfar));
+        atomicMax(&totals[2], (unsigned long long)nfar);
     }
 }
 
@@ -307,7 +308,8 @@ static cudaError_t win_set_smem(K kern, int smem) {
 
 // Builds g's row-window layout from its SELL arrays.  Returns SC_OK with g->win_items == 0 when
 // the graph does not qualify (fewer than kWinMinCover of the stored entries inside the rows' own
-// panels, a z space that is not 16-byte aligned at panel starts, more than 2^31 slices).
+// panels, one slice with more far entries than an item's slots, a z space that is not 16-byte
+// aligned at panel starts, more than 2^26 slices or 2^32 stored entries).
 static int32_t build_windows(sc_graph *g, bool prof) {
     g->win_items = 0;
     if (!g->nslices || g->nslices >= (int64_t(1) << 26) || (g->col_offset & 1)) return SC_OK;
@@ -326,22 +328,22 @@ static int32_t build_windows(sc_graph *g, bool prof) {
     };
     cudaError_t e = cudaMallocAsync((void **)&far_cnt, (size_t)(ns + 1) * 4, s);
     if (!e) e = cudaMallocAsync((void **)&far_off, (size_t)(ns + 1) * 8, s);
-    if (!e) e = cudaMallocAsync((void **)&totals, 16, s);
-    if (!e) e = cudaMemsetAsync(totals, 0, 16, s);
+    if (!e) e = cudaMallocAsync((void **)&totals, 24, s);
+    if (!e) e = cudaMemsetAsync(totals, 0, 24, s);
     if (!e) e = cudaMemsetAsync(far_cnt + ns, 0, 4, s);
     const unsigned wgrid = (unsigned)((ns * 32 + 255) / 256);
     if (!e) {
         k_win_count<<<wgrid, 256, 0, s>>>(g->d_slice_ptr, g->d_col, ns, g->col_offset, far_cnt, totals);
         e = cudaGetLastError();
     }
-    unsigned long long htot[2] = {0, 0};
-    if (!e) e = cudaMemcpyAsync(htot, totals, 16, cudaMemcpyDeviceToHost, s);
+    unsigned long long htot[3] = {0, 0, 0};
+    if (!e) e = cudaMemcpyAsync(htot, totals, 24, cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
     if (e) {
         cleanup();
         return fail(SC_E_CUDA, "window count: %s", cudaGetErrorString(e));
     }
-    if (htot[1] == 0 || (double)htot[0] < kWinMinCover * (double)htot[1]) {
+    if (htot[1] == 0 || (double)htot[0] < kWinMinCover * (double)htot[1] || htot[2] > (unsigned long long)kWinFarMax) {
         if (prof)
             fprintf(stderr, "[sc_graph_create] window layout declined: %.3f of the entries in own panels\n",
                     htot[1] ? (double)htot[0] / (double)htot[1] : 0.0);
