@@ -108,7 +108,34 @@ struct StepArgs {
     int npeer;
     const float *val32;   // fp32 weights (SC_CREATE_FP32_VALUES), SELL / wide layouts
     const float *wval32;
+    int zhint;            // 1: z space larger than the L2 -> 64-byte L2 fetch hint on the gathers
 };
+
+// The z gather of the SELL kernels (read-only path).  An L2 miss of a plain load fetches a whole
+// 128-byte line from DRAM (measured at config 5: 118 B of DRAM reads per random cross-block
+// gather, 32.5 GB per step against 8.9 GB without those edges); the L2::64B prefetch-size hint
+// halves that (21.7 GB per step, 7.50 -> 7.10 ms).  L2::128B equals the default, L2::256B and
+// L1::no_allocate are worse (35.1 / 35.7 GB); there is no 32-byte hint and
+// cudaLimitMaxL2FetchGranularity changes nothing.  When z fits the L2 the hint only costs
+// (config 2 panels 127.3 -> 131.0 us, C3/C4 +0.5 %), so it is used when the z space is larger
+// than the L2 (StepArgs::zhint, set by launch_step).
+__device__ __forceinline__ double ldz64(const double *p) {
+    double v;
+    asm("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+// run-time selected form (wide-row kernel: registers to spare); the slice kernel takes the hint
+// as a template parameter -- either form of a run-time choice spills its 48-register weighted
+// variant (260 -> 279 us at C3)
+__device__ __forceinline__ double ldz(const double *p, int hint64) {
+    double v;
+    asm("{\n .reg .pred h;\n setp.ne.s32 h, %2, 0;\n"
+        " @h ld.global.nc.L2::64B.f64 %0, [%1];\n"
+        " @!h ld.global.nc.f64 %0, [%1];\n}\n"
+        : "=d"(v)
+        : "l"(p), "r"(hint64));
+    return v;
+}
 
 template <bool SYM>
 __device__ __forceinline__ void row_epilogue(const StepArgs &a, int64_t r, double s, double xr,
@@ -204,7 +231,7 @@ __global__ void __launch_bounds__(kStepTPB, SC_WIDE_MINB) k_rw_wide(StepArgs a) 
             zr[q] = 0.0;
             wr[q] = 1.0;
             if (j < hi) {
-                zr[q] = __ldg(a.z_in + c[q]);
+                zr[q] = ldz(a.z_in + c[q], a.zhint);
                 if (!UNIT) wr[q] = F32 ? (double)__ldcs(a.wval32 + j) : __ldcs(a.wval + j);
             }
         }
@@ -254,8 +281,8 @@ __global__ void __launch_bounds__(kStepTPB, SC_WIDE_MINB) k_rw_wide(StepArgs a) 
 #ifndef SC_MINB_W
 #define SC_MINB_W 5  // weighted: 5 CTAs of 256 (C4 539 -> 497 us, C3 275 -> 270; 6 spills and thrashes C4)
 #endif
-template <bool UNIT, bool SYM, bool F32 = false>
-__global__ void __launch_bounds__(kStepTPB, (UNIT || F32) ? SC_MINB_U : SC_MINB_W) k_rw_step(StepArgs a) {
+template <bool UNIT, bool SYM, bool F32 = false, bool BIGZ = false>
+__global__ void __launch_bounds__(kStepTPB, (UNIT || F32 || BIGZ) ? SC_MINB_U : SC_MINB_W) k_rw_step(StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     // ---- SELL slices: one warp per slice, one lane per row
@@ -295,7 +322,7 @@ __global__ void __launch_bounds__(kStepTPB, (UNIT || F32) ? SC_MINB_U : SC_MINB_
         for (int q = 0; q < kUnroll; ++q) {
             p[q] = 0.0;
             if (c[q] != kPad) {
-                const double zv = __ldg(a.z_in + c[q]);
+                const double zv = BIGZ ? ldz64(a.z_in + c[q]) : __ldg(a.z_in + c[q]);
                 const double wv = UNIT ? 1.0
                                   : F32 ? (double)__ldcs(vp32 + (int64_t)(t + q) * kSlice)
                                         : __ldcs(vp + (int64_t)(t + q) * kSlice);
@@ -817,6 +844,7 @@ struct Multi;  // sc_multi.cuh: one handle over several GPUs
 struct sc_graph {
     int device = 0;
     int sm_count = 0;
+    int64_t l2_bytes = 0;
     int64_t n = 0, nnz = 0, ncols = 0, col_offset = 0, global_row0 = 0;
     int64_t n_sell = 0, n_wide = 0, nslices = 0, sell_entries = 0, wide_entries = 0;
     bool unit = false;
@@ -1207,6 +1235,11 @@ static int32_t graph_init(const int64_t *row_ptr, const int32_t *col, const doub
     g->col_offset = col_offset;
     g->global_row0 = global_row0;
     cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
+    {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+        g->l2_bytes = l2;
+    }
     bool unit = (val == nullptr && dval == nullptr);
     if (val) {
         unit = true;
@@ -1500,6 +1533,25 @@ static int32_t ensure_isd(sc_graph *g, cudaStream_t s) {
     return SC_OK;
 }
 
+template <bool BIGZ>
+static void launch_slices_t(const sc_graph *g, const StepArgs &a, bool sym, dim3 grid, cudaStream_t s) {
+    if (g->unit) {
+        if (sym) k_rw_step<true, true, false, BIGZ><<<grid, kStepTPB, 0, s>>>(a);
+        else k_rw_step<true, false, false, BIGZ><<<grid, kStepTPB, 0, s>>>(a);
+    } else if (g->f32) {
+        if (sym) k_rw_step<false, true, true, BIGZ><<<grid, kStepTPB, 0, s>>>(a);
+        else k_rw_step<false, false, true, BIGZ><<<grid, kStepTPB, 0, s>>>(a);
+    } else {
+        if (sym) k_rw_step<false, true, false, BIGZ><<<grid, kStepTPB, 0, s>>>(a);
+        else k_rw_step<false, false, false, BIGZ><<<grid, kStepTPB, 0, s>>>(a);
+    }
+}
+// the slice kernel with the 64-byte L2 fetch hint on its gathers when z does not fit the L2
+static void launch_slices(const sc_graph *g, const StepArgs &a, bool sym, dim3 grid, cudaStream_t s) {
+    if (a.zhint) launch_slices_t<true>(g, a, sym, grid, s);
+    else launch_slices_t<false>(g, a, sym, grid, s);
+}
+
 // rows [row_lo, row_hi) of the renumbered shard; SELL boundaries must be slice-aligned
 static int32_t launch_step(const sc_graph *g, const double *z_in, const double *x_in,
                            double *x_out, double *z_out, double sign, uint32_t flags,
@@ -1536,6 +1588,7 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.nslices = g->nslices;
     a.col_offset = g->col_offset;
     a.hs = sign < 0 ? -0.5 : 0.5;
+    a.zhint = g->l2_bytes > 0 && g->ncols * 8 > g->l2_bytes;
     a.peer_base = g->d_peer_z;
     a.npeer = 0;
     a.peer_off = 0;
@@ -1583,16 +1636,7 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
         SC_CUDA(launch_window_step(g, a, sym, s));
     } else if (sblocks) {
         const dim3 grid((unsigned)sblocks);
-        if (g->unit) {
-            if (sym) k_rw_step<true, true><<<grid, kStepTPB, 0, s>>>(a);
-            else k_rw_step<true, false><<<grid, kStepTPB, 0, s>>>(a);
-        } else if (g->f32) {
-            if (sym) k_rw_step<false, true, true><<<grid, kStepTPB, 0, s>>>(a);
-            else k_rw_step<false, false, true><<<grid, kStepTPB, 0, s>>>(a);
-        } else {
-            if (sym) k_rw_step<false, true><<<grid, kStepTPB, 0, s>>>(a);
-            else k_rw_step<false, false><<<grid, kStepTPB, 0, s>>>(a);
-        }
+        launch_slices(g, a, sym, grid, s);
     }
     if (a.wide_blocks) {
         SC_CUDA(cudaEventRecord(g->ev_join, g->side));
