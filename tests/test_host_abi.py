@@ -59,6 +59,9 @@ def test_abi_rejects_bad_input_without_gpu():
     st = L.sc_graph_create(_lib.ptr(rp), _lib.ptr(col_bad), None, _lib.ptr(deg), 2, 2, 0,
                            ctypes.byref(h))
     assert st == -2 and b"out of range" in L.sc_last_error()
+    # layout builders on a null handle
+    assert L.sc_graph_build_windows(None) == -1 and L.sc_graph_build_panels(None) == -1
+    assert _lib.SC_CREATE_WINDOWS == 0x10 and ctypes.sizeof(_lib.GraphInfo) == 112  # sizeof(sc_graph_info)
 
 
 @pytest.mark.skipif(_lib.load().sc_device_count() > 0, reason="GPU present")
@@ -76,6 +79,7 @@ def test_params_semantics():
     assert SpectralParams(k=5, t=50, mode="one_vector").num_steps(1000) == 50
     assert "one_vector" in MODES
     assert SpectralParams(k=5).layout == "auto"
+    assert SpectralParams(k=5, layout="windows").layout == "windows"
     for bad in (dict(k=1), dict(k=3, mode="nope"), dict(k=3, t=-1), dict(k=3, seed=-2),
                 dict(k=3, epsilon=0.0), dict(k=3, walk_sign=2), dict(k=3, layout="ell")):
         with pytest.raises(InputError):
@@ -175,3 +179,4 @@ def test_bench_helpers():
     assert bench.traffic_from_profiles(4, False, "sell", "bfs") is not None
     assert bench.traffic_from_profiles(5, True, "sell", "none") is not None
     assert bench.traffic_from_profiles(2, True, "panels", "none") is not None
+    assert bench.traffic_from_profiles(4, False, "windows", "bfs") is not None
