@@ -64,6 +64,78 @@ constexpr int kWinUnroll = SC_WIN_UNROLL;  // pair-steps per batch; two batches 
 constexpr int kWinFarPT = (kWinFarMax + kWinTPB - 1) / kWinTPB;  // far slots per thread
 constexpr uint32_t kWinPadPair = (uint32_t)kWinZ | ((uint32_t)kWinZ << 16);
 
+// one slice (32 rows, a lane each) folded in stored order from the staged window wz
+template <bool UNIT, bool SYM, bool F32>
+__device__ __forceinline__ void win_fold_slice(const StepArgs &a, const WinArgs &w,
+                                               const double *wz, int sl, int lane) {
+    const int64_t r = (int64_t)sl * kSlice + lane;
+    const bool live = r < a.n_sell;
+    double xr = 0.0, sc = 1.0;
+    if (live) {
+        xr = __ldcs(a.x_in + r);
+        sc = __ldcs(a.scale + r);
+    }
+    const int64_t base = w.ptr[sl];
+    const int np = (int)((w.ptr[sl + 1] - base) >> 5);
+    const uint32_t *ip = w.idx + base + lane;
+    const double2 *vp = (UNIT || F32) ? nullptr : w.val + base + lane;
+    const float2 *vp32 = F32 ? w.val32 + base + lane : nullptr;
+    // three register sets rotate by name: while one batch of kWinUnroll pair-steps is
+    // gathered from shared memory and added in order, the next two batches' index and
+    // weight pairs are in flight from global memory.  (Tried: one stream per warp across
+    // its slices with two cursors -- 505 us vs 481 us at config 4, and any spilled load
+    // target serialises the prefetch: 607 us.)
+    auto load = [&](int p0, uint32_t (&ci)[kWinUnroll], double2 (&wv)[kWinUnroll]) {
+#pragma unroll
+        for (int q = 0; q < kWinUnroll; ++q) {
+            const int p = p0 + q;
+            const bool in = p < np;
+            ci[q] = in ? __ldcs(ip + (int64_t)p * kSlice) : kWinPadPair;
+            if (!UNIT) {
+                wv[q] = make_double2(0.0, 0.0);
+                if (in) {
+                    if (F32) {
+                        const float2 f = __ldcs(vp32 + (int64_t)p * kSlice);
+                        wv[q] = make_double2((double)f.x, (double)f.y);
+                    } else {
+                        wv[q] = __ldcs(vp + (int64_t)p * kSlice);
+                    }
+                }
+            }
+        }
+    };
+    double s = 0.0;
+    auto fold = [&](const uint32_t (&ci)[kWinUnroll], const double2 (&wv)[kWinUnroll]) {
+        double z0[kWinUnroll], z1[kWinUnroll];
+#pragma unroll
+        for (int q = 0; q < kWinUnroll; ++q) {
+            z0[q] = wz[ci[q] & 0xffffu];
+            z1[q] = wz[ci[q] >> 16];
+        }
+#pragma unroll
+        for (int q = 0; q < kWinUnroll; ++q) {
+            s = __dadd_rn(s, UNIT ? z0[q] : __dmul_rn(wv[q].x, z0[q]));
+            s = __dadd_rn(s, UNIT ? z1[q] : __dmul_rn(wv[q].y, z1[q]));
+        }
+    };
+    uint32_t cA[kWinUnroll], cB[kWinUnroll], cC[kWinUnroll];
+    double2 wA[kWinUnroll], wB[kWinUnroll], wC[kWinUnroll];
+    load(0, cA, wA);
+    load(kWinUnroll, cB, wB);
+    for (int p0 = 0; p0 < np;) {
+        load(p0 + 2 * kWinUnroll, cC, wC);
+        fold(cA, wA);
+        if ((p0 += kWinUnroll) >= np) break;
+        load(p0 + 2 * kWinUnroll, cA, wA);
+        fold(cB, wB);
+        if ((p0 += kWinUnroll) >= np) break;
+        load(p0 + 2 * kWinUnroll, cB, wB);
+        fold(cC, wC);
+        p0 += kWinUnroll;
+    }
+    if (live) row_epilogue<SYM>(a, r, s, xr, sc);
+}
+
 template <bool UNIT, bool SYM, bool F32>
 __global__ void __launch_bounds__(kWinTPB, 2) k_rw_win(StepArgs a, WinArgs w) {
     extern __shared__ __align__(128) double wz[];  // panel (kWinZ) | zero slot | far slots
@@ -103,74 +175,8 @@ __global__ void __launch_bounds__(kWinTPB, 2) k_rw_win(StepArgs a, WinArgs w) {
     pan_mbar_wait(&zfull, 0);
     // slices are dealt round-robin to the warps (an item's slices are consecutive in the
     // length-sorted window, so every warp gets a similar mix)
-    for (int sl = it.slice_lo + warp; sl < it.slice_hi; sl += kWinTPB / 32) {
-        const int64_t r = (int64_t)sl * kSlice + lane;
-        const bool live = r < a.n_sell;
-        double xr = 0.0, sc = 1.0;
-        if (live) {
-            xr = __ldcs(a.x_in + r);
-            sc = __ldcs(a.scale + r);
-        }
-        const int64_t base = w.ptr[sl];
-        const int np = (int)((w.ptr[sl + 1] - base) >> 5);
-        const uint32_t *ip = w.idx + base + lane;
-        const double2 *vp = (UNIT || F32) ? nullptr : w.val + base + lane;
-        const float2 *vp32 = F32 ? w.val32 + base + lane : nullptr;
-        // three register sets rotate by name: while one batch of kWinUnroll pair-steps is
-        // gathered from shared memory and added in order, the next two batches' index and
-        // weight pairs are in flight from global memory.  (Tried: one stream per warp across
-        // its slices with two cursors -- 505 us vs 481 us at config 4, and any spilled load
-        // target serialises the prefetch: 607 us.)
-        auto load = [&](int p0, uint32_t (&ci)[kWinUnroll], double2 (&wv)[kWinUnroll]) {
-#pragma unroll
-            for (int q = 0; q < kWinUnroll; ++q) {
-                const int p = p0 + q;
-                const bool in = p < np;
-                ci[q] = in ? __ldcs(ip + (int64_t)p * kSlice) : kWinPadPair;
-                if (!UNIT) {
-                    wv[q] = make_double2(0.0, 0.0);
-                    if (in) {
-                        if (F32) {
-                            const float2 f = __ldcs(vp32 + (int64_t)p * kSlice);
-                            wv[q] = make_double2((double)f.x, (double)f.y);
-                        } else {
-                            wv[q] = __ldcs(vp + (int64_t)p * kSlice);
-                        }
-                    }
-                }
-            }
-        };
-        double s = 0.0;
-        auto fold = [&](const uint32_t (&ci)[kWinUnroll], const double2 (&wv)[kWinUnroll]) {
-            double z0[kWinUnroll], z1[kWinUnroll];
-#pragma unroll
-            for (int q = 0; q < kWinUnroll; ++q) {
-                z0[q] = wz[ci[q] & 0xffffu];
-                z1[q] = wz[ci[q] >> 16];
-            }
-#pragma unroll
-            for (int q = 0; q < kWinUnroll; ++q) {
-                s = __dadd_rn(s, UNIT ? z0[q] : __dmul_rn(wv[q].x, z0[q]));
-                s = __dadd_rn(s, UNIT ? z1[q] : __dmul_rn(wv[q].y, z1[q]));
-            }
-        };
-        uint32_t cA[kWinUnroll], cB[kWinUnroll], cC[kWinUnroll];
-        double2 wA[kWinUnroll], wB[kWinUnroll], wC[kWinUnroll];
-        load(0, cA, wA);
-        load(kWinUnroll, cB, wB);
-        for (int p0 = 0; p0 < np;) {
-            load(p0 + 2 * kWinUnroll, cC, wC);
-            fold(cA, wA);
-            if ((p0 += kWinUnroll) >= np) break;
-            load(p0 + 2 * kWinUnroll, cA, wA);
-            fold(cB, wB);
-            if ((p0 += kWinUnroll) >= np) break;
-            load(p0 + 2 * kWinUnroll, cB, wB);
-            fold(cC, wC);
-            p0 += kWinUnroll;
-        }
-        if (live) row_epilogue<SYM>(a, r, s, xr, sc);
-    }
+    for (int sl = it.slice_lo + warp; sl < it.slice_hi; sl += kWinTPB / 32)
+        win_fold_slice<UNIT, SYM, F32>(a, w, wz, sl, lane);
     peer_fence(a);
 }
 
@@ -440,6 +446,20 @@ static int32_t build_windows(sc_graph *g, bool prof) {
         fprintf(stderr, "[sc_graph_create] windows: %d items, %.3f of the entries in own panels, %lld far\n",
                 nitems, g->win_cover, (long long)nfar);
     return SC_OK;
+}
+
+// the SELL rows of a whole-handle step through the window layout (wide rows stay with
+// k_rw_wide, launched by the caller)
+// the SELL rows of a whole-handle step through the window layout (wide rows stay with
+// k_rw_wide, launched by the caller)
+template <bool UNIT, bool SYM, bool F32>
+static cudaError_t launch_win2_t(const sc_graph *g, const StepArgs &a, const WinArgs &w, cudaStream_t s) {
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_rw_win2<UNIT, SYM, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kW2Smem);
+    if (attr) return attr;
+    const int grid = std::min(g->win_items, std::max(g->sm_count, 1));
+    k_rw_win2<UNIT, SYM, F32><<<grid, kW2Threads, kW2Smem, s>>>(a, w, g->win_items);
+    return cudaGetLastError();
 }
 
 // the SELL rows of a whole-handle step through the window layout (wide rows stay with
