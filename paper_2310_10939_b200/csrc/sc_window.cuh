@@ -450,20 +450,6 @@ static int32_t build_windows(sc_graph *g, bool prof) {
 
 // the SELL rows of a whole-handle step through the window layout (wide rows stay with
 // k_rw_wide, launched by the caller)
-// the SELL rows of a whole-handle step through the window layout (wide rows stay with
-// k_rw_wide, launched by the caller)
-template <bool UNIT, bool SYM, bool F32>
-static cudaError_t launch_win2_t(const sc_graph *g, const StepArgs &a, const WinArgs &w, cudaStream_t s) {
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        k_rw_win2<UNIT, SYM, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kW2Smem);
-    if (attr) return attr;
-    const int grid = std::min(g->win_items, std::max(g->sm_count, 1));
-    k_rw_win2<UNIT, SYM, F32><<<grid, kW2Threads, kW2Smem, s>>>(a, w, g->win_items);
-    return cudaGetLastError();
-}
-
-// the SELL rows of a whole-handle step through the window layout (wide rows stay with
-// k_rw_wide, launched by the caller)
 static cudaError_t launch_window_step(const sc_graph *g, const StepArgs &a, bool sym, cudaStream_t s) {
     WinArgs w;
     w.items = g->d_win_items;
