@@ -37,6 +37,13 @@ def _full_size_power(cfg, seed=0):
         with DeviceGraph.from_device_csr(d) as dg:
             x0d = dg.sample_irwin_hall(seed, return_host=True)
             xT, f = dg.power_iterate(T)
+        if cfg == 4:
+            # the bench's layout at this config: BFS pre-order + row windows (sc_window.cuh)
+            with DeviceGraph.from_device_csr(d, reorder="bfs", windows=True) as dw:
+                assert dw.info()["window_items"] > 0
+                dw.sample_irwin_hall(seed)
+                xw, fw = dw.power_iterate(T)
+            assert np.array_equal(xw, xT) and np.array_equal(fw, f), "window layout differs"
     x0 = O.irwin_hall(g.degrees, seed, threads=THREADS)
     assert np.array_equal(x0d, x0), "Irwin-Hall x0 differs from the oracle"
     xo, fo = O.power_iterate(g.row_offsets, g.col_indices, g.weights, g.degrees, x0, T,
