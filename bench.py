@@ -314,7 +314,7 @@ def smem_ceiling(cfg: int, kernel_ms: float):
     t_us = wf / sms / (ghz * 1e3)
     return {"wavefronts_per_launch": wf, "bound_us": t_us, "kernel_us": kernel_ms * 1e3,
             "frac": t_us / (kernel_ms * 1e3),
-            "source": "profiles/r01_spmv_panel_ncu_full.txt (l1tex__data_pipe_lsu_wavefronts_mem_shared.sum), "
+            "source": "profiles/r02_spmv_panel_ncu_full.txt (l1tex__data_pipe_lsu_wavefronts_mem_shared.sum), "
                       "148 SMs x 1.965 GHz x 1 wavefront/cycle"}
 
 
