@@ -443,12 +443,33 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
 
 
+class _QuietStdout:
+    """stdout carries exactly ONE JSON line: while the bench runs, file descriptor 1 points at
+    stderr (libraries chat there: NCCL prints its version banner to stdout under
+    NCCL_DEBUG=VERSION/WARN), and print() goes to a Python stream over the saved descriptor."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self._saved = os.dup(1)
+        os.dup2(2, 1)
+        self._old = sys.stdout
+        sys.stdout = os.fdopen(self._saved, "w", buffering=1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self._saved, 1)
+        sys.stdout = self._old
+        return False
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_b200(args)
+    with _QuietStdout():
+        if args.impl == "reference":
+            run_reference(args)
+        else:
+            run_b200(args)
 
 
 if __name__ == "__main__":

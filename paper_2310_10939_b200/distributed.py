@@ -695,6 +695,9 @@ def _init_dist():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     if not dist.is_initialized():
+        # NCCL writes its debug output (the version banner under NCCL_DEBUG=VERSION/INFO) to
+        # stdout by default; the bench prints exactly one JSON line there
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 

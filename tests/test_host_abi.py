@@ -180,3 +180,24 @@ def test_bench_helpers():
     assert bench.traffic_from_profiles(5, True, "sell", "none") is not None
     assert bench.traffic_from_profiles(2, True, "panels", "none") is not None
     assert bench.traffic_from_profiles(4, False, "windows", "bfs") is not None
+
+
+def test_bench_stdout_is_one_json_line(tmp_path):
+    """library chatter on file descriptor 1 (NCCL's version banner) must not reach the bench's
+    stdout: inside bench._QuietStdout fd 1 points at stderr and print() keeps the real stdout"""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import importlib.util, os\n"
+        f"spec = importlib.util.spec_from_file_location('bench', {os.path.join(root, 'bench.py')!r})\n"
+        "b = importlib.util.module_from_spec(spec); spec.loader.exec_module(b)\n"
+        "with b._QuietStdout():\n"
+        "    os.write(1, b'NCCL version x\\n')\n"
+        "    print('{\"json\": 1}', flush=True)\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout == '{"json": 1}\n'
+    assert "NCCL version x" in r.stderr
