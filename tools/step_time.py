@@ -22,7 +22,7 @@ elif cfg == 4:  # the BFS pre-order needs the host graph path (as the bench)
     dg = DeviceGraph(g, reorder="auto", panels=T >= 64, windows=win, fp32_values=f32)
 else:
     with config_device_csr(cfg) as d:
-        dg = DeviceGraph.from_device_csr(d, panels=T >= 64)
+        dg = DeviceGraph.from_device_csr(d, panels=T >= 64, windows=win, fp32_values=f32)
 dg.sample_irwin_hall(0)
 ts = []
 for rep in range(4):
