@@ -1588,7 +1588,13 @@ static int32_t launch_step(const sc_graph *g, const double *z_in, const double *
     a.nslices = g->nslices;
     a.col_offset = g->col_offset;
     a.hs = sign < 0 ? -0.5 : 0.5;
-    a.zhint = g->l2_bytes > 0 && g->ncols * 8 > g->l2_bytes;
+    // (SC_ZHINT=1 / 0 forces the 64-byte fetch hint on / off: tests run the hinted kernels on
+    // small graphs)
+    static const int zhint_env = [] {
+        const char *e = getenv("SC_ZHINT");
+        return e ? atoi(e) : -1;
+    }();
+    a.zhint = zhint_env >= 0 ? (zhint_env != 0) : (g->l2_bytes > 0 && g->ncols * 8 > g->l2_bytes);
     a.peer_base = g->d_peer_z;
     a.npeer = 0;
     a.peer_off = 0;
