@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -104,6 +106,7 @@ struct sc_kmeans {
     // exact sequential-sum workspaces (sc_seqsum.cuh)
     int64_t cap_chunks = 0;
     double *d_A = nullptr, *d_vmax = nullptr, *d_cstart = nullptr, *d_total = nullptr;
+    double *d_a64 = nullptr;  // fp64 chunk sums of the k-means++ weights (certified fast draw)
     int32_t *d_kpred = nullptr, *d_neg = nullptr, *d_round_on = nullptr, *d_on = nullptr;
     int64_t *d_q0 = nullptr, *d_q1 = nullptr, *d_cofs = nullptr, *d_nchunks = nullptr;
     int64_t *d_segkpp = nullptr;   // [R+1] restart segments over d_best
@@ -714,7 +717,7 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
                  const int64_t *__restrict__ chosen, const int32_t *__restrict__ start,
                  const int32_t *__restrict__ on, const int32_t *__restrict__ round_on,
                  double *__restrict__ best, SeqWork w, int32_t *__restrict__ kmap, int64_t cps,
-                 int R) {
+                 int R, double *__restrict__ a64) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -802,6 +805,14 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
         }
         const bool anybad = __any_sync(0xffffffffu, bad);
         if (need_map) lm = warp_scan_pmap(lm);
+        if (a64) {  // fp64 chunk sum (13 roundings) for the certified fast draw (k_kpp_fast)
+            double s64 = 0.0;
+#pragma unroll
+            for (int q = 0; q < kSeqPerLane; ++q) s64 = __dadd_rn(s64, a[q]);
+#pragma unroll
+            for (int d = 16; d; d >>= 1) s64 = __dadd_rn(s64, __shfl_xor_sync(0xffffffffu, s64, d));
+            if (lane == 31) a64[c] = s64;
+        }
         if (lane == 31) {
             w.A[c] = (double)sum;
             w.vmax[c] = (double)mx;
@@ -814,6 +825,123 @@ k_kpp_update_map(const double *__restrict__ x, int64_t n, int k, int i,
                 kmap[c] = kNoMap;  // the old map no longer describes the chunk
             }
         }
+    }
+}
+
+// Certified fast k-means++ draw (kmeans.py:116-118), one CTA per restart.  The reference picks
+// idx = searchsorted(cum, u * cum[-1], 'right') on the SEQUENTIAL fp64 cumsum of the weights.
+// Sums of nonnegative terms computed with m roundings in ANY order lie within m u / (1 - m u)
+// of the real sum (u = 2^-53), so every sequential prefix cum[j] lies in [q (1 - eps),
+// q (1 + eps)] for the tree-order prefix q of the same terms, eps >= (n + roundings of q) u (the
+// host passes 1.0625 (n + 128 + tiles) u).  With T the tree total, the target u * cum[-1]
+// (one more rounding) lies in [tl, th] = [u T (1 - eps - 2u), u T (1 + eps + 2u)] (directed
+// roundings).  The draw is j exactly when cum[j-1] <= target < cum[j]; it is CERTIFIED when
+// q[j-1] (1 + eps) <= tl and q[j] (1 - eps) > th (cum is nondecreasing, so j-1 covers all
+// earlier indices).  Then chosen is written and the restart's round flag cleared, so the exact
+// pipeline below (prediction, chunk maps, compose, search) skips it; otherwise nothing is
+// written and the exact pipeline decides (probability ~2 eps T / weight per draw).  A zero tree
+// total means every weight is zero exactly: the degenerate branch (kmeans.py:128-134), reported
+// as k_kpp_search2 does.
+__global__ void __launch_bounds__(256) k_kpp_fast(const double *__restrict__ best,
+                                                  const double *__restrict__ a64, int64_t n,
+                                                  int64_t nb, int64_t cps, int k, int i,
+                                                  const double *__restrict__ u,
+                                                  int64_t *__restrict__ chosen, int32_t *__restrict__ on,
+                                                  int32_t *__restrict__ round_on,
+                                                  int32_t *__restrict__ degen, double eps,
+                                                  unsigned long long *__restrict__ stats) {
+    using Reduce = cub::BlockReduce<double, 256>;
+    using Scan = cub::BlockScan<double, 256>;
+    __shared__ union {
+        typename Reduce::TempStorage tr;
+        typename Scan::TempStorage ts;
+    } tmp;
+    __shared__ double s_T, s_start;
+    __shared__ long long s_chunk;
+    const int r = blockIdx.x, tid = threadIdx.x;
+    if (!round_on[r]) return;
+    const double *A = a64 + (int64_t)r * cps;
+    double part = 0.0;
+    for (int64_t c = tid; c < cps; c += 256) part = __dadd_rn(part, A[c]);
+    const double tot = Reduce(tmp.tr).Sum(part);
+    if (tid == 0) {
+        s_T = tot;
+        s_chunk = -1;
+    }
+    __syncthreads();
+    const double T = s_T;
+    if (T == 0.0) {  // all weights are +0.0: degenerate round
+        if (tid == 0) {
+            degen[r] = i;
+            on[r] = 0;
+            round_on[r] = 0;
+        }
+        return;
+    }
+    if (!(T > 1e-280) || !(T < 1e280)) return;  // (NaN, overflow, near-subnormal: exact path)
+    const double ur = u[(int64_t)r * (k - 1) + (i - 1)];
+    const double dn = 1.0 - eps - 2.3e-16, up = 1.0 + eps + 2.3e-16;
+    const double tl = __dmul_rd(__dmul_rd(ur, T), dn), th = __dmul_ru(__dmul_ru(ur, T), up);
+    const double e_up = 1.0 + eps, e_dn = 1.0 - eps;
+    // the chunk whose [start, end) certainly holds the target
+    double carry = 0.0;
+    for (int64_t c0 = 0; c0 < cps; c0 += 256) {
+        const int64_t c = c0 + tid;
+        const double v = c < cps ? A[c] : 0.0;
+        double excl, agg;
+        __syncthreads();
+        Scan(tmp.ts).ExclusiveSum(v, excl, agg);
+        const double st = __dadd_rn(carry, excl);
+        const double end = __dadd_rn(carry, __dadd_rn(excl, v));
+        carry = __dadd_rn(carry, agg);
+        if (c < cps && __dmul_ru(st, e_up) <= tl && __dmul_rd(end, e_dn) > th) {
+            s_chunk = (long long)c;
+            s_start = st;
+        }
+    }
+    __syncthreads();
+    const long long cs = s_chunk;
+    if (cs < 0) return;
+    if (tid >= 32) return;
+    // inside the chunk: lane-local sequential prefixes on top of a warp scan of the lane sums
+    const int lane = tid;
+    const double *wv = best + (int64_t)r * nb + cs * kSeqChunk + lane * kSeqPerLane;
+    double a[kSeqPerLane], loc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSeqPerLane; ++q) {
+        a[q] = wv[q];
+        loc = __dadd_rn(loc, a[q]);
+    }
+    double inc = loc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc = __dadd_rn(inc, o);
+    }
+    double q = __dadd_rn(s_start, __shfl_up_sync(0xffffffffu, inc, 1));  // prefix before this lane
+    if (lane == 0) q = s_start;
+    int hit = -1;
+    bool okp = false;
+#pragma unroll
+    for (int t = 0; t < kSeqPerLane; ++t) {
+        const double qn = __dadd_rn(q, a[t]);
+        if (hit < 0 && __dmul_rd(qn, e_dn) > th) {
+            hit = t;
+            okp = __dmul_ru(q, e_up) <= tl;
+        }
+        q = qn;
+    }
+    // the first lane that crosses decides (prefixes are nondecreasing)
+    const unsigned mh = __ballot_sync(0xffffffffu, hit >= 0);
+    if (!mh) return;
+    const int wl = __ffs(mh) - 1;
+    const int whit = __shfl_sync(0xffffffffu, hit, wl);
+    const bool wok = __shfl_sync(0xffffffffu, okp, wl);
+    const int64_t idx = cs * kSeqChunk + wl * kSeqPerLane + whit;
+    if (lane == 0 && wok && idx < n) {
+        chosen[(int64_t)r * k + i] = idx;
+        round_on[r] = 0;
+        if (stats) atomicAdd(stats, 1ull);
     }
 }
 
@@ -1827,6 +1955,7 @@ static int32_t ensure(sc_kmeans *km, int R, int k) {
     }
     if ((st = grow(&km->d_empty, (size_t)R, km->stream))) return st;
     if ((st = grow(&km->d_A, (size_t)nch, km->stream))) return st;
+    if ((st = grow(&km->d_a64, (size_t)nch, km->stream))) return st;
     if ((st = grow(&km->d_vmax, (size_t)nch, km->stream))) return st;
     if ((st = grow(&km->d_cstart, (size_t)nch, km->stream))) return st;
     if ((st = grow(&km->d_kpred, (size_t)nch, km->stream))) return st;
@@ -1967,7 +2096,7 @@ void sc_kmeans_destroy(sc_kmeans *km) {
                     km->d_vals, km->d_vals_alt, km->d_cub, km->d_chosen, km->d_u,
                     km->d_start, km->d_degen, km->d_cen, km->d_scen, km->d_sidx, km->d_cmax,
                     km->d_cnt, km->d_seg, km->d_part,
-                    km->d_cost, km->d_changed, km->d_active, km->d_empty, km->d_A,
+                    km->d_cost, km->d_changed, km->d_active, km->d_empty, km->d_A, km->d_a64,
                     km->d_vmax, km->d_cstart, km->d_total, km->d_kpred, km->d_neg,
                     km->d_round_on, km->d_on, km->d_q0, km->d_q1, km->d_cofs, km->d_nchunks,
                     km->d_sq0, km->d_sq1, km->d_svmax, km->d_skp, km->d_idx, km->d_idx_alt,
@@ -2064,10 +2193,19 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     // SC_KPP_STATS: count the chunk maps the fix-up pass had to rebuild (diagnostics)
     unsigned long long *d_stats = nullptr;
     if (getenv("SC_KPP_STATS")) {
-        SC_CUDA(cudaMallocAsync((void **)&d_stats, 8, s));
-        SC_CUDA(cudaMemsetAsync(d_stats, 0, 8, s));
+        SC_CUDA(cudaMallocAsync((void **)&d_stats, 16, s));
+        SC_CUDA(cudaMemsetAsync(d_stats, 0, 16, s));
     }
     const int gu = grid_1d(km, cps * R * 32, 256);
+    // certified fast draw (k_kpp_fast): n up to 2^24 (beyond, the sequential sum's own rounding
+    // bound n * 2^-53 approaches the weights' share of the total and certification fails)
+    const bool fast = fused1d && n <= (int64_t(1) << 24) && getenv("SC_KPP_NOFAST") == nullptr;
+    // (SC_KPP_EPS_SCALE widens the certification margin: tests force the mixed case where some
+    // restarts of a round are certified and others take the exact pipeline)
+    const char *eps_scale = getenv("SC_KPP_EPS_SCALE");
+    const double fast_eps = std::min(0.25, (eps_scale ? atof(eps_scale) : 1.0) * 1.0625 *
+                                               (double)(n + 128 + (cps + 255) / 256) *
+                                               1.1102230246251565e-16);
     for (int i = smin; i < k; ++i) {
         k_kpp_round_on<<<(R + 127) / 128, 128, 0, s>>>(R, i, km->d_start, km->d_on,
                                                        km->d_round_on, km->d_neg);
@@ -2075,7 +2213,11 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
             // one pass: weights, chunk summaries and (speculative) chunk maps; x read once
             k_kpp_update_map<<<gu, 256, 0, s>>>(km->d_x, n, k, i, km->d_chosen, km->d_start,
                                                 km->d_on, km->d_round_on, km->d_best, w,
-                                                km->d_kmap, cps, R);
+                                                km->d_kmap, cps, R, fast ? km->d_a64 : nullptr);
+            if (fast)
+                k_kpp_fast<<<R, 256, 0, s>>>(km->d_best, km->d_a64, n, nb, cps, k, i, km->d_u,
+                                             km->d_chosen, km->d_on, km->d_round_on, km->d_degen,
+                                             fast_eps, d_stats ? d_stats + 1 : nullptr);
             k_seq_predict<32><<<R, 32 * 32, 0, s>>>(v, w);
             k_seq_chunkmap_fix<<<grid_1d(km, nch, 256), 256, 0, s>>>(v, w, km->d_kmap,
                                                                     km->d_nchunks, d_stats);
@@ -2102,11 +2244,13 @@ int32_t sc_kmeans_pp(sc_kmeans *km, int32_t k, int32_t R, const int32_t *start_r
     SC_CUDA(cudaMemcpyAsync(degenerate_out, km->d_degen, (size_t)R * 4, cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
     if (d_stats) {
-        unsigned long long h = 0;
-        cudaMemcpy(&h, d_stats, 8, cudaMemcpyDeviceToHost);
+        unsigned long long hh[2] = {0, 0};
+        cudaMemcpy(hh, d_stats, 16, cudaMemcpyDeviceToHost);
         cudaFree(d_stats);
-        fprintf(stderr, "[kpp] rounds %d..%d, R=%d, chunks %lld: chunk maps rebuilt %llu (%.2f per round per restart)\n",
-                smin, k - 1, R, (long long)cps, h, (double)h / std::max(1, k - smin) / R);
+        const unsigned long long h = hh[0];
+        fprintf(stderr, "[kpp] rounds %d..%d, R=%d, chunks %lld: chunk maps rebuilt %llu (%.2f per round per restart); "
+                "draws certified by the fast path %llu\n",
+                smin, k - 1, R, (long long)cps, h, (double)h / std::max(1, k - smin) / R, hh[1]);
     }
     return SC_OK;
 }

@@ -52,3 +52,22 @@ def test_kmeanspp_restart_counts():
         with KMeans1D(x) as km:
             ch = km.seed_centers(12, 9, R)
         assert np.array_equal(ch, _oracle_seeds(x, 12, 9, R))
+
+
+@pytest.mark.parametrize("case", ["band_300k", "uniform_1m", "negative_500k", "duplicates",
+                                  "wide_band_300k"])
+@pytest.mark.parametrize("mode", ["nofast", "scale_1e4", "scale_1e7", "scale_1e12"])
+def test_certified_fast_draw_and_fallback(case, mode, monkeypatch):
+    """the certified fast draw (k_kpp_fast: tree-order prefix sums with a rigorous bound against
+    the reference's sequential cumsum) against the exact pipeline: off, and with its margin
+    widened so that a growing share of the draws is NOT certified and falls back to the exact
+    pipeline within the same round (1e12: every draw) -- the seeds never change"""
+    make, k = CASES[case]
+    x = make(np.random.default_rng(11))
+    if mode == "nofast":
+        monkeypatch.setenv("SC_KPP_NOFAST", "1")
+    else:
+        monkeypatch.setenv("SC_KPP_EPS_SCALE", mode.split("_")[1])
+    with KMeans1D(x) as km:
+        ch = km.seed_centers(k, 5, 10)
+    assert np.array_equal(ch, _oracle_seeds(x, k, 5, 10))
