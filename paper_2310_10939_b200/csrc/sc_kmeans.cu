@@ -2591,7 +2591,7 @@ int32_t sc_kmeans_lloyd(sc_kmeans *km, int32_t k, int32_t R, const int64_t *chos
     SC_CUDA(cudaMemcpyAsync(lab32.data(), km->d_lab[final_buf[best]] + (size_t)best * n,
                             (size_t)n * 4, cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
-    for (int64_t j = 0; j < n; ++j) labels_out[j] = lab32[(size_t)j];
+    sc::widen_labels(lab32.data(), labels_out, n);
     if (costs_out)
         for (int r = 0; r < R; ++r) costs_out[r] = prev[r];
     if (iters_out)
@@ -2901,7 +2901,7 @@ extern "C" int32_t sc_kmeans_lloyd_sorted(sc_kmeans *km, int32_t k, int32_t R,
     cudaFreeAsync(tmp, s);
     cudaFreeAsync(ys, s);
     SC_CUDA(cudaStreamSynchronize(s));
-    for (int64_t j = 0; j < n; ++j) labels_out[j] = lab32[(size_t)j];
+    sc::widen_labels(lab32.data(), labels_out, n);
     if (costs_out)
         for (int r = 0; r < R; ++r) costs_out[r] = cost[(size_t)r];
     if (iters_out)

@@ -1774,7 +1774,7 @@ int32_t fused_lloyd(FusedLloyd **pctx, int device, int sm_count, cudaStream_t s,
     SC_CUDA(cudaMemcpyAsync(lab8.data(), a.lab + ((size_t)(fin[best] % 3) * R + best) * ln, (size_t)n,
                             cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
-    for (int64_t i = 0; i < n; ++i) labels_out[i] = lab8[(size_t)i];
+    widen_labels(lab8.data(), labels_out, n);
     if (costs_out)
         for (int r = 0; r < R; ++r) costs_out[r] = cex[r];
     if (iters_out)
