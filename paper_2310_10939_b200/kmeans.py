@@ -63,6 +63,16 @@ class Partition:
             raise InputError(f"labels must lie in [0, {self.k})")
 
     @classmethod
+    def _from_device(cls, labels: np.ndarray, k: int) -> "Partition":
+        """labels written by the device Lloyd (int64, C-contiguous; every value is an argmin or
+        repair index over k centres, so it lies in [0, k) by construction): the two O(n) range
+        scans of __post_init__ (~0.7 ms per 1e6 points) are skipped."""
+        self = object.__new__(cls)
+        self.labels = labels
+        self.k = int(k)
+        return self
+
+    @classmethod
     def from_labels(cls, labels, k: int | None = None) -> "Partition":
         labels = np.asarray(labels, dtype=np.int64)
         if k is None:
@@ -195,7 +205,7 @@ class KMeans1D:
             _lib.ptr(costs), _lib.ptr(iters), ctypes.byref(best), ctypes.byref(ms)))
         self.last = {"costs": costs, "iters": iters, "best_restart": best.value,
                      "chosen": chosen, "lloyd_ms": ms.value}
-        return Partition(labels=labels, k=k)
+        return Partition._from_device(labels, k)
 
 
 def _nth_unchosen(taken_sorted: np.ndarray, m: int) -> int:
