@@ -757,6 +757,7 @@ def bench_main(args, metric: str, unit: str):
             plan = exchange_plan(rp, starts, rank, world, pieces=pieces,
                                  align=8192 if pieces == 1 else 1)
             shard = CudaShard.from_device_csr(dcsr, plan, rank, local)
+            n_total, weighted = int(dcsr.n), bool(dcsr.weighted)
         del rp_all
     else:
         starts = np.arange(world + 1, dtype=np.int64) * n_loc
@@ -771,6 +772,7 @@ def bench_main(args, metric: str, unit: str):
             plan = exchange_plan(rp, starts, rank, world, pieces=pieces,
                                  align=8192 if pieces == 1 else 1)
         shard = CudaShard(rp, plan.rename(col), None, deg, plan, rank, local)
+        n_total, weighted = int(params.n), False
     # column panels for whole-shard steps (as the single-GPU pipeline at T >= 64); the peer
     # exchange and multi-piece steps stay on SELL
     panels = False
@@ -869,6 +871,7 @@ def bench_main(args, metric: str, unit: str):
             "exchange": {"kind": "halo send/recv" if halo else "all-gather",
                          "ms_per_step": ag_ms, "recv_bytes_per_gpu": recv_bytes,
                          "gbs_per_gpu": recv_bytes / (ag_ms / 1e3) / 1e9 if world > 1 else 0.0},
+            "roofline": _shard_roofline(nnz_total, n_total, weighted, tot_ms / (args.steps * T), world),
             "clocks": clk.summary(),
             "gpu_launches": args.steps * (1 + (T + 1) * plan.pieces
                                           + ((T + 1) if p2p and world > 1 else 0)
@@ -881,6 +884,28 @@ def bench_main(args, metric: str, unit: str):
         comm.close()
     shard.close()
     dist.destroy_process_group()
+
+
+def _shard_roofline(nnz_total: int, n_total: int, weighted: bool, step_ms: float, world: int) -> dict:
+    """Whole-job HBM roofline of one sharded step (SURVEY.md §8(d) byte formula over all ranks
+    against world x the measured per-GPU peak; the all-gather's bytes are reported separately
+    under "exchange")."""
+    peak, kind = 6650.0, "fallback"
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            peak, kind = float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        pass
+    idx_val = 12 if weighted else 4
+    alg = nnz_total * idx_val + 16 * n_total
+    achieved = alg / (step_ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+            "frac": achieved / (peak * world), "traffic": None, "peak_kind": kind,
+            "alg_bytes_per_launch": alg,
+            "alg_bytes_formula": f"nnz*{idx_val} + 16n over all {world} ranks"
+                                 + (" (idx+val)" if weighted else " (unit weights: val elided)"),
+            "kernel_ms": step_ms}
 
 
 def gather_to_rank0(v_local_original: np.ndarray, plan: ShardPlan, rank: int, group=None):
