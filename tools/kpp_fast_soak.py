@@ -1,6 +1,6 @@
 """Randomised soak of the certified fast k-means++ draw: seeds with the fast path (default and
 with its margin widened) against the exact pipeline (SC_KPP_NOFAST) on random inputs.
-Usage: kpp_fast_soak.py [trials]"""
+Usage: kpp_fast_soak.py [trials] [n_lo] [n_hi]"""
 import os
 import sys
 
@@ -11,10 +11,12 @@ import numpy as np  # noqa: E402
 from paper_2310_10939_b200 import KMeans1D  # noqa: E402
 
 trials = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+n_lo = int(float(sys.argv[2])) if len(sys.argv) > 2 else 5_000
+n_hi = int(float(sys.argv[3])) if len(sys.argv) > 3 else 3_000_000
 rng = np.random.default_rng(2024)
 bad = 0
 for t in range(trials):
-    n = int(rng.integers(5_000, 3_000_000))
+    n = int(rng.integers(n_lo, n_hi))
     kind = t % 6
     if kind == 0:
         x = 0.5 + 10.0 ** rng.integers(-12, -3) * rng.standard_normal(n)
