@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="torchrun path: skip the in-process multi-GPU end-to-end leg")
     ap.add_argument("--weighted", action="store_true",
                     help="force the weighted kernel (reads val even for unit weights)")
     ap.add_argument("--no-weighted-probe", action="store_true")
